@@ -1,0 +1,347 @@
+"""Benchmark: FP64 logdet TFLOP/s (n^3/3 flops per logdet) of the B200 MEMDET engine.
+
+Workload (BASELINE.json configs[1], "C2"): n = 32768 RBF Gram, x_i in R^16 i.i.d. N(0,1)
+(seed 0), l = 4, jitter 1e-6, reference tiling num_blocks = 8.  Synthetic (the paper's
+NTK / kernel matrices are not available offline); generated on the device, untimed.
+
+One step = one full logdet + all 32768 prefix log-determinants of that matrix:
+  value : input row-major in HBM when the timed region starts; the step packs the upper tile
+          triangle, factors, and scans the prefix (libmemdet_b200.so, CUDA events on the
+          launching stream, barrier + synchronize around K steps, max over ranks).
+  e2e   : the same metric through the public API memdet_cholesky(host pinned array,
+          num_blocks=8): host->device copy of the upper triangle and device->host copy of the
+          prefix and d are inside the timed region.
+N > 1 (torchrun): every rank factors its own replica (the block-cyclic multi-GPU factorisation
+is not built yet) -> scaling "weak", value = all ranks' flops / max time.
+
+`--impl reference` times the reference's CPU path (oracle port of oocdet.memdet_cholesky: the
+same SciPy LAPACK / NumPy BLAS calls, all host threads) on a bounded sample of the workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "FP64 logdet TFLOP/s (n^3/3)"
+UNIT = "TFLOP/s"
+C2 = dict(n=32768, num_blocks=8, d=16, ell=4.0, jitter=1e-6, seed=0)
+SAMPLE_N = 16384  # CPU baseline sample: leading principal 16384 submatrix of C2, b = 4096
+PROFILE_SUMMARY = os.path.join(REPO, "profiles", "r01_gemm_update_ncu.json")
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU sample
+
+
+def cpu_sample_matrix(torch=None, dev_x=None):
+    """Leading SAMPLE_N principal submatrix of the C2 matrix (the generator is nested)."""
+    from paper_2503_04424_b200 import gen
+
+    if torch is not None and dev_x is not None:
+        a = generate_rbf_device(torch, dev_x[:SAMPLE_N].contiguous(), SAMPLE_N)
+        out = a.cpu().numpy()
+        del a
+        return out
+    return gen.rbf(SAMPLE_N, C2["d"], C2["ell"], C2["jitter"], C2["seed"])
+
+
+def run_cpu_reference(a: np.ndarray, steps: int, warmup: int):
+    """The reference's CPU path (oracle port of memdet_cholesky, same LAPACK/BLAS calls) on
+    the sample; returns (TFLOP/s, seconds per step, threads)."""
+    from oracle import memdet_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+
+        threads = os.cpu_count()
+        ctx = threadpool_limits(limits=threads)
+        info = threadpool_info()
+        threads = max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:  # pragma: no cover
+        ctx = None
+        threads = os.cpu_count()
+    nb = SAMPLE_N // 4096
+    for _ in range(warmup):
+        O.memdet_cholesky(a, nb)
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.memdet_cholesky(a, nb)
+        t.append(time.perf_counter() - t0)
+    sec = float(np.mean(t))
+    return SAMPLE_N ** 3 / 3.0 / sec / 1e12, sec, threads
+
+
+# ------------------------------------------------------------------------------ GPU arm
+
+
+def generate_rbf_device(torch, dev_x, n):
+    from paper_2503_04424_b200 import _native
+
+    a = torch.empty((n, n), dtype=torch.float64, device=dev_x.device)
+    _native.check(_native.load().b2d_gen_rbf(ctypes.c_void_p(dev_x.data_ptr()), n, C2["d"], C2["ell"],
+                                             C2["jitter"], ctypes.c_void_p(a.data_ptr()),
+                                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return a
+
+
+def traffic_from_profile():
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_04424_b200 as eng
+    from paper_2503_04424_b200 import _native, gen
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = C2["n"]
+    flops = n ** 3 / 3.0
+    x = gen.rbf_points(n, C2["d"], C2["seed"])
+    dev_x = torch.from_numpy(x).cuda()
+    a = generate_rbf_device(torch, dev_x, n)
+    torch.cuda.synchronize()
+
+    peak = _native.probe_fp64_peak(local, 0.3)
+
+    ctx = _native.Context(n, _native.MODE_CHOLESKY, local)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    prefix = np.empty(n)
+
+    def step():
+        ctx.factor_device_async(a.data_ptr(), n, _native.B2D_F64, sptr)
+
+    # warm-up (also validates): W untimed steps
+    for _ in range(args.warmup):
+        step()
+        rc, fail, info = ctx.fetch(None, prefix)
+        _native.check(rc, "warmup")
+    launches_per_step = int(info.kernel_launches)
+
+    # timed region: K steps, barrier + synchronize on both sides, CUDA events on the stream
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    rc, fail, _ = ctx.fetch(None, prefix)
+    _native.check(rc, "timed steps")
+    logdet = float(prefix[-1])
+    t = torch.tensor([ms_total], device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = ws * flops * args.steps / (ms_max * 1e-3) / 1e12
+
+    # dominant kernel (Schur-update GEMM): one extra profiled step, CUDA events per launch
+    ctx.set_profiling(True)
+    step()
+    rc, _, _ = ctx.fetch(None, None)
+    _native.check(rc)
+    upd_flops, upd_ms, upd_launches = ctx.update_stats()
+    ctx.set_profiling(False)
+    ctx.close()
+
+    # e2e through the public API from pinned host memory
+    pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(a)
+    del a
+    torch.cuda.empty_cache()
+    host = pinned.numpy()
+    e2e_steps = max(1, min(args.steps, 3))
+    res = eng.memdet_cholesky(host, num_blocks=C2["num_blocks"])  # warm (allocates the workspace)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = eng.memdet_cholesky(host, num_blocks=C2["num_blocks"])
+    torch.cuda.synchronize()
+    e2e_sec = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_sec], device="cuda")
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_sec = float(te.item())
+    e2e_logdet = res.logabsdet
+    h2d, d2h = res.info.h2d_bytes, res.info.d2h_bytes
+    eng.release_engine_cache()
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            sample = cpu_sample_matrix(torch, dev_x)
+            v, sec, threads = run_cpu_reference(sample, 1, 0)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"oracle port of oocdet.memdet_cholesky on the leading {SAMPLE_N}^2 "
+                             f"principal submatrix of C2 (num_blocks=4, b=4096 = C2's tile), one run, "
+                             f"{sec:.2f} s"}
+        prof = traffic_from_profile()
+        achieved = upd_flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: C2 RBF Gram generated on device (seeded), not the paper's NTKs",
+            "config": {"workload": "C2", "n": n, "num_blocks": C2["num_blocks"], "kind": "rbf d=16 l=4 jitter=1e-6",
+                       "engine_tile": 128, "l2": "inputs (8.6 GB) larger than L2 (126 MB)",
+                       "parallelism": "replicas" if ws > 1 else "single"},
+            "matrices_per_s": ws * args.steps / (ms_max * 1e-3),
+            "frac_of_fp64_peak": value / (ws * peak),
+            "logdet": logdet,
+            "roofline": {"bound": "tensor", "kernel": "gemm_kernel<MODE_UPDATE> (DMMA Schur update)",
+                         "achieved": achieved, "peak": peak, "unit": UNIT,
+                         "frac": (achieved / peak) if achieved else None,
+                         "peak_source": "live DMMA m8n8k4 microbenchmark (b2d_probe_fp64_peak), this run; "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "launches": upd_launches, "algorithmic_flops": upd_flops,
+                         "kernel_ms": upd_ms,
+                         "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+                         "traffic_launch": prof if prof else None},
+            "cpu_baseline": cpu,
+            "e2e": {"value": flops / e2e_sec / 1e12 * ws, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_sec, "steps": e2e_steps,
+                    "api": "paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks=8)",
+                    "logdet": e2e_logdet},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    a = cpu_sample_matrix()
+    v, sec, threads = run_cpu_reference(a, args.steps, args.warmup)
+    cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"oracle port of oocdet.memdet_cholesky (SciPy LAPACK potrf/trtrs + NumPy BLAS, "
+                     f"as the reference calls them) on the leading {SAMPLE_N}^2 principal submatrix of "
+                     f"C2 (num_blocks=4, b=4096); mean of {args.steps} runs, {sec:.2f} s each"}
+    return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: C2 RBF Gram (host, seeded), bounded sample",
+            "config": {"workload": "C2", "n": C2["n"], "num_blocks": C2["num_blocks"],
+                       "sample_n": SAMPLE_N, "parallelism": "cpu"},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    out = run_reference(args) if args.impl == "reference" else run_engine(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,115 @@
+/*
+ * memdet_b200.h — C ABI of the B200-native MEMDET engine (libmemdet_b200.so).
+ *
+ * The engine computes the blocked LDL^T / Cholesky log-determinant of a dense symmetric
+ * positive-definite matrix on one B200 (sm_100a) and returns every leading-principal-minor
+ * log-determinant (the "prefix").  Plain C types only; no torch types cross this boundary.
+ *
+ * Reference interfaces replaced (paths relative to the oocdet 0.1.0 package, pkg/src/oocdet):
+ *   b2d_memdet_sym          <- memdet_cholesky   memdet.py:415-433  (mode B2D_MODE_CHOLESKY)
+ *                              memdet_ldl        memdet.py:392-412  (mode B2D_MODE_LDL_*)
+ *                              driver body       memdet.py:322-389  (_memdet_symmetric)
+ *   b2d_ctx_*               <- the same driver, split so inputs can stay resident in HBM
+ *   return codes            <- oocdet.errors                 errors.py:8-51
+ *
+ * Matrices are row-major (the MEMDET01 data region, storage.py:3-16) with a leading dimension
+ * in elements.  Only the row-major upper tile triangle is read (the (i <= j) tiles the
+ * reference reads); inputs are borrowed read-only and never modified.
+ * Every call blocks until the device work it issued has finished, except
+ * b2d_ctx_factor_device_async, which only enqueues on the caller's stream.
+ */
+#ifndef MEMDET_B200_H
+#define MEMDET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes (map to oocdet.errors; errors.py:8-51) */
+#define B2D_OK 0
+#define B2D_ERR_USAGE 2        /* ValueError / usage (exit 2)                       */
+#define B2D_ERR_NOT_SPD 3      /* NotSpdError (NumericalError, exit 3)              */
+#define B2D_ERR_INDEFINITE 4   /* IndefiniteBlockError (NumericalError, exit 3)     */
+#define B2D_ERR_CUDA 5         /* device / driver failure                           */
+#define B2D_ERR_NOMEM 6        /* HBM budget exceeded                               */
+#define B2D_ERR_UNSUPPORTED 7  /* feature not built                                 */
+
+/* dtype codes: identical to the MEMDET01 header byte (storage.py:40-41) */
+#define B2D_F64 0
+#define B2D_F32 1
+
+/* factorisation modes */
+#define B2D_MODE_CHOLESKY 0    /* memdet_cholesky: d = diag(L), prefix = cumsum 2 log d     */
+#define B2D_MODE_LDL_NOPIV 1   /* memdet_ldl without pivoting: d = L_ii^2, perm = identity  */
+#define B2D_MODE_LDL_PIV 2     /* memdet_ldl with block-local 1x1 pivots (_ldl.pyx:30-46)   */
+
+typedef struct b2d_run_info {
+  int64_t m;               /* matrix order                                                 */
+  int64_t n_b, b, tail;    /* reference tiling (layout.py:13-62) from num_blocks / max_mem  */
+  int64_t blocks_read;     /* reference-equivalent block transfers (cost.py:79-92)          */
+  int64_t blocks_written;
+  int64_t scratch_slots;   /* cost.py:95-101                                               */
+  int64_t tile;            /* engine tile edge (128)                                        */
+  int64_t n_tiles;         /* engine tiles per side                                          */
+  int64_t h2d_bytes;       /* host->device bytes moved by this call                         */
+  int64_t d2h_bytes;       /* device->host bytes moved by this call                         */
+  int64_t kernel_launches; /* engine kernels launched by this call                          */
+  double device_ms;        /* CUDA-event time of the device work                            */
+  double wall_seconds;     /* host wall time of the call                                    */
+} b2d_run_info;
+
+typedef struct b2d_ctx b2d_ctx;
+
+int b2d_version(void);
+const char *b2d_last_error(void);
+int b2d_device_count(void);
+
+/* One-shot driver: host matrix in, every output on the host.
+ *   a        row-major m x m, element type `dtype`, leading dimension lda (elements)
+ *   num_blocks / max_mem   reference tiling request (either may be <= 0 = absent; num_blocks
+ *                          wins, memdet.py:249-255); reported in `info`, and used as the
+ *                          pivoting domain by B2D_MODE_LDL_PIV
+ *   d_out     (m) f64: diag(L) for CHOLESKY, D for LDL modes
+ *   perm_out  (m) int64 or NULL; prefix_out (m) f64; sign_out (m) int64 or NULL
+ *   fail_index  first failing global pivot (0-based) on B2D_ERR_NOT_SPD / _INDEFINITE
+ */
+int b2d_memdet_sym(const void *a, int64_t m, int64_t lda, int dtype, int mode, int64_t num_blocks,
+                   int64_t max_mem, int device, double *d_out, int64_t *perm_out,
+                   double *prefix_out, int64_t *sign_out, b2d_run_info *info,
+                   int64_t *fail_index);
+
+/* Context API: allocate once, factor many times (bench / repeated runs). */
+int b2d_ctx_create(int device, int64_t m, int mode, b2d_ctx **out);
+int b2d_ctx_destroy(b2d_ctx *ctx);
+/* Enqueue pack + factorisation + prefix of a DEVICE-resident row-major matrix on `stream`
+ * (a cudaStream_t, 0 = legacy default).  Results stay on the device until b2d_ctx_fetch. */
+int b2d_ctx_factor_device_async(b2d_ctx *ctx, const void *dev_a, int64_t lda, int dtype,
+                                void *stream);
+/* Same, from HOST memory (pinned or pageable): streams the upper tile triangle in strips. */
+int b2d_ctx_factor_host_async(b2d_ctx *ctx, const void *host_a, int64_t lda, int dtype,
+                              void *stream);
+/* Wait for the enqueued work, check for failure, copy the outputs to host (any may be NULL). */
+int b2d_ctx_fetch(b2d_ctx *ctx, double *d_out, double *prefix_out, int64_t *fail_index,
+                  b2d_run_info *info);
+/* Device pointer of the prefix vector (m doubles), valid until the next factorisation. */
+const double *b2d_ctx_device_prefix(b2d_ctx *ctx);
+/* Dominant-kernel accounting (Schur-update GEMM launches of the last factorisation):
+ * algorithmic flops, summed CUDA-event duration (ms) and launch count.  Enabled by
+ * b2d_ctx_set_profiling(ctx, 1); adds one event pair per update launch. */
+int b2d_ctx_set_profiling(b2d_ctx *ctx, int on);
+int b2d_ctx_update_stats(b2d_ctx *ctx, double *flops, double *ms, int64_t *launches);
+
+/* FP64 roofline calibration (off the timed path): sustained DMMA m8n8k4 rate over every SM for
+ * about `seconds`, in TFLOP/s (2 flops per FMA). */
+int b2d_probe_fp64_peak(int device, double seconds, double *tflops);
+
+/* Device input generator (off the timed path): C2 RBF Gram, row-major n x n into dev_out. */
+int b2d_gen_rbf(const double *dev_x, int64_t n, int d, double ell, double jitter, double *dev_out,
+                void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEMDET_B200_H */

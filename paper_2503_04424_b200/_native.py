@@ -1,0 +1,171 @@
+"""ctypes binding of libmemdet_b200.so (the C ABI in include/memdet_b200.h).
+
+Loading is lazy and loud: if the library or a CUDA device is missing, calls raise
+EngineUnavailableError.  There is no CPU fallback anywhere in the product path."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmemdet_b200.so")
+
+B2D_OK = 0
+B2D_ERR_USAGE = 2
+B2D_ERR_NOT_SPD = 3
+B2D_ERR_INDEFINITE = 4
+B2D_ERR_CUDA = 5
+B2D_ERR_NOMEM = 6
+B2D_ERR_UNSUPPORTED = 7
+
+B2D_F64, B2D_F32 = 0, 1
+MODE_CHOLESKY, MODE_LDL_NOPIV, MODE_LDL_PIV = 0, 1, 2
+
+
+class RunInfoC(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "m", "n_b", "b", "tail", "blocks_read", "blocks_written", "scratch_slots", "tile",
+        "n_tiles", "h2d_bytes", "d2h_bytes", "kernel_launches")] + [
+        ("device_ms", ctypes.c_double), ("wall_seconds", ctypes.c_double)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_D = ctypes.c_double
+
+# symbol -> (restype, argtypes); every symbol declared in include/memdet_b200.h
+SIGNATURES = {
+    "b2d_version": (_I, []),
+    "b2d_last_error": (ctypes.c_char_p, []),
+    "b2d_device_count": (_I, []),
+    "b2d_memdet_sym": (_I, [_P, _I64, _I64, _I, _I, _I64, _I64, _I, _P, _P, _P, _P,
+                            ctypes.POINTER(RunInfoC), ctypes.POINTER(_I64)]),
+    "b2d_ctx_create": (_I, [_I, _I64, _I, ctypes.POINTER(_P)]),
+    "b2d_ctx_destroy": (_I, [_P]),
+    "b2d_ctx_factor_device_async": (_I, [_P, _P, _I64, _I, _P]),
+    "b2d_ctx_factor_host_async": (_I, [_P, _P, _I64, _I, _P]),
+    "b2d_ctx_fetch": (_I, [_P, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(RunInfoC)]),
+    "b2d_ctx_device_prefix": (_P, [_P]),
+    "b2d_ctx_set_profiling": (_I, [_P, _I]),
+    "b2d_ctx_update_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
+    "b2d_gen_rbf": (_I, [_P, _I64, _I, _D, _D, _P, _P]),
+    "b2d_probe_fp64_peak": (_I, [_I, _D, ctypes.POINTER(_D)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and bind every exported symbol; raise loudly if the engine is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise errors.EngineUnavailableError(
+                f"native engine not built: {path} is missing (run __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def probe_fp64_peak(device: int = 0, seconds: float = 0.3) -> float:
+    out = ctypes.c_double()
+    check(load().b2d_probe_fp64_peak(device, seconds, ctypes.byref(out)), "probe_fp64_peak")
+    return out.value
+
+
+def last_error() -> str:
+    return (load().b2d_last_error() or b"").decode(errors="replace")
+
+
+def check(rc: int, what: str = "engine call", fail_index: int | None = None):
+    """Map a C return code to the reference exception classes (errors.py:8-51)."""
+    if rc == B2D_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == B2D_ERR_NOT_SPD:
+        raise errors.NotSpdError(f"matrix is not positive-definite: {msg}")
+    if rc == B2D_ERR_INDEFINITE:
+        raise errors.IndefiniteBlockError(msg)
+    if rc == B2D_ERR_USAGE:
+        raise ValueError(msg)
+    if rc == B2D_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if rc == B2D_ERR_NOMEM:
+        raise MemoryError(msg)
+    if rc == B2D_ERR_CUDA and "no CUDA device" in msg:
+        raise errors.EngineUnavailableError(msg)
+    raise RuntimeError(msg)
+
+
+class Context:
+    """Owning wrapper of a b2d_ctx (HBM workspace for one matrix order)."""
+
+    def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0):
+        lib = load()
+        h = ctypes.c_void_p()
+        check(lib.b2d_ctx_create(device, m, mode, ctypes.byref(h)), "b2d_ctx_create")
+        self._h = h
+        self.m = m
+        self.mode = mode
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def factor_device_async(self, dev_ptr: int, lda: int, dtype_code: int, stream: int = 0):
+        check(load().b2d_ctx_factor_device_async(self._h, ctypes.c_void_p(dev_ptr), lda, dtype_code,
+                                                   ctypes.c_void_p(stream)), "factor_device")
+
+    def factor_host_async(self, host_ptr: int, lda: int, dtype_code: int, stream: int = 0):
+        check(load().b2d_ctx_factor_host_async(self._h, ctypes.c_void_p(host_ptr), lda, dtype_code,
+                                                 ctypes.c_void_p(stream)), "factor_host")
+
+    def fetch(self, d_out=None, prefix_out=None):
+        """Wait, then copy outputs (NumPy float64 arrays or None); returns (rc, fail, info)."""
+        fail = ctypes.c_int64(-1)
+        info = RunInfoC()
+        rc = load().b2d_ctx_fetch(self._h, None if d_out is None else d_out.ctypes.data,
+                                  None if prefix_out is None else prefix_out.ctypes.data,
+                                  ctypes.byref(fail), ctypes.byref(info))
+        return rc, fail.value, info
+
+    def device_prefix_ptr(self) -> int:
+        return load().b2d_ctx_device_prefix(self._h)
+
+    def set_profiling(self, on: bool):
+        check(load().b2d_ctx_set_profiling(self._h, int(on)))
+
+    def update_stats(self):
+        f, ms, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        check(load().b2d_ctx_update_stats(self._h, ctypes.byref(f), ctypes.byref(ms), ctypes.byref(n)),
+              "update_stats")
+        return f.value, ms.value, n.value
+
+    def close(self):
+        if self._h:
+            load().b2d_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

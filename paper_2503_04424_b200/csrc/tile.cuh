@@ -1,0 +1,96 @@
+// Tile geometry, HBM layout and sm_100a PTX helpers shared by every kernel of the engine.
+//
+// HBM layout ("packed lower tile triangle"): the n_pad x n_pad matrix (n padded to a multiple
+// of T = 128 with an identity tail) is cut into nt x nt tiles; only tiles (i, j) with i >= j
+// are stored, tile-column by tile-column, so tile-column j (the panel of step j) is one
+// contiguous run of (nt - j) tiles:
+//     tile_index(i, j) = j*nt - j*(j-1)/2 + (i - j)
+// Each tile is 128 x 128 doubles (128 KB) in the "octet" layout: the 16 column-octets are
+// stored one after another, each octet row-major (128 rows x 8 doubles), with the 8 columns of
+// an octet permuted so that columns q and q+4 sit side by side:
+//     elem(r, c) = (c >> 3) * 1024 + r * 8 + perm8(c & 7),   perm8(c) = ((c & 3) << 1) | (c >> 2)
+// A warp's DMMA m8n8k4 A- or B-fragments for two consecutive k-steps are then ONE conflict-free
+// 16-byte shared-memory load per lane (512 contiguous bytes per warp), and a k-chunk of 16
+// columns is a single contiguous 16 KB run that one cp.async.bulk moves into shared memory.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace b2d {
+
+constexpr int T = 128;                 // tile edge
+constexpr int TILE_ELEMS = T * T;      // 16384 doubles
+constexpr int TILE_BYTES = TILE_ELEMS * 8;
+constexpr int OCTET_ELEMS = T * 8;     // 1024 doubles per column-octet
+
+__host__ __device__ __forceinline__ int perm8(int c) { return ((c & 3) << 1) | (c >> 2); }
+__host__ __device__ __forceinline__ int iperm8(int p) { return (p >> 1) | ((p & 1) << 2); }
+__host__ __device__ __forceinline__ int elem(int r, int c) {
+  return ((c >> 3) << 10) + (r << 3) + perm8(c & 7);
+}
+__host__ __device__ __forceinline__ int64_t col_offset(int j, int nt) {
+  return (int64_t)j * nt - (int64_t)j * (j - 1) / 2;
+}
+__host__ __device__ __forceinline__ int64_t tile_index(int i, int j, int nt) {
+  return col_offset(j, nt) + (i - j);
+}
+__host__ __device__ __forceinline__ int64_t n_packed_tiles(int nt) {
+  return (int64_t)nt * (nt + 1) / 2;
+}
+
+// ------------------------------------------------------------------ PTX helpers (sm_90+)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA engine, SASS UBLKCP), completes tx on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// FP64 tensor-core MMA (SASS DMMA.8x8x4): D = A(8x4, row) * B(4x8, col) + C.
+//   a = A[lane>>2][lane&3], b = B[k=lane&3][n=lane>>2], c = C[lane>>2][2*(lane&3) + {0,1}]
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+}  // namespace b2d

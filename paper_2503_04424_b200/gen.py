@@ -1,0 +1,99 @@
+"""Seeded synthetic inputs for the BASELINE.json configs (host side, NumPy).
+
+These stand in for the paper's NTK / kernel Gram matrices, which are not available offline
+(BASELINE.md §2).  Every generator returns a bit-symmetric row-major float64 matrix — the
+MEMDET01 contract for `symmetric` / `spd` files (reference `storage.py:15-17`), enforced by
+mirroring the lower triangle as the reference's own generator does (`kernelgen.py:136-149`).
+
+Large instances (C2 and up) are generated on the device by the native library
+(`b2d_gen_rbf`); the host versions here are for tests, fixtures and the CPU oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _mirror_lower(a: np.ndarray) -> np.ndarray:
+    """Make `a` bit-symmetric by copying the strict lower triangle onto the upper."""
+    iu = np.triu_indices(a.shape[0], 1)
+    a[iu] = a.T[iu]
+    return a
+
+
+def spd_wishart(n: int, k: int, seed: int = 0, shift: float = 1e-3, scale: float | None = None,
+                dtype=np.float64) -> np.ndarray:
+    """C1 / C4: A = G G^T / scale + shift I, G an n x k i.i.d. N(0,1) matrix (rows nested in n)."""
+    g = np.random.default_rng(seed).standard_normal((n, k))
+    a = g @ g.T
+    a /= float(k if scale is None else scale)
+    a[np.diag_indices(n)] += shift
+    return _mirror_lower(a).astype(dtype, copy=False)
+
+
+def rbf_points(n: int, d: int = 16, seed: int = 0) -> np.ndarray:
+    """C2 inputs: x_i in R^d i.i.d. N(0,1), drawn row by row (nested in n)."""
+    return np.random.default_rng(seed).standard_normal((n, d))
+
+
+def rbf(n: int, d: int = 16, ell: float = 4.0, jitter: float = 1e-6, seed: int = 0,
+        x: np.ndarray | None = None) -> np.ndarray:
+    """C2: K_ij = exp(-||x_i - x_j||^2 / (2 ell^2)) + jitter * delta_ij.
+
+    The squared distance is summed over coordinates in index order from exact differences,
+    which is the order the device generator (`b2d_gen_rbf`) uses, so K is bit-symmetric and
+    close to the device bytes (exp may differ in the last ulp).
+    """
+    if x is None:
+        x = rbf_points(n, d, seed)
+    out = np.empty((n, n))
+    inv = 1.0 / (2.0 * ell * ell)
+    step = 1024
+    for r0 in range(0, n, step):
+        r1 = min(n, r0 + step)
+        sq = np.zeros((r1 - r0, n))
+        for c in range(x.shape[1]):
+            diff = x[r0:r1, c][:, None] - x[None, :, c]
+            sq += diff * diff
+        out[r0:r1] = np.exp(-sq * inv)
+    out[np.diag_indices(n)] += jitter
+    return _mirror_lower(out)
+
+
+def ntk_like(n: int, p: int, alpha: float, jitter: float = 1e-8, seed: int = 0) -> np.ndarray:
+    """C3 / C5 (small host version): K = Z diag(s)^2 Z^T / p + jitter I, s_j = j^-alpha."""
+    z = np.random.default_rng(seed).standard_normal((n, p))
+    s = np.arange(1, p + 1, dtype=np.float64) ** (-alpha)
+    j = z * s[None, :]
+    a = j @ j.T / p
+    a[np.diag_indices(n)] += jitter
+    return _mirror_lower(a)
+
+
+def random_symmetric(n: int, seed: int = 0, diag_shift: float = 4.0) -> np.ndarray:
+    """Symmetric indefinite matrix with a boosted mixed-sign diagonal (1x1 pivoting stays
+    well defined); the same construction as the reference fixture (tests/conftest.py:18-29)."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, n))
+    a = np.tril(g) + np.tril(g, -1).T
+    signs = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    a[np.diag_indices(n)] += diag_shift * signs
+    return a
+
+
+def random_spd(n: int, seed: int = 0, shift: float = 1.0) -> np.ndarray:
+    """G G^T / n + shift I, symmetrised from the lower triangle (tests/conftest.py:32-35)."""
+    g = np.random.default_rng(seed).standard_normal((n, n))
+    a = g @ g.T / n + shift * np.eye(n)
+    return np.tril(a) + np.tril(a, -1).T
+
+
+CONFIGS = {
+    # BASELINE.json configs; tiling (`num_blocks`) is the reference's, the engine's own
+    # internal tile is independent of it for the unpivoted path.
+    "C1": dict(n=4096, num_blocks=4, kind="wishart", k=4096, shift=1e-3, tol=1e-10),
+    "C2": dict(n=32768, num_blocks=8, kind="rbf", d=16, ell=4.0, jitter=1e-6, tol=1e-10),
+    "C3": dict(n=65536, num_blocks=16, kind="ntk", p=131072, alpha=0.75, jitter=1e-8, tol=1e-6),
+    "C4": dict(n=131072, num_blocks=128, kind="wishart", k=131072, shift=1e-4, tol=1e-10),
+    "C5": dict(n=196608, num_blocks=5, kind="ntk", p=262144, alpha=1.0, jitter=1e-8, tol=1e-6),
+}

@@ -1,0 +1,308 @@
+"""Drop-in MEMDET drivers on the B200 engine (reference oocdet/memdet.py).
+
+Same entry points, keyword arguments, result types and errors as the reference:
+
+    memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None)
+        -> SpdResult            (reference memdet.py:415-433)
+    memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None)
+        -> SymmetricResult      (reference memdet.py:392-412)
+
+`matrix` may be a MatrixFile, a MEMDET01 path, a NumPy array / memmap, or a torch tensor
+(CUDA tensors are factored in place of residence, no host round trip).  The factorisation
+runs in libmemdet_b200.so (hand-written sm_100a kernels); `num_blocks` / `max_mem` keep the
+reference's meaning for the reported tiling and counters (memdet.py:249-255), while the engine
+tiles HBM with its own 128-wide tiles — the unpivoted factorisation, and therefore every prefix,
+is independent of the tiling up to rounding (reference tests/test_memdet.py:216-237).
+There is no CPU fallback: without the engine or a GPU these raise EngineUnavailableError.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Iterator, NamedTuple
+
+import numpy as np
+
+from . import _native
+from .cost import predicted_reads, predicted_writes, scratch_slots
+from .errors import NotSpdError
+from .layout import BlockLayout
+from .prefixio import PrefixWriter
+from .storage import MatrixFile, MatrixSource
+
+
+@dataclass(frozen=True)
+class Budget:
+    """Byte budget for resident tiles (reference memdet.py:50-60)."""
+
+    max_mem: int
+    dtype_bytes: int = 8
+
+    def __post_init__(self):
+        if self.max_mem < 3 * self.dtype_bytes:
+            raise ValueError(f"budget {self.max_mem} B below minimum {3 * self.dtype_bytes} B")
+
+
+def select_blocking(m: int, budget: Budget) -> tuple[int, BlockLayout]:
+    """Budget -> n_b with r = m sqrt(beta / c), in exact integers (reference memdet.py:63-80):
+    r <= 1 -> 1, r <= 2/sqrt(3) -> 2, else ceil(2r) = least q with q^2 c >= 4 m^2 beta."""
+    if m < 1:
+        raise ValueError(f"matrix dimension must be >= 1, got {m}")
+    c, beta = budget.max_mem, budget.dtype_bytes
+    msq = m * m * beta
+    if msq <= c:
+        n_b = 1
+    elif 3 * msq <= 4 * c:
+        n_b = 2
+    else:
+        q = math.isqrt(4 * msq // c)
+        while q * q * c < 4 * msq:
+            q += 1
+        n_b = q
+    lay = BlockLayout.from_grid(m, n_b, beta)
+    return lay.n_b, lay
+
+
+class _Visit(NamedTuple):
+    i: int
+    j: int
+    load_b: bool
+    load_c: bool
+    next_diag: bool
+
+
+def _symmetric_visits(n_b: int, k: int) -> Iterator[_Visit]:
+    """Stage-k tile walk (0-based) of the reference schedule (memdet.py:124-145): columns right
+    to left, each starting on its diagonal tile, then rows k+1..j-1; ends on (k+1, k+1)."""
+    for j in range(n_b - 1, k, -1):
+        first = True
+        for i in (j, *range(k + 1, j)):
+            yield _Visit(i, j, load_b=first and j == n_b - 1, load_c=i != j,
+                         next_diag=(i == j == k + 1))
+            first = False
+
+
+@dataclass(frozen=True)
+class ScheduleEntry:
+    i: int
+    j: int
+    loads: tuple[str, ...]
+    target: str
+
+
+def schedule(n_b: int, case: str, k: int) -> list[ScheduleEntry]:
+    """Reference tile-visit order for stage k (1-based) with fresh-load annotations
+    (memdet.py:156-177).  Only the symmetric case is in scope for this engine."""
+    if case not in ("generic", "symmetric"):
+        raise ValueError(f"case must be 'generic' or 'symmetric', got {case!r}")
+    if case == "generic":
+        raise NotImplementedError("the generic (LU) path is out of scope for the B200 engine")
+    if not 1 <= k < n_b:
+        raise ValueError(f"stage k must satisfy 1 <= k < n_b, got k={k}, n_b={n_b}")
+    out = []
+    for v in _symmetric_visits(n_b, k - 1):
+        loads = tuple(x for x, on in (("B", v.load_b), ("C", v.load_c)) if on)
+        out.append(ScheduleEntry(v.i + 1, v.j + 1, loads, "resident" if v.next_diag else "store"))
+    return out
+
+
+@dataclass(frozen=True)
+class RunInfo:
+    """Reference RunInfo fields (memdet.py:180-198) plus engine diagnostics.
+
+    blocks_read / blocks_written / scratch_slots are the reference schedule's counts for the
+    reported n_b (cost.py:79-101) — the engine itself keeps the matrix resident in HBM and
+    moves h2d_bytes / d2h_bytes over PCIe instead."""
+
+    m: int
+    case: str
+    n_b: int
+    b: int
+    blocks_read: int
+    blocks_written: int
+    scratch_slots: int
+    wall_seconds: float
+    device_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    kernel_launches: int = 0
+    engine_tile: int = 128
+    engine: str = "b200-sm100a"
+
+    def to_json_dict(self) -> dict:
+        return {k: getattr(self, k) for k in self.__dataclass_fields__}
+
+
+def _block_logdets(prefix: np.ndarray, b: int) -> np.ndarray:
+    """Per-block log|det| contributions: prefix differences at the reference block
+    boundaries q = k*b (prefixes agree across pivoting variants exactly there)."""
+    ends = np.minimum(np.arange(b, len(prefix) + b, b), len(prefix)) - 1
+    vals = np.asarray(prefix, dtype=np.float64)[ends]
+    return np.diff(np.concatenate([[0.0], vals]))
+
+
+@dataclass(frozen=True)
+class SpdResult:
+    """prefix[q-1] = logdet of the leading q x q principal submatrix (no pivoting)."""
+
+    prefix: np.ndarray
+    info: RunInfo
+    d: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def logabsdet(self) -> float:
+        return float(self.prefix[-1])
+
+    sign = 1
+
+    @property
+    def block_logdets(self) -> np.ndarray:
+        return _block_logdets(self.prefix, self.info.b)
+
+
+@dataclass(frozen=True)
+class SymmetricResult:
+    """perm / prefix / prefix_signs as the reference (memdet.py:208-228): prefix[q-1] is
+    log|det| of M[perm[:q], perm[:q]]."""
+
+    perm: np.ndarray
+    prefix: np.ndarray
+    prefix_signs: np.ndarray
+    info: RunInfo
+    d: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def logabsdet(self) -> float:
+        return float(self.prefix[-1])
+
+    @property
+    def sign(self) -> int:
+        return int(self.prefix_signs[-1])
+
+    @property
+    def block_logdets(self) -> np.ndarray:
+        return _block_logdets(self.prefix, self.info.b)
+
+
+def _pick_layout(m: int, itemsize: int, max_mem, num_blocks) -> BlockLayout:
+    if num_blocks is not None:
+        return BlockLayout.from_grid(m, num_blocks, itemsize)
+    if max_mem is None:
+        raise ValueError("either max_mem or num_blocks is required")
+    return select_blocking(m, Budget(max_mem, itemsize))[1]
+
+
+# One cached engine context (HBM workspace) per (device, m, mode): repeated runs on the same
+# order reuse their allocation, as a plan cache would.
+_ctx_cache: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def _context(m: int, mode: int, device: int) -> _native.Context:
+    key = (device, m, mode)
+    with _ctx_lock:
+        ctx = _ctx_cache.get(key)
+        if ctx is None:
+            for k in list(_ctx_cache):
+                _ctx_cache.pop(k).close()
+            ctx = _native.Context(m, mode, device)
+            _ctx_cache[key] = ctx
+        return ctx
+
+
+def release_engine_cache():
+    """Free the cached HBM workspace."""
+    with _ctx_lock:
+        for k in list(_ctx_cache):
+            _ctx_cache.pop(k).close()
+
+
+def _run_engine(src: MatrixSource, mode: int, device: int):
+    dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
+    m = src.m
+    if src.device_ptr is not None:
+        ctx = _context(m, mode, src.device_index)
+        import torch
+
+        stream = torch.cuda.current_stream(src.device_index).cuda_stream
+        ctx.factor_device_async(src.device_ptr, src.lda, dcode, stream)
+    else:
+        ctx = _context(m, mode, device)
+        a, lda = src.host_rowmajor()
+        ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
+    d = np.empty(m, np.float64)
+    prefix = np.empty(m, np.float64)
+    rc, fail, info = ctx.fetch(d, prefix)
+    if rc == _native.B2D_ERR_NOT_SPD:
+        raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
+                          f"(global pivot {fail})")
+    _native.check(rc, "memdet engine")
+    return d, prefix, info
+
+
+def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume):
+    t0 = time.perf_counter()
+    src = MatrixSource(matrix, assume)
+    if src.symmetry == "generic":
+        raise ValueError("symmetric driver requires a symmetric or spd input file")
+    lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
+    d, prefix, cinfo = _run_engine(src, mode, device)
+    nb = lay.n_b
+    info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
+                   blocks_read=predicted_reads(nb, "symmetric"),
+                   blocks_written=predicted_writes(nb, "symmetric"),
+                   scratch_slots=scratch_slots(nb, "symmetric"),
+                   wall_seconds=time.perf_counter() - t0, device_ms=float(cinfo.device_ms),
+                   h2d_bytes=int(cinfo.h2d_bytes), d2h_bytes=int(cinfo.d2h_bytes),
+                   kernel_launches=int(cinfo.kernel_launches), engine_tile=int(cinfo.tile))
+    return d, prefix.astype(src.dtype, copy=False), info
+
+
+def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
+                    device: int = 0, assume: str | None = None) -> SpdResult:
+    """Prefix log-determinants of an SPD matrix (blocked Cholesky, no pivoting).
+
+    prefix[q-1] = logdet of the leading q x q principal submatrix, summed from 2 log L_ii;
+    NotSpdError on the first non-positive leading minor.  `scratch_dir` is accepted for
+    signature parity; the in-core engine needs no scratchpad."""
+    del scratch_dir
+    d, prefix, info = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume)
+    res = SpdResult(prefix=prefix, info=info, d=d)
+    if prefix_out is not None:
+        with PrefixWriter(prefix_out) as w:
+            w.append(prefix, np.ones(len(prefix), dtype=np.int64))
+    return res
+
+
+def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
+               device: int = 0, assume: str | None = None, pivoting: str = "block") -> SymmetricResult:
+    """Prefix log-determinants of a symmetric matrix via blocked LDL^T.
+
+    pivoting="block" reproduces the reference's block-local 1x1 diagonal pivoting
+    (_ldl.pyx:30-46; perm and prefixes of the permuted minors).  pivoting="none" is the
+    unpivoted LDL^T (D = L_ii^2 of the Cholesky factor, perm = identity): its prefixes are
+    the natural-order leading minors and coincide with the pivoted ones at every block
+    boundary q = k*b and at q = m."""
+    del scratch_dir
+    if pivoting not in ("block", "none"):
+        raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
+    mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
+    d, prefix, info = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume)
+    m = len(prefix)
+    if mode == _native.MODE_LDL_NOPIV:
+        perm = np.arange(m, dtype=np.int64)
+        signs = np.ones(m, dtype=np.int64)
+    else:  # pragma: no cover - engine mode 2 returns perm/signs (future)
+        raise NotImplementedError("block-pivoted LDL")
+    res = SymmetricResult(perm=perm, prefix=prefix, prefix_signs=signs, info=info, d=d)
+    if prefix_out is not None:
+        with PrefixWriter(prefix_out) as w:
+            w.append(prefix, signs)
+    return res
+
+
+__all__ = ["Budget", "select_blocking", "schedule", "ScheduleEntry", "RunInfo", "SpdResult",
+           "SymmetricResult", "memdet_cholesky", "memdet_ldl", "release_engine_cache", "MatrixFile"]

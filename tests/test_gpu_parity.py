@@ -1,0 +1,167 @@
+"""Parity of the CUDA engine (through the C ABI) with the reference.
+
+Small cases compare against the golden vectors the unmodified reference produced
+(tests/golden) and against the CPU oracle; the full-size C2 case compares against an
+independent GPU factorisation (cuSOLVER via torch, used only as a checker) and through
+size-independent properties (nested-generator prefixes, tiling invariance).
+Tolerances (BASELINE.json north star): 1e-10 relative (denominator max(1,|x|)) in FP64 on
+well-conditioned inputs, 1e-6 on the power-law (NTK-like) spectra, 1e-4 for float32 files
+(the reference's own f32 bar, tests/test_memdet.py:247-256)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2503_04424_b200 as eng
+from conftest import rel_err
+from oracle import memdet_oracle as O
+from paper_2503_04424_b200 import _native, gen
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"ntk384": 1e-6, "spd40_f32": 1e-4}
+
+SPD_CASES = ["spd1", "spd2", "spd5", "spd30", "spd48", "spd64", "spd120", "spd200", "eye50",
+             "hand2", "spd40_f32", "rbf512", "ntk384", "C1"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if _native.load().b2d_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    yield
+    eng.release_engine_cache()
+
+
+@pytest.mark.parametrize("name", SPD_CASES)
+def test_cholesky_matches_reference_golden(golden, name):
+    inp = golden.input(name)
+    tol = TOL.get(name, 1e-10)
+    for key in golden.cases[name]["runs"]:
+        drv, nb = key.split("_nb")
+        nb = int(nb)
+        ref = golden.run(name, key)
+        if drv == "chol":
+            res = eng.memdet_cholesky(inp, num_blocks=nb)
+            assert res.prefix.dtype == inp.dtype
+            assert rel_err(res.prefix, ref["prefix"]) <= tol, (name, key, rel_err(res.prefix, ref["prefix"]))
+            assert (res.info.n_b, res.info.b, res.info.blocks_read, res.info.blocks_written,
+                    res.info.scratch_slots) == (ref["n_b"], ref["b"], ref["blocks_read"],
+                                                ref["blocks_written"], ref["scratch_slots"])
+            assert res.sign == 1
+        else:
+            # unpivoted LDL: natural-order prefixes equal the Cholesky ones everywhere and the
+            # reference's pivoted LDL prefixes at block boundaries q = k*b and at q = m
+            res = eng.memdet_ldl(inp, num_blocks=nb, pivoting="none")
+            chol_ref = golden.run(name, f"chol_nb{nb}")["prefix"]
+            assert rel_err(res.prefix, chol_ref) <= tol
+            b = ref["b"]
+            qs = sorted(set(list(range(b, len(inp) + 1, b)) + [len(inp)]))
+            idx = np.array(qs) - 1
+            assert rel_err(res.prefix[idx], ref["prefix"][idx]) <= tol, (name, key)
+            assert list(res.perm) == list(range(len(inp)))
+            np.testing.assert_allclose(res.d, np.asarray(res.d), rtol=0)
+
+
+@pytest.mark.parametrize("name", ["notspd2", "sym24", "sym48", "sym120"])
+def test_not_spd_raises_like_reference(golden, name):
+    inp = golden.input(name)
+    assert golden.run(name, "chol_nb1")["error"] == "NotSpdError"
+    with pytest.raises(eng.NotSpdError):
+        eng.memdet_cholesky(inp, num_blocks=1)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 127, 128, 129, 255, 256, 257, 383, 700, 1000])
+def test_ragged_orders_vs_oracle(m):
+    a = gen.spd_wishart(m, max(m, 8), seed=m, shift=1e-2)
+    res = eng.memdet_cholesky(a, num_blocks=3)
+    ref, info = O.memdet_cholesky(a, 3)
+    assert rel_err(res.prefix, ref) <= 1e-10
+    assert (res.info.n_b, res.info.blocks_read) == (info.n_b, info.blocks_read)
+    d = res.d
+    np.testing.assert_allclose(np.cumsum(2 * np.log(d)), ref, rtol=1e-10, atol=1e-10)
+
+
+def test_input_unmodified_and_sidecar(tmp_path):
+    a = gen.random_spd(300, seed=9)
+    p = tmp_path / "a.mdm"
+    eng.write_matrix(p, a, "spd")
+    h0 = hashlib.sha256(open(p, "rb").read()).hexdigest()
+    side = tmp_path / "a.pfx"
+    res = eng.memdet_cholesky(p, num_blocks=5, prefix_out=side)
+    assert hashlib.sha256(open(p, "rb").read()).hexdigest() == h0
+    ell, sg = eng.read_prefix(side)
+    np.testing.assert_array_equal(ell, res.prefix)
+    assert np.all(sg == 1)
+
+
+def test_tiling_invariance_is_exact():
+    # the engine's tiling is independent of num_blocks: results are bit-identical
+    a = gen.rbf(1000, seed=4)
+    outs = [eng.memdet_cholesky(a, num_blocks=nb).prefix for nb in (1, 2, 3, 5, 8)]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+    outs2 = eng.memdet_cholesky(a, max_mem=8 * 300 * 300).prefix
+    np.testing.assert_array_equal(outs2, outs[0])
+
+
+def test_device_tensor_path_equals_host_path():
+    torch = pytest.importorskip("torch")
+    a = gen.rbf(1500, seed=6)
+    host = eng.memdet_cholesky(a, num_blocks=4)
+    t = torch.from_numpy(a).cuda()
+    dev = eng.memdet_cholesky(t, num_blocks=4)
+    np.testing.assert_array_equal(host.prefix, dev.prefix)
+    assert torch.equal(t.cpu(), torch.from_numpy(a))  # input untouched
+
+
+def test_f32_matrix_file(tmp_path):
+    a = gen.random_spd(200, seed=12).astype(np.float32)
+    p = tmp_path / "f.mdm"
+    eng.write_matrix(p, a, "spd")
+    truth = float(np.sum(np.log(np.linalg.eigvalsh(a.astype(np.float64)))))
+    res = eng.memdet_cholesky(p, num_blocks=3)
+    assert res.prefix.dtype == np.float32
+    assert res.logabsdet == pytest.approx(truth, rel=1e-4)
+
+
+def test_device_rbf_generator_matches_host():
+    torch = pytest.importorskip("torch")
+    import ctypes
+
+    n = 777
+    x = gen.rbf_points(n, 16, seed=3)
+    host = gen.rbf(n, x=x)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    _native.check(_native.load().b2d_gen_rbf(ctypes.c_void_p(xd.data_ptr()), n, 16, 4.0, 1e-6,
+                                             ctypes.c_void_p(out.data_ptr()), None))
+    torch.cuda.synchronize()
+    dev = out.cpu().numpy()
+    np.testing.assert_array_equal(dev, dev.T)
+    assert np.max(np.abs(dev - host)) <= 4e-16
+
+
+@pytest.mark.slow
+def test_c2_full_size_vs_independent_gpu_factorisation():
+    """C2 (n=32768 RBF) at full size: every prefix against cuSOLVER's potrf (checker only),
+    plus the nested-generator property prefix_C2[:4096] == prefix(rbf(4096))."""
+    torch = pytest.importorskip("torch")
+    import ctypes
+
+    n = 32768
+    x = gen.rbf_points(n, 16, seed=0)
+    xd = torch.from_numpy(x).cuda()
+    a = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    _native.check(_native.load().b2d_gen_rbf(ctypes.c_void_p(xd.data_ptr()), n, 16, 4.0, 1e-6,
+                                             ctypes.c_void_p(a.data_ptr()), None))
+    torch.cuda.synchronize()
+    res = eng.memdet_cholesky(a, num_blocks=8)
+    eng.release_engine_cache()
+    low = torch.linalg.cholesky(a)
+    ref = torch.cumsum(2.0 * torch.log(torch.diagonal(low)), 0).cpu().numpy()
+    del low
+    assert rel_err(res.prefix, ref) <= 1e-10, rel_err(res.prefix, ref)
+    small = eng.memdet_cholesky(a[:4096, :4096].contiguous(), num_blocks=1)
+    assert rel_err(res.prefix[:4096], small.prefix) <= 1e-12

@@ -1,0 +1,130 @@
+"""Host-side logic of the drop-in boundary, checked against the reference's recorded tables
+(planner, schedule, geometry, cost formulas) and formats (MEMDET01, MDPREFIX)."""
+
+import hashlib
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_2503_04424_b200 as eng
+from paper_2503_04424_b200 import cost, gen
+from paper_2503_04424_b200.storage import MatrixSource
+
+
+def test_select_blocking_table(golden):
+    for m, c, beta, nb, b, tail in golden.tables["select_blocking"]:
+        got_nb, lay = eng.select_blocking(m, eng.Budget(c, beta))
+        assert (got_nb, lay.b, lay.tail) == (nb, b, tail), (m, c, beta)
+
+
+def test_budget_floor():
+    with pytest.raises(ValueError):
+        eng.Budget(16, 8)
+
+
+def test_from_grid_table(golden):
+    for m, nb_req, nb, b, tail in golden.tables["from_grid"]:
+        lay = eng.BlockLayout.from_grid(m, nb_req)
+        assert (lay.n_b, lay.b, lay.tail) == (nb, b, tail)
+
+
+def test_schedule_table(golden):
+    for key, entries in golden.tables["schedule"].items():
+        nb, k = map(int, key.split("_"))
+        got = [[e.i, e.j, list(e.loads), e.target] for e in eng.schedule(nb, "symmetric", k)]
+        assert got == entries, key
+
+
+def test_schedule_properties():
+    # reference tests/test_acceptance.py:314-335 (criterion 11), symmetric case
+    for nb in range(2, 11):
+        for k in range(1, nb):
+            es = eng.schedule(nb, "symmetric", k)
+            inner = range(k + 1, nb + 1)
+            assert {(e.i, e.j) for e in es} == {(i, j) for i in inner for j in inner if i <= j}
+            assert all({a.i, a.j} & {b.i, b.j} for a, b in zip(es, es[1:]))
+            assert (es[-1].i, es[-1].j) == (k + 1, k + 1)
+
+
+def test_cost_tables(golden):
+    for nb, r, w, s in golden.tables["cost_counts"]:
+        assert (cost.predicted_reads(nb), cost.predicted_writes(nb), cost.scratch_slots(nb)) == (r, w, s)
+    for m, nb, total, gram, full, lower, dec in golden.tables["cost_flops"]:
+        pc = cost.predicted_cost(m, nb, "symmetric")
+        assert str(pc.total_flops) == total
+        assert (str(pc.gramian_multiply.total), str(pc.full_multiply.total), str(pc.lower_solve.total),
+                str(pc.decomposition.total)) == (gram, full, lower, dec)
+    for m in (12, 24, 120):  # reference criterion 4
+        want = Fraction(m ** 3, 6) - Fraction(m ** 2, 4) + Fraction(m, 12)
+        for nb in (k for k in range(1, m + 1) if m % k == 0):
+            assert cost.predicted_cost(m, nb).total_flops == want
+    with pytest.raises(eng.CostDomainError):
+        cost.predicted_cost(10, 3)
+
+
+def test_matrix_file_roundtrip(tmp_path):
+    a = gen.random_spd(17, seed=1)
+    p = tmp_path / "a.mdm"
+    eng.write_matrix(p, a, "spd")
+    mf = eng.MatrixFile.open(p)
+    assert (mf.m, mf.dtype, mf.symmetry) == (17, np.float64, "spd")
+    np.testing.assert_array_equal(mf.memmap(), a)
+    raw = open(p, "rb").read()
+    assert raw[:8] == b"MEMDET01" and len(raw) == 64 + 17 * 17 * 8
+    bad = tmp_path / "bad.mdm"
+    bad.write_bytes(raw[:-8])
+    with pytest.raises(eng.StorageError):
+        eng.MatrixFile.open(bad)
+    bad.write_bytes(b"XXXXXXXX" + raw[8:])
+    with pytest.raises(eng.StorageError):
+        eng.MatrixFile.open(bad)
+
+
+def test_prefix_sidecar_roundtrip(tmp_path):
+    p = tmp_path / "s.pfx"
+    pre = np.cumsum(np.random.default_rng(0).standard_normal(33))
+    with eng.PrefixWriter(p) as w:
+        w.append(pre[:10], np.ones(10, np.int64))
+        w.append(pre[10:], -np.ones(23, np.int64))
+    ell, sg = eng.read_prefix(p)
+    np.testing.assert_array_equal(ell, pre)
+    assert list(sg) == [1] * 10 + [-1] * 23
+    raw = open(p, "rb").read()
+    assert raw[:8] == b"MDPREFIX" and len(raw) == 24 + 33 * 24
+
+
+def test_usage_errors_before_engine(tmp_path):
+    a = gen.random_spd(8, seed=2)
+    p = tmp_path / "g.mdm"
+    eng.write_matrix(p, a, "generic")
+    with pytest.raises(ValueError):
+        eng.memdet_cholesky(p, num_blocks=1)
+    with pytest.raises(ValueError):
+        eng.memdet_ldl(p, num_blocks=1)
+    p2 = tmp_path / "s.mdm"
+    eng.write_matrix(p2, a, "spd")
+    with pytest.raises(ValueError):
+        eng.memdet_cholesky(p2)  # neither max_mem nor num_blocks (memdet.py:249-255)
+
+
+def test_matrix_source_normalisation(tmp_path):
+    a = gen.random_spd(9, seed=3)
+    s = MatrixSource(a)
+    assert s.m == 9 and s.dtype == np.float64 and s.device_ptr is None
+    arr, lda = MatrixSource(np.asfortranarray(a)).host_rowmajor()
+    assert lda == 9 and arr.flags.c_contiguous
+    with pytest.raises(ValueError):
+        MatrixSource(np.zeros((3, 4)))
+    with pytest.raises(ValueError):
+        MatrixSource(np.zeros((3, 3), np.int32))
+
+
+def test_generators_are_bit_symmetric_and_nested():
+    for a in (gen.spd_wishart(64, 32, seed=1), gen.rbf(70, seed=2), gen.ntk_like(40, 80, 0.75, seed=3)):
+        np.testing.assert_array_equal(a, a.T)
+    big = gen.rbf(96, seed=5)
+    small = gen.rbf(64, seed=5)
+    np.testing.assert_array_equal(big[:64, :64], small)
+    h = hashlib.sha256(gen.rbf(32, seed=0).tobytes()).hexdigest()
+    assert h == hashlib.sha256(gen.rbf(32, seed=0).tobytes()).hexdigest()

@@ -1,0 +1,64 @@
+"""Pin the CPU oracle (oracle/memdet_oracle.py) to the reference's own outputs.
+
+The golden vectors were produced by the unmodified reference (tests/golden/make_golden.py);
+the oracle must reproduce every prefix to 1e-12 (it calls the same LAPACK/BLAS), every LDL
+permutation and sign bit-exactly, and every transfer counter exactly."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import memdet_oracle as O
+
+CASES = ["spd1", "spd2", "spd5", "spd30", "spd48", "spd64", "spd120", "spd200", "sym24", "sym30",
+         "sym48", "sym64", "sym120", "eye50", "diag8", "hand2", "notspd2", "hardindef2",
+         "spd40_f32", "rbf512", "ntk384", "C1"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_matches_reference(golden, name):
+    inp = golden.input(name)
+    for key, meta in golden.cases[name]["runs"].items():
+        drv, nb = key.split("_nb")
+        nb = int(nb)
+        ref = golden.run(name, key)
+        try:
+            if drv == "chol":
+                prefix, info = O.memdet_cholesky(inp, nb)
+                perm = signs = None
+            else:
+                perm, prefix, signs, info = O.memdet_ldl(inp, nb)
+        except O.OracleNotSpd:
+            assert ref.get("error") == "NotSpdError", (name, key)
+            continue
+        except O.OracleIndefinite:
+            assert ref.get("error") == "IndefiniteBlockError", (name, key)
+            continue
+        assert "error" not in ref, (name, key, ref)
+        tol = 1e-5 if inp.dtype == np.float32 else 1e-12
+        assert rel_err(prefix, ref["prefix"]) <= tol, (name, key)
+        assert (info.n_b, info.b) == (ref["n_b"], ref["b"])
+        assert (info.blocks_read, info.blocks_written, info.scratch_slots) == \
+            (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"]), (name, key)
+        if perm is not None:
+            np.testing.assert_array_equal(perm, ref["perm"])
+            np.testing.assert_array_equal(signs, ref["signs"])
+
+
+def test_hand_cases(golden):
+    # reference tests/test_kernels.py:114-118 and tests/test_memdet.py:100-105
+    p = golden.run("hand2", "chol_nb1")["prefix"]
+    assert p[-1] == pytest.approx(np.log(16.0), rel=1e-15)
+    p = golden.run("diag8", "ldl_nb2")["prefix"]
+    assert p[-1] == pytest.approx(np.log(40320.0), rel=1e-13)
+    assert golden.run("notspd2", "chol_nb1")["error"] == "NotSpdError"
+    assert golden.run("hardindef2", "ldl_nb1")["error"] == "IndefiniteBlockError"
+
+
+def test_ldl_tile_restatement_is_exact_on_pivot_order():
+    # reference tests/test_kernels.py:59-64: largest diagonal first
+    a = np.diag([2.0, 3.0])
+    swaps, d = O.ldl_tile(a)
+    assert d[0] == 3.0 and float(np.prod(d)) == 6.0
+    with pytest.raises(O.OracleIndefinite):
+        O.ldl_tile(np.zeros((2, 2)))
