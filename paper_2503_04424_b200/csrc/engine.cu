@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -42,14 +43,20 @@ static int set_err(int code, const char* fmt, ...) {
                      __FILE__, __LINE__);                                                \
   } while (0)
 
-// outer panel width in tiles: the trailing Schur update runs with K = W_TILES * 128
-constexpr int W_TILES = 2;
+// outer panel width in tiles: the trailing Schur update runs with K = panel_tiles * 128
+// (default 4; B2D_PANEL_TILES overrides for tuning)
+static int panel_tiles_default() {
+  const char* e = getenv("B2D_PANEL_TILES");
+  int w = e ? atoi(e) : 4;
+  return w < 1 ? 1 : (w > 16 ? 16 : w);
+}
 
 struct Ctx {
   int device = 0;
   int64_t m = 0;
   int mode = B2D_MODE_CHOLESKY;
   int nt = 0;
+  int W_TILES = 4;
   double* tiles = nullptr;   // packed lower tile triangle
   double* inv = nullptr;     // nt inverse diagonal tiles
   double* ell = nullptr;     // n_pad: 2 log L_ii
@@ -125,6 +132,7 @@ static int create(int device, int64_t m, int mode, Ctx** out) {
   c->m = m;
   c->mode = mode;
   c->nt = (int)((m + T - 1) / T);
+  c->W_TILES = panel_tiles_default();
   const int64_t npad = (int64_t)c->nt * T;
   const size_t tile_bytes = (size_t)n_packed_tiles(c->nt) * TILE_BYTES;
   size_t free_b = 0, total_b = 0;
@@ -163,7 +171,7 @@ static int create(int device, int64_t m, int mode, Ctx** out) {
   cudaEventCreate(&c->ev_start);
   cudaEventCreate(&c->ev_stop);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  const int nsteps = (c->nt + W_TILES - 1) / W_TILES;
+  const int nsteps = (c->nt + c->W_TILES - 1) / c->W_TILES;
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
   for (int s = 0; s < nsteps; ++s) {
@@ -233,6 +241,7 @@ static void launch_panel_column(Ctx* c, cudaStream_t s, int p) {
 // The factorisation proper on packed tiles already in HBM (stream order after `s_main`).
 static void enqueue_factor(Ctx* c) {
   const int nt = c->nt;
+  const int W_TILES = c->W_TILES;
   const int nsteps = (nt + W_TILES - 1) / W_TILES;
   for (int st = 0; st < nsteps; ++st) {
     const int k0 = st * W_TILES;

@@ -184,6 +184,11 @@ __global__ void __launch_bounds__(128) potrf_inv_kernel(double* __restrict__ til
 
 enum { MODE_UPDATE = 0, MODE_TRSM = 1 };
 
+// sign flip on the integer pipe (no FP64 pipe slot)
+__device__ __forceinline__ double neg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
 struct GemmTask {
   double* tiles;
   const double* binv;  // MODE_TRSM: L_kk^{-1} tile
@@ -252,11 +257,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
 
   // ---------------- consumers: 8 warps, warp tile 64 x 32, DMMA m8n8k4
   const int wm = warp >> 2, wn = warp & 3;
+  double* C = t.tiles + tile_index(i, jout, t.nt) * TILE_ELEMS;
+  // MODE_UPDATE: the accumulators start as the C tile (64 independent loads issued before the
+  // first stage lands, so their latency hides under the pipeline fill) and the B fragments are
+  // negated, giving acc = C - A B^T with a store-only epilogue.
   double acc[8][4][2];
 #pragma unroll
-  for (int g = 0; g < 8; ++g)
+  for (int g = 0; g < 8; ++g) {
+    const int r = wm * 64 + g * 8 + (lane >> 2);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) acc[g][h][0] = acc[g][h][1] = 0.0;
+    for (int h = 0; h < 4; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        acc[g][h][e] = (MODE == MODE_UPDATE) ? C[elem(r, wn * 32 + h * 8 + (lane & 3) * 2 + e)] : 0.0;
+  }
 
   const int fr = (lane >> 2) * 8 + (lane & 3) * 2;  // fragment offset inside an octet
   for (int c = 0; c < nchunks; ++c) {
@@ -266,39 +280,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
     const double* b_st = sB + s * STAGE_ELEMS + wn * 32 * 8 + fr;
 #pragma unroll
     for (int o = 0; o < 2; ++o) {
-      double2 af[8], bf[4];
+      // B fragments for two k-steps stay in registers; A fragments stream one row-group at a
+      // time (keeps the live set under the 168-register cap of a 9-warp CTA)
+      double2 bf[4];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) af[g] = *reinterpret_cast<const double2*>(a_st + o * OCTET_ELEMS + g * 64);
+      for (int h = 0; h < 4; ++h) {
+        bf[h] = *reinterpret_cast<const double2*>(b_st + o * OCTET_ELEMS + h * 64);
+        if (MODE == MODE_UPDATE) { bf[h].x = neg(bf[h].x); bf[h].y = neg(bf[h].y); }
+      }
 #pragma unroll
-      for (int h = 0; h < 4; ++h) bf[h] = *reinterpret_cast<const double2*>(b_st + o * OCTET_ELEMS + h * 64);
+      for (int g = 0; g < 8; ++g) {
+        const double2 af = *reinterpret_cast<const double2*>(a_st + o * OCTET_ELEMS + g * 64);
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
+        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af.x, bf[h].x);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g].x, bf[h].x);
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-#pragma unroll
-        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g].y, bf[h].y);
+        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af.y, bf[h].y);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   // ---------------- epilogue: straight to HBM in tile layout
-  double* C = t.tiles + tile_index(i, jout, t.nt) * TILE_ELEMS;
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const int r = wm * 64 + g * 8 + (lane >> 2);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
+    for (int h = 0; h < 4; ++h)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = wn * 32 + h * 8 + (lane & 3) * 2 + e;
-        double* p = C + elem(r, cc);
-        if (MODE == MODE_TRSM) *p = acc[g][h][e];
-        else *p = *p - acc[g][h][e];
-      }
-    }
+      for (int e = 0; e < 2; ++e) C[elem(r, wn * 32 + h * 8 + (lane & 3) * 2 + e)] = acc[g][h][e];
   }
 }
 
