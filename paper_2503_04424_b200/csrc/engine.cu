@@ -84,7 +84,7 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
   const int sm_tile = T * 129 * 8;
-  CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_tile));
+  CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)POTRF_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_tile));
   CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_tile));
   done = true;
@@ -222,7 +222,7 @@ static void launch_update(Ctx* c, cudaStream_t s, int j0, int j1, int p0, int p1
 static void launch_panel_column(Ctx* c, cudaStream_t s, int p) {
   const int nt = c->nt;
   double* invp = c->inv + (int64_t)p * TILE_ELEMS;
-  potrf_inv_kernel<<<1, T, T * 129 * 8, s>>>(c->tiles, nt, p, invp, c->ell, c->diag, c->fail, c->m);
+  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(c->tiles, nt, p, invp, c->ell, c->diag, c->fail, c->m);
   c->launches++;
   if (p + 1 < nt) {
     GemmTask t{};

@@ -56,128 +56,251 @@ __global__ void __launch_bounds__(512) pack_tiles_kernel(const Tin* __restrict__
 
 // ------------------------------------------------------------------------------ potrf + inverse
 
-// One CTA of 128 threads factors diagonal tile (k, k) in shared memory.
-// Cholesky: left-looking over 8-column blocks, one thread per row; the 8x8 diagonal block is
-// factored warp-synchronously with shuffles.  Then X = L^{-1} in place (row-major, one thread
-// per column) and X is written to `inv` in tile layout as the B operand of the panel solve.
-// ell[g] = 2*log(L_gg) (the reference's per-row prefix increment, memdet.py:428),
-// diag[g] = L_gg; fail = first global row whose pivot is not positive (atomicMin).
-__global__ void __launch_bounds__(128) potrf_inv_kernel(double* __restrict__ tiles, int nt, int k,
-                                                        double* __restrict__ inv,
-                                                        double* __restrict__ ell,
-                                                        double* __restrict__ diag,
-                                                        unsigned long long* __restrict__ fail,
-                                                        int64_t m) {
-  extern __shared__ double L[];  // [128][129] row-major: L[r*129 + c]
+// One CTA of 256 threads factors diagonal tile (k, k) in shared memory M[128][129].
+// Phase A (Cholesky, right-looking over 8-column blocks, two barriers per block):
+//   A2  one thread per row solves the block column below the current 8x8 diagonal block;
+//   A3  all threads apply the rank-8 update to the trailing lower triangle in 4x4 register
+//       blocks, while thread 0 updates AND factors the next 8x8 diagonal block (look-ahead,
+//       so the serial rsqrt chain hides under the update).
+// Phase B (X = L^{-1}): row blocks of 8 in order; per block, 256 threads form the partial
+//   products L[rb, :rb] X[:rb, c] (two threads per column), then one thread per column does
+//   the 8x8 forward substitution.  X[r][c] (r > c) lives transposed in the free upper
+//   triangle M[c][r]; X[c][c] = dinv[c].
+// Outputs: L_kk back to its tile (lower, zero upper), X to `inv` (tile layout, B operand of
+// the panel solve), ell[g] = 2 log L_gg (memdet.py:428), diag[g] = L_gg, fail = first global
+// row with a non-positive pivot (atomicMin; dense.py:86-89 raises NotSpdError there).
+constexpr int POTRF_THREADS = 256;
+constexpr int MLD = 129;
+constexpr size_t POTRF_SMEM = (size_t)(T * MLD + 8 * T) * 8;
+
+// Serial Cholesky of the 8x8 block at rows/cols c0..c0+7 (one thread, registers only).
+__device__ __forceinline__ void factor_diag8(double* M, double* dinv, int c0) {
+  double a[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) a[r][c] = M[(c0 + r) * MLD + c0 + c];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double rq = rsqrt(a[q][q]);
+    a[q][q] *= rq;
+    dinv[c0 + q] = rq;
+#pragma unroll
+    for (int r = q + 1; r < 8; ++r) a[r][q] *= rq;
+#pragma unroll
+    for (int r = q + 1; r < 8; ++r)
+#pragma unroll
+      for (int c = q + 1; c <= r; ++c) a[r][c] = fma(-a[r][q], a[c][q], a[r][c]);
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) M[(c0 + r) * MLD + c0 + c] = a[r][c];
+}
+
+__global__ void __launch_bounds__(POTRF_THREADS) potrf_inv_kernel(double* __restrict__ tiles, int nt,
+                                                                  int k, double* __restrict__ inv,
+                                                                  double* __restrict__ ell,
+                                                                  double* __restrict__ diag,
+                                                                  unsigned long long* __restrict__ fail,
+                                                                  int64_t m, long long* prof = nullptr) {
+#define PROF(i) if (prof && tid == 0) prof[i] = clock64();
+  extern __shared__ double M[];   // [T][MLD], then S[8][T] scratch
+  double* S = M + T * MLD;
   __shared__ double dinv[T];
-  constexpr int LD = 129;
-  const int i = threadIdx.x;  // row owned in the factorization, column owned in the inverse
-  const int lane = i & 31, warp = i >> 5;
-  const double* tile = tiles + tile_index(k, k, nt) * TILE_ELEMS;
-  for (int o = i; o < TILE_ELEMS; o += T) {
-    const int r = (o >> 3) & 127;
-    const int c = ((o >> 10) << 3) + iperm8(o & 7);
-    L[r * LD + c] = tile[o];
+  const int tid = threadIdx.x;
+  PROF(0)
+  double* tile = tiles + tile_index(k, k, nt) * TILE_ELEMS;
+  {
+    double2 v[TILE_ELEMS / 2 / POTRF_THREADS];  // all 32 loads in flight
+#pragma unroll
+    for (int u = 0; u < TILE_ELEMS / 2 / POTRF_THREADS; ++u)
+      v[u] = reinterpret_cast<const double2*>(tile)[tid + u * POTRF_THREADS];
+#pragma unroll
+    for (int u = 0; u < TILE_ELEMS / 2 / POTRF_THREADS; ++u) {
+      const int o = 2 * (tid + u * POTRF_THREADS);  // positions (o, o+1): columns c and c+4
+      const int r = (o >> 3) & 127;
+      const int c = ((o >> 10) << 3) + iperm8(o & 7);
+      M[r * MLD + c] = v[u].x;
+      M[r * MLD + c + 4] = v[u].y;
+    }
   }
   __syncthreads();
+  PROF(1)
+  if (tid == 0) factor_diag8(M, dinv, 0);
+  __syncthreads();
+  PROF(2)
 
-  for (int c0 = 0; c0 < T; c0 += 8) {
-    double s[8];
-    if (i >= c0) {
+  for (int c0 = 0; c0 + 8 < T; c0 += 8) {
+    // A2: block column below the (already factored) diagonal block
+    {
+      const int i = c0 + 8 + tid;
+      if (i < T) {
+        double s[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s[q] = L[i * LD + c0 + q];
-      for (int p = 0; p < c0; ++p) {
-        const double lp = L[i * LD + p];
+        for (int q = 0; q < 8; ++q) s[q] = M[i * MLD + c0 + q];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s[q] = fma(-lp, L[(c0 + q) * LD + p], s[q]);
+        for (int q = 0; q < 8; ++q) {
+          double v = s[q];
+#pragma unroll
+          for (int q2 = 0; q2 < q; ++q2) v = fma(-s[q2], M[(c0 + q) * MLD + c0 + q2], v);
+          s[q] = v * dinv[c0 + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) M[i * MLD + c0 + q] = s[q];
       }
     }
-    if (warp == (c0 >> 5)) {
-      const int base = c0 & 31;
-      const int t = lane - base;  // row within the 8x8 diagonal block if 0 <= t < 8
-      const bool mine = (t >= 0 && t < 8);
+    __syncthreads();
+    if (c0 == 0) PROF(3)
+    // A3: rank-8 trailing update in 4x4 blocks; thread 0 takes the next diagonal 8x8 block
+    {
+      const int base = c0 + 8;
+      if (tid < 32) {
+        // warp 0: the 36 lower entries of the next diagonal block, then lane 0 factors it
+        for (int e = tid; e < 36; e += 32) {
+          int r = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+          while ((r + 1) * (r + 2) / 2 <= e) ++r;
+          while (r * (r + 1) / 2 > e) --r;
+          const int c = e - r * (r + 1) / 2;
+          double lr[8], lc[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double dq = __shfl_sync(0xffffffffu, s[q], base + q);
-        const double lqq = sqrt(dq);
-        const double rq = 1.0 / lqq;
-        if (mine) {
-          if (t == q) {
-            const int64_t g = (int64_t)k * T + c0 + q;
-            if (!(dq > 0.0) && g < m) atomicMin(fail, (unsigned long long)g);
-            s[q] = lqq;
-            ell[g] = 2.0 * log(lqq);
-            diag[g] = lqq;
-            dinv[c0 + q] = rq;
-          } else if (t > q) {
-            s[q] *= rq;
+          for (int q = 0; q < 8; ++q) {
+            lr[q] = M[(base + r) * MLD + c0 + q];
+            lc[q] = M[(base + c) * MLD + c0 + q];
+          }
+          double v = M[(base + r) * MLD + base + c];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v = fma(-lr[q], lc[q], v);
+          M[(base + r) * MLD + base + c] = v;
+        }
+        __syncwarp();
+        if (c0 == 0) PROF(4)
+        if (tid == 0) factor_diag8(M, dinv, base);
+        if (c0 == 0) PROF(5)
+      }
+      // warps 0 and 4 share SMSP 0: keep that scheduler for the serial diagonal chain
+      const int w = tid >> 5;
+      const int nb4 = (T - base) >> 2;
+      const int nblk = nb4 * (nb4 + 1) / 2;
+      const int slot = w < 4 ? tid - 32 : tid - 64;  // 0..191 over warps 1-3, 5-7
+      for (int b = 3 + slot; (w & 3) != 0 && b < nblk; b += 192) {  // 0..2: next diag 8x8
+        int bi = (int)((sqrtf(8.0f * b + 1.0f) - 1.0f) * 0.5f);
+        while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+        while (bi * (bi + 1) / 2 > b) --bi;
+        const int bj = b - bi * (bi + 1) / 2;
+        const int i0 = base + 4 * bi, j0 = base + 4 * bj;
+        double li[4][8], lj[4][8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            li[r][q] = M[(i0 + r) * MLD + c0 + q];
+            lj[r][q] = M[(j0 + r) * MLD + c0 + q];
+          }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            double v = M[(i0 + r) * MLD + j0 + cc];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v = fma(-li[r][q], lj[cc][q], v);
+            M[(i0 + r) * MLD + j0 + cc] = v;
+          }
+      }
+    }
+    __syncthreads();
+    if (c0 == 0) PROF(6)
+  }
+  PROF(7)
+
+  // Phase B: thread t pairs columns j and 127-j (balanced work), rows 2h, 2h+1 per block
+  {
+    const int j = tid & 63, h = tid >> 6;
+    const int cA = j, cB = 127 - j;
+    const int pwA = cA & ~31, pwB = cB & ~31;  // warp-uniform starts (broadcast L reads)
+    const double dA = dinv[cA], dB = dinv[cB];
+    for (int r0 = 0; r0 < T; r0 += 8) {
+      const double* L0 = M + (r0 + 2 * h) * MLD;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int c = side ? cB : cA;
+        const int pw = side ? pwB : pwA;
+        const double dc = side ? dB : dA;
+        if (r0 + 7 < pw) continue;
+        const double* Xc = M + c * MLD;
+        double s0 = 0.0, s1 = 0.0;
+        for (int p0 = pw; p0 < r0; p0 += 8) {
+          double x[8], l0[8], l1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int p = p0 + u;
+            const double xv = Xc[p];
+            x[u] = p < c ? 0.0 : (p == c ? dc : xv);
+            l0[u] = L0[p];
+            l1[u] = L0[MLD + p];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            s0 = fma(l0[u], x[u], s0);
+            s1 = fma(l1[u], x[u], s1);
           }
         }
+        S[(2 * h) * T + c] = s0;
+        S[(2 * h + 1) * T + c] = s1;
+      }
+      __syncthreads();
+      if (tid < T && r0 + 7 > tid) {
+        const int c = tid;
+        const double dc = dinv[c];
+        double ld[8][8], sv[8], di[8];
 #pragma unroll
-        for (int q2 = q + 1; q2 < 8; ++q2) {
-          const double l2 = __shfl_sync(0xffffffffu, s[q], base + q2);
-          if (mine && t > q) s[q2] = fma(-s[q], l2, s[q2]);
+        for (int q = 0; q < 8; ++q) {
+          sv[q] = (r0 + 7 >= (c & ~31)) ? S[q * T + c] : 0.0;
+          di[q] = dinv[r0 + q];
+#pragma unroll
+          for (int q2 = 0; q2 < q; ++q2) ld[q][q2] = M[(r0 + q) * MLD + r0 + q2];
+        }
+        double xq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = r0 + q;
+          double acc = sv[q];
+#pragma unroll
+          for (int q2 = 0; q2 < q; ++q2) acc = fma(ld[q][q2], xq[q2], acc);
+          const double v = r < c ? 0.0 : (r == c ? dc : -acc * di[q]);
+          if (r > c) M[c * MLD + r] = v;
+          xq[q] = v;
         }
       }
-      if (mine) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) L[i * LD + c0 + q] = s[q];
-      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (i >= c0 + 8) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        double v = s[q];
-#pragma unroll
-        for (int q2 = 0; q2 < q; ++q2) v = fma(-s[q2], L[(c0 + q) * LD + c0 + q2], v);
-        s[q] = v * dinv[c0 + q];
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) L[i * LD + c0 + q] = s[q];
-    }
-    __syncthreads();
   }
-
-  // L_kk back to its tile (lower triangle, zero upper) so the packed storage holds the factor
-  {
-    double* out = tiles + tile_index(k, k, nt) * TILE_ELEMS;
-    for (int o = i; o < TILE_ELEMS; o += T) {
-      const int r = (o >> 3) & 127;
-      const int cc = ((o >> 10) << 3) + iperm8(o & 7);
-      out[o] = cc <= r ? L[r * LD + cc] : 0.0;
-    }
+  PROF(8)
+  if (tid < T) {
+    // pivots: log, diagonal, and the NotSpd check, off the serial chain
+    const int r = tid;
+    const int64_t g = (int64_t)k * T + r;
+    const double l = M[r * MLD + r];
+    if (!(l > 0.0) && g < m) atomicMin(fail, (unsigned long long)g);
+    ell[g] = 2.0 * log(l);
+    diag[g] = l;
+  }
+#pragma unroll 8
+  for (int o2 = tid; o2 < TILE_ELEMS / 2; o2 += POTRF_THREADS) {
+    const int o = 2 * o2;
+    const int r = (o >> 3) & 127;
+    const int c = ((o >> 10) << 3) + iperm8(o & 7);
+    double2 lv, xv;
+    lv.x = c < r ? M[r * MLD + c] : (c == r ? M[r * MLD + r] : 0.0);
+    lv.y = c + 4 < r ? M[r * MLD + c + 4] : (c + 4 == r ? M[r * MLD + r] : 0.0);
+    xv.x = c < r ? M[c * MLD + r] : (c == r ? dinv[r] : 0.0);
+    xv.y = c + 4 < r ? M[(c + 4) * MLD + r] : (c + 4 == r ? dinv[r] : 0.0);
+    reinterpret_cast<double2*>(tile)[o2] = lv;
+    reinterpret_cast<double2*>(inv)[o2] = xv;
   }
   __syncthreads();
-
-  // In-place inverse, row by row: X[r][c] = -(sum_{p<r} L[r][p] X[p][c]) / L[r][r] (c < r).
-  const int c = i;
-  const int p_start = warp * 32;  // X[p][c] == 0 for p < c, so a warp may start at its min c
-  for (int r = 0; r < T; ++r) {
-    double x = 0.0;
-    if (c < r) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int p = p_start;
-      for (; p + 3 < r; p += 4) {
-        a0 = fma(L[r * LD + p], L[p * LD + c], a0);
-        a1 = fma(L[r * LD + p + 1], L[(p + 1) * LD + c], a1);
-        a2 = fma(L[r * LD + p + 2], L[(p + 2) * LD + c], a2);
-        a3 = fma(L[r * LD + p + 3], L[(p + 3) * LD + c], a3);
-      }
-      for (; p < r; ++p) a0 = fma(L[r * LD + p], L[p * LD + c], a0);
-      x = -((a0 + a1) + (a2 + a3)) * dinv[r];
-    } else if (c == r) {
-      x = dinv[r];
-    }
-    __syncthreads();
-    L[r * LD + c] = x;
-    __syncthreads();
-  }
-  for (int o = i; o < TILE_ELEMS; o += T) {
-    const int r = (o >> 3) & 127;
-    const int cc = ((o >> 10) << 3) + iperm8(o & 7);
-    inv[o] = L[r * LD + cc];
-  }
+  PROF(9)
+#undef PROF
 }
 
 // ------------------------------------------------------------------------------ DMMA GEMM
@@ -203,6 +326,7 @@ constexpr int KC = 16;                  // columns per pipeline stage (two octet
 constexpr int STAGE_ELEMS = T * KC;     // 2048 doubles = 16 KB per operand
 constexpr int STAGES = 4;
 constexpr int GEMM_THREADS = 288;       // 8 consumer warps + 1 producer warp
+constexpr int RASTER_G = 8;             // super-tile edge of the CTA raster (tile_order)
 constexpr size_t GEMM_SMEM = (size_t)STAGES * 2 * STAGE_ELEMS * 8 + 2 * STAGES * 8 + 128;
 
 template <int MODE>
@@ -213,10 +337,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * STAGE_ELEMS);
   uint64_t* empty = full + STAGES;
 
-  // decode the output tile (i, j) of this CTA
-  int b = blockIdx.x, j = t.j0;
-  while (b >= t.nt - j - t.row_off) { b -= t.nt - j - t.row_off; ++j; }
-  const int i = j + t.row_off + b;
+  // output tile (i, j) of this CTA, in L2-friendly super-tile order
+  int i, j;
+  tile_order(blockIdx.x, t.nt, t.j0, t.j1, t.row_off, RASTER_G, &i, &j);
   const int jout = (MODE == MODE_TRSM) ? t.k : j;
   const int nchunks = (MODE == MODE_TRSM) ? (T / KC) : (t.p1 - t.p0) * (T / KC);
 
@@ -279,23 +402,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
     const double* a_st = sA + s * STAGE_ELEMS + wm * 64 * 8 + fr;
     const double* b_st = sB + s * STAGE_ELEMS + wn * 32 * 8 + fr;
 #pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      // B fragments for two k-steps stay in registers; A fragments stream one row-group at a
-      // time (keeps the live set under the 168-register cap of a 9-warp CTA)
-      double2 bf[4];
+    for (int kk = 0; kk < 4; ++kk) {
+      // k-step kk of the chunk: octet kk>>1, half kk&1 of each lane's 16-byte fragment pair.
+      // One k-step's 8 A + 4 B fragments stay in registers (168-register cap of a 9-warp CTA)
+      // and the 32 DMMAs of a k-step are independent, so dependent DMMAs are 32 issues apart.
+      const int off = (kk >> 1) * OCTET_ELEMS + (kk & 1);
+      double af[8], bf[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        bf[h] = *reinterpret_cast<const double2*>(b_st + o * OCTET_ELEMS + h * 64);
-        if (MODE == MODE_UPDATE) { bf[h].x = neg(bf[h].x); bf[h].y = neg(bf[h].y); }
+        bf[h] = b_st[off + h * 64];
+        if (MODE == MODE_UPDATE) bf[h] = neg(bf[h]);
       }
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const double2 af = *reinterpret_cast<const double2*>(a_st + o * OCTET_ELEMS + g * 64);
+      for (int g = 0; g < 8; ++g) af[g] = a_st[off + g * 64];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af.x, bf[h].x);
+      for (int g = 0; g < 8; ++g)
 #pragma unroll
-        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af.y, bf[h].y);
-      }
+        for (int h = 0; h < 4; ++h) dmma(acc[g][h][0], acc[g][h][1], af[g], bf[h]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

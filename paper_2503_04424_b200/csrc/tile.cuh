@@ -38,6 +38,43 @@ __host__ __device__ __forceinline__ int64_t n_packed_tiles(int nt) {
   return (int64_t)nt * (nt + 1) / 2;
 }
 
+// Output-tile order of a GEMM launch over the trapezoid {(i, j): j0 <= j < j1, j + row_off <= i < nt}.
+// CTAs walk column bands of G tiles; inside a band, the triangular head first, then row
+// blocks of G rows (column-major inside a block), so a wave of ~148 CTAs touches ~2-3 G x G
+// super-tiles and its A/B panel tiles stay L2-resident.  Bijective (tests/test_tile_order.py).
+__host__ __device__ inline void tile_order(int64_t b, int nt, int j0, int j1, int row_off, int G,
+                                           int* out_i, int* out_j) {
+  for (int jb0 = j0; jb0 < j1; jb0 += G) {
+    const int wb = (j1 - jb0) < G ? (j1 - jb0) : G;
+    const int head_end = jb0 + wb;  // rows [.., head_end) form the band's triangular head
+    int64_t tri = 0;
+    for (int j = jb0; j < jb0 + wb; ++j) {
+      const int lo = j + row_off, hi = head_end < nt ? head_end : nt;
+      tri += hi > lo ? hi - lo : 0;
+    }
+    const int64_t rows = nt > head_end ? nt - head_end : 0;
+    const int64_t band = tri + rows * wb;
+    if (b >= band) { b -= band; continue; }
+    if (b < tri) {
+      for (int j = jb0; j < jb0 + wb; ++j) {
+        const int lo = j + row_off, hi = head_end < nt ? head_end : nt;
+        const int cnt = hi > lo ? hi - lo : 0;
+        if (b < cnt) { *out_i = lo + (int)b; *out_j = j; return; }
+        b -= cnt;
+      }
+    }
+    b -= tri;
+    const int64_t rb = b / ((int64_t)G * wb);
+    const int64_t e = b - rb * G * wb;
+    const int64_t rows_here = (rows - rb * G) < G ? (rows - rb * G) : G;
+    *out_j = jb0 + (int)(e / rows_here);
+    *out_i = head_end + (int)(rb * G + e % rows_here);
+    return;
+  }
+  *out_i = -1;
+  *out_j = -1;
+}
+
 // ------------------------------------------------------------------ PTX helpers (sm_90+)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

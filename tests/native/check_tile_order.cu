@@ -1,0 +1,28 @@
+// Host-side check that tile_order() is a bijection onto its trapezoid (run by tests).
+#include <cstdio>
+#include <set>
+#include <utility>
+#include "../../paper_2503_04424_b200/csrc/tile.cuh"
+int main() {
+  int bad = 0, cases = 0;
+  for (int nt = 1; nt <= 40; ++nt)
+    for (int j0 = 0; j0 < nt; ++j0)
+      for (int j1 = j0 + 1; j1 <= nt; ++j1)
+        for (int row_off = 0; row_off <= 1; ++row_off)
+          for (int G : {1, 3, 8}) {
+            std::set<std::pair<int, int>> want, got;
+            for (int j = j0; j < j1; ++j)
+              for (int i = j + row_off; i < nt; ++i) want.insert({i, j});
+            for (long b = 0; b < (long)want.size(); ++b) {
+              int i, j;
+              b2d::tile_order(b, nt, j0, j1, row_off, G, &i, &j);
+              got.insert({i, j});
+            }
+            ++cases;
+            if (got != want) {
+              if (bad++ < 5) printf("mismatch nt=%d j0=%d j1=%d off=%d G=%d\n", nt, j0, j1, row_off, G);
+            }
+          }
+  printf("%d cases, %d bad\n", cases, bad);
+  return bad != 0;
+}
