@@ -284,15 +284,23 @@ def run_engine(args):
             "matrices_per_s": ws * args.steps / (ms_max * 1e-3),
             "frac_of_fp64_peak": value / (ws * peak),
             "logdet": logdet,
-            "roofline": {"bound": "tensor", "kernel": "gemm_kernel<MODE_UPDATE> (DMMA Schur update)",
+            "roofline": {"bound": "tensor",
+                         "kernel": "gemm_kernel<MODE_UPDATE>, trailing Schur-update launches (DMMA)",
                          "achieved": achieved, "peak": peak, "unit": UNIT,
                          "frac": (achieved / peak) if achieved else None,
                          "peak_source": "live DMMA m8n8k4 microbenchmark (b2d_probe_fp64_peak), this run; "
                                         "MEASURED_PEAKS.json has no FP64 entry",
+                         "achieved_note": "algorithmic flops of the trailing-update launches (2*128^2*K per "
+                                          "off-diagonal tile, 128*129*K per diagonal tile) / their summed "
+                                          "CUDA-event time on their stream, one extra untimed step; panel "
+                                          "kernels run concurrently on a second stream",
                          "launches": upd_launches, "algorithmic_flops": upd_flops,
                          "kernel_ms": upd_ms,
                          "traffic": prof.get("dram_bytes_per_launch") if prof else None,
-                         "traffic_launch": prof if prof else None},
+                         "traffic_launch": {k: prof[k] for k in ("kernel", "grid", "K", "duration_ms",
+                                                                 "algorithmic_flops", "algorithmic_bytes_min",
+                                                                 "dram_bytes_read", "dram_bytes_write")}
+                         if prof else None},
             "cpu_baseline": cpu,
             "e2e": {"value": flops / e2e_sec / 1e12 * ws, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_sec, "steps": e2e_steps,

@@ -95,9 +95,10 @@ int b2d_ctx_fetch(b2d_ctx *ctx, double *d_out, double *prefix_out, int64_t *fail
                   b2d_run_info *info);
 /* Device pointer of the prefix vector (m doubles), valid until the next factorisation. */
 const double *b2d_ctx_device_prefix(b2d_ctx *ctx);
-/* Dominant-kernel accounting (Schur-update GEMM launches of the last factorisation):
- * algorithmic flops, summed CUDA-event duration (ms) and launch count.  Enabled by
- * b2d_ctx_set_profiling(ctx, 1); adds one event pair per update launch. */
+/* Dominant-kernel accounting (the trailing "rest" Schur-update GEMM launches of the last
+ * factorisation; they run back to back on one stream, ~95% of the flops): algorithmic flops,
+ * summed CUDA-event duration (ms) and launch count.  Enabled by b2d_ctx_set_profiling(ctx, 1);
+ * adds one event pair per such launch. */
 int b2d_ctx_set_profiling(b2d_ctx *ctx, int on);
 int b2d_ctx_update_stats(b2d_ctx *ctx, double *flops, double *ms, int64_t *launches);
 

@@ -44,10 +44,10 @@ static int set_err(int code, const char* fmt, ...) {
   } while (0)
 
 // outer panel width in tiles: the trailing Schur update runs with K = panel_tiles * 128
-// (default 4; B2D_PANEL_TILES overrides for tuning)
+// (default 8; B2D_PANEL_TILES overrides for tuning)
 static int panel_tiles_default() {
   const char* e = getenv("B2D_PANEL_TILES");
-  int w = e ? atoi(e) : 4;
+  int w = e ? atoi(e) : 8;
   return w < 1 ? 1 : (w > 16 ? 16 : w);
 }
 
@@ -56,7 +56,7 @@ struct Ctx {
   int64_t m = 0;
   int mode = B2D_MODE_CHOLESKY;
   int nt = 0;
-  int W_TILES = 4;
+  int W_TILES = 8;
   double* tiles = nullptr;   // packed lower tile triangle
   double* inv = nullptr;     // nt inverse diagonal tiles
   double* ell = nullptr;     // n_pad: 2 log L_ii
@@ -257,7 +257,7 @@ static void enqueue_factor(Ctx* c) {
     // next-cols(k0): the next panel's columns, on the critical path
     const int ne = std::min(ke + W_TILES, nt);
     if (st >= 1) cudaStreamWaitEvent(c->s_main, c->ev_rest[st - 1], 0);
-    launch_update(c, c->s_main, ke, ne, k0, ke, true);
+    launch_update(c, c->s_main, ke, ne, k0, ke, false);
     // rest(k0): everything right of the next panel, overlapping the next panel's factorisation
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
     launch_update(c, c->s_side, ne, nt, k0, ke, true);
