@@ -51,6 +51,9 @@ static int panel_tiles_default() {
   return w < 1 ? 1 : (w > 16 ? 16 : w);
 }
 
+constexpr int NSTAGE = 8;   // host-ingest staging strips in flight
+constexpr int BAND = 4;     // tile-columns per ingest band
+
 struct Ctx {
   int device = 0;
   int64_t m = 0;
@@ -63,10 +66,14 @@ struct Ctx {
   double* diag = nullptr;    // n_pad: L_ii
   double* prefix = nullptr;  // n_pad
   unsigned long long* fail = nullptr;
-  double* strip[2] = {nullptr, nullptr};  // host-ingest staging strips (128 x n_pad each)
-  cudaStream_t s_main = nullptr, s_side = nullptr;
+  double* strip[NSTAGE] = {};  // host-ingest staging strips (128 x n_pad doubles each)
+  cudaStream_t s_main = nullptr, s_side = nullptr, s_copy = nullptr, s_pack = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_join = nullptr;
-  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_strip;
+  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_catch, ev_stage, ev_copied, ev_band;
+  // band activation (host ingest): band b = tile-columns [b*BAND, (b+1)*BAND) joins the
+  // right-looking updates at outer step act[b] (-1: from the start) after one catch-up update
+  std::vector<int> act;
+  bool trace = false;  // B2D_TRACE: print a per-step event timeline on fetch
   bool profiling = false;
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
@@ -83,10 +90,9 @@ static int configure_kernels() {
                                 (int)GEMM_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
-  const int sm_tile = T * 129 * 8;
   CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)POTRF_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_tile));
-  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_tile));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   done = true;
   return B2D_OK;
 }
@@ -102,15 +108,19 @@ static void destroy(Ctx* c) {
   cudaFree(c->diag);
   cudaFree(c->prefix);
   cudaFree(c->fail);
-  cudaFree(c->strip[0]);
-  cudaFree(c->strip[1]);
-  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_strip, &c->prof_ev})
+  if (c->s_copy) cudaStreamSynchronize(c->s_copy);
+  for (auto* p : c->strip) cudaFree(p);
+  if (c->s_pack) cudaStreamSynchronize(c->s_pack);
+  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
+                  &c->prof_ev})
     for (auto e : *v) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_stop) cudaEventDestroy(c->ev_stop);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->s_main) cudaStreamDestroy(c->s_main);
   if (c->s_side) cudaStreamDestroy(c->s_side);
+  if (c->s_copy) cudaStreamDestroy(c->s_copy);
+  if (c->s_pack) cudaStreamDestroy(c->s_pack);
   delete c;
 }
 
@@ -164,7 +174,9 @@ static int create(int device, int64_t m, int mode, Ctx** out) {
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   // panel chain (critical path) gets the highest priority; trailing updates the lowest
   if (cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->s_side, cudaStreamNonBlocking, lo) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->s_side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->s_copy, cudaStreamNonBlocking, hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->s_pack, cudaStreamNonBlocking, hi) != cudaSuccess) {
     destroy(c);
     return set_err(B2D_ERR_CUDA, "stream creation failed");
   }
@@ -174,10 +186,22 @@ static int create(int device, int64_t m, int mode, Ctx** out) {
   const int nsteps = (c->nt + c->W_TILES - 1) / c->W_TILES;
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
+  c->ev_catch.resize(nsteps);
+  c->trace = getenv("B2D_TRACE") != nullptr;
+  const unsigned evf = c->trace ? cudaEventDefault : cudaEventDisableTiming;
   for (int s = 0; s < nsteps; ++s) {
-    cudaEventCreateWithFlags(&c->ev_panel[s], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&c->ev_rest[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_panel[s], evf);
+    cudaEventCreateWithFlags(&c->ev_rest[s], evf);
+    cudaEventCreateWithFlags(&c->ev_catch[s], evf);
   }
+  const int nbands = (c->nt + BAND - 1) / BAND;
+  c->ev_band.resize(nbands);
+  for (auto& e : c->ev_band) cudaEventCreateWithFlags(&e, evf);
+  c->ev_stage.resize(NSTAGE);
+  for (auto& e : c->ev_stage) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  c->ev_copied.resize(NSTAGE);
+  for (auto& e : c->ev_copied) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  c->act.assign(nbands, -1);
   *out = c;
   return B2D_OK;
 }
@@ -238,29 +262,56 @@ static void launch_panel_column(Ctx* c, cudaStream_t s, int p) {
   }
 }
 
-// The factorisation proper on packed tiles already in HBM (stream order after `s_main`).
-static void enqueue_factor(Ctx* c) {
+// The factorisation proper.  Tile-columns of bands with act[b] == -1 are in HBM (or their
+// band event is waited on) before step 0; a band with act[b] = s >= 0 first receives one
+// catch-up update with every panel of steps < s (K = 128*k0, on s_side, after its band event),
+// then joins the regular next-cols / rest updates from step s on.  act[b] <= the step whose
+// next-cols update first touches band b, so every column is current before it is factored.
+static void enqueue_factor(Ctx* c, bool wait_bands) {
   const int nt = c->nt;
   const int W_TILES = c->W_TILES;
   const int nsteps = (nt + W_TILES - 1) / W_TILES;
+  const int nbands = (nt + BAND - 1) / BAND;
+  if (wait_bands) {
+    for (int b = 0; b < nbands; ++b)
+      if (c->act[b] < 0) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
+  }
+  int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel column)
   for (int st = 0; st < nsteps; ++st) {
     const int k0 = st * W_TILES;
     const int ke = std::min(k0 + W_TILES, nt);
     // panel(k0): its columns were last touched by next-cols(st-1) (same stream) and rest(st-2)
     if (st >= 2) cudaStreamWaitEvent(c->s_main, c->ev_rest[st - 2], 0);
     for (int p = k0; p < ke; ++p) {
+      if (wait_bands) {
+        // an initial band must be in HBM before the first panel column that reads it (the
+        // intra-panel update touches columns up to ke-1)
+        const int need = std::min(nbands, (ke - 1) / BAND + 1);
+        while (main_waited < need && c->act[main_waited] < 0)
+          cudaStreamWaitEvent(c->s_main, c->ev_band[main_waited++], 0);
+      }
       launch_panel_column(c, c->s_main, p);
       if (p + 1 < ke) launch_update(c, c->s_main, p + 1, ke, p, p + 1, false);
     }
     cudaEventRecord(c->ev_panel[st], c->s_main);
     if (ke >= nt) break;
-    // next-cols(k0): the next panel's columns, on the critical path
     const int ne = std::min(ke + W_TILES, nt);
-    if (st >= 1) cudaStreamWaitEvent(c->s_main, c->ev_rest[st - 1], 0);
+    // catch-up of the bands that join at this step (panels of steps < st, already factored)
+    int end_active = 0;
+    for (int b = 0; b < nbands; ++b) {
+      if (c->act[b] == st) {
+        if (wait_bands) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
+        launch_update(c, c->s_side, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
+      }
+      if (c->act[b] <= st) end_active = std::min(nt, (b + 1) * BAND);
+    }
+    cudaEventRecord(c->ev_catch[st], c->s_side);
+    // next-cols(k0): the next panel's columns, on the critical path
+    cudaStreamWaitEvent(c->s_main, c->ev_catch[st], 0);
     launch_update(c, c->s_main, ke, ne, k0, ke, false);
-    // rest(k0): everything right of the next panel, overlapping the next panel's factorisation
+    // rest(k0): active columns right of the next panel, overlapping the next panel
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
-    launch_update(c, c->s_side, ne, nt, k0, ke, true);
+    launch_update(c, c->s_side, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
   }
   // join the side stream, then the prefix scan
@@ -280,6 +331,8 @@ static void begin(Ctx* c, cudaStream_t user) {
   cudaEventRecord(c->ev_start, user);
   cudaStreamWaitEvent(c->s_main, c->ev_start, 0);
   cudaStreamWaitEvent(c->s_side, c->ev_start, 0);
+  cudaStreamWaitEvent(c->s_copy, c->ev_start, 0);
+  cudaStreamWaitEvent(c->s_pack, c->ev_start, 0);
   cudaMemsetAsync(c->fail, 0xff, 8, c->s_main);
 }
 
@@ -297,54 +350,116 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
   begin(c, user);
   const unsigned ntiles = (unsigned)n_packed_tiles(c->nt);
   if (dtype == B2D_F64)
-    pack_tiles_kernel<double><<<ntiles, 512, T * 129 * 8, c->s_main>>>((const double*)a, lda, 0, c->m,
-                                                                      c->tiles, c->nt, 0);
+    pack_tiles_kernel<double><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
+        (const double*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   else
-    pack_tiles_kernel<float><<<ntiles, 512, T * 129 * 8, c->s_main>>>((const float*)a, lda, 0, c->m,
-                                                                     c->tiles, c->nt, 0);
+    pack_tiles_kernel<float><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
+        (const float*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   c->launches++;
-  enqueue_factor(c);
+  cudaEventRecord(c->ev_join, c->s_main);
+  cudaStreamWaitEvent(c->s_side, c->ev_join, 0);
+  std::fill(c->act.begin(), c->act.end(), -1);
+  enqueue_factor(c, false);
   end(c, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
 }
 
-// Host ingest: row strip J (rows [128J, 128J+128), columns [128J, m)) -> staging -> tile-column J.
+// Band activation schedule for host ingest (static, data-independent => deterministic).
+// A small event simulation of the pipeline: bands arrive at a modelled PCIe rate (~52 GB/s);
+// each outer step costs its panel chain plus its update flops at ~34 TFLOP/s; a band joins at
+// the first step that starts after its arrival, and never later than the step whose next-cols
+// update first touches it (then the device waits for it).  Deferred panels are applied by one
+// catch-up update when the band joins, so early steps are not held up by late strips.
+static void plan_bands(Ctx* c, size_t esz) {
+  const int nt = c->nt, W = c->W_TILES;
+  const int nbands = (nt + BAND - 1) / BAND;
+  const int nsteps = (nt + W - 1) / W;
+  const double m = (double)c->m, pcie = 48e9, rate = 34e12, chain_rate = 20e12, col_lat = 200e-6;
+  const double tile_flops = 2.0 * T * T * T;
+  std::vector<double> arrival(nbands);
+  double bytes = 0.0;
+  for (int b = 0; b < nbands; ++b) {
+    for (int J = b * BAND; J < std::min(nt, (b + 1) * BAND); ++J) {
+      const double r0 = (double)J * T;
+      bytes += std::max(0.0, std::min((double)T, m - r0)) * std::max(0.0, m - r0) * (double)esz;
+    }
+    arrival[b] = bytes / pcie;
+  }
+  auto tiles = [nt](int j0, int j1) {
+    double n = 0;
+    for (int j = j0; j < std::min(j1, nt); ++j) n += nt - j;
+    return n;
+  };
+  double t = 0.0;
+  int next = 0;
+  while (next < nbands && (next * BAND) / W - 1 < 0) {  // needed by step 0's panel / next-cols
+    c->act[next] = -1;
+    t = std::max(t, arrival[next]);
+    ++next;
+  }
+  for (int st = 0; st < nsteps && next < nbands; ++st) {
+    const int k0 = st * W, ke = std::min(k0 + W, nt), ne = std::min(ke + W, nt);
+    // critical chain of the step (s_main): panel columns + intra-panel and next-cols updates
+    const double chain = W * col_lat +
+                         (0.5 * W * (W - 1) * (nt - k0) * tile_flops + tiles(ke, ne) * tile_flops * W) /
+                             chain_rate;
+    double side = 0.0;  // s_side: catch-ups of joining bands + rest over active bands
+    while (next < nbands && (arrival[next] <= t || (next * BAND) / W - 1 <= st)) {
+      c->act[next] = st;
+      t = std::max(t, arrival[next]);
+      side += tiles(next * BAND, (next + 1) * BAND) * tile_flops * k0;
+      ++next;
+    }
+    const int end_active = std::min(nt, next * BAND);
+    side += tiles(ne, std::max(ne, end_active)) * tile_flops * W;
+    t += std::max(chain, side / rate);
+  }
+}
+
+// Host ingest: row strip J (rows [128J, 128J+128), columns [128J, m)) = tile-column J of the
+// packed lower triangle.  Strips stream through NSTAGE staging buffers on s_copy (H2D copy,
+// then a pack kernel that co-resides with the Schur-update CTAs); each band of BAND strips
+// records an event, and the factorisation waits per band, so PCIe overlaps the DMMA work.
 static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   CUDA_TRY(cudaSetDevice(c->device));
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < NSTAGE; ++b)
     if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
-  if (c->ev_strip.empty()) {
-    c->ev_strip.resize(2);
-    for (auto& e : c->ev_strip) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  }
   begin(c, user);
+  plan_bands(c, esz);
   for (int J = 0; J < c->nt; ++J) {
-    const int b = J & 1;
+    const int b = J % NSTAGE;
     const int64_t r0 = (int64_t)J * T;
     const int64_t rows = std::min<int64_t>(T, c->m - r0);
-    const int64_t cols = c->m - r0;  // columns [r0, m)
-    // strip buffer b is free once the pack of strip J-2 finished (same stream: ordered)
+    const int64_t cols = c->m - r0;  // columns [r0, m): the upper triangle of this strip
+    // staging buffer b is free once the pack of strip J - NSTAGE has run
+    if (J >= NSTAGE) cudaStreamWaitEvent(c->s_copy, c->ev_stage[b], 0);
     const char* src = (const char*)a + (size_t)(r0 * lda + r0) * esz;
     // staged with leading dimension npad, offset so that column r0 lands at index r0
     char* dst = (char*)c->strip[b] + (size_t)r0 * esz;
     CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)npad * esz, src, (size_t)lda * esz, (size_t)cols * esz,
-                               (size_t)rows, cudaMemcpyHostToDevice, c->s_main));
+                               (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+    cudaEventRecord(c->ev_copied[b], c->s_copy);
     c->h2d += rows * cols * (int64_t)esz;
+    cudaStreamWaitEvent(c->s_pack, c->ev_copied[b], 0);
     const unsigned ntile = (unsigned)(c->nt - J);
     if (dtype == B2D_F64)
-      pack_tiles_kernel<double><<<ntile, 512, T * 129 * 8, c->s_main>>>(
+      pack_tiles_kernel<double><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
           (const double*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
     else
-      pack_tiles_kernel<float><<<ntile, 512, T * 129 * 8, c->s_main>>>(
+      pack_tiles_kernel<float><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
           (const float*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
     c->launches++;
+    cudaEventRecord(c->ev_stage[b], c->s_pack);
+    if ((J + 1) % BAND == 0 || J + 1 == c->nt) cudaEventRecord(c->ev_band[J / BAND], c->s_pack);
   }
-  enqueue_factor(c);
+  enqueue_factor(c, true);
+  cudaEventRecord(c->ev_join, c->s_pack);
+  cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
   end(c, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
@@ -380,6 +495,20 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
     info->device_ms = ms;
     info->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - c->t0).count();
+  }
+  if (c->trace) {
+    const int nsteps = (int)c->ev_panel.size();
+    auto at = [&](cudaEvent_t e) {
+      float x = -1.f;
+      if (cudaEventElapsedTime(&x, c->ev_start, e) != cudaSuccess) { cudaGetLastError(); x = -1.f; }
+      return x;
+    };
+    fprintf(stderr, "[b2d trace] total %.2f ms\n", ms);
+    for (size_t b = 0; b < c->ev_band.size(); ++b)
+      fprintf(stderr, "[b2d trace] band %zu act %d arrived %.2f\n", b, c->act[b], at(c->ev_band[b]));
+    for (int st = 0; st < nsteps; ++st)
+      fprintf(stderr, "[b2d trace] step %d panel %.2f catch %.2f rest %.2f\n", st, at(c->ev_panel[st]),
+              at(c->ev_catch[st]), at(c->ev_rest[st]));
   }
   if (fail_index) *fail_index = fail == ULLONG_MAX ? -1 : (int64_t)fail;
   if (fail != ULLONG_MAX)

@@ -23,34 +23,44 @@ namespace b2d {
 // Tile element (r, c) = src[C][R] (R = 128I + r, C = 128J + c): the row-major UPPER triangle,
 // i.e. the (i <= j) tiles the reference reads (memdet.py:364, 376, 384); identity padding
 // beyond m.
+// Two passes of 64 columns keep shared memory at 66 KB, so a pack CTA co-resides with a
+// Schur-update CTA (128 KB) on one SM while host strips stream in under the factorisation.
+constexpr int PACK_THREADS = 256;
+constexpr size_t PACK_SMEM = (size_t)64 * 129 * 8;
+
 template <typename Tin>
-__global__ void __launch_bounds__(512) pack_tiles_kernel(const Tin* __restrict__ src, int64_t lda,
-                                                         int64_t row_base, int64_t m,
-                                                         double* __restrict__ tiles, int nt,
-                                                         int j_lo) {
-  extern __shared__ double sm[];  // [128][129]: sm[c*129 + r]
+__global__ void __launch_bounds__(PACK_THREADS) pack_tiles_kernel(const Tin* __restrict__ src,
+                                                                  int64_t lda, int64_t row_base,
+                                                                  int64_t m,
+                                                                  double* __restrict__ tiles,
+                                                                  int nt, int j_lo) {
+  extern __shared__ double sm[];  // [64][129]: sm[c*129 + r] for the current 64 columns
   int64_t b = blockIdx.x;
   int J = j_lo;
   while (b >= nt - J) { b -= nt - J; ++J; }
   const int I = J + (int)b;
   const int tid = threadIdx.x;
   const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
-#pragma unroll 4
-  for (int idx = tid; idx < TILE_ELEMS; idx += 512) {
-    const int c = idx >> 7, r = idx & 127;
-    const int64_t R = R0 + r, C = C0 + c;
-    double v;
-    if (R < m && C < m) v = (double)src[(C - row_base) * lda + R];
-    else v = (R == C) ? 1.0 : 0.0;
-    sm[c * 129 + r] = v;
-  }
-  __syncthreads();
   double* out = tiles + tile_index(I, J, nt) * TILE_ELEMS;
-#pragma unroll 4
-  for (int o = tid; o < TILE_ELEMS; o += 512) {
-    const int r = (o >> 3) & 127;
-    const int c = ((o >> 10) << 3) + iperm8(o & 7);
-    out[o] = sm[c * 129 + r];
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll 8
+    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
+      const int c = idx >> 7, r = idx & 127;
+      const int64_t R = R0 + r, C = C0 + 64 * half + c;
+      double v;
+      if (R < m && C < m) v = (double)src[(C - row_base) * lda + R];
+      else v = (R == C) ? 1.0 : 0.0;
+      sm[c * 129 + r] = v;
+    }
+    __syncthreads();
+    // octets 8*half .. 8*half+7 are the contiguous half-tile [half*8192, half*8192 + 8192)
+#pragma unroll 8
+    for (int o = tid; o < 64 * T; o += PACK_THREADS) {
+      const int r = (o >> 3) & 127;
+      const int c = ((o >> 10) << 3) + iperm8(o & 7);  // 0..63 within this half
+      out[half * 64 * T + o] = sm[c * 129 + r];
+    }
+    __syncthreads();
   }
 }
 

@@ -7,6 +7,7 @@ from paper_2503_04424_b200 import _native, gen
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=32768)
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--host", action="store_true", help="pinned host input (e2e path)")
 args = ap.parse_args()
 n = args.n
 x = torch.from_numpy(gen.rbf_points(n, 16, 0)).cuda()
@@ -15,9 +16,17 @@ _native.check(_native.load().b2d_gen_rbf(ctypes.c_void_p(x.data_ptr()), n, 16, 4
 torch.cuda.synchronize()
 ctx = _native.Context(n)
 pre = np.empty(n)
+if args.host:
+    h = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    h.copy_(a)
+    del a
+    torch.cuda.empty_cache()
 for s in range(args.steps):
     t0 = time.perf_counter()
-    ctx.factor_device_async(a.data_ptr(), n, _native.B2D_F64, 0)
+    if args.host:
+        ctx.factor_host_async(h.data_ptr(), n, _native.B2D_F64, 0)
+    else:
+        ctx.factor_device_async(a.data_ptr(), n, _native.B2D_F64, 0)
     rc, fail, info = ctx.fetch(None, pre)
     _native.check(rc)
     dt = time.perf_counter() - t0
