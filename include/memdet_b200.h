@@ -58,7 +58,21 @@ typedef struct b2d_run_info {
   int64_t kernel_launches; /* engine kernels launched by this call                          */
   double device_ms;        /* CUDA-event time of the device work                            */
   double wall_seconds;     /* host wall time of the call                                    */
+  int64_t ooc_blocks;      /* out-of-core: engine block grid n_b (0 = in-core run)          */
+  int64_t ooc_block;       /* out-of-core: engine block edge b                              */
+  int64_t ooc_reads;       /* out-of-core: whole-block host->HBM loads actually performed   */
+  int64_t ooc_writes;      /* out-of-core: whole-block HBM->host scratch writes performed   */
+  int64_t ooc_scratch;     /* out-of-core: distinct scratch blocks used                      */
 } b2d_run_info;
+
+/* Engine options (b2d_ctx_create_ex). */
+typedef struct b2d_options {
+  int64_t hbm_budget;      /* bytes of HBM the engine may use; 0 = free memory less a margin */
+  int64_t num_blocks;      /* reference n_b for the out-of-core tile walk; 0 = from max_mem  */
+  int64_t max_mem;         /* reference byte budget (memdet.py:63-80) when num_blocks is 0   */
+  int32_t force_out_of_core; /* 1: stream blocks through HBM even if the matrix fits          */
+  int32_t reserved;
+} b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;
 
@@ -82,6 +96,13 @@ int b2d_memdet_sym(const void *a, int64_t m, int64_t lda, int dtype, int mode, i
 
 /* Context API: allocate once, factor many times (bench / repeated runs). */
 int b2d_ctx_create(int device, int64_t m, int mode, b2d_ctx **out);
+/* With options: an order whose packed lower triangle exceeds the HBM budget (or
+ * force_out_of_core) gets the out-of-core plan — the reference tile walk (memdet.py:124-145,
+ * 322-389) over b x b blocks streamed between host memory and HBM, prefetched on copy streams
+ * against the DMMA work; b follows num_blocks / max_mem, grown until six blocks fit. */
+int b2d_ctx_create_ex(int device, int64_t m, int mode, const b2d_options *opt, b2d_ctx **out);
+/* 1 if the context runs out of core (then only host inputs are accepted), 0 if in-core. */
+int b2d_ctx_is_out_of_core(b2d_ctx *ctx);
 int b2d_ctx_destroy(b2d_ctx *ctx);
 /* Enqueue pack + factorisation + prefix of a DEVICE-resident row-major matrix on `stream`
  * (a cudaStream_t, 0 = legacy default).  Results stay on the device until b2d_ctx_fetch. */

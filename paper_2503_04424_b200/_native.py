@@ -29,7 +29,15 @@ class RunInfoC(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "m", "n_b", "b", "tail", "blocks_read", "blocks_written", "scratch_slots", "tile",
         "n_tiles", "h2d_bytes", "d2h_bytes", "kernel_launches")] + [
-        ("device_ms", ctypes.c_double), ("wall_seconds", ctypes.c_double)]
+        ("device_ms", ctypes.c_double), ("wall_seconds", ctypes.c_double)] + [
+        (name, ctypes.c_int64) for name in ("ooc_blocks", "ooc_block", "ooc_reads", "ooc_writes",
+                                            "ooc_scratch")]
+
+
+class OptionsC(ctypes.Structure):
+    _fields_ = [("hbm_budget", ctypes.c_int64), ("num_blocks", ctypes.c_int64),
+                ("max_mem", ctypes.c_int64), ("force_out_of_core", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -45,6 +53,8 @@ SIGNATURES = {
     "b2d_memdet_sym": (_I, [_P, _I64, _I64, _I, _I, _I64, _I64, _I, _P, _P, _P, _P,
                             ctypes.POINTER(RunInfoC), ctypes.POINTER(_I64)]),
     "b2d_ctx_create": (_I, [_I, _I64, _I, ctypes.POINTER(_P)]),
+    "b2d_ctx_create_ex": (_I, [_I, _I64, _I, ctypes.POINTER(OptionsC), ctypes.POINTER(_P)]),
+    "b2d_ctx_is_out_of_core": (_I, [_P]),
     "b2d_ctx_destroy": (_I, [_P]),
     "b2d_ctx_factor_device_async": (_I, [_P, _P, _I64, _I, _P]),
     "b2d_ctx_factor_host_async": (_I, [_P, _P, _I64, _I, _P]),
@@ -111,14 +121,24 @@ def check(rc: int, what: str = "engine call", fail_index: int | None = None):
 class Context:
     """Owning wrapper of a b2d_ctx (HBM workspace for one matrix order)."""
 
-    def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0):
+    def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0, hbm_budget: int = 0,
+                 num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False):
         lib = load()
         h = ctypes.c_void_p()
-        check(lib.b2d_ctx_create(device, m, mode, ctypes.byref(h)), "b2d_ctx_create")
+        opt = OptionsC(int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
+                       int(bool(force_out_of_core)), 0)
+        check(lib.b2d_ctx_create_ex(device, m, mode, ctypes.byref(opt), ctypes.byref(h)),
+              "b2d_ctx_create_ex")
         self._h = h
         self.m = m
         self.mode = mode
         self.device = device
+        self.key = (device, m, mode, int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
+                    bool(force_out_of_core))
+
+    @property
+    def out_of_core(self) -> bool:
+        return bool(load().b2d_ctx_is_out_of_core(self._h))
 
     @property
     def handle(self):

@@ -1,6 +1,7 @@
 // Host side of the B200 MEMDET engine: HBM planner, right-looking tiled factorisation driver
-// with one-panel look-ahead on two prioritised streams, host<->HBM strip streamer, and the
-// C ABI declared in include/memdet_b200.h.
+// with one-panel look-ahead on two prioritised streams, host->HBM strip streamer overlapped
+// with the factorisation, the out-of-core block streamer (the reference tile walk over blocks
+// that live in host memory), and the C ABI declared in include/memdet_b200.h.
 //
 // Reference driver mirrored: _memdet_symmetric (memdet.py:322-389).  The reference walks an
 // n_b x n_b tile grid out of core with four resident b x b buffers; here the whole lower tile
@@ -15,7 +16,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/memdet_b200.h"
@@ -53,6 +57,37 @@ static int panel_tiles_default() {
 
 constexpr int NSTAGE = 8;   // host-ingest staging strips in flight
 constexpr int BAND = 4;     // tile-columns per ingest band
+constexpr int NSLOT = 6;    // out-of-core: HBM block slots (A, B, C, T + two for prefetch)
+
+// The lower tile triangle of an nt x nt tile matrix to factor in place: the whole packed
+// matrix (in-core) or one diagonal block slot (out-of-core).  g0 = global index of its row 0.
+struct FactorTarget {
+  TileMap map;
+  int nt;
+  int64_t g0;
+};
+
+// Out-of-core state: b x b blocks of the reference tile grid stream between host memory (the
+// input matrix, and a pinned scratchpad of updated blocks in the engine's tile format) and
+// NSLOT HBM slots of nbt x nbt tiles.
+struct Ooc {
+  int nb = 0;
+  int64_t b = 0, tail = 0;
+  int nbt = 0;
+  double* slot[NSLOT] = {};
+  cudaEvent_t ev_loaded[NSLOT] = {}, ev_used[NSLOT] = {}, ev_stored[NSLOT] = {};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  double* stage = nullptr;                         // one 128-row file strip
+  std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
+  std::map<std::pair<int, int>, cudaEvent_t> ev_key;  // last store of each scratch block
+  std::set<std::pair<int, int>> written;           // cache table of the current run
+  int64_t reads = 0, writes = 0;
+  int rr = 0;
+  int64_t size(int k) const { return k == nb - 1 ? tail : b; }
+  int tiles(int k) const { return (int)((size(k) + T - 1) / T); }
+  TileMap map(int s) const { return TileMap{slot[s], nbt, 0}; }
+  size_t slot_bytes() const { return (size_t)nbt * nbt * TILE_BYTES; }
+};
 
 struct Ctx {
   int device = 0;
@@ -81,6 +116,8 @@ struct Ctx {
   int64_t h2d = 0, d2h = 0;
   bool pending = false;
   std::chrono::steady_clock::time_point t0;
+  bool ooc = false;
+  Ooc o;
 };
 
 static int configure_kernels() {
@@ -93,6 +130,8 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)POTRF_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   done = true;
   return B2D_OK;
 }
@@ -121,65 +160,88 @@ static void destroy(Ctx* c) {
   if (c->s_side) cudaStreamDestroy(c->s_side);
   if (c->s_copy) cudaStreamDestroy(c->s_copy);
   if (c->s_pack) cudaStreamDestroy(c->s_pack);
+  Ooc& o = c->o;
+  if (o.s_h2d) cudaStreamSynchronize(o.s_h2d);
+  if (o.s_d2h) cudaStreamSynchronize(o.s_d2h);
+  for (int s = 0; s < NSLOT; ++s) {
+    cudaFree(o.slot[s]);
+    if (o.ev_loaded[s]) cudaEventDestroy(o.ev_loaded[s]);
+    if (o.ev_used[s]) cudaEventDestroy(o.ev_used[s]);
+    if (o.ev_stored[s]) cudaEventDestroy(o.ev_stored[s]);
+  }
+  cudaFree(o.stage);
+  for (auto& kv : o.scratch) cudaFreeHost(kv.second);
+  for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
+  if (o.s_h2d) cudaStreamDestroy(o.s_h2d);
+  if (o.s_d2h) cudaStreamDestroy(o.s_d2h);
   delete c;
 }
 
-static int create(int device, int64_t m, int mode, Ctx** out) {
-  if (m < 1) return set_err(B2D_ERR_USAGE, "matrix dimension must be >= 1, got %lld", (long long)m);
-  if (mode == B2D_MODE_LDL_PIV)
-    return set_err(B2D_ERR_UNSUPPORTED, "block-pivoted LDL is not built in this engine version");
-  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV)
-    return set_err(B2D_ERR_USAGE, "unknown mode %d", mode);
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-    return set_err(B2D_ERR_CUDA, "no CUDA device visible: the B200 engine has no CPU fallback");
-  if (device < 0 || device >= ndev) return set_err(B2D_ERR_USAGE, "bad device %d", device);
-  CUDA_TRY(cudaSetDevice(device));
-  int rc = configure_kernels();
-  if (rc) return rc;
-  Ctx* c = new Ctx();
-  c->device = device;
-  c->m = m;
-  c->mode = mode;
-  c->nt = (int)((m + T - 1) / T);
-  c->W_TILES = panel_tiles_default();
-  const int64_t npad = (int64_t)c->nt * T;
-  const size_t tile_bytes = (size_t)n_packed_tiles(c->nt) * TILE_BYTES;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  const size_t need = tile_bytes + (size_t)c->nt * TILE_BYTES + 3 * npad * 8 + 2 * (size_t)T * npad * 8;
-  if (need + (size_t)(1 << 28) > free_b) {
-    destroy(c);
-    return set_err(B2D_ERR_NOMEM,
-                   "in-core plan needs %.2f GB of HBM (%.2f GB free); the out-of-core streamer is not "
-                   "built in this engine version",
-                   need / 1e9, free_b / 1e9);
+// ---------------------------------------------------------------- reference tiling bookkeeping
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static void ref_layout(int64_t m, int64_t nb, int64_t* n_b, int64_t* b, int64_t* tail) {
+  // layout.py:35-51
+  nb = std::min(nb, m);
+  for (;;) {
+    const int64_t bb = 1 + (m - 1) / nb;
+    const int64_t need = ceil_div(m, bb);
+    if (need == nb) {
+      *n_b = nb;
+      *b = bb;
+      *tail = m - (nb - 1) * bb;
+      return;
+    }
+    nb = need;
   }
-#define ALLOC(ptr, bytes)                                        \
-  do {                                                           \
-    cudaError_t e_ = cudaMalloc((void**)&(ptr), (bytes));        \
-    if (e_ != cudaSuccess) {                                     \
-      destroy(c);                                                \
-      return set_err(B2D_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", (size_t)(bytes), cudaGetErrorString(e_)); \
-    }                                                            \
-  } while (0)
-  ALLOC(c->tiles, tile_bytes);
-  ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
-  ALLOC(c->ell, npad * 8);
-  ALLOC(c->diag, npad * 8);
-  ALLOC(c->prefix, npad * 8);
-  ALLOC(c->fail, 8);
-#undef ALLOC
+}
+
+static int64_t isqrt_u(unsigned __int128 x) {
+  unsigned __int128 r = 0, bit = (unsigned __int128)1 << 126;
+  while (bit > x) bit >>= 2;
+  while (bit) {
+    if (x >= r + bit) { x -= r + bit; r = (r >> 1) + bit; }
+    else r >>= 1;
+    bit >>= 2;
+  }
+  return (int64_t)r;
+}
+
+static int64_t ref_select_blocking(int64_t m, int64_t c, int64_t beta) {
+  // memdet.py:63-80 (exact integer arithmetic)
+  const unsigned __int128 msq = (unsigned __int128)m * m * beta;
+  if (msq <= (unsigned __int128)c) return 1;
+  if (3 * msq <= 4 * (unsigned __int128)c) return 2;
+  const unsigned __int128 target = 4 * msq;
+  int64_t q = isqrt_u(target / c);
+  while ((unsigned __int128)q * q * c < target) ++q;
+  return q;
+}
+
+static void fill_ref_info(b2d_run_info* info, int64_t m, int64_t num_blocks, int64_t max_mem, int esz) {
+  int64_t nb = num_blocks > 0 ? num_blocks : (max_mem > 0 ? ref_select_blocking(m, max_mem, esz) : 1);
+  int64_t n_b, b, tail;
+  ref_layout(m, nb, &n_b, &b, &tail);
+  info->n_b = n_b;
+  info->b = b;
+  info->tail = tail;
+  const int64_t n = n_b;
+  info->blocks_read = (2 * n * n * n - 3 * n * n + 7 * n) / 6;                       // cost.py:79-83
+  info->blocks_written = n <= 2 ? 0 : (n * n * n + 3 * n * n - 22 * n + 24) / 6;     // cost.py:86-92
+  info->scratch_slots = n <= 2 ? 0 : (n * n + n - 8) / 2;                            // cost.py:95-101
+}
+
+
+static int create_streams_events(Ctx* c) {
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  // panel chain (critical path) gets the highest priority; trailing updates the lowest
+  // panel chain (critical path) and ingest get the highest priority; trailing updates the lowest
   if (cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, hi) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->s_side, cudaStreamNonBlocking, lo) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->s_copy, cudaStreamNonBlocking, hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->s_pack, cudaStreamNonBlocking, hi) != cudaSuccess) {
-    destroy(c);
+      cudaStreamCreateWithPriority(&c->s_pack, cudaStreamNonBlocking, hi) != cudaSuccess)
     return set_err(B2D_ERR_CUDA, "stream creation failed");
-  }
   cudaEventCreate(&c->ev_start);
   cudaEventCreate(&c->ev_stop);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
@@ -202,81 +264,181 @@ static int create(int device, int64_t m, int mode, Ctx** out) {
   c->ev_copied.resize(NSTAGE);
   for (auto& e : c->ev_copied) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   c->act.assign(nbands, -1);
+  return B2D_OK;
+}
+
+// HBM planner.  In-core: the packed lower tile triangle, the inverse diagonal tiles, three
+// n_pad vectors and NSTAGE ingest strips.  Out-of-core (budget exceeded or forced): NSLOT
+// block slots of nbt^2 tiles; the block grid starts at the reference n_b (num_blocks, else
+// select_blocking(max_mem), memdet.py:63-80, 249-255) and grows until the slots fit.
+static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx** out) {
+  if (m < 1) return set_err(B2D_ERR_USAGE, "matrix dimension must be >= 1, got %lld", (long long)m);
+  if (mode == B2D_MODE_LDL_PIV)
+    return set_err(B2D_ERR_UNSUPPORTED, "block-pivoted LDL is not built in this engine version");
+  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV)
+    return set_err(B2D_ERR_USAGE, "unknown mode %d", mode);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(B2D_ERR_CUDA, "no CUDA device visible: the B200 engine has no CPU fallback");
+  if (device < 0 || device >= ndev) return set_err(B2D_ERR_USAGE, "bad device %d", device);
+  CUDA_TRY(cudaSetDevice(device));
+  int rc = configure_kernels();
+  if (rc) return rc;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t margin = (size_t)1 << 30;
+  size_t budget = free_b > margin ? free_b - margin : 0;
+  if (opt && opt->hbm_budget > 0) budget = std::min(budget, (size_t)opt->hbm_budget);
+
+  Ctx* c = new Ctx();
+  c->device = device;
+  c->m = m;
+  c->mode = mode;
+  c->W_TILES = panel_tiles_default();
+  const int nt_full = (int)((m + T - 1) / T);
+  const int64_t npad_full = (int64_t)nt_full * T;
+  const size_t incore_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + (size_t)nt_full * TILE_BYTES +
+                             3 * (size_t)npad_full * 8 + (size_t)NSTAGE * T * npad_full * 8;
+  const bool force = opt && opt->force_out_of_core;
+  int64_t vec_len = npad_full;
+#define ALLOC(ptr, bytes)                                        \
+  do {                                                           \
+    cudaError_t e_ = cudaMalloc((void**)&(ptr), (bytes));        \
+    if (e_ != cudaSuccess) {                                     \
+      destroy(c);                                                \
+      return set_err(B2D_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", (size_t)(bytes), cudaGetErrorString(e_)); \
+    }                                                            \
+  } while (0)
+  if (!force && incore_need <= budget) {
+    c->nt = nt_full;
+    ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
+    ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
+  } else {
+    Ooc& o = c->o;
+    c->ooc = true;
+    int64_t nb = 2;
+    if (opt && opt->num_blocks > 0) nb = opt->num_blocks;
+    else if (opt && opt->max_mem > 0) nb = ref_select_blocking(m, opt->max_mem, 8);
+    nb = std::max<int64_t>(1, nb);
+    for (;;) {
+      int64_t n_b, b, tail;
+      ref_layout(m, nb, &n_b, &b, &tail);
+      const int nbt = (int)((b + T - 1) / T);
+      const size_t need = (size_t)NSLOT * nbt * nbt * TILE_BYTES + (size_t)nbt * TILE_BYTES +
+                          (size_t)T * nbt * T * 8 + 3 * (size_t)(m + (int64_t)(nbt + 1) * T) * 8;
+      if (need <= budget || n_b >= m) {
+        if (need > budget) {
+          destroy(c);
+          return set_err(B2D_ERR_NOMEM, "no out-of-core plan fits %.2f GB of HBM", budget / 1e9);
+        }
+        o.nb = (int)n_b;
+        o.b = b;
+        o.tail = tail;
+        o.nbt = nbt;
+        break;
+      }
+      nb = n_b + 1;
+    }
+    c->nt = o.nbt;  // the in-core machinery factors one diagonal block at a time
+    vec_len = m + (int64_t)(o.nbt + 1) * T;
+    for (int s = 0; s < NSLOT; ++s) {
+      ALLOC(o.slot[s], o.slot_bytes());
+      cudaEventCreateWithFlags(&o.ev_loaded[s], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&o.ev_used[s], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&o.ev_stored[s], cudaEventDisableTiming);
+    }
+    ALLOC(o.stage, (size_t)T * o.nbt * T * 8);
+    ALLOC(c->inv, (size_t)o.nbt * TILE_BYTES);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&o.s_h2d, cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&o.s_d2h, cudaStreamNonBlocking, hi);
+  }
+  ALLOC(c->ell, vec_len * 8);
+  ALLOC(c->diag, vec_len * 8);
+  ALLOC(c->prefix, vec_len * 8);
+  ALLOC(c->fail, 8);
+#undef ALLOC
+  rc = create_streams_events(c);
+  if (rc) {
+    destroy(c);
+    return rc;
+  }
   *out = c;
   return B2D_OK;
 }
 
-static int64_t tiles_in(int nt, int j0, int j1, int row_off) {
-  int64_t n = 0;
-  for (int j = j0; j < j1; ++j) n += std::max(0, nt - j - row_off);
-  return n;
-}
-
-// MODE_UPDATE over output tile-columns [j0, j1) with K tile-columns [p0, p1)
-static void launch_update(Ctx* c, cudaStream_t s, int j0, int j1, int p0, int p1, bool prof) {
-  const int64_t ntile = tiles_in(c->nt, j0, j1, 0);
-  if (ntile <= 0 || p1 <= p0) return;
-  GemmTask t{};
-  t.tiles = c->tiles;
-  t.nt = c->nt;
-  t.j0 = j0;
-  t.j1 = j1;
-  t.row_off = 0;
-  t.p0 = p0;
-  t.p1 = p1;
+static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, bool prof, double flops) {
+  const int64_t ntile = t.out.count();
+  if (ntile <= 0) return;
+  if (mode == MODE_UPDATE && t.p1 <= t.p0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof && c->profiling) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  gemm_kernel<MODE_UPDATE><<<(unsigned)ntile, GEMM_THREADS, GEMM_SMEM, s>>>(t);
+  if (mode == MODE_UPDATE)
+    gemm_kernel<MODE_UPDATE><<<(unsigned)ntile, GEMM_THREADS, GEMM_SMEM, s>>>(t);
+  else
+    gemm_kernel<MODE_TRSM><<<(unsigned)ntile, GEMM_THREADS, GEMM_SMEM, s>>>(t);
   c->launches++;
   if (e0) {
     cudaEventRecord(e1, s);
     c->prof_ev.push_back(e0);
     c->prof_ev.push_back(e1);
-    // algorithmic flops: off-diagonal tiles 2*T*T*K, diagonal (SYRK, lower half) T*(T+1)*K
-    const double K = (double)(p1 - p0) * T;
-    const int64_t ndiag = j1 - j0;
-    c->prof_flops.push_back((double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
+    c->prof_flops.push_back(flops);
   }
 }
 
-static void launch_panel_column(Ctx* c, cudaStream_t s, int p) {
-  const int nt = c->nt;
+// Schur update of the target's lower tiles in tile-columns [j0, j1) with K tile-columns [p0, p1)
+static void launch_update(Ctx* c, cudaStream_t s, const FactorTarget& ft, int j0, int j1, int p0, int p1,
+                          bool prof) {
+  GemmTask t{};
+  t.a = t.b = t.c = ft.map;
+  t.out = TileSet{0, ft.nt, j0, std::min(j1, ft.nt), 1, 0};
+  t.p0 = p0;
+  t.p1 = p1;
+  // algorithmic flops: off-diagonal tiles 2*T*T*K, diagonal (SYRK, lower half) T*(T+1)*K
+  const double K = (double)(p1 - p0) * T;
+  const int64_t ntile = t.out.count();
+  const int64_t ndiag = std::max(0, t.out.j1 - t.out.j0);
+  launch_gemm(c, s, MODE_UPDATE, t, prof, (double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
+}
+
+static void launch_panel_column(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p) {
   double* invp = c->inv + (int64_t)p * TILE_ELEMS;
-  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(c->tiles, nt, p, invp, c->ell, c->diag, c->fail, c->m);
+  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(ft.map.tile(p, p), invp, c->ell, c->diag, c->fail,
+                                                         ft.g0 + (int64_t)p * T, c->m);
   c->launches++;
-  if (p + 1 < nt) {
+  if (p + 1 < ft.nt) {
     GemmTask t{};
-    t.tiles = c->tiles;
+    t.c = ft.map;
     t.binv = invp;
-    t.nt = nt;
-    t.j0 = p;
-    t.j1 = p + 1;
-    t.row_off = 1;
+    t.out = TileSet{0, ft.nt, p, p + 1, 1, 1};
     t.k = p;
-    gemm_kernel<MODE_TRSM><<<nt - p - 1, GEMM_THREADS, GEMM_SMEM, s>>>(t);
-    c->launches++;
+    launch_gemm(c, s, MODE_TRSM, t, false, 0.0);
   }
 }
 
-// The factorisation proper.  Tile-columns of bands with act[b] == -1 are in HBM (or their
-// band event is waited on) before step 0; a band with act[b] = s >= 0 first receives one
-// catch-up update with every panel of steps < s (K = 128*k0, on s_side, after its band event),
-// then joins the regular next-cols / rest updates from step s on.  act[b] <= the step whose
-// next-cols update first touches band b, so every column is current before it is factored.
-static void enqueue_factor(Ctx* c, bool wait_bands) {
-  const int nt = c->nt;
+// The factorisation proper of ft (streams s_main / s_side, joined back into s_main).
+// In the in-core host-ingest path, tile-columns of bands with act[b] == -1 are waited for before
+// first use; a band with act[b] = s >= 0 first receives one catch-up update with every panel of
+// steps < s (K = 128*k0, on s_side, after its band event), then joins the regular next-cols /
+// rest updates from step s on.  act[b] <= the step whose next-cols update first touches band b,
+// so every column is current before it is factored.
+static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
+  const int nt = ft.nt;
   const int W_TILES = c->W_TILES;
   const int nsteps = (nt + W_TILES - 1) / W_TILES;
   const int nbands = (nt + BAND - 1) / BAND;
+  cudaEventRecord(c->ev_join, c->s_main);
+  cudaStreamWaitEvent(c->s_side, c->ev_join, 0);
   if (wait_bands) {
     for (int b = 0; b < nbands; ++b)
       if (c->act[b] < 0) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
   }
-  int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel column)
+  int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel)
   for (int st = 0; st < nsteps; ++st) {
     const int k0 = st * W_TILES;
     const int ke = std::min(k0 + W_TILES, nt);
@@ -290,33 +452,39 @@ static void enqueue_factor(Ctx* c, bool wait_bands) {
         while (main_waited < need && c->act[main_waited] < 0)
           cudaStreamWaitEvent(c->s_main, c->ev_band[main_waited++], 0);
       }
-      launch_panel_column(c, c->s_main, p);
-      if (p + 1 < ke) launch_update(c, c->s_main, p + 1, ke, p, p + 1, false);
+      launch_panel_column(c, c->s_main, ft, p);
+      if (p + 1 < ke) launch_update(c, c->s_main, ft, p + 1, ke, p, p + 1, false);
     }
     cudaEventRecord(c->ev_panel[st], c->s_main);
     if (ke >= nt) break;
     const int ne = std::min(ke + W_TILES, nt);
     // catch-up of the bands that join at this step (panels of steps < st, already factored)
-    int end_active = 0;
-    for (int b = 0; b < nbands; ++b) {
-      if (c->act[b] == st) {
-        if (wait_bands) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
-        launch_update(c, c->s_side, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
+    int end_active = nt;
+    if (wait_bands) {
+      end_active = 0;
+      for (int b = 0; b < nbands; ++b) {
+        if (c->act[b] == st) {
+          cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
+          launch_update(c, c->s_side, ft, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
+        }
+        if (c->act[b] <= st) end_active = std::min(nt, (b + 1) * BAND);
       }
-      if (c->act[b] <= st) end_active = std::min(nt, (b + 1) * BAND);
     }
     cudaEventRecord(c->ev_catch[st], c->s_side);
     // next-cols(k0): the next panel's columns, on the critical path
     cudaStreamWaitEvent(c->s_main, c->ev_catch[st], 0);
-    launch_update(c, c->s_main, ke, ne, k0, ke, false);
+    launch_update(c, c->s_main, ft, ke, ne, k0, ke, false);
     // rest(k0): active columns right of the next panel, overlapping the next panel
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
-    launch_update(c, c->s_side, ne, std::max(ne, end_active), k0, ke, true);
+    launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
   }
-  // join the side stream, then the prefix scan
+  // join the side stream
   cudaEventRecord(c->ev_join, c->s_side);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+}
+
+static void enqueue_prefix(Ctx* c) {
   prefix_kernel<<<1, 1024, 0, c->s_main>>>(c->ell, c->m, c->prefix);
   c->launches++;
 }
@@ -346,6 +514,8 @@ static void end(Ctx* c, cudaStream_t user) {
 static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  if (c->ooc)
+    return set_err(B2D_ERR_UNSUPPORTED, "out-of-core contexts take host inputs (the matrix exceeds the HBM budget)");
   CUDA_TRY(cudaSetDevice(c->device));
   begin(c, user);
   const unsigned ntiles = (unsigned)n_packed_tiles(c->nt);
@@ -356,10 +526,9 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
     pack_tiles_kernel<float><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
         (const float*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   c->launches++;
-  cudaEventRecord(c->ev_join, c->s_main);
-  cudaStreamWaitEvent(c->s_side, c->ev_join, 0);
   std::fill(c->act.begin(), c->act.end(), -1);
-  enqueue_factor(c, false);
+  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, false);
+  enqueue_prefix(c);
   end(c, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
@@ -421,9 +590,12 @@ static void plan_bands(Ctx* c, size_t esz) {
 // packed lower triangle.  Strips stream through NSTAGE staging buffers on s_copy (H2D copy,
 // then a pack kernel that co-resides with the Schur-update CTAs); each band of BAND strips
 // records an event, and the factorisation waits per band, so PCIe overlaps the DMMA work.
+static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
+
 static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  if (c->ooc) return run_ooc(c, a, lda, dtype, user);
   CUDA_TRY(cudaSetDevice(c->device));
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
@@ -457,8 +629,219 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
     cudaEventRecord(c->ev_stage[b], c->s_pack);
     if ((J + 1) % BAND == 0 || J + 1 == c->nt) cudaEventRecord(c->ev_band[J / BAND], c->s_pack);
   }
-  enqueue_factor(c, true);
+  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, true);
+  enqueue_prefix(c);
   cudaEventRecord(c->ev_join, c->s_pack);
+  cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+  end(c, user);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+// ---------------------------------------------------------------- out-of-core block streamer
+
+// One visit of the reference's symmetric tile walk, stage k (memdet.py:83-145).
+struct Visit {
+  int i, j;
+  bool col_start, load_b, load_c, solve_c, write_c, next_diag;
+};
+
+static std::vector<Visit> stage_visits(int nb, int k) {
+  std::vector<Visit> v;
+  for (int j = nb - 1; j > k; --j) {
+    const bool last_col = j == nb - 1;
+    std::vector<int> rows{j};
+    for (int i = k + 1; i < j; ++i) rows.push_back(i);
+    for (size_t pos = 0; pos < rows.size(); ++pos) {
+      const int i = rows[pos];
+      const bool off = i != j;
+      v.push_back(Visit{i, j, pos == 0, pos == 0 && last_col, off, off && last_col,
+                        off && last_col && nb > 2 && i < j - 1, i == k + 1 && j == k + 1});
+    }
+  }
+  return v;
+}
+
+// Load reference block (ri, rj), ri <= rj (the row-major upper tile the reference reads), into
+// slot s as the engine's lower block (rj, ri): from the scratchpad if it was written this run
+// (the reference cache table, storage.py:134-144), else from the input in 128-row strips
+// (H2D + pack_block_kernel).  Waits until the slot's previous contents are consumed and stored.
+static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, int dtype) {
+  Ooc& o = c->o;
+  cudaStreamWaitEvent(o.s_h2d, o.ev_used[s], 0);
+  cudaStreamWaitEvent(o.s_h2d, o.ev_stored[s], 0);
+  auto key = std::make_pair(ri, rj);
+  if (o.written.count(key)) {
+    cudaStreamWaitEvent(o.s_h2d, o.ev_key[key], 0);  // the scratch copy must have landed
+    CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyHostToDevice, o.s_h2d));
+    c->h2d += (int64_t)o.slot_bytes();
+  } else {
+    const size_t esz = dtype == B2D_F64 ? 8 : 4;
+    const int64_t rows_blk = o.size(rj), cols_blk = o.size(ri);  // engine block: rows of rj, cols of ri
+    const int64_t ld_stage = (int64_t)o.nbt * T;
+    for (int J = 0; J < o.tiles(ri); ++J) {
+      const int64_t frow = (int64_t)ri * o.b + (int64_t)J * T;            // first file row of the strip
+      const int64_t nrows = std::min<int64_t>(T, cols_blk - (int64_t)J * T);
+      const char* src = (const char*)a + ((size_t)frow * lda + (size_t)rj * o.b) * esz;
+      CUDA_TRY(cudaMemcpy2DAsync(o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)rows_blk * esz,
+                                 (size_t)nrows, cudaMemcpyHostToDevice, o.s_h2d));
+      c->h2d += nrows * rows_blk * (int64_t)esz;
+      if (dtype == B2D_F64)
+        pack_block_kernel<double><<<o.tiles(rj), PACK_THREADS, PACK_SMEM, o.s_h2d>>>(
+            (const double*)o.stage, ld_stage, rows_blk, cols_blk, ri == rj, o.map(s), J);
+      else
+        pack_block_kernel<float><<<o.tiles(rj), PACK_THREADS, PACK_SMEM, o.s_h2d>>>(
+            (const float*)o.stage, ld_stage, rows_blk, cols_blk, ri == rj, o.map(s), J);
+      c->launches++;
+    }
+  }
+  cudaEventRecord(o.ev_loaded[s], o.s_h2d);
+  o.reads++;
+  return B2D_OK;
+}
+
+// Write slot s to the scratchpad as reference block (ri, rj) (storage.py:258-263).
+static int ooc_store(Ctx* c, int ri, int rj, int s) {
+  Ooc& o = c->o;
+  auto key = std::make_pair(ri, rj);
+  auto it = o.scratch.find(key);
+  if (it == o.scratch.end()) {
+    double* h = nullptr;
+    CUDA_TRY(cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault));
+    it = o.scratch.emplace(key, h).first;
+  }
+  cudaStreamWaitEvent(o.s_d2h, o.ev_used[s], 0);
+  CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDeviceToHost, o.s_d2h));
+  cudaEventRecord(o.ev_stored[s], o.s_d2h);
+  auto ek = o.ev_key.find(key);
+  if (ek == o.ev_key.end()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ek = o.ev_key.emplace(key, e).first;
+  }
+  cudaEventRecord(ek->second, o.s_d2h);
+  c->d2h += (int64_t)o.slot_bytes();
+  o.written.insert(key);
+  o.writes++;
+  return B2D_OK;
+}
+
+// Panel solve of slot s (engine lower block (x, k), x's rows) against the factored diagonal
+// block in slot sa: right-looking over L_kk's tile-columns in groups of W (dense.py:94-99).
+static void ooc_trsm(Ctx* c, int s, int x, int sa, int k) {
+  Ooc& o = c->o;
+  cudaStreamWaitEvent(c->s_main, o.ev_loaded[s], 0);
+  const int R = o.tiles(x), Q = o.tiles(k), W = c->W_TILES;
+  for (int q0 = 0; q0 < Q; q0 += W) {
+    const int qe = std::min(q0 + W, Q);
+    for (int q = q0; q < qe; ++q) {
+      GemmTask t{};
+      t.c = o.map(s);
+      t.binv = c->inv + (int64_t)q * TILE_ELEMS;
+      t.out = TileSet{0, R, q, q + 1, 0, 0};
+      t.k = q;
+      launch_gemm(c, c->s_main, MODE_TRSM, t, false, 0.0);
+      if (q + 1 < qe) {
+        GemmTask u{};
+        u.a = o.map(s);
+        u.b = o.map(sa);
+        u.c = o.map(s);
+        u.out = TileSet{0, R, q + 1, qe, 0, 0};
+        u.p0 = q;
+        u.p1 = q + 1;
+        launch_gemm(c, c->s_main, MODE_UPDATE, u, false, 0.0);
+      }
+    }
+    if (qe < Q) {
+      GemmTask u{};
+      u.a = o.map(s);
+      u.b = o.map(sa);
+      u.c = o.map(s);
+      u.out = TileSet{0, R, qe, Q, 0, 0};
+      u.p0 = q0;
+      u.p1 = qe;
+      launch_gemm(c, c->s_main, MODE_UPDATE, u, false, 0.0);
+    }
+  }
+  cudaEventRecord(o.ev_used[s], c->s_main);
+  cudaEventRecord(o.ev_used[sa], c->s_main);
+}
+
+// Schur update of slot st (engine block (j, i)) -= L(j,k) L(i,k)^T (dense.py:109-116).
+static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
+  Ooc& o = c->o;
+  for (int x : {st, sbj, sci}) cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
+  GemmTask t{};
+  t.a = o.map(sbj);
+  t.b = o.map(sci);
+  t.c = o.map(st);
+  t.out = TileSet{0, o.tiles(j), 0, o.tiles(i), i == j ? 1 : 0, 0};
+  t.p0 = 0;
+  t.p1 = o.tiles(k);
+  const double K = (double)t.p1 * T;
+  launch_gemm(c, c->s_main, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
+  cudaEventRecord(o.ev_used[st], c->s_main);
+  cudaEventRecord(o.ev_used[sbj], c->s_main);
+  cudaEventRecord(o.ev_used[sci], c->s_main);
+}
+
+// The reference driver (memdet.py:322-389) with HBM slots for its A/B/C/S buffers: every read
+// and scratch write the reference performs happens here too (so the transfer counters are the
+// reference's), issued on copy streams that run ahead of the DMMA work by the spare slots.
+static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
+  Ooc& o = c->o;
+  CUDA_TRY(cudaSetDevice(c->device));
+  begin(c, user);
+  cudaStreamWaitEvent(o.s_h2d, c->ev_start, 0);
+  cudaStreamWaitEvent(o.s_d2h, c->ev_start, 0);
+  o.written.clear();
+  o.reads = o.writes = 0;
+  o.rr = 0;
+  auto alloc = [&](std::initializer_list<int> busy) {
+    for (int tries = 0; tries < NSLOT; ++tries) {
+      const int s = o.rr;
+      o.rr = (o.rr + 1) % NSLOT;
+      bool ok = true;
+      for (int x : busy) ok = ok && x != s;
+      if (ok) return s;
+    }
+    return -1;
+  };
+  int sa = alloc({});
+  int rc = ooc_load(c, 0, 0, sa, a, lda, dtype);
+  if (rc) return rc;
+  for (int k = 0; k < o.nb; ++k) {
+    cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
+    enqueue_factor(c, FactorTarget{o.map(sa), o.tiles(k), (int64_t)k * o.b}, false);
+    cudaEventRecord(o.ev_used[sa], c->s_main);
+    if (k == o.nb - 1) break;
+    int sb = -1, sc = -1, next_a = -1;
+    for (const Visit& v : stage_visits(o.nb, k)) {
+      if (v.col_start) {
+        if (v.load_b) {
+          sb = alloc({sa, sb, sc});
+          if ((rc = ooc_load(c, k, v.j, sb, a, lda, dtype))) return rc;
+          ooc_trsm(c, sb, v.j, sa, k);
+        } else {
+          sb = sc;  // the previous visit's C is this column's row-k tile (memdet.py:359-360)
+        }
+      }
+      if (v.load_c) {
+        sc = alloc({sa, sb, sc});
+        if ((rc = ooc_load(c, k, v.i, sc, a, lda, dtype))) return rc;
+        if (v.solve_c) ooc_trsm(c, sc, v.i, sa, k);
+        if (v.write_c && (rc = ooc_store(c, k, v.i, sc))) return rc;
+      }
+      const int st = alloc({sa, sb, sc});
+      if ((rc = ooc_load(c, v.i, v.j, st, a, lda, dtype))) return rc;
+      ooc_schur(c, st, v.j, v.i, sb, v.i == v.j ? sb : sc, k);
+      if (v.next_diag) next_a = st;
+      else if ((rc = ooc_store(c, v.i, v.j, st))) return rc;
+    }
+    sa = next_a;
+  }
+  enqueue_prefix(c);
+  cudaEventRecord(c->ev_join, o.s_d2h);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
   end(c, user);
   CUDA_TRY(cudaGetLastError());
@@ -493,6 +876,11 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
     info->d2h_bytes = c->d2h;
     info->kernel_launches = c->launches;
     info->device_ms = ms;
+    info->ooc_blocks = c->ooc ? c->o.nb : 0;
+    info->ooc_block = c->ooc ? c->o.b : 0;
+    info->ooc_reads = c->ooc ? c->o.reads : 0;
+    info->ooc_writes = c->ooc ? c->o.writes : 0;
+    info->ooc_scratch = c->ooc ? (int64_t)c->o.written.size() : 0;
     info->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - c->t0).count();
   }
@@ -517,61 +905,6 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
   return B2D_OK;
 }
 
-// ---------------------------------------------------------------- reference tiling bookkeeping
-
-static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-
-static void ref_layout(int64_t m, int64_t nb, int64_t* n_b, int64_t* b, int64_t* tail) {
-  // layout.py:35-51
-  nb = std::min(nb, m);
-  for (;;) {
-    const int64_t bb = 1 + (m - 1) / nb;
-    const int64_t need = ceil_div(m, bb);
-    if (need == nb) {
-      *n_b = nb;
-      *b = bb;
-      *tail = m - (nb - 1) * bb;
-      return;
-    }
-    nb = need;
-  }
-}
-
-static int64_t isqrt_u(unsigned __int128 x) {
-  unsigned __int128 r = 0, bit = (unsigned __int128)1 << 126;
-  while (bit > x) bit >>= 2;
-  while (bit) {
-    if (x >= r + bit) { x -= r + bit; r = (r >> 1) + bit; }
-    else r >>= 1;
-    bit >>= 2;
-  }
-  return (int64_t)r;
-}
-
-static int64_t ref_select_blocking(int64_t m, int64_t c, int64_t beta) {
-  // memdet.py:63-80 (exact integer arithmetic)
-  const unsigned __int128 msq = (unsigned __int128)m * m * beta;
-  if (msq <= (unsigned __int128)c) return 1;
-  if (3 * msq <= 4 * (unsigned __int128)c) return 2;
-  const unsigned __int128 target = 4 * msq;
-  int64_t q = isqrt_u(target / c);
-  while ((unsigned __int128)q * q * c < target) ++q;
-  return q;
-}
-
-static void fill_ref_info(b2d_run_info* info, int64_t m, int64_t num_blocks, int64_t max_mem, int esz) {
-  int64_t nb = num_blocks > 0 ? num_blocks : (max_mem > 0 ? ref_select_blocking(m, max_mem, esz) : 1);
-  int64_t n_b, b, tail;
-  ref_layout(m, nb, &n_b, &b, &tail);
-  info->n_b = n_b;
-  info->b = b;
-  info->tail = tail;
-  const int64_t n = n_b;
-  info->blocks_read = (2 * n * n * n - 3 * n * n + 7 * n) / 6;                       // cost.py:79-83
-  info->blocks_written = n <= 2 ? 0 : (n * n * n + 3 * n * n - 22 * n + 24) / 6;     // cost.py:86-92
-  info->scratch_slots = n <= 2 ? 0 : (n * n + n - 8) / 2;                            // cost.py:95-101
-}
-
 }  // namespace b2d
 
 using namespace b2d;
@@ -589,9 +922,15 @@ int b2d_device_count(void) {
 }
 
 int b2d_ctx_create(int device, int64_t m, int mode, b2d_ctx** out) {
+  return b2d_ctx_create_ex(device, m, mode, nullptr, out);
+}
+
+int b2d_ctx_is_out_of_core(b2d_ctx* ctx) { return ctx && ctx->ooc ? 1 : 0; }
+
+int b2d_ctx_create_ex(int device, int64_t m, int mode, const b2d_options* opt, b2d_ctx** out) {
   if (!out) return set_err(B2D_ERR_USAGE, "null out pointer");
   Ctx* c = nullptr;
-  int rc = create(device, m, mode, &c);
+  int rc = create(device, m, mode, opt, &c);
   if (rc) return rc;
   *out = static_cast<b2d_ctx*>(c);
   return B2D_OK;
@@ -653,7 +992,10 @@ int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, i
     return set_err(B2D_ERR_USAGE, "budget %lld B below minimum %d B", (long long)max_mem, 3 * esz);
   auto t0 = std::chrono::steady_clock::now();
   Ctx* c = nullptr;
-  int rc = create(device, m, mode, &c);
+  b2d_options opt{};
+  opt.num_blocks = num_blocks;
+  opt.max_mem = max_mem;
+  int rc = create(device, m, mode, &opt, &c);
   if (rc) return rc;
   rc = factor_host(c, a, lda, dtype, 0);
   b2d_run_info local{};

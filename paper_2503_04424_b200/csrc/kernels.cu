@@ -64,6 +64,42 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_tiles_kernel(const Tin* __r
   }
 }
 
+// Out-of-core block ingest: one 128-row strip of the row-major file (rows = the block's
+// tile-column J, columns = the block's rows) into tile-column J of a grid block.  Local row R
+// of the block is valid below rows_valid, local column C below cols_valid; the padding is the
+// identity on a diagonal block and zero elsewhere.  src points at element (first strip row,
+// first block row) of the file, leading dimension lda.
+template <typename Tin>
+__global__ void __launch_bounds__(PACK_THREADS) pack_block_kernel(const Tin* __restrict__ src,
+                                                                  int64_t lda, int64_t rows_valid,
+                                                                  int64_t cols_valid, int diag,
+                                                                  TileMap out, int J) {
+  extern __shared__ double sm[];
+  const int I = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
+  double* dst = out.tile(I, J);
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll 8
+    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
+      const int c = idx >> 7, r = idx & 127;
+      const int64_t R = R0 + r, C = C0 + 64 * half + c;
+      double v;
+      if (R < rows_valid && C < cols_valid) v = (double)src[(C - C0) * lda + R];
+      else v = (diag && R == C) ? 1.0 : 0.0;
+      sm[c * 129 + r] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int o = tid; o < 64 * T; o += PACK_THREADS) {
+      const int r = (o >> 3) & 127;
+      const int c = ((o >> 10) << 3) + iperm8(o & 7);
+      dst[half * 64 * T + o] = sm[c * 129 + r];
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------ potrf + inverse
 
 // One CTA of 256 threads factors diagonal tile (k, k) in shared memory M[128][129].
@@ -108,19 +144,20 @@ __device__ __forceinline__ void factor_diag8(double* M, double* dinv, int c0) {
     for (int c = 0; c <= r; ++c) M[(c0 + r) * MLD + c0 + c] = a[r][c];
 }
 
-__global__ void __launch_bounds__(POTRF_THREADS) potrf_inv_kernel(double* __restrict__ tiles, int nt,
-                                                                  int k, double* __restrict__ inv,
+// tile: the diagonal tile; g0: global index of its first row (ell/diag/fail), m: global order
+__global__ void __launch_bounds__(POTRF_THREADS) potrf_inv_kernel(double* __restrict__ tile,
+                                                                  double* __restrict__ inv,
                                                                   double* __restrict__ ell,
                                                                   double* __restrict__ diag,
                                                                   unsigned long long* __restrict__ fail,
-                                                                  int64_t m, long long* prof = nullptr) {
+                                                                  int64_t g0, int64_t m,
+                                                                  long long* prof = nullptr) {
 #define PROF(i) if (prof && tid == 0) prof[i] = clock64();
   extern __shared__ double M[];   // [T][MLD], then S[8][T] scratch
   double* S = M + T * MLD;
   __shared__ double dinv[T];
   const int tid = threadIdx.x;
   PROF(0)
-  double* tile = tiles + tile_index(k, k, nt) * TILE_ELEMS;
   {
     double2 v[TILE_ELEMS / 2 / POTRF_THREADS];  // all 32 loads in flight
 #pragma unroll
@@ -289,7 +326,7 @@ __global__ void __launch_bounds__(POTRF_THREADS) potrf_inv_kernel(double* __rest
   if (tid < T) {
     // pivots: log, diagonal, and the NotSpd check, off the serial chain
     const int r = tid;
-    const int64_t g = (int64_t)k * T + r;
+    const int64_t g = g0 + r;
     const double l = M[r * MLD + r];
     if (!(l > 0.0) && g < m) atomicMin(fail, (unsigned long long)g);
     ell[g] = 2.0 * log(l);
@@ -323,13 +360,11 @@ __device__ __forceinline__ double neg(double x) {
 }
 
 struct GemmTask {
-  double* tiles;
-  const double* binv;  // MODE_TRSM: L_kk^{-1} tile
-  int nt;
-  int j0, j1;     // output tile-columns [j0, j1)
-  int row_off;    // output rows i in [j + row_off, nt)
-  int p0, p1;     // K tile-columns (MODE_UPDATE)
-  int k;          // MODE_TRSM panel column
+  TileMap a, b, c;      // A(i, p), B(j, p), C(i, j); MODE_TRSM: A = C = c at (i, k)
+  const double* binv;   // MODE_TRSM: L_kk^{-1} tile (B operand)
+  TileSet out;          // output tiles
+  int p0, p1;           // K tile-columns (MODE_UPDATE)
+  int k;                // MODE_TRSM panel column
 };
 
 constexpr int KC = 16;                  // columns per pipeline stage (two octets)
@@ -349,7 +384,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
 
   // output tile (i, j) of this CTA, in L2-friendly super-tile order
   int i, j;
-  tile_order(blockIdx.x, t.nt, t.j0, t.j1, t.row_off, RASTER_G, &i, &j);
+  tile_order(blockIdx.x, t.out, RASTER_G, &i, &j);
   const int jout = (MODE == MODE_TRSM) ? t.k : j;
   const int nchunks = (MODE == MODE_TRSM) ? (T / KC) : (t.p1 - t.p0) * (T / KC);
 
@@ -372,13 +407,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
         const double* ga;
         const double* gb;
         if (MODE == MODE_TRSM) {
-          ga = t.tiles + tile_index(i, t.k, t.nt) * TILE_ELEMS + c * STAGE_ELEMS;
+          ga = t.c.tile(i, t.k) + c * STAGE_ELEMS;
           gb = t.binv + c * STAGE_ELEMS;
         } else {
           const int p = t.p0 + c / (T / KC);
           const int off = (c % (T / KC)) * STAGE_ELEMS;
-          ga = t.tiles + tile_index(i, p, t.nt) * TILE_ELEMS + off;
-          gb = t.tiles + tile_index(j, p, t.nt) * TILE_ELEMS + off;
+          ga = t.a.tile(i, p) + off;
+          gb = t.b.tile(j, p) + off;
         }
         mbar_arrive_expect_tx(&full[s], 2 * STAGE_ELEMS * 8);
         bulk_g2s(sA + s * STAGE_ELEMS, ga, STAGE_ELEMS * 8, &full[s]);
@@ -390,7 +425,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
 
   // ---------------- consumers: 8 warps, warp tile 64 x 32, DMMA m8n8k4
   const int wm = warp >> 2, wn = warp & 3;
-  double* C = t.tiles + tile_index(i, jout, t.nt) * TILE_ELEMS;
+  double* C = t.c.tile(i, jout);
   // MODE_UPDATE: the accumulators start as the C tile (64 independent loads issued before the
   // first stage lands, so their latency hides under the pipeline fill) and the B fragments are
   // negated, giving acc = C - A B^T with a store-only epilogue.

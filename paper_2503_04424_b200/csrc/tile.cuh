@@ -38,28 +38,50 @@ __host__ __device__ __forceinline__ int64_t n_packed_tiles(int nt) {
   return (int64_t)nt * (nt + 1) / 2;
 }
 
-// Output-tile order of a GEMM launch over the trapezoid {(i, j): j0 <= j < j1, j + row_off <= i < nt}.
-// CTAs walk column bands of G tiles; inside a band, the triangular head first, then row
-// blocks of G rows (column-major inside a block), so a wave of ~148 CTAs touches ~2-3 G x G
-// super-tiles and its A/B panel tiles stay L2-resident.  Bijective (tests/test_tile_order.py).
-__host__ __device__ inline void tile_order(int64_t b, int nt, int j0, int j1, int row_off, int G,
-                                           int* out_i, int* out_j) {
-  for (int jb0 = j0; jb0 < j1; jb0 += G) {
-    const int wb = (j1 - jb0) < G ? (j1 - jb0) : G;
-    const int head_end = jb0 + wb;  // rows [.., head_end) form the band's triangular head
+// Where a tile lives: the packed lower triangle (packed_nt > 0) or a row-major grid of tiles
+// with `ld` tiles per row (out-of-core blocks).
+struct TileMap {
+  double* base;
+  int64_t ld;
+  int packed_nt;
+  __host__ __device__ __forceinline__ double* tile(int i, int j) const {
+    return base + (packed_nt > 0 ? tile_index(i, j, packed_nt) : (int64_t)i * ld + j) * TILE_ELEMS;
+  }
+};
+
+// Output-tile set of a GEMM launch: columns j in [j0, j1), rows i in [lo(j), i1) with
+// lo(j) = max(i0, j + row_off) when `lower`, else i0.
+// CTAs walk column bands of G tiles; inside a band the triangular head first (rows below the
+// band's last lo), then row blocks of G rows (column-major inside a block), so a wave of ~148
+// CTAs touches ~2-3 G x G super-tiles and its A/B operand tiles stay L2-resident.
+// Bijective onto the set (tests/test_tile_order.py).
+struct TileSet {
+  int i0, i1, j0, j1, lower, row_off;
+  __host__ __device__ __forceinline__ int lo(int j) const {
+    if (!lower) return i0;
+    return (j + row_off) > i0 ? (j + row_off) : i0;
+  }
+  __host__ __device__ inline int64_t count() const {
+    int64_t n = 0;
+    for (int j = j0; j < j1; ++j) n += i1 > lo(j) ? i1 - lo(j) : 0;
+    return n;
+  }
+};
+
+__host__ __device__ inline void tile_order(int64_t b, const TileSet& s, int G, int* out_i, int* out_j) {
+  for (int jb0 = s.j0; jb0 < s.j1; jb0 += G) {
+    const int wb = (s.j1 - jb0) < G ? (s.j1 - jb0) : G;
+    int head_end = s.lo(jb0 + wb - 1);
+    if (head_end > s.i1) head_end = s.i1;
     int64_t tri = 0;
-    for (int j = jb0; j < jb0 + wb; ++j) {
-      const int lo = j + row_off, hi = head_end < nt ? head_end : nt;
-      tri += hi > lo ? hi - lo : 0;
-    }
-    const int64_t rows = nt > head_end ? nt - head_end : 0;
+    for (int j = jb0; j < jb0 + wb; ++j) tri += head_end > s.lo(j) ? head_end - s.lo(j) : 0;
+    const int64_t rows = s.i1 > head_end ? s.i1 - head_end : 0;
     const int64_t band = tri + rows * wb;
     if (b >= band) { b -= band; continue; }
     if (b < tri) {
       for (int j = jb0; j < jb0 + wb; ++j) {
-        const int lo = j + row_off, hi = head_end < nt ? head_end : nt;
-        const int cnt = hi > lo ? hi - lo : 0;
-        if (b < cnt) { *out_i = lo + (int)b; *out_j = j; return; }
+        const int cnt = head_end > s.lo(j) ? head_end - s.lo(j) : 0;
+        if (b < cnt) { *out_i = s.lo(j) + (int)b; *out_j = j; return; }
         b -= cnt;
       }
     }

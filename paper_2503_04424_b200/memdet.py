@@ -114,8 +114,10 @@ class RunInfo:
     """Reference RunInfo fields (memdet.py:180-198) plus engine diagnostics.
 
     blocks_read / blocks_written / scratch_slots are the reference schedule's counts for the
-    reported n_b (cost.py:79-101) — the engine itself keeps the matrix resident in HBM and
-    moves h2d_bytes / d2h_bytes over PCIe instead."""
+    reported n_b (cost.py:79-101).  In-core runs keep the matrix resident in HBM and move
+    h2d_bytes / d2h_bytes over PCIe instead; out-of-core runs walk the reference schedule on
+    an ooc_blocks grid and report the block transfers they actually made (ooc_reads /
+    ooc_writes / ooc_scratch — equal to the reference counters when ooc_blocks == n_b)."""
 
     m: int
     case: str
@@ -131,6 +133,12 @@ class RunInfo:
     kernel_launches: int = 0
     engine_tile: int = 128
     engine: str = "b200-sm100a"
+    out_of_core: bool = False
+    ooc_blocks: int = 0
+    ooc_block: int = 0
+    ooc_reads: int = 0
+    ooc_writes: int = 0
+    ooc_scratch: int = 0
 
     def to_json_dict(self) -> dict:
         return {k: getattr(self, k) for k in self.__dataclass_fields__}
@@ -201,15 +209,20 @@ _ctx_cache: dict = {}
 _ctx_lock = threading.Lock()
 
 
-def _context(m: int, mode: int, device: int) -> _native.Context:
-    key = (device, m, mode)
+def _context(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
+             out_of_core=None) -> _native.Context:
+    kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
+              max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core))
+    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"])
     with _ctx_lock:
-        ctx = _ctx_cache.get(key)
-        if ctx is None:
-            for k in list(_ctx_cache):
-                _ctx_cache.pop(k).close()
-            ctx = _native.Context(m, mode, device)
-            _ctx_cache[key] = ctx
+        ctx = _ctx_cache.get(base)
+        # an in-core plan ignores the reference tiling; an out-of-core one is built from it
+        if ctx is not None and (not ctx.out_of_core or ctx.key[4:6] == (kw["num_blocks"], kw["max_mem"])):
+            return ctx
+        for k in list(_ctx_cache):
+            _ctx_cache.pop(k).close()
+        ctx = _native.Context(m, mode, device, **kw)
+        _ctx_cache[base] = ctx
         return ctx
 
 
@@ -220,17 +233,22 @@ def release_engine_cache():
             _ctx_cache.pop(k).close()
 
 
-def _run_engine(src: MatrixSource, mode: int, device: int):
+def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max_mem, hbm_budget,
+                out_of_core):
     dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
     m = src.m
+    # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
+    ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
     if src.device_ptr is not None:
+        if out_of_core:
+            raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
         ctx = _context(m, mode, src.device_index)
         import torch
 
         stream = torch.cuda.current_stream(src.device_index).cuda_stream
         ctx.factor_device_async(src.device_ptr, src.lda, dcode, stream)
     else:
-        ctx = _context(m, mode, device)
+        ctx = _context(m, mode, device, **ooc_kw)
         a, lda = src.host_rowmajor()
         ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
     d = np.empty(m, np.float64)
@@ -240,16 +258,17 @@ def _run_engine(src: MatrixSource, mode: int, device: int):
         raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
                           f"(global pivot {fail})")
     _native.check(rc, "memdet engine")
-    return d, prefix, info
+    return d, prefix, info, ctx.out_of_core
 
 
-def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume):
+def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
+            out_of_core=None):
     t0 = time.perf_counter()
     src = MatrixSource(matrix, assume)
     if src.symmetry == "generic":
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
-    d, prefix, cinfo = _run_engine(src, mode, device)
+    d, prefix, cinfo, ooc = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core)
     nb = lay.n_b
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
                    blocks_read=predicted_reads(nb, "symmetric"),
@@ -257,19 +276,26 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume):
                    scratch_slots=scratch_slots(nb, "symmetric"),
                    wall_seconds=time.perf_counter() - t0, device_ms=float(cinfo.device_ms),
                    h2d_bytes=int(cinfo.h2d_bytes), d2h_bytes=int(cinfo.d2h_bytes),
-                   kernel_launches=int(cinfo.kernel_launches), engine_tile=int(cinfo.tile))
+                   kernel_launches=int(cinfo.kernel_launches), engine_tile=int(cinfo.tile),
+                   out_of_core=ooc, ooc_blocks=int(cinfo.ooc_blocks), ooc_block=int(cinfo.ooc_block),
+                   ooc_reads=int(cinfo.ooc_reads), ooc_writes=int(cinfo.ooc_writes),
+                   ooc_scratch=int(cinfo.ooc_scratch))
     return d, prefix.astype(src.dtype, copy=False), info
 
 
 def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
-                    device: int = 0, assume: str | None = None) -> SpdResult:
+                    device: int = 0, assume: str | None = None, hbm_budget: int | None = None,
+                    out_of_core: bool | None = None) -> SpdResult:
     """Prefix log-determinants of an SPD matrix (blocked Cholesky, no pivoting).
 
     prefix[q-1] = logdet of the leading q x q principal submatrix, summed from 2 log L_ii;
-    NotSpdError on the first non-positive leading minor.  `scratch_dir` is accepted for
-    signature parity; the in-core engine needs no scratchpad."""
+    NotSpdError on the first non-positive leading minor.  A matrix whose packed lower triangle
+    exceeds `hbm_budget` (default: free HBM) — or any host matrix with out_of_core=True — runs
+    the reference's out-of-core tile walk, blocks streamed between host memory and HBM (the
+    scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity)."""
     del scratch_dir
-    d, prefix, info = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume)
+    d, prefix, info = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
+                              hbm_budget, out_of_core)
     res = SpdResult(prefix=prefix, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:
@@ -278,7 +304,8 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
 
 
 def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
-               device: int = 0, assume: str | None = None, pivoting: str = "block") -> SymmetricResult:
+               device: int = 0, assume: str | None = None, pivoting: str = "block",
+               hbm_budget: int | None = None, out_of_core: bool | None = None) -> SymmetricResult:
     """Prefix log-determinants of a symmetric matrix via blocked LDL^T.
 
     pivoting="block" reproduces the reference's block-local 1x1 diagonal pivoting
@@ -290,7 +317,8 @@ def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefi
     if pivoting not in ("block", "none"):
         raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
     mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
-    d, prefix, info = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume)
+    d, prefix, info = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
+                              out_of_core)
     m = len(prefix)
     if mode == _native.MODE_LDL_NOPIV:
         perm = np.arange(m, dtype=np.int64)

@@ -165,3 +165,50 @@ def test_c2_full_size_vs_independent_gpu_factorisation():
     assert rel_err(res.prefix, ref) <= 1e-10, rel_err(res.prefix, ref)
     small = eng.memdet_cholesky(a[:4096, :4096].contiguous(), num_blocks=1)
     assert rel_err(res.prefix[:4096], small.prefix) <= 1e-12
+
+
+# ------------------------------------------------------------------ out-of-core block streamer
+
+
+@pytest.mark.parametrize("m,nb", [(700, 3), (1000, 4), (1536, 4), (2000, 5), (640, 1), (900, 2)])
+def test_out_of_core_matches_oracle_and_reference_counters(m, nb):
+    """Forced out-of-core: the reference tile walk over HBM slots; every prefix matches the
+    oracle and the block transfers equal the reference's own counters (cost.py:79-101)."""
+    a = gen.spd_wishart(m, m, seed=100 + m, shift=1e-2)
+    res = eng.memdet_cholesky(a, num_blocks=nb, out_of_core=True)
+    ref, info = O.memdet_cholesky(a, nb)
+    assert res.info.out_of_core
+    assert rel_err(res.prefix, ref) <= 1e-10, rel_err(res.prefix, ref)
+    assert res.info.ooc_blocks == info.n_b
+    assert (res.info.ooc_reads, res.info.ooc_writes, res.info.ooc_scratch) == \
+        (info.blocks_read, info.blocks_written, info.scratch_slots)
+    # and the same numbers as the in-core engine, to rounding
+    inc = eng.memdet_cholesky(a, num_blocks=nb)
+    assert not inc.info.out_of_core
+    assert rel_err(res.prefix, inc.prefix) <= 1e-12
+
+
+def test_out_of_core_golden_c1(golden):
+    """C1 (n=4096, num_blocks=4) through the out-of-core streamer vs the reference's prefixes."""
+    inp = golden.input("C1")
+    ref = golden.run("C1", "chol_nb4")
+    res = eng.memdet_cholesky(inp, num_blocks=4, out_of_core=True)
+    assert rel_err(res.prefix, ref["prefix"]) <= 1e-10
+    assert (res.info.ooc_reads, res.info.ooc_writes, res.info.ooc_scratch) == \
+        (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
+
+
+def test_out_of_core_budget_planner_grows_grid():
+    """A tiny HBM budget forces a finer grid than the requested num_blocks; results unchanged."""
+    a = gen.rbf(1500, seed=8)
+    res = eng.memdet_cholesky(a, num_blocks=2, hbm_budget=20 << 20,
+                              out_of_core=True)
+    assert res.info.ooc_blocks > 2
+    ref, _ = O.memdet_cholesky(a, 2)
+    assert rel_err(res.prefix, ref) <= 1e-10
+
+
+def test_out_of_core_not_spd():
+    a = gen.random_symmetric(500, seed=3)
+    with pytest.raises(eng.NotSpdError):
+        eng.memdet_cholesky(a, num_blocks=3, out_of_core=True)
