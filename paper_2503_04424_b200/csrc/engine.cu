@@ -80,6 +80,7 @@ struct Ooc {
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
   std::map<std::pair<int, int>, cudaEvent_t> ev_key;  // last store of each scratch block
+  std::vector<double*> pool;                       // pinned scratch slots, bound in first-write order
   std::set<std::pair<int, int>> written;           // cache table of the current run
   int64_t reads = 0, writes = 0;
   int rr = 0;
@@ -170,7 +171,7 @@ static void destroy(Ctx* c) {
     if (o.ev_stored[s]) cudaEventDestroy(o.ev_stored[s]);
   }
   cudaFree(o.stage);
-  for (auto& kv : o.scratch) cudaFreeHost(kv.second);
+  for (double* h : o.pool) cudaFreeHost(h);
   for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
   if (o.s_h2d) cudaStreamDestroy(o.s_h2d);
   if (o.s_d2h) cudaStreamDestroy(o.s_d2h);
@@ -349,6 +350,17 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     ALLOC(o.stage, (size_t)T * o.nbt * T * 8);
     ALLOC(c->inv, (size_t)o.nbt * TILE_BYTES);
+    // pinned scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front
+    const int64_t nsc = o.nb <= 2 ? 0 : ((int64_t)o.nb * o.nb + o.nb - 8) / 2;
+    for (int64_t q = 0; q < nsc; ++q) {
+      double* h = nullptr;
+      if (cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault) != cudaSuccess) {
+        destroy(c);
+        return set_err(B2D_ERR_NOMEM, "pinned scratchpad of %lld x %.2f GB failed", (long long)nsc,
+                       o.slot_bytes() / 1e9);
+      }
+      o.pool.push_back(h);
+    }
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&o.s_h2d, cudaStreamNonBlocking, hi);
@@ -706,9 +718,10 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
   auto key = std::make_pair(ri, rj);
   auto it = o.scratch.find(key);
   if (it == o.scratch.end()) {
-    double* h = nullptr;
-    CUDA_TRY(cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault));
-    it = o.scratch.emplace(key, h).first;
+    // slots are bound in first-write order and never reassigned (storage.py:167-181)
+    if (o.scratch.size() >= o.pool.size())
+      return set_err(B2D_ERR_CUDA, "scratchpad full (%zu slots) writing block (%d, %d)", o.pool.size(), ri, rj);
+    it = o.scratch.emplace(key, o.pool[o.scratch.size()]).first;
   }
   cudaStreamWaitEvent(o.s_d2h, o.ev_used[s], 0);
   CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDeviceToHost, o.s_d2h));
