@@ -123,6 +123,41 @@ const double *b2d_ctx_device_prefix(b2d_ctx *ctx);
 int b2d_ctx_set_profiling(b2d_ctx *ctx, int on);
 int b2d_ctx_update_stats(b2d_ctx *ctx, double *flops, double *ms, int64_t *launches);
 
+/* Tile-level device API, the building blocks of multi-GPU drivers (paper_2503_04424_b200/
+ * distributed.py).  All pointers are DEVICE pointers; work is enqueued on `stream` and not
+ * waited for.  Tiles are 128 x 128 doubles in the engine's octet layout.
+ *   b2d_tilemap: tile (i, j) lives at base + r*ld + j tiles, r = i, or with rmod > 0
+ *                r = (i % rmod) * rstride + i / rmod (row-cyclic blocks gathered from ranks);
+ *                packed_nt > 0 selects the packed lower triangle instead.
+ *   b2d_tileset: columns [j0, j1), rows [lo(j), i1), lo = i0, or with lower = 1
+ *                lo(j) = max(i0, ceil((j + row_off - off) / stride)) (rows may be local indices
+ *                of a row-cyclic distribution, global row = i * stride + off). */
+typedef struct b2d_tilemap {
+  double *base;
+  int64_t ld;
+  int32_t packed_nt;
+  int32_t rmod;
+  int64_t rstride;
+} b2d_tilemap;
+typedef struct b2d_tileset {
+  int32_t i0, i1, j0, j1, lower, row_off, stride, off;
+} b2d_tileset;
+/* Diagonal tile: Cholesky in place (L, zero upper), inv = L^{-1}, ell[g0+r] = 2 log L_rr,
+ * diag[g0+r] = L_rr, *fail = min(*fail, first global row g < m with a non-positive pivot). */
+int b2d_tile_potrf_inv(double *tile, double *inv, double *ell, double *diag, uint64_t *fail,
+                       int64_t g0, int64_t m, void *stream);
+/* mode 0: C(i,j) -= sum_{p in [p0,p1)} A(i,p) B(j,p)^T over the tile set (Schur update);
+ * mode 1: C(i,k) = C(i,k) binv^T over the tile set's rows (panel solve, k = column). */
+int b2d_tile_gemm(int mode, const b2d_tilemap *a, const b2d_tilemap *b, const b2d_tilemap *c,
+                  const double *binv, const b2d_tileset *out, int32_t p0, int32_t p1, int32_t k,
+                  void *stream);
+/* Pack the set's tiles from a row-major DEVICE matrix (f64/f32, leading dimension lda, first
+ * stored row row_base; only the row-major upper tile triangle is read, identity beyond m). */
+int b2d_pack_tiles(const void *src, int64_t lda, int dtype, int64_t row_base, int64_t m,
+                   const b2d_tilemap *out, const b2d_tileset *set, void *stream);
+/* prefix[q] = sum_{g <= q} ell[g] (double-double, rounded once), q < m. */
+int b2d_prefix_scan(const double *ell, int64_t m, double *prefix, void *stream);
+
 /* FP64 roofline calibration (off the timed path): sustained DMMA m8n8k4 rate over every SM for
  * about `seconds`, in TFLOP/s (2 flops per FMA). */
 int b2d_probe_fp64_peak(int device, double seconds, double *tflops);

@@ -40,6 +40,15 @@ class OptionsC(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+class TileMapC(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("ld", ctypes.c_int64), ("packed_nt", ctypes.c_int32),
+                ("rmod", ctypes.c_int32), ("rstride", ctypes.c_int64)]
+
+
+class TileSetC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("i0", "i1", "j0", "j1", "lower", "row_off", "stride", "off")]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
@@ -64,6 +73,13 @@ SIGNATURES = {
     "b2d_ctx_update_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "b2d_gen_rbf": (_I, [_P, _I64, _I, _D, _D, _P, _P]),
     "b2d_probe_fp64_peak": (_I, [_I, _D, ctypes.POINTER(_D)]),
+    "b2d_tile_potrf_inv": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
+    "b2d_tile_gemm": (_I, [_I, ctypes.POINTER(TileMapC), ctypes.POINTER(TileMapC),
+                           ctypes.POINTER(TileMapC), _P, ctypes.POINTER(TileSetC), ctypes.c_int32,
+                           ctypes.c_int32, ctypes.c_int32, _P]),
+    "b2d_pack_tiles": (_I, [_P, _I64, _I, _I64, _I64, ctypes.POINTER(TileMapC),
+                            ctypes.POINTER(TileSetC), _P]),
+    "b2d_prefix_scan": (_I, [_P, _I64, _P, _P]),
 }
 
 _lib = None

@@ -133,6 +133,8 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   done = true;
   return B2D_OK;
 }
@@ -1071,6 +1073,77 @@ extern "C" int b2d_probe_fp64_peak(int device, double seconds, double* tflops) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(out);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+static TileMap to_map(const b2d_tilemap* m) {
+  return m ? TileMap{m->base, m->ld, m->packed_nt, m->rmod, m->rstride} : TileMap{nullptr, 0, 0, 0, 0};
+}
+static TileSet to_set(const b2d_tileset* t) {
+  return TileSet{t->i0, t->i1, t->j0, t->j1, t->lower, t->row_off, t->stride, t->off};
+}
+
+extern "C" int b2d_tile_potrf_inv(double* tile, double* inv, double* ell, double* diag, uint64_t* fail,
+                                  int64_t g0, int64_t m, void* stream) {
+  if (!tile || !inv || !ell || !diag || !fail) return set_err(B2D_ERR_USAGE, "null argument");
+  int rc = configure_kernels();
+  if (rc) return rc;
+  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, (cudaStream_t)stream>>>(
+      tile, inv, ell, diag, (unsigned long long*)fail, g0, m);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_tile_gemm(int mode, const b2d_tilemap* a, const b2d_tilemap* b, const b2d_tilemap* c,
+                             const double* binv, const b2d_tileset* out, int32_t p0, int32_t p1, int32_t k,
+                             void* stream) {
+  if (!c || !out || (mode == MODE_UPDATE && (!a || !b)) || (mode == MODE_TRSM && !binv) ||
+      (mode != MODE_UPDATE && mode != MODE_TRSM))
+    return set_err(B2D_ERR_USAGE, "bad b2d_tile_gemm arguments");
+  int rc = configure_kernels();
+  if (rc) return rc;
+  GemmTask t{};
+  t.a = to_map(a);
+  t.b = to_map(b);
+  t.c = to_map(c);
+  t.binv = binv;
+  t.out = to_set(out);
+  t.p0 = p0;
+  t.p1 = p1;
+  t.k = k;
+  const int64_t n = t.out.count();
+  if (n <= 0 || (mode == MODE_UPDATE && p1 <= p0)) return B2D_OK;
+  if (mode == MODE_UPDATE)
+    gemm_kernel<MODE_UPDATE><<<(unsigned)n, GEMM_THREADS, GEMM_SMEM, (cudaStream_t)stream>>>(t);
+  else
+    gemm_kernel<MODE_TRSM><<<(unsigned)n, GEMM_THREADS, GEMM_SMEM, (cudaStream_t)stream>>>(t);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_pack_tiles(const void* src, int64_t lda, int dtype, int64_t row_base, int64_t m,
+                              const b2d_tilemap* out, const b2d_tileset* set, void* stream) {
+  if (!src || !out || !set || (dtype != B2D_F64 && dtype != B2D_F32))
+    return set_err(B2D_ERR_USAGE, "bad b2d_pack_tiles arguments");
+  int rc = configure_kernels();
+  if (rc) return rc;
+  const TileSet ts = to_set(set);
+  const int64_t n = ts.count();
+  if (n <= 0) return B2D_OK;
+  if (dtype == B2D_F64)
+    pack_set_kernel<double><<<(unsigned)n, PACK_THREADS, PACK_SMEM, (cudaStream_t)stream>>>(
+        (const double*)src, lda, row_base, m, to_map(out), ts);
+  else
+    pack_set_kernel<float><<<(unsigned)n, PACK_THREADS, PACK_SMEM, (cudaStream_t)stream>>>(
+        (const float*)src, lda, row_base, m, to_map(out), ts);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_prefix_scan(const double* ell, int64_t m, double* prefix, void* stream) {
+  if (!ell || !prefix || m < 1) return set_err(B2D_ERR_USAGE, "bad b2d_prefix_scan arguments");
+  prefix_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ell, m, prefix);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
 }

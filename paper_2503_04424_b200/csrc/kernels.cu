@@ -64,6 +64,42 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_tiles_kernel(const Tin* __r
   }
 }
 
+// Distributed ingest: the tiles of a TileSet (rows possibly local indices of a row-cyclic
+// distribution, global row = i * stride + off) from a row-major source (first stored row
+// row_base) into map `out` at (local row, column).  Same element rule as pack_tiles_kernel.
+template <typename Tin>
+__global__ void __launch_bounds__(PACK_THREADS) pack_set_kernel(const Tin* __restrict__ src, int64_t lda,
+                                                                int64_t row_base, int64_t m, TileMap out,
+                                                                TileSet set) {
+  extern __shared__ double sm[];
+  int li, J;
+  tile_order(blockIdx.x, set, 1, &li, &J);
+  const int st = set.stride > 1 ? set.stride : 1;
+  const int I = li * st + set.off;
+  const int tid = threadIdx.x;
+  const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
+  double* dst = out.tile(li, J);
+  for (int half = 0; half < 2; ++half) {
+#pragma unroll 8
+    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
+      const int c = idx >> 7, r = idx & 127;
+      const int64_t R = R0 + r, C = C0 + 64 * half + c;
+      double v;
+      if (R < m && C < m) v = (double)src[(C - row_base) * lda + R];
+      else v = (R == C) ? 1.0 : 0.0;
+      sm[c * 129 + r] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int o = tid; o < 64 * T; o += PACK_THREADS) {
+      const int r = (o >> 3) & 127;
+      const int c = ((o >> 10) << 3) + iperm8(o & 7);
+      dst[half * 64 * T + o] = sm[c * 129 + r];
+    }
+    __syncthreads();
+  }
+}
+
 // Out-of-core block ingest: one 128-row strip of the row-major file (rows = the block's
 // tile-column J, columns = the block's rows) into tile-column J of a grid block.  Local row R
 // of the block is valid below rows_valid, local column C below cols_valid; the padding is the

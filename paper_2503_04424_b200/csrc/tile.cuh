@@ -40,26 +40,38 @@ __host__ __device__ __forceinline__ int64_t n_packed_tiles(int nt) {
 
 // Where a tile lives: the packed lower triangle (packed_nt > 0) or a row-major grid of tiles
 // with `ld` tiles per row (out-of-core blocks).
+// A third form serves row-cyclic storage gathered from several ranks: with rmod > 0, tile row
+// i lives at grid row (i % rmod) * rstride + i / rmod (rank-major blocks of rstride rows).
 struct TileMap {
   double* base;
   int64_t ld;
   int packed_nt;
+  int rmod;
+  int64_t rstride;
   __host__ __device__ __forceinline__ double* tile(int i, int j) const {
-    return base + (packed_nt > 0 ? tile_index(i, j, packed_nt) : (int64_t)i * ld + j) * TILE_ELEMS;
+    if (packed_nt > 0) return base + tile_index(i, j, packed_nt) * TILE_ELEMS;
+    const int64_t r = rmod > 0 ? (int64_t)(i % rmod) * rstride + i / rmod : (int64_t)i;
+    return base + (r * ld + j) * TILE_ELEMS;
   }
 };
 
 // Output-tile set of a GEMM launch: columns j in [j0, j1), rows i in [lo(j), i1) with
-// lo(j) = max(i0, j + row_off) when `lower`, else i0.
+// lo(j) = max(i0, j + row_off) when `lower`, else i0.  Rows may be local indices of a
+// row-cyclic distribution (global row = i * stride + off; stride 0 means 1): then `lower`
+// keeps global rows >= j + row_off, i.e. lo(j) = max(i0, ceil((j + row_off - off) / stride)).
 // CTAs walk column bands of G tiles; inside a band the triangular head first (rows below the
 // band's last lo), then row blocks of G rows (column-major inside a block), so a wave of ~148
 // CTAs touches ~2-3 G x G super-tiles and its A/B operand tiles stay L2-resident.
 // Bijective onto the set (tests/test_tile_order.py).
 struct TileSet {
   int i0, i1, j0, j1, lower, row_off;
+  int stride, off;
   __host__ __device__ __forceinline__ int lo(int j) const {
     if (!lower) return i0;
-    return (j + row_off) > i0 ? (j + row_off) : i0;
+    const int x = j + row_off - off;
+    const int st = stride > 1 ? stride : 1;
+    const int l = x <= 0 ? -((-x) / st) : (x + st - 1) / st;
+    return l > i0 ? l : i0;
   }
   __host__ __device__ inline int64_t count() const {
     int64_t n = 0;

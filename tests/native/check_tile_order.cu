@@ -11,11 +11,15 @@ int main() {
         for (int lower = 0; lower <= 1; ++lower)
           for (int row_off = 0; row_off <= 1; ++row_off)
             for (int i0 : {0, 3})
-              for (int G : {1, 3, 8}) {
-                b2d::TileSet ts{i0, nt, j0, j1, lower, row_off};
+              for (int G : {1, 3, 8})
+               for (int stride : {0, 2, 3})
+                for (int off = 0; off < (stride > 1 ? stride : 1); ++off) {
+                b2d::TileSet ts{i0, nt, j0, j1, lower, row_off, stride, off};
                 std::set<std::pair<int, int>> want, got;
+                const int st = stride > 1 ? stride : 1;
                 for (int j = j0; j < j1; ++j)
-                  for (int i = ts.lo(j); i < nt; ++i) want.insert({i, j});
+                  for (int i = i0; i < nt; ++i)
+                    if (!lower || i * st + off >= j + row_off) want.insert({i, j});
                 if ((long)want.size() != ts.count()) ++bad;
                 for (long b = 0; b < (long)want.size(); ++b) {
                   int i, j;
