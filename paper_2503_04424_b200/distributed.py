@@ -114,6 +114,7 @@ class CudaTileOps:
         self.prefix_buf = torch.empty(npad, **f64)
         self.fail = torch.empty(1, dtype=torch.int64, device=self.dev)
         self.lib = _native.load()
+        self.launches = 0  # engine kernels enqueued (potrf / gemm / pack / prefix calls)
 
     # -------------------------------------------------------------------- helpers
     def _stream(self):
@@ -139,6 +140,7 @@ class CudaTileOps:
                                               ctypes.byref(self._grid_map()),
                                               ctypes.byref(self._set(0, self.dist.nt)), self._stream()),
                       "b2d_pack_tiles")
+        self.launches += 1
 
     def begin(self):
         self.ell.zero_()
@@ -150,12 +152,14 @@ class CudaTileOps:
             ctypes.c_void_p(self._tile_ptr(li, p)), ctypes.c_void_p(self.inv.data_ptr()),
             ctypes.c_void_p(self.ell.data_ptr()), ctypes.c_void_p(self.diag.data_ptr()),
             ctypes.c_void_p(self.fail.data_ptr()), p * T, self.m, self._stream()), "potrf")
+        self.launches += 1
 
     def trsm(self, p: int):
         s = self._set(p, p + 1, row_off=1)
         _native.check(self.lib.b2d_tile_gemm(1, None, None, ctypes.byref(self._grid_map()),
                                              ctypes.c_void_p(self.inv.data_ptr()), ctypes.byref(s),
                                              0, 0, p, self._stream()), "trsm")
+        self.launches += 1
 
     def fill_diag_buffer(self, p: int, k0: int, ke: int):
         self.diag_buffer.zero_()
@@ -170,6 +174,7 @@ class CudaTileOps:
         g = self._grid_map()
         _native.check(self.lib.b2d_tile_gemm(0, ctypes.byref(g), ctypes.byref(bmap), ctypes.byref(g), None,
                                              ctypes.byref(s), p0, p1, 0, self._stream()), "update")
+        self.launches += 1
 
     def update_intra(self, p: int, k0: int, ke: int):
         # B(j, p) = diag_buffer[j - k0]: base shifted so tile(j, p) = base + (j + p) tiles
@@ -202,6 +207,7 @@ class CudaTileOps:
         _native.check(self.lib.b2d_prefix_scan(ctypes.c_void_p(self.ell.data_ptr()), self.m,
                                                ctypes.c_void_p(self.prefix_buf.data_ptr()), self._stream()),
                       "prefix")
+        self.launches += 1
         return self.prefix_buf[: self.m]
 
 
@@ -240,20 +246,32 @@ class TorchComm:
         self._run(gather, out, inp)
 
 
+class DistributedMemdet:
+    """Reusable per-rank workspace for repeated distributed factorisations of order m."""
+
+    def __init__(self, m: int, group=None, panel_tiles: int = 8, device=None):
+        import torch.distributed as dist_mod
+
+        self.group = group
+        self.m = m
+        self.panel_tiles = panel_tiles
+        self.dist = RowCyclic(-(-m // T), dist_mod.get_world_size(group), dist_mod.get_rank(group))
+        self.ops = CudaTileOps(self.dist, m, panel_tiles, device)
+        self.comm = TorchComm(group)
+
+    def run(self, a):
+        """Enqueue pack + factorisation of the CUDA row-major matrix `a` (every rank passes the
+        matrix; each packs its own tile rows).  Returns (device prefix view, fail)."""
+        self.ops.load(a)
+        return factor_distributed(self.ops, self.comm, self.dist, self.panel_tiles)
+
+
 def memdet_cholesky_distributed(a, group=None, panel_tiles: int = 8):
     """Distributed logdet of a CUDA row-major SPD matrix visible to every rank (each rank packs
     only its own tile rows).  Returns (prefix as a NumPy array, fail index) on every rank."""
     import torch
-    import torch.distributed as dist_mod
 
-    world = dist_mod.get_world_size(group)
-    rank = dist_mod.get_rank(group)
-    m = int(a.shape[0])
-    nt = -(-m // T)
-    dist = RowCyclic(nt, world, rank)
-    ops = CudaTileOps(dist, m, panel_tiles, a.device)
-    ops.load(a)
-
-    prefix, fail = factor_distributed(ops, TorchComm(group), dist, panel_tiles)
+    runner = DistributedMemdet(int(a.shape[0]), group, panel_tiles, a.device)
+    prefix, fail = runner.run(a)
     torch.cuda.synchronize(a.device)
     return prefix.cpu().numpy(), fail
