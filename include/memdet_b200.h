@@ -43,7 +43,8 @@ extern "C" {
 /* factorisation modes */
 #define B2D_MODE_CHOLESKY 0    /* memdet_cholesky: d = diag(L), prefix = cumsum 2 log d     */
 #define B2D_MODE_LDL_NOPIV 1   /* memdet_ldl without pivoting: d = L_ii^2, perm = identity  */
-#define B2D_MODE_LDL_PIV 2     /* memdet_ldl with block-local 1x1 pivots (_ldl.pyx:30-46)   */
+#define B2D_MODE_LDL_PIV 2     /* memdet_ldl with block-local 1x1 pivots (_ldl.pyx:30-46):
+                                  the reference's b x b block walk, d = D, perm = pivots    */
 
 typedef struct b2d_run_info {
   int64_t m;               /* matrix order                                                 */
@@ -114,6 +115,9 @@ int b2d_ctx_factor_host_async(b2d_ctx *ctx, const void *host_a, int64_t lda, int
 /* Wait for the enqueued work, check for failure, copy the outputs to host (any may be NULL). */
 int b2d_ctx_fetch(b2d_ctx *ctx, double *d_out, double *prefix_out, int64_t *fail_index,
                   b2d_run_info *info);
+/* The permutation of the last factorisation (block-local pivots offset by the block origin,
+ * memdet.py:352-353; identity for unpivoted modes), after b2d_ctx_fetch. */
+int b2d_ctx_fetch_perm(b2d_ctx *ctx, int64_t *perm_out);
 /* Device pointer of the prefix vector (m doubles), valid until the next factorisation. */
 const double *b2d_ctx_device_prefix(b2d_ctx *ctx);
 /* Dominant-kernel accounting (the trailing "rest" Schur-update GEMM launches of the last

@@ -69,6 +69,7 @@ SIGNATURES = {
     "b2d_ctx_factor_host_async": (_I, [_P, _P, _I64, _I, _P]),
     "b2d_ctx_fetch": (_I, [_P, _P, _P, ctypes.POINTER(_I64), ctypes.POINTER(RunInfoC)]),
     "b2d_ctx_device_prefix": (_P, [_P]),
+    "b2d_ctx_fetch_perm": (_I, [_P, _P]),
     "b2d_ctx_set_profiling": (_I, [_P, _I]),
     "b2d_ctx_update_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "b2d_gen_rbf": (_I, [_P, _I64, _I, _D, _D, _P, _P]),
@@ -176,6 +177,9 @@ class Context:
                                   None if prefix_out is None else prefix_out.ctypes.data,
                                   ctypes.byref(fail), ctypes.byref(info))
         return rc, fail.value, info
+
+    def fetch_perm(self, perm_out):
+        check(load().b2d_ctx_fetch_perm(self._h, perm_out.ctypes.data), "fetch_perm")
 
     def device_prefix_ptr(self) -> int:
         return load().b2d_ctx_device_prefix(self._h)

@@ -24,6 +24,7 @@
 
 #include "../../include/memdet_b200.h"
 #include "kernels.cu"
+#include "ldl.cu"
 
 namespace b2d {
 
@@ -57,7 +58,9 @@ static int panel_tiles_default() {
 
 constexpr int NSTAGE = 8;   // host-ingest staging strips in flight
 constexpr int BAND = 4;     // tile-columns per ingest band
-constexpr int NSLOT = 6;    // out-of-core: HBM block slots (A, B, C, T + two for prefetch)
+constexpr int NSLOT = 6;      // out-of-core: HBM block slots (A, B, C, T + two for prefetch)
+constexpr int NSLOT_LDL = 8;  // pivoted LDL: A, B (scaled), B (unscaled), C, T, two spare, permute temp
+constexpr int MAXSLOT = 8;
 
 // The lower tile triangle of an nt x nt tile matrix to factor in place: the whole packed
 // matrix (in-core) or one diagonal block slot (out-of-core).  g0 = global index of its row 0.
@@ -74,8 +77,18 @@ struct Ooc {
   int nb = 0;
   int64_t b = 0, tail = 0;
   int nbt = 0;
-  double* slot[NSLOT] = {};
-  cudaEvent_t ev_loaded[NSLOT] = {}, ev_used[NSLOT] = {}, ev_stored[NSLOT] = {};
+  int nslot = NSLOT;
+  double* slot[MAXSLOT] = {};
+  cudaEvent_t ev_loaded[MAXSLOT] = {}, ev_used[MAXSLOT] = {}, ev_stored[MAXSLOT] = {};
+  // pivoted LDL: dense diagonal block, pivots and permutations
+  double* dense = nullptr;
+  int64_t* swaps = nullptr;
+  int64_t* perm_local = nullptr;
+  int64_t* perm_global = nullptr;
+  double* dblk = nullptr;
+  void* part = nullptr;
+  unsigned long long* amax = nullptr;
+  int coop_blocks = 0;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
@@ -134,6 +147,7 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   done = true;
   return B2D_OK;
@@ -166,12 +180,19 @@ static void destroy(Ctx* c) {
   Ooc& o = c->o;
   if (o.s_h2d) cudaStreamSynchronize(o.s_h2d);
   if (o.s_d2h) cudaStreamSynchronize(o.s_d2h);
-  for (int s = 0; s < NSLOT; ++s) {
+  for (int s = 0; s < MAXSLOT; ++s) {
     cudaFree(o.slot[s]);
     if (o.ev_loaded[s]) cudaEventDestroy(o.ev_loaded[s]);
     if (o.ev_used[s]) cudaEventDestroy(o.ev_used[s]);
     if (o.ev_stored[s]) cudaEventDestroy(o.ev_stored[s]);
   }
+  cudaFree(o.dense);
+  cudaFree(o.swaps);
+  cudaFree(o.perm_local);
+  cudaFree(o.perm_global);
+  cudaFree(o.dblk);
+  cudaFree(o.part);
+  cudaFree(o.amax);
   cudaFree(o.stage);
   for (double* h : o.pool) cudaFreeHost(h);
   for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
@@ -276,9 +297,7 @@ static int create_streams_events(Ctx* c) {
 // select_blocking(max_mem), memdet.py:63-80, 249-255) and grows until the slots fit.
 static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx** out) {
   if (m < 1) return set_err(B2D_ERR_USAGE, "matrix dimension must be >= 1, got %lld", (long long)m);
-  if (mode == B2D_MODE_LDL_PIV)
-    return set_err(B2D_ERR_UNSUPPORTED, "block-pivoted LDL is not built in this engine version");
-  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV)
+  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV && mode != B2D_MODE_LDL_PIV)
     return set_err(B2D_ERR_USAGE, "unknown mode %d", mode);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -302,7 +321,9 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   const int64_t npad_full = (int64_t)nt_full * T;
   const size_t incore_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + (size_t)nt_full * TILE_BYTES +
                              3 * (size_t)npad_full * 8 + (size_t)NSTAGE * T * npad_full * 8;
-  const bool force = opt && opt->force_out_of_core;
+  // block-pivoted LDL pivots inside the reference's b x b diagonal blocks: always the block walk
+  const bool force = (opt && opt->force_out_of_core) || mode == B2D_MODE_LDL_PIV;
+  const int nslot = mode == B2D_MODE_LDL_PIV ? NSLOT_LDL : NSLOT;
   int64_t vec_len = npad_full;
 #define ALLOC(ptr, bytes)                                        \
   do {                                                           \
@@ -327,7 +348,8 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       int64_t n_b, b, tail;
       ref_layout(m, nb, &n_b, &b, &tail);
       const int nbt = (int)((b + T - 1) / T);
-      const size_t need = (size_t)NSLOT * nbt * nbt * TILE_BYTES + (size_t)nbt * TILE_BYTES +
+      const size_t need = (size_t)(nslot + (mode == B2D_MODE_LDL_PIV ? 1 : 0)) * nbt * nbt * TILE_BYTES +
+                          (size_t)nbt * TILE_BYTES +
                           (size_t)T * nbt * T * 8 + 3 * (size_t)(m + (int64_t)(nbt + 1) * T) * 8;
       if (need <= budget || n_b >= m) {
         if (need > budget) {
@@ -344,7 +366,8 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     c->nt = o.nbt;  // the in-core machinery factors one diagonal block at a time
     vec_len = m + (int64_t)(o.nbt + 1) * T;
-    for (int s = 0; s < NSLOT; ++s) {
+    o.nslot = nslot;
+    for (int s = 0; s < nslot; ++s) {
       ALLOC(o.slot[s], o.slot_bytes());
       cudaEventCreateWithFlags(&o.ev_loaded[s], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&o.ev_used[s], cudaEventDisableTiming);
@@ -352,6 +375,20 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     ALLOC(o.stage, (size_t)T * o.nbt * T * 8);
     ALLOC(c->inv, (size_t)o.nbt * TILE_BYTES);
+    if (mode == B2D_MODE_LDL_PIV) {
+      const int64_t ld = (int64_t)o.nbt * T;
+      ALLOC(o.dense, (size_t)ld * ld * 8);
+      ALLOC(o.swaps, (size_t)ld * 8);
+      ALLOC(o.perm_local, (size_t)ld * 8);
+      ALLOC(o.perm_global, (size_t)(m + ld) * 8);
+      ALLOC(o.dblk, (size_t)ld * 8);
+      int per_sm = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ldl_pivot_kernel, LDL_THREADS, 0);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      o.coop_blocks = std::max(1, std::min(per_sm, 2) * sms);
+      ALLOC(o.part, (size_t)o.coop_blocks * sizeof(ArgMax));
+      ALLOC(o.amax, 8);
+    }
     // pinned scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front
     const int64_t nsc = o.nb <= 2 ? 0 : ((int64_t)o.nb * o.nb + o.nb - 8) / 2;
     for (int64_t q = 0; q < nsc; ++q) {
@@ -800,6 +837,57 @@ static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
   cudaEventRecord(o.ev_used[sci], c->s_main);
 }
 
+// Pivoted LDL^T of the diagonal block in slot sa (stage k): dense copy, tolerance scale, the
+// cooperative 1x1-pivot factorisation, permutation / log|d| bookkeeping, then the unit factor
+// back into the slot and the inverses of its diagonal tiles for the panel solves.
+static int ooc_ldl_factor(Ctx* c, int sa, int k) {
+  Ooc& o = c->o;
+  const int nt = o.tiles(k);
+  int64_t n = o.size(k);
+  const int64_t ld = (int64_t)o.nbt * T, g0 = (int64_t)k * o.b;
+  cudaStream_t s = c->s_main;
+  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
+  const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
+  unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld);
+  cudaMemsetAsync(o.amax, 0, 8, s);
+  block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
+  double* A = o.dense;
+  ArgMax* part = (ArgMax*)o.part;
+  int64_t g0v = g0;
+  void* args[] = {&A, (void*)&ld, &n, &o.amax, &o.dblk, &o.swaps, &part, &c->fail, &g0v};
+  CUDA_TRY(cudaLaunchCooperativeKernel((void*)ldl_pivot_kernel, dim3(o.coop_blocks), dim3(LDL_THREADS), args, 0, s));
+  ldl_finish_kernel<<<std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
+                                                                         o.perm_global, c->ell, c->diag);
+  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
+  for (int q = 0; q < nt; ++q)
+    tile_inv_unit_kernel<<<1, T, T * 129 * 8, s>>>(o.map(sa).tile(q, q), c->inv + (int64_t)q * TILE_ELEMS);
+  c->launches += 6 + nt;
+  cudaEventRecord(o.ev_used[sa], s);
+  return B2D_OK;
+}
+
+// Panel block in slot x (engine rows of block `rows`): columns permuted by the stage's block
+// permutation into the temp slot, which then takes slot x's place (memdet.py:365-366, 378-379).
+static void ooc_permute(Ctx* c, int x, int rows, int k) {
+  Ooc& o = c->o;
+  const int tmp = o.nslot - 1;
+  cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
+  permute_cols_kernel<<<2048, 256, 0, c->s_main>>>(o.map(x), o.map(tmp), o.tiles(rows), o.tiles(k), o.size(k),
+                                                   o.perm_local);
+  c->launches++;
+  std::swap(o.slot[x], o.slot[tmp]);
+}
+
+// dst = src * D^{-1} over the stage's columns (memdet.py:368-371: B /= d, the unscaled copy kept).
+static void ooc_scale(Ctx* c, int src, int dst, int rows, int k) {
+  Ooc& o = c->o;
+  cudaStreamWaitEvent(c->s_main, o.ev_stored[dst], 0);
+  scale_cols_kernel<<<2048, 256, 0, c->s_main>>>(o.map(src), o.map(dst), o.tiles(rows), o.tiles(k), o.size(k), o.dblk);
+  c->launches++;
+  cudaEventRecord(o.ev_used[src], c->s_main);
+  cudaEventRecord(o.ev_used[dst], c->s_main);
+}
+
 // The reference driver (memdet.py:322-389) with HBM slots for its A/B/C/S buffers: every read
 // and scratch write the reference performs happens here too (so the transfer counters are the
 // reference's), issued on copy streams that run ahead of the DMMA work by the spare slots.
@@ -813,43 +901,61 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   o.reads = o.writes = 0;
   o.rr = 0;
   auto alloc = [&](std::initializer_list<int> busy) {
-    for (int tries = 0; tries < NSLOT; ++tries) {
+    const int pool = c->mode == B2D_MODE_LDL_PIV ? o.nslot - 1 : o.nslot;  // last LDL slot: permute temp
+    for (int tries = 0; tries < pool; ++tries) {
       const int s = o.rr;
-      o.rr = (o.rr + 1) % NSLOT;
+      o.rr = (o.rr + 1) % pool;
       bool ok = true;
       for (int x : busy) ok = ok && x != s;
       if (ok) return s;
     }
     return -1;
   };
+  const bool piv = c->mode == B2D_MODE_LDL_PIV;
   int sa = alloc({});
   int rc = ooc_load(c, 0, 0, sa, a, lda, dtype);
   if (rc) return rc;
   for (int k = 0; k < o.nb; ++k) {
-    cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
-    enqueue_factor(c, FactorTarget{o.map(sa), o.tiles(k), (int64_t)k * o.b}, false);
-    cudaEventRecord(o.ev_used[sa], c->s_main);
+    if (piv) {
+      if ((rc = ooc_ldl_factor(c, sa, k))) return rc;
+    } else {
+      cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
+      enqueue_factor(c, FactorTarget{o.map(sa), o.tiles(k), (int64_t)k * o.b}, false);
+      cudaEventRecord(o.ev_used[sa], c->s_main);
+    }
     if (k == o.nb - 1) break;
-    int sb = -1, sc = -1, next_a = -1;
+    // bx: the column's solved row-k block (unscaled); by: its D^{-1}-scaled copy (LDL) or bx
+    int bx = -1, by = -1, sc = -1, next_a = -1;
     for (const Visit& v : stage_visits(o.nb, k)) {
       if (v.col_start) {
         if (v.load_b) {
-          sb = alloc({sa, sb, sc});
-          if ((rc = ooc_load(c, k, v.j, sb, a, lda, dtype))) return rc;
-          ooc_trsm(c, sb, v.j, sa, k);
+          bx = alloc({sa, bx, by, sc});
+          if ((rc = ooc_load(c, k, v.j, bx, a, lda, dtype))) return rc;
+          if (piv) ooc_permute(c, bx, v.j, k);
+          ooc_trsm(c, bx, v.j, sa, k);
         } else {
-          sb = sc;  // the previous visit's C is this column's row-k tile (memdet.py:359-360)
+          bx = sc;  // the previous visit's C is this column's row-k block (memdet.py:359-360)
+        }
+        if (piv) {
+          by = alloc({sa, bx, sc});
+          ooc_scale(c, bx, by, v.j, k);
+        } else {
+          by = bx;
         }
       }
       if (v.load_c) {
-        sc = alloc({sa, sb, sc});
+        sc = alloc({sa, bx, by, sc});
         if ((rc = ooc_load(c, k, v.i, sc, a, lda, dtype))) return rc;
-        if (v.solve_c) ooc_trsm(c, sc, v.i, sa, k);
+        if (v.solve_c) {
+          if (piv) ooc_permute(c, sc, v.i, k);
+          ooc_trsm(c, sc, v.i, sa, k);
+        }
         if (v.write_c && (rc = ooc_store(c, k, v.i, sc))) return rc;
       }
-      const int st = alloc({sa, sb, sc});
+      const int st = alloc({sa, bx, by, sc});
       if ((rc = ooc_load(c, v.i, v.j, st, a, lda, dtype))) return rc;
-      ooc_schur(c, st, v.j, v.i, sb, v.i == v.j ? sb : sc, k);
+      // T(j, i) -= [D^{-1}] L(j, k) * L(i, k)^T (the unscaled copy on the diagonal visit)
+      ooc_schur(c, st, v.j, v.i, by, v.i == v.j ? bx : sc, k);
       if (v.next_diag) next_a = st;
       else if ((rc = ooc_store(c, v.i, v.j, st))) return rc;
     }
@@ -914,9 +1020,22 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
               at(c->ev_catch[st]), at(c->ev_rest[st]));
   }
   if (fail_index) *fail_index = fail == ULLONG_MAX ? -1 : (int64_t)fail;
+  if (fail != ULLONG_MAX && c->mode == B2D_MODE_LDL_PIV)
+    return set_err(B2D_ERR_INDEFINITE, "LDL pivot %lld below tolerance (block-local 1x1 pivoting)",
+                   (long long)fail);
   if (fail != ULLONG_MAX)
     return set_err(B2D_ERR_NOT_SPD, "leading minor of order %lld is not positive definite",
                    (long long)fail + 1);
+  return B2D_OK;
+}
+
+static int fetch_perm(Ctx* c, int64_t* perm) {
+  if (!perm) return set_err(B2D_ERR_USAGE, "null perm");
+  if (c->mode == B2D_MODE_LDL_PIV && c->ooc && c->o.perm_global) {
+    CUDA_TRY(cudaMemcpy(perm, c->o.perm_global, c->m * 8, cudaMemcpyDeviceToHost));
+  } else {
+    for (int64_t g = 0; g < c->m; ++g) perm[g] = g;
+  }
   return B2D_OK;
 }
 
@@ -973,6 +1092,11 @@ int b2d_ctx_fetch(b2d_ctx* ctx, double* d_out, double* prefix_out, int64_t* fail
 
 const double* b2d_ctx_device_prefix(b2d_ctx* ctx) { return ctx ? ctx->prefix : nullptr; }
 
+int b2d_ctx_fetch_perm(b2d_ctx* ctx, int64_t* perm_out) {
+  if (!ctx) return set_err(B2D_ERR_USAGE, "null ctx");
+  return fetch_perm(ctx, perm_out);
+}
+
 int b2d_ctx_set_profiling(b2d_ctx* ctx, int on) {
   if (!ctx) return set_err(B2D_ERR_USAGE, "null ctx");
   ctx->profiling = on != 0;
@@ -1014,17 +1138,27 @@ int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, i
   if (rc) return rc;
   rc = factor_host(c, a, lda, dtype, 0);
   b2d_run_info local{};
-  if (rc == B2D_OK) rc = fetch(c, d_out, prefix_out, fail_index, &local);
+  std::vector<double> dtmp;
+  if (rc == B2D_OK) {
+    if (!d_out && sign_out) {
+      dtmp.resize(m);
+      d_out = dtmp.data();
+    }
+    rc = fetch(c, d_out, prefix_out, fail_index, &local);
+  }
+  if (rc == B2D_OK && perm_out) rc = fetch_perm(c, perm_out);
   destroy(c);
   if (rc != B2D_OK && rc != B2D_ERR_NOT_SPD) return rc;
   fill_ref_info(&local, m, num_blocks, max_mem, esz);
   local.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (info) *info = local;
-  if (rc == B2D_OK) {
-    if (perm_out)
-      for (int64_t g = 0; g < m; ++g) perm_out[g] = g;
-    if (sign_out)
-      for (int64_t g = 0; g < m; ++g) sign_out[g] = 1;
+  if (rc == B2D_OK && sign_out) {
+    // cumprod(sign d) (memdet.py:407); Cholesky pivots are positive
+    int64_t sg = 1;
+    for (int64_t g = 0; g < m; ++g) {
+      if (mode == B2D_MODE_LDL_PIV) sg *= d_out[g] > 0 ? 1 : (d_out[g] < 0 ? -1 : 0);
+      sign_out[g] = sg;
+    }
   }
   return rc;
 }

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native
 from .cost import predicted_reads, predicted_writes, scratch_slots
-from .errors import NotSpdError
+from .errors import IndefiniteBlockError, NotSpdError
 from .layout import BlockLayout
 from .prefixio import PrefixWriter
 from .storage import MatrixFile, MatrixSource
@@ -239,6 +239,9 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     m = src.m
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
     ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
+    if src.device_ptr is not None and mode == _native.MODE_LDL_PIV:
+        # the block-pivoted walk streams reference blocks from host memory
+        src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
     if src.device_ptr is not None:
         if out_of_core:
             raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
@@ -257,8 +260,14 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     if rc == _native.B2D_ERR_NOT_SPD:
         raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
                           f"(global pivot {fail})")
+    if rc == _native.B2D_ERR_INDEFINITE:
+        raise IndefiniteBlockError(f"LDL pivot {fail} below tolerance: {_native.last_error()}")
     _native.check(rc, "memdet engine")
-    return d, prefix, info, ctx.out_of_core
+    perm = None
+    if mode == _native.MODE_LDL_PIV:
+        perm = np.empty(m, np.int64)
+        ctx.fetch_perm(perm)
+    return d, prefix, info, ctx.out_of_core, perm
 
 
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
@@ -268,7 +277,7 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
     if src.symmetry == "generic":
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
-    d, prefix, cinfo, ooc = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core)
+    d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core)
     nb = lay.n_b
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
                    blocks_read=predicted_reads(nb, "symmetric"),
@@ -280,7 +289,7 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
                    out_of_core=ooc, ooc_blocks=int(cinfo.ooc_blocks), ooc_block=int(cinfo.ooc_block),
                    ooc_reads=int(cinfo.ooc_reads), ooc_writes=int(cinfo.ooc_writes),
                    ooc_scratch=int(cinfo.ooc_scratch))
-    return d, prefix.astype(src.dtype, copy=False), info
+    return d, prefix.astype(src.dtype, copy=False), info, perm
 
 
 def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
@@ -294,8 +303,8 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
     the reference's out-of-core tile walk, blocks streamed between host memory and HBM (the
     scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity)."""
     del scratch_dir
-    d, prefix, info = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
-                              hbm_budget, out_of_core)
+    d, prefix, info, _ = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
+                                 hbm_budget, out_of_core)
     res = SpdResult(prefix=prefix, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:
@@ -317,14 +326,14 @@ def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefi
     if pivoting not in ("block", "none"):
         raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
     mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
-    d, prefix, info = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
-                              out_of_core)
+    d, prefix, info, perm = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
+                                    out_of_core)
     m = len(prefix)
     if mode == _native.MODE_LDL_NOPIV:
         perm = np.arange(m, dtype=np.int64)
         signs = np.ones(m, dtype=np.int64)
-    else:  # pragma: no cover - engine mode 2 returns perm/signs (future)
-        raise NotImplementedError("block-pivoted LDL")
+    else:  # memdet.py:407: cumprod(sign d)
+        signs = np.cumprod(np.sign(d)).astype(np.int64)
     res = SymmetricResult(perm=perm, prefix=prefix, prefix_signs=signs, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:

@@ -267,3 +267,49 @@ def test_distributed_driver_cuda_tile_ops(world, backend, m, panel):
     for rank, prefix, fail in results:
         assert fail == -1
         assert rel_err(prefix, ref) <= 1e-10, (rank, rel_err(prefix, ref))
+
+
+# ------------------------------------------------------------------ block-pivoted LDL (memdet_ldl)
+
+LDL_CASES = ["spd1", "spd2", "spd5", "spd30", "spd48", "spd64", "spd120", "spd200", "sym24", "sym30",
+             "sym48", "sym64", "sym120", "eye50", "diag8", "hand2", "hardindef2", "spd40_f32",
+             "rbf512", "ntk384", "C1"]
+
+
+@pytest.mark.parametrize("name", LDL_CASES)
+def test_pivoted_ldl_matches_reference_golden(golden, name):
+    """memdet_ldl with the reference's block-local 1x1 pivoting: perm and signs exactly, every
+    permuted-minor prefix within tolerance, IndefiniteBlockError where the reference raises."""
+    inp = golden.input(name)
+    tol = TOL.get(name, 1e-10)
+    for key in golden.cases[name]["runs"]:
+        drv, nb = key.split("_nb")
+        if drv != "ldl":
+            continue
+        nb = int(nb)
+        ref = golden.run(name, key)
+        if ref.get("error") == "IndefiniteBlockError":
+            with pytest.raises(eng.IndefiniteBlockError):
+                eng.memdet_ldl(inp, num_blocks=nb)
+            continue
+        res = eng.memdet_ldl(inp, num_blocks=nb)
+        np.testing.assert_array_equal(res.perm, ref["perm"], err_msg=f"{name} {key}")
+        np.testing.assert_array_equal(res.prefix_signs, ref["signs"], err_msg=f"{name} {key}")
+        assert rel_err(res.prefix, ref["prefix"]) <= tol, (name, key, rel_err(res.prefix, ref["prefix"]))
+        assert res.prefix.dtype == inp.dtype
+        assert (res.info.ooc_reads, res.info.ooc_writes, res.info.ooc_scratch) == \
+            (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
+
+
+def test_pivoted_ldl_prefix_is_permuted_minor_logdet():
+    """reference tests/test_memdet.py:117-129: prefix[q-1] = log|det M[perm[:q], perm[:q]]|."""
+    m = 48
+    a = gen.random_symmetric(m, seed=5)
+    for nb in (1, 2, 4):
+        res = eng.memdet_ldl(a, num_blocks=nb)
+        assert sorted(res.perm) == list(range(m))
+        for q in range(1, m + 1):
+            idx = res.perm[:q]
+            sign, ld = np.linalg.slogdet(a[np.ix_(idx, idx)])
+            assert res.prefix_signs[q - 1] == int(sign)
+            assert res.prefix[q - 1] == pytest.approx(ld, rel=1e-9, abs=1e-9)
