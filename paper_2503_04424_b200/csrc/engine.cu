@@ -577,8 +577,20 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
     pack_tiles_kernel<float><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
         (const float*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   c->launches++;
-  std::fill(c->act.begin(), c->act.end(), -1);
-  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, false);
+  // Lazy trailing updates: band b (BAND tile-columns) joins the right-looking updates only
+  // `lazy` outer steps before its first use, after one catch-up GEMM with every panel factored
+  // so far (K = 128 * k0).  Same flops; far bands get few large-K updates instead of one K = 128*W
+  // update per step (B2D_LAZY_STEPS; default -1 = eager, which measured faster at C2 and C3).
+  const char* ls = getenv("B2D_LAZY_STEPS");
+  const int lazy = ls ? atoi(ls) : -1;
+  const int nb = (c->nt + BAND - 1) / BAND;
+  for (int b = 0; b < nb; ++b) {
+    const int deadline = (b * BAND) / c->W_TILES - 1;
+    c->act[b] = lazy < 0 ? -1 : std::max(-1, deadline - lazy);
+  }
+  cudaEventRecord(c->ev_join, c->s_main);
+  for (auto& e : c->ev_band) cudaEventRecord(e, c->s_main);  // everything is resident already
+  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, true);
   enqueue_prefix(c);
   end(c, user);
   CUDA_TRY(cudaGetLastError());

@@ -69,9 +69,9 @@ struct TileSet {
   __host__ __device__ __forceinline__ int lo(int j) const {
     if (!lower) return i0;
     const int x = j + row_off - off;
-    const int st = stride > 1 ? stride : 1;
-    const int l = x <= 0 ? -((-x) / st) : (x + st - 1) / st;
-    return l > i0 ? l : i0;
+    int l = x;
+    if (stride > 1) l = x <= 0 ? -((-x) / stride) : (x + stride - 1) / stride;  // no division on the
+    return l > i0 ? l : i0;                                                         // single-GPU path
   }
   __host__ __device__ inline int64_t count() const {
     int64_t n = 0;

@@ -97,3 +97,28 @@ CONFIGS = {
     "C4": dict(n=131072, num_blocks=128, kind="wishart", k=131072, shift=1e-4, tol=1e-10),
     "C5": dict(n=196608, num_blocks=5, kind="ntk", p=262144, alpha=1.0, jitter=1e-8, tol=1e-6),
 }
+
+
+def ntk_like_device(n: int, p: int, alpha: float, jitter: float = 1e-8, seed: int = 0,
+                    chunk: int = 8192, device: str = "cuda"):
+    """C3 / C5 on the device: K = Z diag(s)^2 Z^T / p + jitter I, s_j = j^-alpha, with Z drawn
+    chunk by chunk of columns from torch's counter-based (Philox) CUDA generator and the rank-k
+    updates done by cuBLAS (input formation is off the timed path).  Returns a bit-symmetric
+    row-major CUDA tensor."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    k = torch.zeros((n, n), dtype=torch.float64, device=device)
+    for c0 in range(0, p, chunk):
+        c1 = min(p, c0 + chunk)
+        z = torch.randn((n, c1 - c0), dtype=torch.float64, device=device, generator=g)
+        s = torch.arange(c0 + 1, c1 + 1, dtype=torch.float64, device=device).pow_(-alpha)
+        z.mul_(s)
+        k.addmm_(z, z.T)
+        del z
+    k.div_(p)
+    k.diagonal().add_(jitter)
+    # bit-symmetric: mirror the lower triangle onto the upper (kernelgen.py:136-149 precedent)
+    k.copy_(torch.tril(k) + torch.tril(k, -1).T)
+    return k
