@@ -607,7 +607,8 @@ static void plan_bands(Ctx* c, size_t esz) {
   const int nt = c->nt, W = c->W_TILES;
   const int nbands = (nt + BAND - 1) / BAND;
   const int nsteps = (nt + W - 1) / W;
-  const double m = (double)c->m, pcie = 48e9, rate = 34e12, chain_rate = 20e12, col_lat = 200e-6;
+  const double m = (double)c->m, pcie = 48e9, rate = 34e12, chain_rate = 20e12;
+  const double col_lat = getenv("B2D_COL_LAT_US") ? atof(getenv("B2D_COL_LAT_US")) * 1e-6 : 900e-6;
   const double tile_flops = 2.0 * T * T * T;
   std::vector<double> arrival(nbands);
   double bytes = 0.0;
