@@ -1,0 +1,169 @@
+"""Command line of the drop-in (the hot-path subcommands of `oocdet`, reference cli.py:1-318).
+
+    python -m paper_2503_04424_b200 memdet --in K.mdm --assume spd --num-blocks 8 --json
+    python -m paper_2503_04424_b200 gen --kind rbf --n 4096 --out K.mdm
+    python -m paper_2503_04424_b200 cost --m 4096 --nb 4 --case sym --json
+
+Same flags, JSON payload (schema_version 1) and exit codes as the reference: 0 success,
+2 usage error, 3 numerical failure, 4 I/O failure.  `--assume gen` (the LU path) and the
+FLODANCE / SLQ / block-diagonal subcommands are outside this engine's scope.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+from . import __version__, gen
+from .cost import predicted_cost
+from .errors import NumericalError, OocdetError, StorageError
+from .memdet import memdet_cholesky, memdet_ldl
+from .storage import write_matrix
+
+SCHEMA_VERSION = 1
+_SUFFIXES = {"k": 1 << 10, "m": 1 << 20, "g": 1 << 30}
+
+
+def parse_size(text: str) -> int:
+    """Byte count with an optional K/M/G suffix (powers of 1024), as reference cli.py:35-48."""
+    s = text.strip().lower().removesuffix("b")
+    mult = 1
+    if s and s[-1] in _SUFFIXES:
+        mult, s = _SUFFIXES[s[-1]], s[:-1]
+    try:
+        value = int(float(s) * mult) if "." in s else int(s) * mult
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"cannot parse size {text!r}") from None
+    if value < 0:
+        raise argparse.ArgumentTypeError(f"size must be non-negative: {text!r}")
+    return value
+
+
+def _emit(args, payload: dict, lines):
+    if args.json:
+        json.dump(payload, sys.stdout, sort_keys=True)
+        sys.stdout.write("\n")
+    else:
+        for line in lines:
+            print(line)
+
+
+def cmd_memdet(args) -> int:
+    if args.assume == "gen":
+        raise ValueError("--assume gen (LU) is outside the B200 engine's scope; use sym or spd")
+    driver = memdet_cholesky if args.assume == "spd" else memdet_ldl
+    res = driver(args.infile, max_mem=args.max_mem, num_blocks=args.num_blocks,
+                 scratch_dir=args.scratch_dir, prefix_out=args.prefix_out)
+    info = res.info
+    payload = {
+        "schema_version": SCHEMA_VERSION, "logabsdet": res.logabsdet, "sign": res.sign,
+        "n_b": info.n_b, "b": info.b, "blocks_read": info.blocks_read,
+        "blocks_written": info.blocks_written, "scratch_slots": info.scratch_slots,
+        "wall_seconds": info.wall_seconds,
+        "engine": {"device_ms": info.device_ms, "h2d_bytes": info.h2d_bytes,
+                   "d2h_bytes": info.d2h_bytes, "kernel_launches": info.kernel_launches,
+                   "out_of_core": info.out_of_core, "ooc_blocks": info.ooc_blocks,
+                   "ooc_reads": info.ooc_reads, "ooc_writes": info.ooc_writes},
+    }
+    _emit(args, payload, [
+        f"logabsdet = {res.logabsdet:.12e} (sign {res.sign:+d})",
+        f"n_b = {info.n_b}, b = {info.b}, reads = {info.blocks_read}, writes = {info.blocks_written}, "
+        f"scratch slots = {info.scratch_slots}",
+        f"wall time {info.wall_seconds:.3f} s (device {info.device_ms:.1f} ms)",
+    ])
+    return 0
+
+
+def cmd_gen(args) -> int:
+    kinds = {
+        "wishart": lambda: (gen.spd_wishart(args.n, args.k or args.n, args.seed, args.jitter or 1e-3), "spd"),
+        "rbf": lambda: (gen.rbf(args.n, args.d, args.ell, args.jitter or 1e-6, args.seed), "spd"),
+        "ntk-like": lambda: (gen.ntk_like(args.n, args.k or 2 * args.n, args.alpha, args.jitter or 1e-8,
+                                          args.seed), "spd"),
+        "spd-random": lambda: (gen.random_spd(args.n, args.seed), "spd"),
+        "sym-random": lambda: (gen.random_symmetric(args.n, args.seed), "symmetric"),
+    }
+    a, sym = kinds[args.kind]()
+    mf = write_matrix(args.out, a, sym)
+    _emit(args, {"schema_version": SCHEMA_VERSION, "path": mf.path, "m": mf.m, "dtype": str(mf.dtype),
+                 "symmetry": mf.symmetry, "kind": args.kind, "seed": args.seed},
+          [f"wrote {mf.symmetry} {mf.m}x{mf.m} matrix to {mf.path}"])
+    return 0
+
+
+def cmd_cost(args) -> int:
+    case = {"gen": "generic", "sym": "symmetric"}[args.case]
+    pc = predicted_cost(args.m, args.nb, case)
+    ops = {}
+    for name in ("decomposition", "lower_solve", "upper_solve", "full_multiply", "gramian_multiply"):
+        op = getattr(pc, name)
+        ops[name] = {"count": float(op.count), "flops_per_op": float(op.flops_per_op), "total": float(op.total)}
+    payload = {"schema_version": SCHEMA_VERSION, "m": pc.m, "n_b": pc.n_b, "b": pc.m // pc.n_b,
+               "case": pc.case, "operations": ops, "total_flops": float(pc.total_flops),
+               "blocks_read": pc.blocks_read, "blocks_written": pc.blocks_written,
+               "scratch_slots": pc.scratch_slots}
+    _emit(args, payload, [f"total FMA {float(pc.total_flops):.6g}, reads {pc.blocks_read}, "
+                          f"writes {pc.blocks_written}, scratch slots {pc.scratch_slots}"])
+    return 0
+
+
+def build_parser() -> argparse.ArgumentParser:
+    parser = argparse.ArgumentParser(prog="paper_2503_04424_b200",
+                                     description="B200 MEMDET log-determinants (drop-in for oocdet memdet)")
+    parser.add_argument("--version", action="version", version=__version__)
+    sub = parser.add_subparsers(dest="command", required=True)
+
+    p = sub.add_parser("memdet", help="exact log-determinant and prefixes on the B200 engine")
+    p.add_argument("--in", dest="infile", required=True)
+    p.add_argument("--assume", choices=("gen", "sym", "spd"), required=True)
+    p.add_argument("--max-mem", type=parse_size, default=None)
+    p.add_argument("--num-blocks", type=int, default=None)
+    p.add_argument("--scratch-dir", default=None)
+    p.add_argument("--prefix-out", default=None)
+    p.add_argument("--json", action="store_true")
+    p.set_defaults(func=cmd_memdet)
+
+    p = sub.add_parser("gen", help="write a seeded BASELINE-family matrix (MEMDET01)")
+    p.add_argument("--kind", default="rbf", choices=("wishart", "rbf", "ntk-like", "spd-random", "sym-random"))
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--k", type=int, default=None, help="inner dimension (wishart / ntk-like)")
+    p.add_argument("--d", type=int, default=16, help="RBF point dimension")
+    p.add_argument("--ell", type=float, default=4.0, help="RBF length scale")
+    p.add_argument("--alpha", type=float, default=0.75, help="NTK-like power-law exponent")
+    p.add_argument("--jitter", type=float, default=None)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--out", required=True)
+    p.add_argument("--json", action="store_true")
+    p.set_defaults(func=cmd_gen)
+
+    p = sub.add_parser("cost", help="analytical cost model query")
+    p.add_argument("--m", type=int, required=True)
+    p.add_argument("--nb", type=int, required=True)
+    p.add_argument("--case", choices=("gen", "sym"), default="sym")
+    p.add_argument("--json", action="store_true")
+    p.set_defaults(func=cmd_cost)
+    return parser
+
+
+def main(argv=None) -> int:
+    """Exit codes as reference cli.py:298-314."""
+    args = build_parser().parse_args(argv)
+    try:
+        return args.func(args)
+    except (ValueError, argparse.ArgumentTypeError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+    except NumericalError as exc:
+        print(f"numerical failure: {exc}", file=sys.stderr)
+        return 3
+    except (StorageError, OSError) as exc:
+        print(f"I/O failure: {exc}", file=sys.stderr)
+        return 4
+    except OocdetError as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return exc.exit_code
+
+
+if __name__ == "__main__":
+    sys.exit(main())
