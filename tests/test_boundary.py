@@ -54,3 +54,20 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(eng.EngineUnavailableError):
         eng.memdet_cholesky(np.eye(4), num_blocks=1)
+
+
+def test_run_info_struct_matches_header():
+    """The ctypes mirror of b2d_run_info / b2d_options must have the header's field order."""
+    import re
+
+    text = open(HEADER).read()
+    for cname, pyname in (("b2d_run_info", "RunInfoC"), ("b2d_options", "OptionsC"),
+                          ("b2d_tilemap", "TileMapC"), ("b2d_tileset", "TileSetC")):
+        body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (cname, cname), text, re.S).group(1)
+        names = []
+        for decl in re.sub(r"/\*.*?\*/", "", body, flags=re.S).split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            names += [n.strip().lstrip("*") for n in decl.split(None, 1)[1].split(",")]
+        assert names == [f[0] for f in getattr(_native, pyname)._fields_], cname
