@@ -5,15 +5,16 @@ Layout.  The n_pad x n_pad lower tile triangle (128-wide tiles) i
 row: rank r owns tile rows i = r, r + P, r + 2P, ...  (row i holds i + 1 tiles, so the cyclic
 deal balances the triangle).  Each rank stores its rows as a local grid [maxloc][nt] of tiles.
 
-Step (outer panel of W tile-columns [k0, ke)), for p in the panel:
-  1. the owner of tile row p factors the diagonal tile (potrf + inverse, fused 2 log L_pp);
-  2. broadcast of L_pp^{-1} (128 KB) from the owner;
-  3. every rank solves its tiles (i, p), i > p (DMMA TRSM against the inverse);
-  4. the solved tiles L(j, p), j in (p, ke), meet in a W-tile buffer (all-reduce of disjoint
-     contributions: exact) and every rank updates its tiles in the panel columns (p, ke).
-After the panel: all-gather of the panel (each rank's rows x W tiles) and the trailing Schur
-update of every rank's own tiles with K = 128*W (DMMA).  The 2 log L_ii values meet in one
-all-reduce at the end and every rank scans the prefix.
+Step s (outer panel of W tile-columns [k0, ke)), two collectives per panel:
+  1. the W x W diagonal block meets on every rank (all-reduce of disjoint row contributions,
+     exact) and every rank factors it redundantly (potrf + inverse per tile, intra-block
+     solves and updates) -> identical L_blk, L_pp^{-1} and 2 log L_ii everywhere;
+  2. every rank solves its own panel rows i >= ke against L_blk (DMMA TRSM + updates);
+  3. all-gather of the solved panel (each rank's rows x W tiles, double-buffered);
+  4. next-cols: every rank updates its tiles in the next panel's columns [ke, ke+W) (main
+     stream, the critical path), then the rest [ke+W, nt) on a side stream that overlaps the
+     next panel's steps 1-3 (one-panel look-ahead, as the single-GPU driver).
+Every rank holds every 2 log L_ii at the end and scans the prefix itself.
 
 The driver is written against a small tile-ops interface so the same host logic runs on the
 GPUs (`CudaTileOps`, the C ABI's tile-level entry points on device buffers, NCCL) and in the
@@ -65,33 +66,35 @@ class RowCyclic:
 def factor_distributed(ops, comm, dist: RowCyclic, panel_tiles: int = 8):
     """Factor the distributed lower tile triangle held by `ops`; returns (prefix, fail) on
     every rank (fail = first non-positive pivot's global row, or -1)."""
-    nt, P, W = dist.nt, dist.world, panel_tiles
+    nt, W = dist.nt, panel_tiles
     ops.begin()
-    for k0 in range(0, nt, W):
-        ke = min(k0 + W, nt)
-        for p in range(k0, ke):
-            owner = dist.owner(p)
-            if dist.rank == owner:
-                ops.potrf(dist.local(p), p)
-            comm.broadcast(ops.inv, src=owner)
-            ops.trsm(p)
-            if p + 1 < ke:
-                ops.fill_diag_buffer(p, k0, ke)
-                comm.all_reduce(ops.diag_buffer)
-                ops.update_intra(p, k0, ke)
+    steps = [(k0, min(k0 + W, nt)) for k0 in range(0, nt, W)]
+    for s, (k0, ke) in enumerate(steps):
+        ne = min(ke + W, nt)
+        ops.wait_rest(s - 2)                    # columns [k0, ke) carry every earlier panel
+        ops.fill_diag_block(k0, ke)
+        comm.all_reduce(ops.diag_block)
+        ops.factor_diag_block(k0, ke)
         if ke >= nt:
             break
-        comm.all_gather_into_tensor(ops.panel_all, ops.local_panel(k0, ke))
-        ops.update_trailing(k0, ke)
-    comm.all_reduce(ops.ell)
+        ops.solve_panel(k0, ke)
+        comm.all_gather_into_tensor(ops.panel_buffer(s), ops.local_panel(k0, ke))
+        ops.update_trailing(s, k0, ke, ke, ne)                 # next panel's columns (main)
+        ops.mark_panel(s)
+        with ops.side():
+            ops.wait_panel(s)
+            ops.update_trailing(s, k0, ke, ne, nt)             # the rest (side stream)
+            ops.mark_rest(s)
+    ops.join()
     fail = ops.fail_tensor()
     comm.all_reduce(fail, op=comm.ReduceOp.MIN)
     return ops.prefix(), ops.fail_value(fail)
 
 
 class CudaTileOps:
-    """Per-rank device state and the C-ABI tile kernels (all enqueued on torch's current
-    stream).  Local grid [maxloc][nt] tiles; gathered panel [P][maxloc][W] tiles."""
+    """Per-rank device state and the C-ABI tile kernels (enqueued on torch's current stream;
+    the rest updates on a side stream).  Local grid [maxloc][nt] tiles; W x W diagonal block;
+    gathered panels [P][maxloc][W] tiles, double-buffered."""
 
     def __init__(self, dist: RowCyclic, m: int, panel_tiles: int = 8, device=None):
         import torch
@@ -102,19 +105,23 @@ class CudaTileOps:
         self.W = panel_tiles
         self.dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         f64 = dict(dtype=torch.float64, device=self.dev)
-        nt, ml = dist.nt, dist.maxloc
+        nt, ml, W = dist.nt, dist.maxloc, self.W
         self.grid = torch.empty(ml * nt * TILE_ELEMS, **f64)
-        self.inv = torch.empty(TILE_ELEMS, **f64)
-        self.diag_buffer = torch.empty(self.W * TILE_ELEMS, **f64)
-        self.panel_loc = torch.empty(ml * self.W * TILE_ELEMS, **f64)
-        self.panel_all = torch.empty(dist.world * ml * self.W * TILE_ELEMS, **f64)
+        self.diag_block = torch.empty(W * W * TILE_ELEMS, **f64)
+        self.inv = torch.empty(W * TILE_ELEMS, **f64)
+        self.panel_loc = torch.empty(ml * W * TILE_ELEMS, **f64)
+        self.panels = [torch.empty(dist.world * ml * W * TILE_ELEMS, **f64) for _ in range(2)]
         npad = nt * T
         self.ell = torch.zeros(npad, **f64)
         self.diag = torch.zeros(npad, **f64)
         self.prefix_buf = torch.empty(npad, **f64)
         self.fail = torch.empty(1, dtype=torch.int64, device=self.dev)
         self.lib = _native.load()
-        self.launches = 0  # engine kernels enqueued (potrf / gemm / pack / prefix calls)
+        self.side_stream = torch.cuda.Stream(self.dev)
+        nsteps = -(-nt // W)
+        self.ev_panel = [torch.cuda.Event() for _ in range(nsteps)]
+        self.ev_rest = [torch.cuda.Event() for _ in range(nsteps)]
+        self.launches = 0  # engine kernels enqueued
 
     # -------------------------------------------------------------------- helpers
     def _stream(self):
@@ -123,12 +130,23 @@ class CudaTileOps:
     def _grid_map(self):
         return _native.TileMapC(self.grid.data_ptr(), self.dist.nt, 0, 0, 0)
 
-    def _set(self, j0, j1, row_off=0):
-        d = self.dist
-        return _native.TileSetC(0, d.nloc, j0, j1, 1, row_off, d.world, d.rank)
+    def _blk_map(self, k0):
+        # diag block tile (i, j), global indices in [k0, ke): base shifted so tile(i, j) lands at
+        # ((i - k0) * W + (j - k0))
+        base = self.diag_block.data_ptr() - (k0 * self.W + k0) * TILE_BYTES
+        return _native.TileMapC(base, self.W, 0, 0, 0)
 
-    def _tile_ptr(self, li, j):
-        return self.grid.data_ptr() + (li * self.dist.nt + j) * TILE_BYTES
+    def _rows_from(self, g):
+        """First local row whose global row is >= g."""
+        d = self.dist
+        return max(0, -(-(g - d.rank) // d.world))
+
+    def _gemm(self, mode, amap, bmap, cmap, binv, tset, p0, p1, k):
+        _native.check(self.lib.b2d_tile_gemm(mode, None if amap is None else ctypes.byref(amap),
+                                             None if bmap is None else ctypes.byref(bmap), ctypes.byref(cmap),
+                                             None if binv is None else ctypes.c_void_p(binv), ctypes.byref(tset),
+                                             p0, p1, k, self._stream()), "b2d_tile_gemm")
+        self.launches += 1
 
     # -------------------------------------------------------------------- interface
     def load(self, a, lda: int | None = None):
@@ -136,9 +154,10 @@ class CudaTileOps:
         torch = self.torch
         dcode = _native.B2D_F64 if a.dtype == torch.float64 else _native.B2D_F32
         lda = lda or a.stride(0)
+        d = self.dist
+        s = _native.TileSetC(0, d.nloc, 0, d.nt, 1, 0, d.world, d.rank)
         _native.check(self.lib.b2d_pack_tiles(ctypes.c_void_p(a.data_ptr()), lda, dcode, 0, self.m,
-                                              ctypes.byref(self._grid_map()),
-                                              ctypes.byref(self._set(0, self.dist.nt)), self._stream()),
+                                              ctypes.byref(self._grid_map()), ctypes.byref(s), self._stream()),
                       "b2d_pack_tiles")
         self.launches += 1
 
@@ -146,40 +165,44 @@ class CudaTileOps:
         self.ell.zero_()
         self.diag.zero_()
         self.fail.fill_(-1)  # all ones = UINT64_MAX for the kernel's atomicMin
+        self.side_stream.wait_stream(self.torch.cuda.current_stream(self.dev))
 
-    def potrf(self, li: int, p: int):
-        _native.check(self.lib.b2d_tile_potrf_inv(
-            ctypes.c_void_p(self._tile_ptr(li, p)), ctypes.c_void_p(self.inv.data_ptr()),
-            ctypes.c_void_p(self.ell.data_ptr()), ctypes.c_void_p(self.diag.data_ptr()),
-            ctypes.c_void_p(self.fail.data_ptr()), p * T, self.m, self._stream()), "potrf")
-        self.launches += 1
+    def wait_rest(self, s):
+        if s >= 0:
+            self.torch.cuda.current_stream(self.dev).wait_event(self.ev_rest[s])
 
-    def trsm(self, p: int):
-        s = self._set(p, p + 1, row_off=1)
-        _native.check(self.lib.b2d_tile_gemm(1, None, None, ctypes.byref(self._grid_map()),
-                                             ctypes.c_void_p(self.inv.data_ptr()), ctypes.byref(s),
-                                             0, 0, p, self._stream()), "trsm")
-        self.launches += 1
-
-    def fill_diag_buffer(self, p: int, k0: int, ke: int):
-        self.diag_buffer.zero_()
-        buf = self.diag_buffer.view(self.W, TILE_ELEMS)
+    def fill_diag_block(self, k0, ke):
+        self.diag_block.zero_()
+        blk = self.diag_block.view(self.W, self.W, TILE_ELEMS)
         grid = self.grid.view(self.dist.maxloc, self.dist.nt, TILE_ELEMS)
-        for j in range(p + 1, ke):
-            if self.dist.owner(j) == self.dist.rank:
-                buf[j - k0].copy_(grid[self.dist.local(j), p])
+        for i in range(k0, ke):
+            if self.dist.owner(i) == self.dist.rank:
+                blk[i - k0, : i - k0 + 1].copy_(grid[self.dist.local(i), k0:i + 1])
 
-    def _gemm_update(self, bmap, j0, j1, p0, p1):
-        s = self._set(j0, j1)
-        g = self._grid_map()
-        _native.check(self.lib.b2d_tile_gemm(0, ctypes.byref(g), ctypes.byref(bmap), ctypes.byref(g), None,
-                                             ctypes.byref(s), p0, p1, 0, self._stream()), "update")
-        self.launches += 1
+    def factor_diag_block(self, k0, ke):
+        """Redundant on every rank: right-looking Cholesky of the W x W diagonal block."""
+        bm = self._blk_map(k0)
+        for p in range(k0, ke):
+            invp = self.inv.data_ptr() + (p - k0) * TILE_BYTES
+            _native.check(self.lib.b2d_tile_potrf_inv(
+                ctypes.c_void_p(bm.base + ((p * self.W) + p) * TILE_BYTES), ctypes.c_void_p(invp),
+                ctypes.c_void_p(self.ell.data_ptr()), ctypes.c_void_p(self.diag.data_ptr()),
+                ctypes.c_void_p(self.fail.data_ptr()), p * T, self.m, self._stream()), "potrf")
+            self.launches += 1
+            if p + 1 < ke:
+                self._gemm(1, None, None, bm, invp, _native.TileSetC(p + 1, ke, p, p + 1, 0, 0, 0, 0), 0, 0, p)
+                self._gemm(0, bm, bm, bm, None, _native.TileSetC(p + 1, ke, p + 1, ke, 1, 0, 0, 0), p, p + 1, 0)
 
-    def update_intra(self, p: int, k0: int, ke: int):
-        # B(j, p) = diag_buffer[j - k0]: base shifted so tile(j, p) = base + (j + p) tiles
-        base = self.diag_buffer.data_ptr() - (k0 + p) * TILE_BYTES
-        self._gemm_update(_native.TileMapC(base, 1, 0, 0, 0), p + 1, ke, p, p + 1)
+    def solve_panel(self, k0, ke):
+        """Own rows i >= ke: X(i, [k0, ke)) = A L_blk^{-T}, right-looking over the block."""
+        d = self.dist
+        i0 = self._rows_from(ke)
+        g, bm = self._grid_map(), self._blk_map(k0)
+        for p in range(k0, ke):
+            invp = self.inv.data_ptr() + (p - k0) * TILE_BYTES
+            self._gemm(1, None, None, g, invp, _native.TileSetC(i0, d.nloc, p, p + 1, 0, 0, 0, 0), 0, 0, p)
+            if p + 1 < ke:
+                self._gemm(0, g, bm, g, None, _native.TileSetC(i0, d.nloc, p + 1, ke, 0, 0, 0, 0), p, p + 1, 0)
 
     def local_panel(self, k0: int, ke: int):
         grid = self.grid.view(self.dist.maxloc, self.dist.nt, TILE_ELEMS)
@@ -187,11 +210,34 @@ class CudaTileOps:
         loc[:, : ke - k0].copy_(grid[:, k0:ke])
         return self.panel_loc
 
-    def update_trailing(self, k0: int, ke: int):
-        # gathered panel [P][maxloc][W]: tile (j, p) at ((j % P) * maxloc + j // P) * W + p - k0
-        base = self.panel_all.data_ptr() - k0 * TILE_BYTES
-        bmap = _native.TileMapC(base, self.W, 0, self.dist.world, self.dist.maxloc)
-        self._gemm_update(bmap, ke, self.dist.nt, k0, ke)
+    def panel_buffer(self, s):
+        return self.panels[s % 2]
+
+    def update_trailing(self, s, k0, ke, j0, j1):
+        """Own tiles in columns [j0, j1) -= L(i, panel) L(j, panel)^T; the gathered panel
+        [P][maxloc][W] is read through a row-cyclic tile map."""
+        if j1 <= j0:
+            return
+        d = self.dist
+        base = self.panels[s % 2].data_ptr() - k0 * TILE_BYTES
+        bmap = _native.TileMapC(base, self.W, 0, d.world, d.maxloc)
+        g = self._grid_map()
+        self._gemm(0, g, bmap, g, None, _native.TileSetC(0, d.nloc, j0, j1, 1, 0, d.world, d.rank), k0, ke, 0)
+
+    def mark_panel(self, s):
+        self.ev_panel[s].record(self.torch.cuda.current_stream(self.dev))
+
+    def side(self):
+        return self.torch.cuda.stream(self.side_stream)
+
+    def wait_panel(self, s):
+        self.side_stream.wait_event(self.ev_panel[s])
+
+    def mark_rest(self, s):
+        self.ev_rest[s].record(self.side_stream)
+
+    def join(self):
+        self.torch.cuda.current_stream(self.dev).wait_stream(self.side_stream)
 
     def fail_tensor(self):
         # the kernel's "no failure" is UINT64_MAX (int64 -1); make it the largest int64 for MIN

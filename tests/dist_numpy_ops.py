@@ -2,6 +2,8 @@
 paper_2503_04424_b200.distributed runs under gloo on CPU (the container has no GPU).  Tiles are
 plain 128x128 row-major blocks here; only the tile-op semantics must match the device ones."""
 
+import contextlib
+
 import numpy as np
 import torch
 from scipy.linalg import cholesky
@@ -14,12 +16,12 @@ T = 128
 class NumpyTileOps:
     def __init__(self, dist: RowCyclic, m: int, panel_tiles: int = 8):
         self.dist, self.m, self.W = dist, m, panel_tiles
-        nt, ml = dist.nt, dist.maxloc
+        nt, ml, W = dist.nt, dist.maxloc, self.W
         self.grid = torch.zeros((ml, nt, T, T), dtype=torch.float64)
-        self.inv = torch.zeros((T, T), dtype=torch.float64)
-        self.diag_buffer = torch.zeros((self.W, T, T), dtype=torch.float64)
-        self.panel_loc = torch.zeros((ml, self.W, T, T), dtype=torch.float64)
-        self.panel_all = torch.zeros((dist.world * ml, self.W, T, T), dtype=torch.float64)
+        self.diag_block = torch.zeros((W, W, T, T), dtype=torch.float64)
+        self.inv = torch.zeros((W, T, T), dtype=torch.float64)
+        self.panel_loc = torch.zeros((ml, W, T, T), dtype=torch.float64)
+        self.panels = [torch.zeros((dist.world * ml, W, T, T), dtype=torch.float64) for _ in range(2)]
         self.ell = torch.zeros(nt * T, dtype=torch.float64)
         self.fail = INT64_MAX
 
@@ -35,48 +37,76 @@ class NumpyTileOps:
         self.ell.zero_()
         self.fail = INT64_MAX
 
-    def potrf(self, li, p):
-        t = self.grid[li, p].numpy()
+    def wait_rest(self, s):
+        pass
+
+    def fill_diag_block(self, k0, ke):
+        self.diag_block.zero_()
+        for i in range(k0, ke):
+            if self.dist.owner(i) == self.dist.rank:
+                for j in range(k0, i + 1):
+                    self.diag_block[i - k0, j - k0] = self.grid[self.dist.local(i), j]
+
+    def factor_diag_block(self, k0, ke):
+        n = ke - k0
+        blk = np.zeros((n * T, n * T))
+        for i in range(n):
+            for j in range(i + 1):
+                blk[i * T:(i + 1) * T, j * T:(j + 1) * T] = self.diag_block[i, j].numpy()
         try:
-            low = cholesky(np.tril(t) + np.tril(t, -1).T, lower=True)
+            low = cholesky(np.tril(blk) + np.tril(blk, -1).T, lower=True)
         except np.linalg.LinAlgError:
-            self.fail = min(self.fail, p * T)
-            low = np.eye(T)
-        self.grid[li, p] = torch.from_numpy(low)
-        self.inv.copy_(torch.from_numpy(np.linalg.inv(low)))
-        self.ell[p * T:(p + 1) * T] = torch.from_numpy(2.0 * np.log(np.diagonal(low)))
+            self.fail = min(self.fail, k0 * T)
+            low = np.eye(n * T)
+        for i in range(n):
+            for j in range(i + 1):
+                self.diag_block[i, j] = torch.from_numpy(low[i * T:(i + 1) * T, j * T:(j + 1) * T].copy())
+        self.low = low
+        self.ell[k0 * T:ke * T] = torch.from_numpy(2.0 * np.log(np.diagonal(low)))
 
-    def trsm(self, p):
+    def solve_panel(self, k0, ke):
+        n = ke - k0
+        linv_t = np.linalg.inv(self.low).T
         for i in self.dist.rows:
-            if i > p:
+            if i >= ke:
                 li = self.dist.local(i)
-                self.grid[li, p] = self.grid[li, p] @ self.inv.T
-
-    def fill_diag_buffer(self, p, k0, ke):
-        self.diag_buffer.zero_()
-        for j in range(p + 1, ke):
-            if self.dist.owner(j) == self.dist.rank:
-                self.diag_buffer[j - k0] = self.grid[self.dist.local(j), p]
-
-    def update_intra(self, p, k0, ke):
-        for i in self.dist.rows:
-            li = self.dist.local(i)
-            for j in range(p + 1, min(ke, i + 1)):
-                self.grid[li, j] -= self.grid[li, p] @ self.diag_buffer[j - k0].T
+                row = np.concatenate([self.grid[li, k0 + q].numpy() for q in range(n)], axis=1)
+                x = row @ linv_t
+                for q in range(n):
+                    self.grid[li, k0 + q] = torch.from_numpy(x[:, q * T:(q + 1) * T].copy())
 
     def local_panel(self, k0, ke):
         self.panel_loc.zero_()
         self.panel_loc[:, : ke - k0] = self.grid[:, k0:ke]
         return self.panel_loc
 
-    def update_trailing(self, k0, ke):
+    def panel_buffer(self, s):
+        return self.panels[s % 2]
+
+    def update_trailing(self, s, k0, ke, j0, j1):
         P, ml = self.dist.world, self.dist.maxloc
+        g = self.panels[s % 2]
         for i in self.dist.rows:
             li = self.dist.local(i)
-            for j in range(ke, i + 1):
-                g = self.panel_all[(j % P) * ml + j // P]
+            for j in range(j0, min(j1, i + 1)):
+                gj = g[(j % P) * ml + j // P]
                 for p in range(k0, ke):
-                    self.grid[li, j] -= self.grid[li, p] @ g[p - k0].T
+                    self.grid[li, j] -= self.grid[li, p] @ gj[p - k0].T
+
+    def mark_panel(self, s):
+        pass
+
+    def side(self):
+        return contextlib.nullcontext()
+
+    def wait_panel(self, s):
+        pass
+
+    def mark_rest(self, s):
+        pass
+
+    def join(self):
+        pass
 
     def fail_tensor(self):
         return torch.tensor([self.fail], dtype=torch.int64)
