@@ -109,6 +109,7 @@ struct Ctx {
   int mode = B2D_MODE_CHOLESKY;
   int nt = 0;
   int W_TILES = 8;
+  std::vector<int> bounds;  // outer-panel boundaries k0 of the current factorisation (+ nt)
   double* tiles = nullptr;   // packed lower tile triangle
   double* inv = nullptr;     // nt inverse diagonal tiles
   double* ell = nullptr;     // n_pad: 2 log L_ii
@@ -269,7 +270,7 @@ static int create_streams_events(Ctx* c) {
   cudaEventCreate(&c->ev_start);
   cudaEventCreate(&c->ev_stop);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  const int nsteps = (c->nt + c->W_TILES - 1) / c->W_TILES;
+  const int nsteps = c->nt;  // enough for any panel-width schedule
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
   c->ev_catch.resize(nsteps);
@@ -457,6 +458,42 @@ static void launch_update(Ctx* c, cudaStream_t s, const FactorTarget& ft, int j0
   launch_gemm(c, s, MODE_UPDATE, t, prof, (double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
 }
 
+// Outer-panel schedule: W tile-columns per panel, narrowed to head_w for the first head tiles
+// (host ingest: the chain runs ahead of the arriving strips) and to tail_w once no more than
+// tail tiles remain (the chain-bound end).  B2D_HEAD_TILES/W, B2D_TAIL_TILES/W override.
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static void make_bounds(Ctx* c, int nt, bool host) {
+  const int W = c->W_TILES;
+  const int head = host ? env_int("B2D_HEAD_TILES", 0) : 0, head_w = std::max(1, env_int("B2D_HEAD_W", 4));
+  const int tail = env_int("B2D_TAIL_TILES", 0), tail_w = std::max(1, env_int("B2D_TAIL_W", 4));
+  c->bounds.clear();
+  int k = 0;
+  while (k < nt) {
+    c->bounds.push_back(k);
+    int w = W;
+    if (k < head) w = head_w;
+    if (nt - k <= tail) w = tail_w;
+    k = std::min(nt, k + w);
+  }
+  c->bounds.push_back(nt);
+}
+
+// Latest step at which a band starting at tile-column col may join: -1 if the first panel
+// reads it, else the first step whose next-cols update reaches it.
+static int band_deadline(const Ctx* c, int col) {
+  if (col < c->bounds[1]) return -1;
+  const int nsteps = (int)c->bounds.size() - 1;
+  for (int s = 0; s < nsteps; ++s) {
+    const int ne = s + 2 <= nsteps ? c->bounds[s + 2] : c->bounds[nsteps];
+    if (ne > col) return s;
+  }
+  return nsteps - 1;
+}
+
 static void launch_panel_column(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p) {
   double* invp = c->inv + (int64_t)p * TILE_ELEMS;
   potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(ft.map.tile(p, p), invp, c->ell, c->diag, c->fail,
@@ -480,8 +517,8 @@ static void launch_panel_column(Ctx* c, cudaStream_t s, const FactorTarget& ft, 
 // so every column is current before it is factored.
 static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
   const int nt = ft.nt;
-  const int W_TILES = c->W_TILES;
-  const int nsteps = (nt + W_TILES - 1) / W_TILES;
+  if (c->bounds.empty() || c->bounds.back() != nt) make_bounds(c, nt, false);
+  const int nsteps = (int)c->bounds.size() - 1;
   const int nbands = (nt + BAND - 1) / BAND;
   cudaEventRecord(c->ev_join, c->s_main);
   cudaStreamWaitEvent(c->s_side, c->ev_join, 0);
@@ -491,8 +528,8 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
   }
   int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel)
   for (int st = 0; st < nsteps; ++st) {
-    const int k0 = st * W_TILES;
-    const int ke = std::min(k0 + W_TILES, nt);
+    const int k0 = c->bounds[st];
+    const int ke = c->bounds[st + 1];
     // panel(k0): its columns were last touched by next-cols(st-1) (same stream) and rest(st-2)
     if (st >= 2) cudaStreamWaitEvent(c->s_main, c->ev_rest[st - 2], 0);
     for (int p = k0; p < ke; ++p) {
@@ -508,7 +545,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
     }
     cudaEventRecord(c->ev_panel[st], c->s_main);
     if (ke >= nt) break;
-    const int ne = std::min(ke + W_TILES, nt);
+    const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
     // catch-up of the bands that join at this step (panels of steps < st, already factored)
     int end_active = nt;
     if (wait_bands) {
@@ -583,9 +620,10 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
   // update per step (B2D_LAZY_STEPS; default -1 = eager, which measured faster at C2 and C3).
   const char* ls = getenv("B2D_LAZY_STEPS");
   const int lazy = ls ? atoi(ls) : -1;
+  make_bounds(c, c->nt, false);
   const int nb = (c->nt + BAND - 1) / BAND;
   for (int b = 0; b < nb; ++b) {
-    const int deadline = (b * BAND) / c->W_TILES - 1;
+    const int deadline = band_deadline(c, b * BAND);
     c->act[b] = lazy < 0 ? -1 : std::max(-1, deadline - lazy);
   }
   cudaEventRecord(c->ev_join, c->s_main);
@@ -604,9 +642,10 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
 // update first touches it (then the device waits for it).  Deferred panels are applied by one
 // catch-up update when the band joins, so early steps are not held up by late strips.
 static void plan_bands(Ctx* c, size_t esz) {
-  const int nt = c->nt, W = c->W_TILES;
+  const int nt = c->nt;
+  make_bounds(c, nt, true);
   const int nbands = (nt + BAND - 1) / BAND;
-  const int nsteps = (nt + W - 1) / W;
+  const int nsteps = (int)c->bounds.size() - 1;
   const double m = (double)c->m, pcie = 48e9, rate = 34e12, chain_rate = 20e12;
   const double col_lat = getenv("B2D_COL_LAT_US") ? atof(getenv("B2D_COL_LAT_US")) * 1e-6 : 900e-6;
   const double tile_flops = 2.0 * T * T * T;
@@ -624,21 +663,24 @@ static void plan_bands(Ctx* c, size_t esz) {
     for (int j = j0; j < std::min(j1, nt); ++j) n += nt - j;
     return n;
   };
+  auto deadline = [&](int b) { return band_deadline(c, b * BAND); };
   double t = 0.0;
   int next = 0;
-  while (next < nbands && (next * BAND) / W - 1 < 0) {  // needed by step 0's panel / next-cols
+  while (next < nbands && deadline(next) < 0) {  // needed by step 0's panel / next-cols
     c->act[next] = -1;
     t = std::max(t, arrival[next]);
     ++next;
   }
   for (int st = 0; st < nsteps && next < nbands; ++st) {
-    const int k0 = st * W, ke = std::min(k0 + W, nt), ne = std::min(ke + W, nt);
+    const int k0 = c->bounds[st], ke = c->bounds[st + 1];
+    const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
+    const int W = ke - k0;
     // critical chain of the step (s_main): panel columns + intra-panel and next-cols updates
     const double chain = W * col_lat +
                          (0.5 * W * (W - 1) * (nt - k0) * tile_flops + tiles(ke, ne) * tile_flops * W) /
                              chain_rate;
     double side = 0.0;  // s_side: catch-ups of joining bands + rest over active bands
-    while (next < nbands && (arrival[next] <= t || (next * BAND) / W - 1 <= st)) {
+    while (next < nbands && (arrival[next] <= t || deadline(next) <= st)) {
       c->act[next] = st;
       t = std::max(t, arrival[next]);
       side += tiles(next * BAND, (next + 1) * BAND) * tile_flops * k0;
@@ -933,6 +975,7 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
       if ((rc = ooc_ldl_factor(c, sa, k))) return rc;
     } else {
       cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
+      make_bounds(c, o.tiles(k), false);
       enqueue_factor(c, FactorTarget{o.map(sa), o.tiles(k), (int64_t)k * o.b}, false);
       cudaEventRecord(o.ev_used[sa], c->s_main);
     }
