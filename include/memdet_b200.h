@@ -166,6 +166,16 @@ int b2d_prefix_scan(const double *ell, int64_t m, double *prefix, void *stream);
  * about `seconds`, in TFLOP/s (2 flops per FMA). */
 int b2d_probe_fp64_peak(int device, double seconds, double *tflops);
 
+/* Gram formation straight into an in-core context's packed tiles (BASELINE C3-C5 style
+ * K = G G^T * scale + jitter I, formed chunk by chunk on the device with the engine's own DMMA
+ * Schur kernel; off the timed path): init sets the packed tiles to jitter * I (identity beyond
+ * m), each accumulate adds scale * G G^T for a DEVICE row-major m x k chunk G (leading dimension
+ * ldg), and factor_packed factors the tiles as they are (no input pack). */
+int b2d_ctx_packed_init(b2d_ctx *ctx, double jitter, void *stream);
+int b2d_ctx_gram_accumulate(b2d_ctx *ctx, const double *dev_g, int64_t ldg, int64_t k, double scale,
+                            void *stream);
+int b2d_ctx_factor_packed_async(b2d_ctx *ctx, void *stream);
+
 /* Device input generator (off the timed path): C2 RBF Gram, row-major n x n into dev_out. */
 int b2d_gen_rbf(const double *dev_x, int64_t n, int d, double ell, double jitter, double *dev_out,
                 void *stream);

@@ -73,6 +73,9 @@ SIGNATURES = {
     "b2d_ctx_set_profiling": (_I, [_P, _I]),
     "b2d_ctx_update_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "b2d_gen_rbf": (_I, [_P, _I64, _I, _D, _D, _P, _P]),
+    "b2d_ctx_packed_init": (_I, [_P, _D, _P]),
+    "b2d_ctx_gram_accumulate": (_I, [_P, _P, _I64, _I64, _D, _P]),
+    "b2d_ctx_factor_packed_async": (_I, [_P, _P]),
     "b2d_probe_fp64_peak": (_I, [_I, _D, ctypes.POINTER(_D)]),
     "b2d_tile_potrf_inv": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "b2d_tile_gemm": (_I, [_I, ctypes.POINTER(TileMapC), ctypes.POINTER(TileMapC),

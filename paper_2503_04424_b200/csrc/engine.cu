@@ -117,6 +117,9 @@ struct Ctx {
   double* prefix = nullptr;  // n_pad
   unsigned long long* fail = nullptr;
   double* strip[NSTAGE] = {};  // host-ingest staging strips (128 x n_pad doubles each)
+  double* gram_neg = nullptr;   // Gram formation: -scale * G chunk as tiles
+  double* gram_pos = nullptr;   //                   G chunk as tiles
+  int64_t gram_cap = 0;         // tiles allocated per buffer
   cudaStream_t s_main = nullptr, s_side = nullptr, s_copy = nullptr, s_pack = nullptr;
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_panel, ev_rest, ev_catch, ev_stage, ev_copied, ev_band;
@@ -167,6 +170,8 @@ static void destroy(Ctx* c) {
   cudaFree(c->fail);
   if (c->s_copy) cudaStreamSynchronize(c->s_copy);
   for (auto* p : c->strip) cudaFree(p);
+  cudaFree(c->gram_neg);
+  cudaFree(c->gram_pos);
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
   for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
                   &c->prof_ev})
@@ -1334,6 +1339,62 @@ extern "C" int b2d_pack_tiles(const void* src, int64_t lda, int dtype, int64_t r
 extern "C" int b2d_prefix_scan(const double* ell, int64_t m, double* prefix, void* stream) {
   if (!ell || !prefix || m < 1) return set_err(B2D_ERR_USAGE, "bad b2d_prefix_scan arguments");
   prefix_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ell, m, prefix);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_ctx_packed_init(b2d_ctx* ctx, double jitter, void* stream) {
+  if (!ctx || ctx->ooc) return set_err(B2D_ERR_USAGE, "packed formation needs an in-core context");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  packed_init_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(ctx->tiles, ctx->nt, ctx->m, jitter);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_ctx_gram_accumulate(b2d_ctx* ctx, const double* dev_g, int64_t ldg, int64_t k, double scale,
+                                       void* stream) {
+  if (!ctx || ctx->ooc || !dev_g || k < 1 || ldg < k) return set_err(B2D_ERR_USAGE, "bad gram_accumulate arguments");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int rc = configure_kernels();
+  if (rc) return rc;
+  const int nt = ctx->nt;
+  const int kt = (int)((k + T - 1) / T);
+  const int64_t need = (int64_t)nt * kt;
+  if (need > ctx->gram_cap) {
+    cudaFree(ctx->gram_neg);
+    cudaFree(ctx->gram_pos);
+    ctx->gram_neg = ctx->gram_pos = nullptr;
+    CUDA_TRY(cudaMalloc(&ctx->gram_neg, (size_t)need * TILE_BYTES));
+    CUDA_TRY(cudaMalloc(&ctx->gram_pos, (size_t)need * TILE_BYTES));
+    ctx->gram_cap = need;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const TileMap gneg{ctx->gram_neg, kt, 0, 0, 0}, gpos{ctx->gram_pos, kt, 0, 0, 0};
+  pack_rect_kernel<<<(unsigned)need, 256, 0, s>>>(dev_g, ldg, ctx->m, k, -scale, gneg, kt);
+  pack_rect_kernel<<<(unsigned)need, 256, 0, s>>>(dev_g, ldg, ctx->m, k, 1.0, gpos, kt);
+  // K -= (-scale G) G^T over the packed lower tiles: the engine's DMMA Schur kernel
+  GemmTask t{};
+  t.a = gneg;
+  t.b = gpos;
+  t.c = TileMap{ctx->tiles, 0, nt, 0, 0};
+  t.out = TileSet{0, nt, 0, nt, 1, 0, 0, 0};
+  t.p0 = 0;
+  t.p1 = kt;
+  gemm_kernel<MODE_UPDATE><<<(unsigned)t.out.count(), GEMM_THREADS, GEMM_SMEM, s>>>(t);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+extern "C" int b2d_ctx_factor_packed_async(b2d_ctx* ctx, void* stream) {
+  if (!ctx || ctx->ooc) return set_err(B2D_ERR_USAGE, "factor_packed needs an in-core context");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t user = (cudaStream_t)stream;
+  begin(ctx, user);
+  make_bounds(ctx, ctx->nt, false);
+  std::fill(ctx->act.begin(), ctx->act.end(), -1);
+  enqueue_factor(ctx, FactorTarget{TileMap{ctx->tiles, 0, ctx->nt}, ctx->nt, 0}, false);
+  enqueue_prefix(ctx);
+  end(ctx, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
 }

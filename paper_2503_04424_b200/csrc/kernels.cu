@@ -136,6 +136,52 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_block_kernel(const Tin* __r
   }
 }
 
+// Gram formation helpers.  init: packed lower tiles = jitter * I (identity beyond m, so the
+// padding factors to 1).  pack_rect: a row-major m x k device chunk G into an nt x kt tile grid
+// scaled by `scale` (zero beyond m / k), G's rows along tile rows.
+__global__ void packed_init_kernel(double* __restrict__ tiles, int nt, int64_t m, double jitter) {
+  const int64_t ntiles = n_packed_tiles(nt);
+  for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    // tile-column j: the largest j with col_offset(j, nt) <= tix (quadratic root, then fix up)
+    const double a = nt + 0.5;
+    int j = (int)(a - sqrt(a * a - 2.0 * (double)tix));
+    if (j < 0) j = 0;
+    while (j > 0 && col_offset(j, nt) > tix) --j;
+    while (j + 1 < nt && col_offset(j + 1, nt) <= tix) ++j;
+    const int i = j + (int)(tix - col_offset(j, nt));
+    double* t = tiles + tix * TILE_ELEMS;
+    for (int o = threadIdx.x; o < TILE_ELEMS; o += blockDim.x) {
+      double v = 0.0;
+      if (i == j) {
+        const int r = (o >> 3) & 127, c = ((o >> 10) << 3) + iperm8(o & 7);
+        if (r == c) v = ((int64_t)i * T + r < m) ? jitter : 1.0;
+      }
+      t[o] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) pack_rect_kernel(const double* __restrict__ g, int64_t ldg, int64_t m,
+                                                        int64_t k, double scale, TileMap out, int kt) {
+  __shared__ double sm[32][129];
+  const int I = blockIdx.x / kt, P = blockIdx.x % kt;
+  double* dst = out.tile(I, P);
+  for (int qtr = 0; qtr < 4; ++qtr) {
+    for (int idx = threadIdx.x; idx < 32 * T; idx += 256) {  // rows r, 32 columns: coalesced in c
+      const int r = idx >> 5, c = idx & 31;
+      const int64_t R = (int64_t)I * T + r, C = (int64_t)P * T + 32 * qtr + c;
+      sm[c][r] = (R < m && C < k) ? g[R * ldg + C] * scale : 0.0;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < 32 * T; o += 256) {  // octets 4*qtr .. 4*qtr+3
+      const int r = (o >> 3) & 127;
+      const int c = ((o >> 10) << 3) + iperm8(o & 7);
+      dst[qtr * 32 * T + o] = sm[c][r];
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------ potrf + inverse
 
 // One CTA of 256 threads factors diagonal tile (k, k) in shared memory M[128][129].

@@ -122,3 +122,31 @@ def ntk_like_device(n: int, p: int, alpha: float, jitter: float = 1e-8, seed: in
     # bit-symmetric: mirror the lower triangle onto the upper (kernelgen.py:136-149 precedent)
     k.copy_(torch.tril(k) + torch.tril(k, -1).T)
     return k
+
+
+def gram_into_context(ctx, n: int, k: int, scale: float, jitter: float, seed: int = 0, chunk: int = 8192,
+                      col_scale=None):
+    """Form K = scale * G diag(col_scale)^2 G^T + jitter I directly in an in-core engine
+    context's packed tiles (G: n x k i.i.d. N(0,1) from torch's Philox CUDA generator, drawn
+    chunk by chunk of columns; the rank-k updates run on the engine's DMMA Schur kernel).
+    C4: col_scale=None, scale=1/n; C3/C5: col_scale(j) = j^-alpha, scale = 1/p."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    lib = _native.load()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _native.check(lib.b2d_ctx_packed_init(ctx.handle, jitter, stream), "packed_init")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    for c0 in range(0, k, chunk):
+        c1 = min(k, c0 + chunk)
+        z = torch.randn((n, c1 - c0), dtype=torch.float64, device="cuda", generator=g)
+        if col_scale is not None:
+            z.mul_(col_scale(torch.arange(c0 + 1, c1 + 1, dtype=torch.float64, device="cuda")))
+        _native.check(lib.b2d_ctx_gram_accumulate(ctx.handle, ctypes.c_void_p(z.data_ptr()), c1 - c0, c1 - c0,
+                                                  scale, stream), "gram_accumulate")
+        torch.cuda.current_stream().synchronize()  # z is freed next iteration
+        del z

@@ -313,3 +313,29 @@ def test_pivoted_ldl_prefix_is_permuted_minor_logdet():
             sign, ld = np.linalg.slogdet(a[np.ix_(idx, idx)])
             assert res.prefix_signs[q - 1] == int(sign)
             assert res.prefix[q - 1] == pytest.approx(ld, rel=1e-9, abs=1e-9)
+
+
+def test_gram_formation_in_packed_context_matches_dense():
+    """K = G G^T / n + jitter I formed in the packed tiles by the engine's DMMA kernel, then
+    factored in place, equals the engine's factorisation of the same K formed densely by cuBLAS."""
+    torch = pytest.importorskip("torch")
+    import ctypes
+
+    n, k = 1000, 3000
+    ctx = _native.Context(n)
+    gen.gram_into_context(ctx, n, k, 1.0 / n, 1e-4, seed=5, chunk=1024)
+    _native.check(_native.load().b2d_ctx_factor_packed_async(ctx.handle, None))
+    pre = np.empty(n)
+    rc, fail, info = ctx.fetch(None, pre)
+    _native.check(rc)
+    ctx.close()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    dense = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    for c0 in range(0, k, 1024):
+        z = torch.randn((n, min(k, c0 + 1024) - c0), dtype=torch.float64, device="cuda", generator=g)
+        dense.addmm_(z, z.T)
+    dense.div_(n)
+    dense.diagonal().add_(1e-4)
+    ref, _ = O.memdet_cholesky(dense.cpu().numpy(), 1)
+    assert rel_err(pre, ref) <= 1e-10, rel_err(pre, ref)
