@@ -62,3 +62,40 @@ def test_ldl_tile_restatement_is_exact_on_pivot_order():
     assert d[0] == 3.0 and float(np.prod(d)) == 6.0
     with pytest.raises(O.OracleIndefinite):
         O.ldl_tile(np.zeros((2, 2)))
+
+
+def _ref_ldl():
+    import importlib
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    if not os.path.isdir(ref):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        return importlib.import_module("_ldl")
+    except ImportError:
+        return None
+
+
+@pytest.mark.parametrize("n,seed", [(5, 1), (33, 2), (64, 3), (200, 4)])
+def test_ldl_restatement_bit_exact_vs_reference_compiled_kernel(n, seed):
+    """oracle/ldl_tile.c vs the reference's own compiled _ldl.pyx (built by oracle/build_ref.sh
+    from /root/reference): identical swaps and bit-identical pivots and factors."""
+    ref = _ref_ldl()
+    if ref is None:
+        pytest.skip("oracle/_ref not built (reference not mounted)")
+    from paper_2503_04424_b200 import gen
+
+    a0 = gen.random_symmetric(n, seed=seed)
+    tol = 64.0 * np.finfo(np.float64).eps * np.max(np.abs(a0))
+    a1 = a0.copy()
+    sw1, d1, w1 = np.empty(n, np.int64), np.empty(n), np.empty(n)
+    assert ref.ldl_factor(a1, sw1, d1, w1, tol) == -1
+    a2 = a0.copy()
+    sw2, d2 = O.ldl_tile(a2)
+    np.testing.assert_array_equal(sw1, sw2)
+    np.testing.assert_array_equal(d1, d2)
+    np.testing.assert_array_equal(np.tril(a1, -1), np.tril(a2, -1))
