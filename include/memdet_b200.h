@@ -72,7 +72,8 @@ typedef struct b2d_options {
   int64_t num_blocks;      /* reference n_b for the out-of-core tile walk; 0 = from max_mem  */
   int64_t max_mem;         /* reference byte budget (memdet.py:63-80) when num_blocks is 0   */
   int32_t force_out_of_core; /* 1: stream blocks through HBM even if the matrix fits          */
-  int32_t reserved;
+  int32_t host_scratch;    /* 1: keep the out-of-core scratchpad in pinned host memory even when
+                              it fits in HBM next to the block slots (default: HBM if it fits) */
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;
@@ -102,7 +103,8 @@ int b2d_ctx_create(int device, int64_t m, int mode, b2d_ctx **out);
  * 322-389) over b x b blocks streamed between host memory and HBM, prefetched on copy streams
  * against the DMMA work; b follows num_blocks / max_mem, grown until six blocks fit. */
 int b2d_ctx_create_ex(int device, int64_t m, int mode, const b2d_options *opt, b2d_ctx **out);
-/* 1 if the context runs out of core (then only host inputs are accepted), 0 if in-core. */
+/* 0 in-core; 1 out of core with the scratchpad in pinned host memory; 2 out of core with the
+ * scratchpad in HBM.  Out-of-core contexts accept host inputs only. */
 int b2d_ctx_is_out_of_core(b2d_ctx *ctx);
 int b2d_ctx_destroy(b2d_ctx *ctx);
 /* Enqueue pack + factorisation + prefix of a DEVICE-resident row-major matrix on `stream`

@@ -37,7 +37,7 @@ class RunInfoC(ctypes.Structure):
 class OptionsC(ctypes.Structure):
     _fields_ = [("hbm_budget", ctypes.c_int64), ("num_blocks", ctypes.c_int64),
                 ("max_mem", ctypes.c_int64), ("force_out_of_core", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("host_scratch", ctypes.c_int32)]
 
 
 class TileMapC(ctypes.Structure):
@@ -142,11 +142,12 @@ class Context:
     """Owning wrapper of a b2d_ctx (HBM workspace for one matrix order)."""
 
     def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0, hbm_budget: int = 0,
-                 num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False):
+                 num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False,
+                 host_scratch: bool = False):
         lib = load()
         h = ctypes.c_void_p()
         opt = OptionsC(int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                       int(bool(force_out_of_core)), 0)
+                       int(bool(force_out_of_core)), int(bool(host_scratch)))
         check(lib.b2d_ctx_create_ex(device, m, mode, ctypes.byref(opt), ctypes.byref(h)),
               "b2d_ctx_create_ex")
         self._h = h
@@ -154,7 +155,11 @@ class Context:
         self.mode = mode
         self.device = device
         self.key = (device, m, mode, int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                    bool(force_out_of_core))
+                    bool(force_out_of_core), bool(host_scratch))
+
+    @property
+    def scratch_on_device(self) -> bool:
+        return bool(load().b2d_ctx_is_out_of_core(self._h) == 2)
 
     @property
     def out_of_core(self) -> bool:

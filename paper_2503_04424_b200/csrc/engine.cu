@@ -93,7 +93,8 @@ struct Ooc {
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
   std::map<std::pair<int, int>, cudaEvent_t> ev_key;  // last store of each scratch block
-  std::vector<double*> pool;                       // pinned scratch slots, bound in first-write order
+  std::vector<double*> pool;                       // scratch slots, bound in first-write order
+  bool dev_scratch = false;                        // pool in HBM (fits next to the slots) or pinned host
   std::set<std::pair<int, int>> written;           // cache table of the current run
   int64_t reads = 0, writes = 0;
   int rr = 0;
@@ -200,7 +201,10 @@ static void destroy(Ctx* c) {
   cudaFree(o.part);
   cudaFree(o.amax);
   cudaFree(o.stage);
-  for (double* h : o.pool) cudaFreeHost(h);
+  for (double* h : o.pool) {
+    if (o.dev_scratch) cudaFree(h);
+    else cudaFreeHost(h);
+  }
   for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
   if (o.s_h2d) cudaStreamDestroy(o.s_h2d);
   if (o.s_d2h) cudaStreamDestroy(o.s_d2h);
@@ -395,14 +399,21 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       ALLOC(o.part, (size_t)o.coop_blocks * sizeof(ArgMax));
       ALLOC(o.amax, 8);
     }
-    // pinned scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front
+    // scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front; in HBM
+    // when it fits beside the slots (scratch traffic then moves at HBM instead of PCIe speed),
+    // otherwise in pinned host memory
     const int64_t nsc = o.nb <= 2 ? 0 : ((int64_t)o.nb * o.nb + o.nb - 8) / 2;
+    size_t used = 0, fb = 0, tb = 0;
+    cudaMemGetInfo(&fb, &tb);
+    used = free_b > fb ? free_b - fb : 0;
+    o.dev_scratch = !(opt && opt->host_scratch) && used + (size_t)nsc * o.slot_bytes() <= budget;
     for (int64_t q = 0; q < nsc; ++q) {
       double* h = nullptr;
-      if (cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault) != cudaSuccess) {
+      const cudaError_t e = o.dev_scratch ? cudaMalloc((void**)&h, o.slot_bytes())
+                                          : cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault);
+      if (e != cudaSuccess) {
         destroy(c);
-        return set_err(B2D_ERR_NOMEM, "pinned scratchpad of %lld x %.2f GB failed", (long long)nsc,
-                       o.slot_bytes() / 1e9);
+        return set_err(B2D_ERR_NOMEM, "scratchpad of %lld x %.2f GB failed", (long long)nsc, o.slot_bytes() / 1e9);
       }
       o.pool.push_back(h);
     }
@@ -784,8 +795,8 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
   auto key = std::make_pair(ri, rj);
   if (o.written.count(key)) {
     cudaStreamWaitEvent(o.s_h2d, o.ev_key[key], 0);  // the scratch copy must have landed
-    CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyHostToDevice, o.s_h2d));
-    c->h2d += (int64_t)o.slot_bytes();
+    CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyDefault, o.s_h2d));
+    if (!o.dev_scratch) c->h2d += (int64_t)o.slot_bytes();
   } else {
     const size_t esz = dtype == B2D_F64 ? 8 : 4;
     const int64_t rows_blk = o.size(rj), cols_blk = o.size(ri);  // engine block: rows of rj, cols of ri
@@ -823,7 +834,7 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
     it = o.scratch.emplace(key, o.pool[o.scratch.size()]).first;
   }
   cudaStreamWaitEvent(o.s_d2h, o.ev_used[s], 0);
-  CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDeviceToHost, o.s_d2h));
+  CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDefault, o.s_d2h));
   cudaEventRecord(o.ev_stored[s], o.s_d2h);
   auto ek = o.ev_key.find(key);
   if (ek == o.ev_key.end()) {
@@ -832,7 +843,7 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
     ek = o.ev_key.emplace(key, e).first;
   }
   cudaEventRecord(ek->second, o.s_d2h);
-  c->d2h += (int64_t)o.slot_bytes();
+  if (!o.dev_scratch) c->d2h += (int64_t)o.slot_bytes();
   o.written.insert(key);
   o.writes++;
   return B2D_OK;
@@ -1120,7 +1131,7 @@ int b2d_ctx_create(int device, int64_t m, int mode, b2d_ctx** out) {
   return b2d_ctx_create_ex(device, m, mode, nullptr, out);
 }
 
-int b2d_ctx_is_out_of_core(b2d_ctx* ctx) { return ctx && ctx->ooc ? 1 : 0; }
+int b2d_ctx_is_out_of_core(b2d_ctx* ctx) { return ctx && ctx->ooc ? (ctx->o.dev_scratch ? 2 : 1) : 0; }
 
 int b2d_ctx_create_ex(int device, int64_t m, int mode, const b2d_options* opt, b2d_ctx** out) {
   if (!out) return set_err(B2D_ERR_USAGE, "null out pointer");

@@ -339,3 +339,21 @@ def test_gram_formation_in_packed_context_matches_dense():
     dense.diagonal().add_(1e-4)
     ref, _ = O.memdet_cholesky(dense.cpu().numpy(), 1)
     assert rel_err(pre, ref) <= 1e-10, rel_err(pre, ref)
+
+
+@pytest.mark.parametrize("host_scratch", [False, True])
+def test_out_of_core_scratch_placement(host_scratch):
+    """Scratchpad in HBM (fits) or pinned host memory: same walk, same numbers, same counters."""
+    m, nb = 1100, 5
+    a = gen.rbf(m, seed=21)
+    ctx = _native.Context(m, num_blocks=nb, force_out_of_core=True, host_scratch=host_scratch)
+    assert ctx.out_of_core and ctx.scratch_on_device == (not host_scratch)
+    ctx.factor_host_async(a.ctypes.data, m, _native.B2D_F64, 0)
+    pre = np.empty(m)
+    rc, fail, info = ctx.fetch(None, pre)
+    _native.check(rc)
+    ctx.close()
+    ref, rinfo = O.memdet_cholesky(a, nb)
+    assert rel_err(pre, ref) <= 1e-10
+    assert (info.ooc_reads, info.ooc_writes, info.ooc_scratch) == (rinfo.blocks_read, rinfo.blocks_written,
+                                                                    rinfo.scratch_slots)
