@@ -395,7 +395,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       int per_sm = 0, sms = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ldl_pivot_kernel, LDL_THREADS, 0);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      o.coop_blocks = std::max(1, std::min(per_sm, 2) * sms);
+      o.coop_blocks = std::max(1, std::min(per_sm * sms, getenv("B2D_LDL_BLOCKS") ? atoi(getenv("B2D_LDL_BLOCKS")) : 4 * sms));
       ALLOC(o.part, (size_t)o.coop_blocks * sizeof(ArgMax));
       ALLOC(o.amax, 8);
     }

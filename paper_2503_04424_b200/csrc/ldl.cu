@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(LDL_THREADS) ldl_pivot_kernel(double* __restri
     block_argmax(a);
   }
   grid.sync();
+  // Two grid barriers per column: S(r) finishes column r-1 (L = c / p) while swapping r <-> t,
+  // U(r) checks the pivot and applies the rank-1 update with the unscaled column r.
   for (int64_t r = 0; r < n; ++r) {
     // --- S: pivot t = argmax over the partials, symmetric swap r <-> t (_ldl.pyx:38-46)
     if (wib == 0) {
@@ -120,10 +122,21 @@ __global__ void __launch_bounds__(LDL_THREADS) ldl_pivot_kernel(double* __restri
     __syncthreads();
     const int64_t t = s_t;
     if (gtid == 0) swaps[r] = t;
+    const int64_t q = r - 1;                       // column finished in this phase
+    const double invq = q >= 0 ? 1.0 / d[q] : 1.0;  // d[q] written by gtid 0 in U(q), visible after the sync
+    if (q >= 0) {
+      // a_iq = a_iq * (1/p) for i > q (_ldl.pyx:59-60), rows r and t via the swap below
+      for (int64_t i = q + 1 + gtid; i < n; i += gthreads)
+        if (i != r && i != t) A[q * ld + i] = __dmul_rn(A[q * ld + i], invq);
+    }
     if (t != r) {
       for (int64_t j = gtid; j < r; j += gthreads) {  // rows r and t of the L part
-        const double x = A[j * ld + r];
-        A[j * ld + r] = A[j * ld + t];
+        double x = A[j * ld + r], y = A[j * ld + t];
+        if (j == q) {
+          x = __dmul_rn(x, invq);
+          y = __dmul_rn(y, invq);
+        }
+        A[j * ld + r] = y;
         A[j * ld + t] = x;
       }
       if (gtid == 0) {
@@ -141,6 +154,8 @@ __global__ void __launch_bounds__(LDL_THREADS) ldl_pivot_kernel(double* __restri
         A[r * ld + i] = A[t * ld + i];
         A[t * ld + i] = x;
       }
+    } else if (q >= 0 && gtid == 0) {
+      A[q * ld + r] = __dmul_rn(A[q * ld + r], invq);
     }
     grid.sync();
     // --- U: pivot check, rank-1 update of the trailing lower triangle, next candidates
@@ -161,10 +176,8 @@ __global__ void __launch_bounds__(LDL_THREADS) ldl_pivot_kernel(double* __restri
     }
     block_argmax(cand);
     grid.sync();
-    // --- W: column r of L (a_ir = a_ir * (1/p))
-    for (int64_t i = r + 1 + gtid; i < n; i += gthreads) A[r * ld + i] = __dmul_rn(A[r * ld + i], invp);
-    grid.sync();
   }
+  // the last column has no rows below it; column n-2 was finished in S(n-1)
 }
 
 // swaps -> block permutation (kernels/dense.py:25-30), global perm (memdet.py:352-353),
