@@ -49,10 +49,11 @@ static int set_err(int code, const char* fmt, ...) {
   } while (0)
 
 // outer panel width in tiles: the trailing Schur update runs with K = panel_tiles * 128
-// (default 8; B2D_PANEL_TILES overrides for tuning)
+// (default 16, narrowed to 8 for the last 64 tile-columns where the potrf chain is the critical
+// path; B2D_PANEL_TILES / B2D_TAIL_TILES / B2D_TAIL_W override for tuning)
 static int panel_tiles_default() {
   const char* e = getenv("B2D_PANEL_TILES");
-  int w = e ? atoi(e) : 8;
+  int w = e ? atoi(e) : 16;
   return w < 1 ? 1 : (w > 16 ? 16 : w);
 }
 
@@ -122,6 +123,8 @@ struct Ctx {
   double* gram_pos = nullptr;   //                   G chunk as tiles
   int64_t gram_cap = 0;         // tiles allocated per buffer
   cudaStream_t s_main = nullptr, s_side = nullptr, s_copy = nullptr, s_pack = nullptr;
+  cudaStream_t s_mid = nullptr;  // panel work off the potrf chain (rows below the panel block)
+  cudaEvent_t ev_m2s = nullptr;  // s_main -> s_mid hand-off (potrf + in-block solve of a column)
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ev_panel, ev_rest, ev_catch, ev_stage, ev_copied, ev_band;
   // band activation (host ingest): band b = tile-columns [b*BAND, (b+1)*BAND) joins the
@@ -163,6 +166,7 @@ static void destroy(Ctx* c) {
   cudaSetDevice(c->device);
   if (c->s_main) cudaStreamSynchronize(c->s_main);
   if (c->s_side) cudaStreamSynchronize(c->s_side);
+  if (c->s_mid) cudaStreamSynchronize(c->s_mid);
   cudaFree(c->tiles);
   cudaFree(c->inv);
   cudaFree(c->ell);
@@ -180,7 +184,9 @@ static void destroy(Ctx* c) {
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_stop) cudaEventDestroy(c->ev_stop);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_m2s) cudaEventDestroy(c->ev_m2s);
   if (c->s_main) cudaStreamDestroy(c->s_main);
+  if (c->s_mid) cudaStreamDestroy(c->s_mid);
   if (c->s_side) cudaStreamDestroy(c->s_side);
   if (c->s_copy) cudaStreamDestroy(c->s_copy);
   if (c->s_pack) cudaStreamDestroy(c->s_pack);
@@ -273,12 +279,14 @@ static int create_streams_events(Ctx* c) {
   // panel chain (critical path) and ingest get the highest priority; trailing updates the lowest
   if (cudaStreamCreateWithPriority(&c->s_main, cudaStreamNonBlocking, hi) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->s_side, cudaStreamNonBlocking, lo) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->s_mid, cudaStreamNonBlocking, (lo + hi) / 2) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->s_copy, cudaStreamNonBlocking, hi) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->s_pack, cudaStreamNonBlocking, hi) != cudaSuccess)
     return set_err(B2D_ERR_CUDA, "stream creation failed");
   cudaEventCreate(&c->ev_start);
   cudaEventCreate(&c->ev_stop);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_m2s, cudaEventDisableTiming);
   const int nsteps = c->nt;  // enough for any panel-width schedule
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
@@ -459,19 +467,26 @@ static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, boo
   }
 }
 
-// Schur update of the target's lower tiles in tile-columns [j0, j1) with K tile-columns [p0, p1)
-static void launch_update(Ctx* c, cudaStream_t s, const FactorTarget& ft, int j0, int j1, int p0, int p1,
-                          bool prof) {
+// Schur update of the output tiles `out` of the target with K tile-columns [p0, p1)
+static void launch_update_set(Ctx* c, cudaStream_t s, const FactorTarget& ft, const TileSet& out, int p0, int p1,
+                              bool prof) {
   GemmTask t{};
   t.a = t.b = t.c = ft.map;
-  t.out = TileSet{0, ft.nt, j0, std::min(j1, ft.nt), 1, 0};
+  t.out = out;
   t.p0 = p0;
   t.p1 = p1;
   // algorithmic flops: off-diagonal tiles 2*T*T*K, diagonal (SYRK, lower half) T*(T+1)*K
   const double K = (double)(p1 - p0) * T;
   const int64_t ntile = t.out.count();
-  const int64_t ndiag = std::max(0, t.out.j1 - t.out.j0);
+  int64_t ndiag = 0;
+  for (int j = out.j0; j < out.j1; ++j) ndiag += j >= out.lo(j) && j < out.i1;
   launch_gemm(c, s, MODE_UPDATE, t, prof, (double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
+}
+
+// Schur update of the target's lower tiles in tile-columns [j0, j1) with K tile-columns [p0, p1)
+static void launch_update(Ctx* c, cudaStream_t s, const FactorTarget& ft, int j0, int j1, int p0, int p1,
+                          bool prof) {
+  launch_update_set(c, s, ft, TileSet{0, ft.nt, j0, std::min(j1, ft.nt), 1, 0}, p0, p1, prof);
 }
 
 // Outer-panel schedule: W tile-columns per panel, narrowed to head_w for the first head tiles
@@ -484,8 +499,8 @@ static int env_int(const char* name, int dflt) {
 
 static void make_bounds(Ctx* c, int nt, bool host) {
   const int W = c->W_TILES;
-  const int head = host ? env_int("B2D_HEAD_TILES", 0) : 0, head_w = std::max(1, env_int("B2D_HEAD_W", 4));
-  const int tail = env_int("B2D_TAIL_TILES", 0), tail_w = std::max(1, env_int("B2D_TAIL_W", 4));
+  const int head = env_int(host ? "B2D_HEAD_TILES" : "B2D_DEV_HEAD_TILES", 0), head_w = std::max(1, env_int("B2D_HEAD_W", 4));
+  const int tail = env_int("B2D_TAIL_TILES", 64), tail_w = std::max(1, env_int("B2D_TAIL_W", 8));
   c->bounds.clear();
   int k = 0;
   while (k < nt) {
@@ -510,19 +525,21 @@ static int band_deadline(const Ctx* c, int col) {
   return nsteps - 1;
 }
 
-static void launch_panel_column(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p) {
-  double* invp = c->inv + (int64_t)p * TILE_ELEMS;
-  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(ft.map.tile(p, p), invp, c->ell, c->diag, c->fail,
-                                                         ft.g0 + (int64_t)p * T, c->m);
+static void launch_potrf(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p) {
+  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM, s>>>(ft.map.tile(p, p), c->inv + (int64_t)p * TILE_ELEMS, c->ell,
+                                                         c->diag, c->fail, ft.g0 + (int64_t)p * T, c->m);
   c->launches++;
-  if (p + 1 < ft.nt) {
-    GemmTask t{};
-    t.c = ft.map;
-    t.binv = invp;
-    t.out = TileSet{0, ft.nt, p, p + 1, 1, 1};
-    t.k = p;
-    launch_gemm(c, s, MODE_TRSM, t, false, 0.0);
-  }
+}
+
+// L(i, p) = A(i, p) L_pp^-T for rows i in [i0, i1)
+static void launch_trsm(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p, int i0, int i1) {
+  if (i1 <= i0) return;
+  GemmTask t{};
+  t.c = ft.map;
+  t.binv = c->inv + (int64_t)p * TILE_ELEMS;
+  t.out = TileSet{i0, i1, p, p + 1, 0, 0};
+  t.k = p;
+  launch_gemm(c, s, MODE_TRSM, t, false, 0.0);
 }
 
 // The factorisation proper of ft (streams s_main / s_side, joined back into s_main).
@@ -538,6 +555,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
   const int nbands = (nt + BAND - 1) / BAND;
   cudaEventRecord(c->ev_join, c->s_main);
   cudaStreamWaitEvent(c->s_side, c->ev_join, 0);
+  cudaStreamWaitEvent(c->s_mid, c->ev_join, 0);
   if (wait_bands) {
     for (int b = 0; b < nbands; ++b)
       if (c->act[b] < 0) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
@@ -546,20 +564,32 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
   for (int st = 0; st < nsteps; ++st) {
     const int k0 = c->bounds[st];
     const int ke = c->bounds[st + 1];
-    // panel(k0): its columns were last touched by next-cols(st-1) (same stream) and rest(st-2)
+    // panel(k0): its columns were last touched by next-cols(st-1) and rest(st-2)
     if (st >= 2) cudaStreamWaitEvent(c->s_main, c->ev_rest[st - 2], 0);
+    // The panel's diagonal block [k0, ke)^2 is factored on s_main (potrf, in-block solve and
+    // in-block update per column: the critical chain touches at most W(W+1)/2 tiles); the rows
+    // below it ([ke, nt): solve and update) follow each column on s_mid.  Every tile still
+    // sees the same launches in the same order, so results do not depend on the split.
     for (int p = k0; p < ke; ++p) {
       if (wait_bands) {
         // an initial band must be in HBM before the first panel column that reads it (the
-        // intra-panel update touches columns up to ke-1)
+        // panel's updates touch columns up to ke-1)
         const int need = std::min(nbands, (ke - 1) / BAND + 1);
         while (main_waited < need && c->act[main_waited] < 0)
           cudaStreamWaitEvent(c->s_main, c->ev_band[main_waited++], 0);
       }
-      launch_panel_column(c, c->s_main, ft, p);
-      if (p + 1 < ke) launch_update(c, c->s_main, ft, p + 1, ke, p, p + 1, false);
+      launch_potrf(c, c->s_main, ft, p);
+      launch_trsm(c, c->s_main, ft, p, p + 1, ke);
+      cudaEventRecord(c->ev_m2s, c->s_main);
+      cudaStreamWaitEvent(c->s_mid, c->ev_m2s, 0);
+      launch_trsm(c, c->s_mid, ft, p, ke, nt);
+      if (p + 1 < ke) {
+        launch_update_set(c, c->s_main, ft, TileSet{p + 1, ke, p + 1, ke, 1, 0}, p, p + 1, false);
+        if (ke < nt) launch_update_set(c, c->s_mid, ft, TileSet{ke, nt, p + 1, ke, 0, 0}, p, p + 1, false);
+      }
     }
-    cudaEventRecord(c->ev_panel[st], c->s_main);
+    // the whole panel is solved once s_mid gets here (s_mid waited for every in-block solve)
+    cudaEventRecord(c->ev_panel[st], c->s_mid);
     if (ke >= nt) break;
     const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
     // catch-up of the bands that join at this step (panels of steps < st, already factored)
@@ -575,16 +605,23 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
       }
     }
     cudaEventRecord(c->ev_catch[st], c->s_side);
-    // next-cols(k0): the next panel's columns, on the critical path
+    // next-cols(k0): the next panel's columns [ke, ne); its diagonal block on s_main (the next
+    // potrf chain starts as soon as it is done), the rows below on s_mid.  Both follow rest(st-1)
+    // and the catch-ups (ev_catch) and the whole panel solve (ev_panel).
     cudaStreamWaitEvent(c->s_main, c->ev_catch[st], 0);
-    launch_update(c, c->s_main, ft, ke, ne, k0, ke, false);
+    cudaStreamWaitEvent(c->s_main, c->ev_panel[st], 0);
+    launch_update_set(c, c->s_main, ft, TileSet{ke, ne, ke, ne, 1, 0}, k0, ke, false);
+    cudaStreamWaitEvent(c->s_mid, c->ev_catch[st], 0);
+    if (ne < nt) launch_update_set(c, c->s_mid, ft, TileSet{ne, nt, ke, ne, 0, 0}, k0, ke, false);
     // rest(k0): active columns right of the next panel, overlapping the next panel
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
     launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
   }
-  // join the side stream
+  // join the side streams
   cudaEventRecord(c->ev_join, c->s_side);
+  cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+  cudaEventRecord(c->ev_join, c->s_mid);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
 }
 
@@ -603,6 +640,7 @@ static void begin(Ctx* c, cudaStream_t user) {
   cudaEventRecord(c->ev_start, user);
   cudaStreamWaitEvent(c->s_main, c->ev_start, 0);
   cudaStreamWaitEvent(c->s_side, c->ev_start, 0);
+  cudaStreamWaitEvent(c->s_mid, c->ev_start, 0);
   cudaStreamWaitEvent(c->s_copy, c->ev_start, 0);
   cudaStreamWaitEvent(c->s_pack, c->ev_start, 0);
   cudaMemsetAsync(c->fail, 0xff, 8, c->s_main);
