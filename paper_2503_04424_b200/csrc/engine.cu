@@ -150,8 +150,10 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)GEMM_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(potrf_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)POTRF_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(pack_tiles_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
@@ -662,10 +664,10 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
   begin(c, user);
   const unsigned ntiles = (unsigned)n_packed_tiles(c->nt);
   if (dtype == B2D_F64)
-    pack_tiles_kernel<double><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
+    pack_tiles_kernel<double, 32><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
         (const double*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   else
-    pack_tiles_kernel<float><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
+    pack_tiles_kernel<float, 32><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_main>>>(
         (const float*)a, lda, 0, c->m, c->tiles, c->nt, 0);
   c->launches++;
   // Lazy trailing updates: band b (BAND tile-columns) joins the right-looking updates only
@@ -780,10 +782,10 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
     cudaStreamWaitEvent(c->s_pack, c->ev_copied[b], 0);
     const unsigned ntile = (unsigned)(c->nt - J);
     if (dtype == B2D_F64)
-      pack_tiles_kernel<double><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+      pack_tiles_kernel<double, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
           (const double*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
     else
-      pack_tiles_kernel<float><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+      pack_tiles_kernel<float, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
           (const float*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
     c->launches++;
     cudaEventRecord(c->ev_stage[b], c->s_pack);

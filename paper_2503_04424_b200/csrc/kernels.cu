@@ -26,31 +26,28 @@ namespace b2d {
 // Two passes of 64 columns keep shared memory at 66 KB, so a pack CTA co-resides with a
 // Schur-update CTA (128 KB) on one SM while host strips stream in under the factorisation.
 constexpr int PACK_THREADS = 256;
-constexpr size_t PACK_SMEM = (size_t)64 * 129 * 8;
+constexpr int PACK_LD = 130;  // staging row pitch: conflict-free octet-order reads (2c + r mod 16)
+constexpr size_t PACK_SMEM = (size_t)64 * PACK_LD * 8;
 
-template <typename Tin>
-__global__ void __launch_bounds__(PACK_THREADS) pack_tiles_kernel(const Tin* __restrict__ src,
-                                                                  int64_t lda, int64_t row_base,
-                                                                  int64_t m,
-                                                                  double* __restrict__ tiles,
-                                                                  int nt, int j_lo) {
-  extern __shared__ double sm[];  // [64][129]: sm[c*129 + r] for the current 64 columns
-  int64_t b = blockIdx.x;
-  int J = j_lo;
-  while (b >= nt - J) { b -= nt - J; ++J; }
-  const int I = J + (int)b;
+// One 128 x 128 tile through shared memory: element (r, c) = ld(r, c), where a tile column c
+// is a contiguous source row.  NLOAD loads per thread are issued before the first use, so a
+// CTA keeps 256 * NLOAD * 8 bytes in flight; the octet-layout writes are contiguous.
+template <int NLOAD, typename F>
+__device__ __forceinline__ void pack_tile_body(double* sm, double* __restrict__ dst, F ld) {
   const int tid = threadIdx.x;
-  const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
-  double* out = tiles + tile_index(I, J, nt) * TILE_ELEMS;
   for (int half = 0; half < 2; ++half) {
-#pragma unroll 8
-    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
-      const int c = idx >> 7, r = idx & 127;
-      const int64_t R = R0 + r, C = C0 + 64 * half + c;
-      double v;
-      if (R < m && C < m) v = (double)src[(C - row_base) * lda + R];
-      else v = (R == C) ? 1.0 : 0.0;
-      sm[c * 129 + r] = v;
+    for (int k0 = 0; k0 < 32; k0 += NLOAD) {
+      double v[NLOAD];
+#pragma unroll
+      for (int k = 0; k < NLOAD; ++k) {
+        const int idx = tid + (k0 + k) * PACK_THREADS;
+        v[k] = ld(idx & 127, 64 * half + (idx >> 7));
+      }
+#pragma unroll
+      for (int k = 0; k < NLOAD; ++k) {
+        const int idx = tid + (k0 + k) * PACK_THREADS;
+        sm[(idx >> 7) * PACK_LD + (idx & 127)] = v[k];
+      }
     }
     __syncthreads();
     // octets 8*half .. 8*half+7 are the contiguous half-tile [half*8192, half*8192 + 8192)
@@ -58,17 +55,35 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_tiles_kernel(const Tin* __r
     for (int o = tid; o < 64 * T; o += PACK_THREADS) {
       const int r = (o >> 3) & 127;
       const int c = ((o >> 10) << 3) + iperm8(o & 7);  // 0..63 within this half
-      out[half * 64 * T + o] = sm[c * 129 + r];
+      dst[half * 64 * T + o] = sm[c * PACK_LD + r];
     }
     __syncthreads();
   }
+}
+
+// NLOAD = 32: whole-matrix pack from HBM (nothing else runs; 2 CTAs per SM); NLOAD = 8 keeps
+// 64 registers so that strip packs co-reside with Schur-update CTAs during host ingest.
+template <typename Tin, int NLOAD>
+__global__ void __launch_bounds__(PACK_THREADS, NLOAD >= 32 ? 2 : 4)
+    pack_tiles_kernel(const Tin* __restrict__ src, int64_t lda, int64_t row_base, int64_t m,
+                      double* __restrict__ tiles, int nt, int j_lo) {
+  extern __shared__ double sm[];  // [64][PACK_LD]: sm[c*PACK_LD + r] for the current 64 columns
+  int64_t b = blockIdx.x;
+  int J = j_lo;
+  while (b >= nt - J) { b -= nt - J; ++J; }
+  const int I = J + (int)b;
+  const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
+  pack_tile_body<NLOAD>(sm, tiles + tile_index(I, J, nt) * TILE_ELEMS, [&](int r, int c) {
+    const int64_t R = R0 + r, C = C0 + c;
+    return (R < m && C < m) ? (double)src[(C - row_base) * lda + R] : ((R == C) ? 1.0 : 0.0);
+  });
 }
 
 // Distributed ingest: the tiles of a TileSet (rows possibly local indices of a row-cyclic
 // distribution, global row = i * stride + off) from a row-major source (first stored row
 // row_base) into map `out` at (local row, column).  Same element rule as pack_tiles_kernel.
 template <typename Tin>
-__global__ void __launch_bounds__(PACK_THREADS) pack_set_kernel(const Tin* __restrict__ src, int64_t lda,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_set_kernel(const Tin* __restrict__ src, int64_t lda,
                                                                 int64_t row_base, int64_t m, TileMap out,
                                                                 TileSet set) {
   extern __shared__ double sm[];
@@ -76,28 +91,11 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_set_kernel(const Tin* __res
   tile_order(blockIdx.x, set, 1, &li, &J);
   const int st = set.stride > 1 ? set.stride : 1;
   const int I = li * st + set.off;
-  const int tid = threadIdx.x;
   const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
-  double* dst = out.tile(li, J);
-  for (int half = 0; half < 2; ++half) {
-#pragma unroll 8
-    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
-      const int c = idx >> 7, r = idx & 127;
-      const int64_t R = R0 + r, C = C0 + 64 * half + c;
-      double v;
-      if (R < m && C < m) v = (double)src[(C - row_base) * lda + R];
-      else v = (R == C) ? 1.0 : 0.0;
-      sm[c * 129 + r] = v;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int o = tid; o < 64 * T; o += PACK_THREADS) {
-      const int r = (o >> 3) & 127;
-      const int c = ((o >> 10) << 3) + iperm8(o & 7);
-      dst[half * 64 * T + o] = sm[c * 129 + r];
-    }
-    __syncthreads();
-  }
+  pack_tile_body<8>(sm, out.tile(li, J), [&](int r, int c) {
+    const int64_t R = R0 + r, C = C0 + c;
+    return (R < m && C < m) ? (double)src[(C - row_base) * lda + R] : ((R == C) ? 1.0 : 0.0);
+  });
 }
 
 // Out-of-core block ingest: one 128-row strip of the row-major file (rows = the block's
@@ -106,34 +104,17 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_set_kernel(const Tin* __res
 // identity on a diagonal block and zero elsewhere.  src points at element (first strip row,
 // first block row) of the file, leading dimension lda.
 template <typename Tin>
-__global__ void __launch_bounds__(PACK_THREADS) pack_block_kernel(const Tin* __restrict__ src,
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_block_kernel(const Tin* __restrict__ src,
                                                                   int64_t lda, int64_t rows_valid,
                                                                   int64_t cols_valid, int diag,
                                                                   TileMap out, int J) {
   extern __shared__ double sm[];
   const int I = blockIdx.x;
-  const int tid = threadIdx.x;
   const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
-  double* dst = out.tile(I, J);
-  for (int half = 0; half < 2; ++half) {
-#pragma unroll 8
-    for (int idx = tid; idx < 64 * T; idx += PACK_THREADS) {
-      const int c = idx >> 7, r = idx & 127;
-      const int64_t R = R0 + r, C = C0 + 64 * half + c;
-      double v;
-      if (R < rows_valid && C < cols_valid) v = (double)src[(C - C0) * lda + R];
-      else v = (diag && R == C) ? 1.0 : 0.0;
-      sm[c * 129 + r] = v;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int o = tid; o < 64 * T; o += PACK_THREADS) {
-      const int r = (o >> 3) & 127;
-      const int c = ((o >> 10) << 3) + iperm8(o & 7);
-      dst[half * 64 * T + o] = sm[c * 129 + r];
-    }
-    __syncthreads();
-  }
+  pack_tile_body<8>(sm, out.tile(I, J), [&](int r, int c) {
+    const int64_t R = R0 + r, C = C0 + c;
+    return (R < rows_valid && C < cols_valid) ? (double)src[(C - C0) * lda + R] : ((diag && R == C) ? 1.0 : 0.0);
+  });
 }
 
 // Gram formation helpers.  init: packed lower tiles = jitter * I (identity beyond m, so the
