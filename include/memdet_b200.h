@@ -122,10 +122,11 @@ int b2d_ctx_fetch(b2d_ctx *ctx, double *d_out, double *prefix_out, int64_t *fail
 int b2d_ctx_fetch_perm(b2d_ctx *ctx, int64_t *perm_out);
 /* Device pointer of the prefix vector (m doubles), valid until the next factorisation. */
 const double *b2d_ctx_device_prefix(b2d_ctx *ctx);
-/* Dominant-kernel accounting (the trailing "rest" Schur-update GEMM launches of the last
- * factorisation; they run back to back on one stream, ~95% of the flops): algorithmic flops,
- * summed CUDA-event duration (ms) and launch count.  Enabled by b2d_ctx_set_profiling(ctx, 1);
- * adds one event pair per such launch. */
+/* Dominant-kernel accounting: the trailing "rest" Schur-update GEMM launches of the last
+ * factorisation (~75% of the flops): algorithmic flops, summed CUDA-event duration (ms) and
+ * launch count.  b2d_ctx_set_profiling(ctx, mode): 0 off; 1 events around those launches in a
+ * normal run (where they share the GPU with the panel streams); 2 the same in a serialised
+ * replay (every launch on one stream, so each event pair times the kernel alone). */
 int b2d_ctx_set_profiling(b2d_ctx *ctx, int on);
 int b2d_ctx_update_stats(b2d_ctx *ctx, double *flops, double *ms, int64_t *launches);
 

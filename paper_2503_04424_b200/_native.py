@@ -192,8 +192,10 @@ class Context:
     def device_prefix_ptr(self) -> int:
         return load().b2d_ctx_device_prefix(self._h)
 
-    def set_profiling(self, on: bool):
-        check(load().b2d_ctx_set_profiling(self._h, int(on)))
+    def set_profiling(self, mode: int):
+        """0 off; events on the trailing rest-update launches: 1 in a normal run, 2 in a
+        serialised replay (b2d_ctx_set_profiling)."""
+        check(load().b2d_ctx_set_profiling(self._h, int(mode)))
 
     def update_stats(self):
         f, ms, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()

@@ -131,7 +131,7 @@ struct Ctx {
   // right-looking updates at outer step act[b] (-1: from the start) after one catch-up update
   std::vector<int> act;
   bool trace = false;  // B2D_TRACE: print a per-step event timeline on fetch
-  bool profiling = false;
+  int profiling = 0;  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
   int64_t launches = 0;
@@ -451,7 +451,7 @@ static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, boo
   if (ntile <= 0) return;
   if (mode == MODE_UPDATE && t.p1 <= t.p0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (prof && c->profiling) {
+  if (c->profiling && prof) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
@@ -551,6 +551,14 @@ static void launch_trsm(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p, i
 // rest updates from step s on.  act[b] <= the step whose next-cols update first touches band b,
 // so every column is current before it is factored.
 static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
+  // profiling mode 2: every launch on s_main (serialised replay: per-launch event times are the
+  // kernel's own, nothing runs beside it)
+  struct Restore {
+    Ctx* c;
+    cudaStream_t side, mid;
+    ~Restore() { c->s_side = side; c->s_mid = mid; }
+  } restore{c, c->s_side, c->s_mid};
+  if (c->profiling == 2) c->s_side = c->s_mid = c->s_main;
   const int nt = ft.nt;
   if (c->bounds.empty() || c->bounds.back() != nt) make_bounds(c, nt, false);
   const int nsteps = (int)c->bounds.size() - 1;
@@ -1211,7 +1219,7 @@ int b2d_ctx_fetch_perm(b2d_ctx* ctx, int64_t* perm_out) {
 
 int b2d_ctx_set_profiling(b2d_ctx* ctx, int on) {
   if (!ctx) return set_err(B2D_ERR_USAGE, "null ctx");
-  ctx->profiling = on != 0;
+  ctx->profiling = on < 0 ? 0 : (on > 2 ? 2 : on);
   return B2D_OK;
 }
 
