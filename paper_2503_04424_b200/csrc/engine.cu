@@ -87,9 +87,9 @@ struct Ooc {
   int64_t* perm_local = nullptr;
   int64_t* perm_global = nullptr;
   double* dblk = nullptr;
-  void* part = nullptr;
   unsigned long long* amax = nullptr;
-  int coop_blocks = 0;
+  uint8_t* ltag = nullptr;  // blocked pivoted LDL: per-entry tags, panel columns C / W, diagonal, pivot column
+  double *lC = nullptr, *lW = nullptr, *ldiag = nullptr, *lcol = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
@@ -206,8 +206,12 @@ static void destroy(Ctx* c) {
   cudaFree(o.perm_local);
   cudaFree(o.perm_global);
   cudaFree(o.dblk);
-  cudaFree(o.part);
   cudaFree(o.amax);
+  cudaFree(o.ltag);
+  cudaFree(o.lC);
+  cudaFree(o.lW);
+  cudaFree(o.ldiag);
+  cudaFree(o.lcol);
   cudaFree(o.stage);
   for (double* h : o.pool) {
     if (o.dev_scratch) cudaFree(h);
@@ -402,12 +406,12 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       ALLOC(o.perm_local, (size_t)ld * 8);
       ALLOC(o.perm_global, (size_t)(m + ld) * 8);
       ALLOC(o.dblk, (size_t)ld * 8);
-      int per_sm = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ldl_pivot_kernel, LDL_THREADS, 0);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-      o.coop_blocks = std::max(1, std::min(per_sm * sms, getenv("B2D_LDL_BLOCKS") ? atoi(getenv("B2D_LDL_BLOCKS")) : 4 * sms));
-      ALLOC(o.part, (size_t)o.coop_blocks * sizeof(ArgMax));
       ALLOC(o.amax, 8);
+      ALLOC(o.ltag, (size_t)ld * ld);
+      ALLOC(o.lC, (size_t)LDL_NB * ld * 8);
+      ALLOC(o.lW, (size_t)LDL_NB * ld * 8);
+      ALLOC(o.ldiag, (size_t)ld * 8);
+      ALLOC(o.lcol, (size_t)ld * 8);
     }
     // scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front; in HBM
     // when it fits beside the slots (scratch traffic then moves at HBM instead of PCIe speed),
@@ -970,11 +974,19 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
   unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld);
   cudaMemsetAsync(o.amax, 0, 8, s);
   block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
-  double* A = o.dense;
-  ArgMax* part = (ArgMax*)o.part;
-  int64_t g0v = g0;
-  void* args[] = {&A, (void*)&ld, &n, &o.amax, &o.dblk, &o.swaps, &part, &c->fail, &g0v};
-  CUDA_TRY(cudaLaunchCooperativeKernel((void*)ldl_pivot_kernel, dim3(o.coop_blocks), dim3(LDL_THREADS), args, 0, s));
+  // blocked pivoted LDL: panels of LDL_NB steps (one CTA), then the delayed trailing update
+  const LdlArgs g{o.dense, o.ltag, o.lC, o.lW, o.ldiag, o.lcol, o.dblk, o.swaps, c->fail, o.amax, ld, n, g0};
+  cudaMemsetAsync(o.ltag, 0, (size_t)ld * ld, s);
+  ldl_diag_init_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(g);
+  c->launches += 1;
+  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB) {
+    const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
+    ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
+    ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, ((n - r0) * nbk + 255) / 256)), 256, 0, s>>>(g, r0, nbk);
+    const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT;
+    if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256, 0, s>>>(g, r0, nbk);
+    c->launches += mt > 0 ? 3 : 2;
+  }
   ldl_finish_kernel<<<std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
                                                                          o.perm_global, c->ell, c->diag);
   pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);

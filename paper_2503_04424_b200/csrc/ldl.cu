@@ -6,19 +6,18 @@
 //
 //   unpack_block_kernel    tile grid -> dense column-major block (lower triangle)
 //   block_absmax_kernel    max |a_ij| over the block's lower triangle (the tolerance scale)
-//   ldl_pivot_kernel       cooperative, one column per step: grid-wide argmax, symmetric swap,
-//                          rank-1 trailing update (the reference's a_ij -= c_i * (c_j / p))
+//   ldl_panel_kernel       NB pivot steps in one CTA: argmax of the eager diagonal (lowest index
+//                          on ties), symmetric interchange, pivot column with pending terms
+//   ldl_bulk_kernel        the panel's NB steps applied to the trailing matrix (the reference's
+//                          a_ij -= c_i * (c_j / p), same order and roundings)
 //   ldl_finish_kernel      swaps -> permutation, log|d|, d, global perm
 //   pack_unit_lower_kernel dense unit-lower L -> tile grid
 //   tile_inv_unit_kernel   inverse of a unit-lower 128 x 128 tile (TRSM operand)
 //   permute_cols_kernel    panel block columns by the block permutation (rows of B in the ref)
 //   scale_cols_kernel      panel block columns / d (B /= d, memdet.py:371)
-#include <cooperative_groups.h>
-
 #include "tile.cuh"
 
 namespace b2d {
-namespace cg = cooperative_groups;
 
 __global__ void __launch_bounds__(256) unpack_block_kernel(TileMap src, int ntiles, double* __restrict__ dense,
                                                            int64_t ld) {
@@ -73,111 +72,206 @@ __device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
   return a;
 }
 
-constexpr int LDL_THREADS = 256;
+// ---------------------------------------------------------------------------------------------
+// Pivoted LDL^T of a dense column-major block, blocked with delayed updates and bit-identical to
+// the reference's unblocked loop (_ldl.pyx:21-61; oracle/ldl_tile.c).
+//
+// The reference applies, at step q, a_ij -= c_i * w_j (c = the updated column q, w = c / p_q)
+// to every trailing element, one step at a time.  Here the steps of a block of NB columns are
+// kept as columns of C (c) and W (w) and applied to the trailing matrix once per block, in the
+// same order and with the same two roundings per term, by ldl_bulk_kernel.  In between, a
+// panel kernel (one CTA) runs the NB pivot steps:
+//   * pivot search over an eagerly updated copy of the diagonal (diag_i -= c_i w_i per step is
+//     exactly the reference's update of a_ii);
+//   * the pivot column is computed from the raw (not yet updated) entries plus their pending
+//     terms, each with the association of the position it held (row index -> C, column index -> W);
+//   * the symmetric interchange moves raw entries with their pending terms.  The interchange
+//     moves entries of column r into row t (r < i < t), where the pending terms would change
+//     association (c_t w_i vs c_i w_t, equal in exact arithmetic, not in floating point); those
+//     entries are brought up to date at the move and carry a tag = number of the block's steps
+//     already applied, which the bulk update and later column computations honour.
+// Every entry therefore sees the reference's sequence of roundings, and the pivot order, D and L
+// are bit-identical to the unblocked kernel.
+constexpr int LDL_NB = 32;             // steps per panel (columns of C / W)
+constexpr int LDL_PANEL_THREADS = 1024;
 
-// Dense column-major block A (ld), valid order n; factored in place: strictly lower = unit L,
-// d = pivots, swaps = LAPACK-style swap list.  tol = 64 * eps * amax (amax_bits holds the bits of
-// max |a|).  *fail = g0 + first failing step (atomicMin), and the kernel stops there.
-__global__ void __launch_bounds__(LDL_THREADS) ldl_pivot_kernel(double* __restrict__ A, int64_t ld, int64_t n,
-                                                                const unsigned long long* __restrict__ amax_bits,
-                                                                double* __restrict__ d, int64_t* __restrict__ swaps,
-                                                                ArgMax* __restrict__ part,
-                                                                unsigned long long* __restrict__ fail, int64_t g0) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ ArgMax sred[LDL_THREADS / 32];
+struct LdlArgs {
+  double* A;      // dense block, column-major, leading dimension ld
+  uint8_t* tag;   // per-entry count of this panel's steps already applied (same layout as A)
+  double* C;      // [LDL_NB][ld] unscaled pivot columns of the current panel
+  double* W;      // [LDL_NB][ld] scaled pivot columns (c / p)
+  double* diag;   // eagerly updated diagonal
+  double* col;    // scratch: the pivot column being formed
+  double* d;      // pivots
+  int64_t* swaps; // LAPACK-style interchanges (block-local)
+  unsigned long long* fail;
+  const unsigned long long* amax_bits;
+  int64_t ld, n, g0;
+};
+
+__global__ void ldl_diag_init_kernel(LdlArgs g) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x)
+    g.diag[i] = g.A[i * g.ld + i];
+}
+
+// One panel of nbk pivot steps starting at r0 (one CTA).
+__global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;  // an earlier step failed
+  __shared__ ArgMax sred[LDL_PANEL_THREADS / 32];
   __shared__ int64_t s_t;
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  const int64_t gtid = (int64_t)blockIdx.x * LDL_THREADS + tid;
-  const int64_t gthreads = (int64_t)gridDim.x * LDL_THREADS;
-  const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
-  const double tol = 64.0 * 2.220446049250313e-16 * __longlong_as_double((long long)*amax_bits);
-  auto block_argmax = [&](ArgMax a) {
+  const int64_t n = g.n, ld = g.ld;
+  double* __restrict__ A = g.A;
+  uint8_t* __restrict__ tag = g.tag;
+  const double* __restrict__ C = g.C;
+  const double* __restrict__ W = g.W;
+  const double tol = 64.0 * 2.220446049250313e-16 * __longlong_as_double((long long)*g.amax_bits);
+  // entry (row, col) brought up to date with the panel's steps [tag, k) in its own association
+  auto upd = [&](int64_t row, int64_t col, int k) {
+    double v = A[col * ld + row];
+    for (int q = tag[col * ld + row]; q < k; ++q) v = __dsub_rn(v, __dmul_rn(C[q * ld + row], W[q * ld + col]));
+    return v;
+  };
+  for (int k = 0; k < nbk; ++k) {
+    const int64_t r = r0 + k;
+    // pivot: largest |diag| over [r, n), lowest index on ties (_ldl.pyx:30-36)
+    ArgMax a{-1.0, INT64_MAX};
+    for (int64_t i = r + tid; i < n; i += LDL_PANEL_THREADS) a = better(a, ArgMax{fabs(g.diag[i]), i});
     a = warp_argmax(a);
     if (lane == 0) sred[wib] = a;
     __syncthreads();
     if (wib == 0) {
-      ArgMax b = lane < LDL_THREADS / 32 ? sred[lane] : ArgMax{-1.0, INT64_MAX};
-      b = warp_argmax(b);
-      if (lane == 0) part[blockIdx.x] = b;
-    }
-    __syncthreads();
-  };
-  // initial pivot candidates
-  {
-    ArgMax a{-1.0, INT64_MAX};
-    for (int64_t i = gtid; i < n; i += gthreads) a = better(a, ArgMax{fabs(A[i * ld + i]), i});
-    block_argmax(a);
-  }
-  grid.sync();
-  // Two grid barriers per column: S(r) finishes column r-1 (L = c / p) while swapping r <-> t,
-  // U(r) checks the pivot and applies the rank-1 update with the unscaled column r.
-  for (int64_t r = 0; r < n; ++r) {
-    // --- S: pivot t = argmax over the partials, symmetric swap r <-> t (_ldl.pyx:38-46)
-    if (wib == 0) {
-      ArgMax b{-1.0, INT64_MAX};
-      for (int q = lane; q < (int)gridDim.x; q += 32) b = better(b, part[q]);
+      ArgMax b = sred[lane];
       b = warp_argmax(b);
       if (lane == 0) s_t = b.i;
     }
     __syncthreads();
     const int64_t t = s_t;
-    if (gtid == 0) swaps[r] = t;
-    const int64_t q = r - 1;                       // column finished in this phase
-    const double invq = q >= 0 ? 1.0 / d[q] : 1.0;  // d[q] written by gtid 0 in U(q), visible after the sync
-    if (q >= 0) {
-      // a_iq = a_iq * (1/p) for i > q (_ldl.pyx:59-60), rows r and t via the swap below
-      for (int64_t i = q + 1 + gtid; i < n; i += gthreads)
-        if (i != r && i != t) A[q * ld + i] = __dmul_rn(A[q * ld + i], invq);
+    // interchange r <-> t (_ldl.pyx:38-46) and the new column r, from the pre-interchange entries
+    for (int64_t i = r + 1 + tid; i < n; i += LDL_PANEL_THREADS) {
+      double v;
+      if (t == r) {
+        v = upd(i, r, k);
+      } else if (i < t) {
+        v = upd(t, i, k);                      // (t, i) -> (i, r)
+        A[i * ld + t] = upd(i, r, k);          // (i, r) -> (t, i), association changes: bring up to date
+        tag[i * ld + t] = (uint8_t)k;
+      } else if (i == t) {
+        v = upd(t, r, k);                      // (t, r) stays
+      } else {
+        v = upd(i, t, k);                      // (i, t) -> (i, r)
+        A[t * ld + i] = A[r * ld + i];         // (i, r) -> (i, t), same association: move raw + tag
+        tag[t * ld + i] = tag[r * ld + i];
+      }
+      g.col[i] = v;
     }
-    if (t != r) {
-      for (int64_t j = gtid; j < r; j += gthreads) {  // rows r and t of the L part
-        double x = A[j * ld + r], y = A[j * ld + t];
-        if (j == q) {
-          x = __dmul_rn(x, invq);
-          y = __dmul_rn(y, invq);
-        }
-        A[j * ld + r] = y;
+    if (t != r)
+      for (int64_t j = tid; j < r0; j += LDL_PANEL_THREADS) {  // rows r, t of the finished L columns
+        const double x = A[j * ld + r];
+        A[j * ld + r] = A[j * ld + t];
         A[j * ld + t] = x;
       }
-      if (gtid == 0) {
-        const double x = A[r * ld + r];
-        A[r * ld + r] = A[t * ld + t];
-        A[t * ld + t] = x;
+    __syncthreads();
+    if (t != r) {
+      for (int q = tid; q < 2 * k; q += LDL_PANEL_THREADS) {  // rows r, t of this panel's C / W
+        double* B = (q & 1) ? g.W : g.C;
+        const int qq = q >> 1;
+        const double x = B[qq * ld + r];
+        B[qq * ld + r] = B[qq * ld + t];
+        B[qq * ld + t] = x;
       }
-      for (int64_t i = r + 1 + gtid; i < t; i += gthreads) {  // column r below r <-> row t
-        const double x = A[r * ld + i];
-        A[r * ld + i] = A[i * ld + t];
-        A[i * ld + t] = x;
+      if (tid == 0) {
+        const double x = g.diag[r];
+        g.diag[r] = g.diag[t];
+        g.diag[t] = x;
+        A[t * ld + t] = A[r * ld + r];  // (r, r) -> (t, t) with its pending terms
+        tag[t * ld + t] = tag[r * ld + r];
       }
-      for (int64_t i = t + 1 + gtid; i < n; i += gthreads) {  // below t: columns r and t
-        const double x = A[r * ld + i];
-        A[r * ld + i] = A[t * ld + i];
-        A[t * ld + i] = x;
-      }
-    } else if (q >= 0 && gtid == 0) {
-      A[q * ld + r] = __dmul_rn(A[q * ld + r], invq);
     }
-    grid.sync();
-    // --- U: pivot check, rank-1 update of the trailing lower triangle, next candidates
-    const double p = A[r * ld + r];
+    if (tid == 0) g.swaps[r] = t;
+    __syncthreads();
+    const double p = g.diag[r];
     if (!(fabs(p) >= tol)) {
-      if (gtid == 0) atomicMin(fail, (unsigned long long)(g0 + r));
+      if (tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
       return;  // uniform: every thread read the same p
     }
-    if (gtid == 0) d[r] = p;
+    if (tid == 0) g.d[r] = p;
     const double invp = 1.0 / p;
-    ArgMax cand{-1.0, INT64_MAX};
-    for (int64_t j = r + 1 + gwarp; j < n; j += nwarps) {
-      const double wj = __dmul_rn(A[r * ld + j], invp);  // work[j] = a_jr * (1/p)
-      double* colj = A + j * ld;
-      const double* colr = A + r * ld;
-      for (int64_t i = j + lane; i < n; i += 32) colj[i] = __dsub_rn(colj[i], __dmul_rn(colr[i], wj));
-      if (lane == 0) cand = better(cand, ArgMax{fabs(colj[j]), j});
+    for (int64_t i = r + 1 + tid; i < n; i += LDL_PANEL_THREADS) {
+      const double c = g.col[i];
+      const double w = __dmul_rn(c, invp);  // work[i] = a_ir * (1/p)
+      g.C[k * ld + i] = c;
+      g.W[k * ld + i] = w;
+      g.diag[i] = __dsub_rn(g.diag[i], __dmul_rn(c, w));
     }
-    block_argmax(cand);
-    grid.sync();
+    __syncthreads();
   }
-  // the last column has no rows below it; column n-2 was finished in S(n-1)
+}
+
+// Finished columns [r0, r0 + nbk): L = W below the diagonal (_ldl.pyx:59-60).
+__global__ void ldl_store_l_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;
+  const int64_t rows = g.n - r0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * nbk; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / rows);
+    const int64_t i = r0 + e % rows, r = r0 + k;
+    if (i > r) g.A[r * g.ld + i] = g.W[k * g.ld + i];
+  }
+}
+
+// Trailing update with the panel's nbk steps: a_ij -= c_i^q w_j^q for q = tag_ij .. nbk-1, in
+// order, for j >= r0 + nbk, i >= j; tags reset.  64 x 64 entry tiles, 4 x 4 per thread.
+constexpr int LDL_BT = 64;
+__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;
+  __shared__ double sC[LDL_NB][LDL_BT], sW[LDL_NB][LDL_BT];
+  const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld;
+  // lower-triangular tile (bi >= bj) of blockIdx.x
+  int64_t b = blockIdx.x, bj = 0;
+  const int64_t nbt = (m + LDL_BT - 1) / LDL_BT;
+  while (b >= nbt - bj) { b -= nbt - bj; ++bj; }
+  const int64_t bi = bj + b;
+  const int64_t i0 = re + bi * LDL_BT, j0 = re + bj * LDL_BT;
+  for (int e = threadIdx.x; e < nbk * LDL_BT; e += 256) {
+    const int q = e / LDL_BT, x = e % LDL_BT;
+    sC[q][x] = i0 + x < g.n ? g.C[q * ld + i0 + x] : 0.0;
+    sW[q][x] = j0 + x < g.n ? g.W[q * ld + j0 + x] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double v[4][4];
+  int tg[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t i = i0 + tx + 16 * a, j = j0 + ty + 16 * c;
+      const bool ok = i < g.n && j < g.n && i >= j;
+      v[a][c] = ok ? g.A[j * ld + i] : 0.0;
+      tg[a][c] = ok ? g.tag[j * ld + i] : 255;
+    }
+  for (int q = 0; q < nbk; ++q) {
+    double cc[4], ww[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) cc[a] = sC[q][tx + 16 * a];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ww[c] = sW[q][ty + 16 * c];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (q >= tg[a][c]) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t i = i0 + tx + 16 * a, j = j0 + ty + 16 * c;
+      if (i < g.n && j < g.n && i >= j) {
+        g.A[j * ld + i] = v[a][c];
+        if (tg[a][c]) g.tag[j * ld + i] = 0;
+      }
+    }
 }
 
 // swaps -> block permutation (kernels/dense.py:25-30), global perm (memdet.py:352-353),

@@ -301,6 +301,44 @@ def test_pivoted_ldl_matches_reference_golden(golden, name):
             (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
 
 
+def _ldl_block_input(m, kind):
+    rng = np.random.default_rng(m)
+    if kind == "sym":
+        return gen.random_symmetric(m, seed=m)
+    if kind == "rbf":  # equal diagonal: an exact tie at the first step
+        return gen.rbf(m, seed=m)
+    if kind == "blocks":  # identical diagonal blocks: exact ties at every step
+        b = gen.random_symmetric(16, seed=3)
+        return np.kron(np.eye(m // 16), b)
+    if kind == "int":  # small integers: many exactly equal candidates
+        g = rng.integers(-3, 4, size=(m, m)).astype(np.float64)
+        a = np.tril(g) + np.tril(g, -1).T
+        a[np.diag_indices(m)] = rng.integers(5, 9, size=m) * np.where(rng.random(m) < 0.5, -1.0, 1.0)
+        return a
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("m,kind", [(31, "sym"), (33, "sym"), (100, "sym"), (257, "sym"), (700, "sym"),
+                                    (600, "rbf"), (320, "blocks"), (400, "int")])
+def test_pivoted_ldl_diagonal_block_bit_identical_to_reference_kernel(m, kind):
+    """One diagonal block (num_blocks=1): the blocked panel / delayed-update kernels reproduce the
+    reference's unblocked loop (_ldl.pyx:21-61, restated in oracle/ldl_tile.c) bit for bit:
+    the same interchanges and the same pivots d, across panel boundaries and exact ties."""
+    a = _ldl_block_input(m, kind)
+    ctx = _native.Context(m, _native.MODE_LDL_PIV, num_blocks=1)
+    ctx.factor_host_async(a.ctypes.data, m, _native.B2D_F64, 0)
+    d = np.empty(m)
+    rc, fail, info = ctx.fetch(d, None)
+    _native.check(rc)
+    perm = np.empty(m, np.int64)
+    ctx.fetch_perm(perm)
+    ctx.close()
+    swaps, dref = O.ldl_tile(a.copy())
+    np.testing.assert_array_equal(perm, O.perm_from_swaps(swaps))
+    assert np.array_equal(d.view(np.int64), np.asarray(dref, np.float64).view(np.int64)), \
+        np.max(np.abs(d - dref))
+
+
 def test_pivoted_ldl_prefix_is_permuted_minor_logdet():
     """reference tests/test_memdet.py:117-129: prefix[q-1] = log|det M[perm[:q], perm[:q]]|."""
     m = 48

@@ -9,6 +9,7 @@ for r in rows[hi + 1:]:
     name = r[ki].split("(")[0].replace("void ", "")
     tot[name] += float(r[vi].replace(",", "")) * scale[r[ui]]; cnt[name] += 1
 T = sum(tot.values())
+import signal; signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
     print(f"{k:44s} n={cnt[k]:5d} {v/1e3:9.2f} ms {100*v/T:5.1f}%  avg {v/cnt[k]:9.1f} us")
 print(f"total serialized {T/1e3:.2f} ms")
