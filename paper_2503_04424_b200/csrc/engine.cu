@@ -158,6 +158,9 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   done = true;
   return B2D_OK;
@@ -979,9 +982,28 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
   cudaMemsetAsync(o.ltag, 0, (size_t)ld * ld, s);
   ldl_diag_init_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(g);
   c->launches += 1;
+  // B2D_LDL_SINGLE_CTA forces the one-CTA panel kernel (the path for blocks above 16*384 rows)
+  const bool single_cta = getenv("B2D_LDL_SINGLE_CTA") != nullptr;
   for (int64_t r0 = 0; r0 < n; r0 += LDL_NB) {
     const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
-    ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
+    if (n <= (int64_t)LC * LC_RMAX && !single_cta) {
+      // the panel on a 16-CTA cluster with its rows in distributed shared memory
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = LC;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(LC);
+      cfg.blockDim = dim3(LC_THREADS);
+      cfg.dynamicSmemBytes = ldl_cluster_smem((int)((n + LC - 1) / LC));
+      cfg.stream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk));
+    } else {
+      ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
+    }
     ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, ((n - r0) * nbk + 255) / 256)), 256, 0, s>>>(g, r0, nbk);
     const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT;
     if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256, 0, s>>>(g, r0, nbk);

@@ -15,9 +15,12 @@
 //   tile_inv_unit_kernel   inverse of a unit-lower 128 x 128 tile (TRSM operand)
 //   permute_cols_kernel    panel block columns by the block permutation (rows of B in the ref)
 //   scale_cols_kernel      panel block columns / d (B /= d, memdet.py:371)
+#include <cooperative_groups.h>
+
 #include "tile.cuh"
 
 namespace b2d {
+namespace cg = cooperative_groups;
 
 __global__ void __launch_bounds__(256) unpack_block_kernel(TileMap src, int ntiles, double* __restrict__ dense,
                                                            int64_t ld) {
@@ -205,6 +208,160 @@ __global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs
       g.diag[i] = __dsub_rn(g.diag[i], __dmul_rn(c, w));
     }
     __syncthreads();
+  }
+}
+
+// The same panel on a cluster of LC CTAs (one per SM) with the panel's C / W rows, the eager
+// diagonal and the pivot column in distributed shared memory: row i lives in CTA i % LC at
+// local row i / LC.  Per step: local argmax -> candidates pushed to every CTA -> barrier ->
+// every CTA reads rows r and t (C, W, diag) from their owners -> barrier -> local rows of the
+// new column, interchange, update.  Entry arithmetic is the single-CTA kernel's exactly.
+// Raw entries and tags stay in global memory (read through L2: other CTAs wrote them).
+constexpr int LC = 16;                 // CTAs per cluster (non-portable size)
+constexpr int LC_THREADS = 256;
+constexpr int LC_LD = LDL_NB + 1;      // padded smem row (conflict-free column access)
+constexpr int LC_RMAX = 384;           // local rows per CTA (n <= LC * LC_RMAX)
+__host__ __device__ constexpr size_t ldl_cluster_smem(int rows) { return (size_t)rows * (2 * LC_LD + 2) * 8; }
+
+__global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  extern __shared__ double sm[];
+  const int64_t n = g.n, ld = g.ld;
+  const int R = (int)((n + LC - 1) / LC);
+  double* Cs = sm;                      // [R][LC_LD]
+  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
+  double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal
+  double* col = dg + R;                 // [R] pivot column being formed
+  __shared__ ArgMax cand[2][LC];
+  __shared__ ArgMax sred[LC_THREADS / 32];
+  __shared__ double bCr[LDL_NB], bWr[LDL_NB], bCt[LDL_NB], bWt[LDL_NB], bd[2];
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  double* __restrict__ A = g.A;
+  uint8_t* __restrict__ tag = g.tag;
+  const double tol = 64.0 * 2.220446049250313e-16 * __longlong_as_double((long long)*g.amax_bits);
+  for (int li = tid; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    dg[li] = i < n ? g.diag[i] : 0.0;
+  }
+  // (row, col) up to date with steps [tag, k): cr = C row of `row`, wc = W row of `col`
+  auto upd = [&](int64_t row, int64_t col_, const double* cr, const double* wc, int k) {
+    double v = __ldcg(A + col_ * ld + row);
+    for (int q = __ldcg(tag + col_ * ld + row); q < k; ++q) v = __dsub_rn(v, __dmul_rn(cr[q], wc[q]));
+    return v;
+  };
+  for (int k = 0; k < nbk; ++k) {
+    const int64_t r = r0 + k;
+    ArgMax a{-1.0, INT64_MAX};
+    for (int li = tid; li < R; li += LC_THREADS) {
+      const int64_t i = (int64_t)li * LC + c;
+      if (i >= r && i < n) a = better(a, ArgMax{fabs(dg[li]), i});
+    }
+    a = warp_argmax(a);
+    if (lane == 0) sred[wib] = a;
+    __syncthreads();
+    if (wib == 0) {
+      ArgMax b = lane < LC_THREADS / 32 ? sred[lane] : ArgMax{-1.0, INT64_MAX};
+      b = warp_argmax(b);
+      if (lane < LC) *cl.map_shared_rank(&cand[k & 1][c], lane) = b;  // push to every CTA
+    }
+    cl.sync();  // A: candidates (and the previous step's rows) visible cluster-wide
+    ArgMax b{-1.0, INT64_MAX};
+    for (int q = 0; q < LC; ++q) b = better(b, cand[k & 1][q]);
+    const int64_t t = b.i;
+    const int orr = (int)(r % LC), ort = (int)(t % LC);
+    const int lr = (int)(r / LC), lt = (int)(t / LC);
+    for (int q = tid; q < k; q += LC_THREADS) {
+      bCr[q] = cl.map_shared_rank(Cs, orr)[(size_t)lr * LC_LD + q];
+      bWr[q] = cl.map_shared_rank(Ws, orr)[(size_t)lr * LC_LD + q];
+      bCt[q] = cl.map_shared_rank(Cs, ort)[(size_t)lt * LC_LD + q];
+      bWt[q] = cl.map_shared_rank(Ws, ort)[(size_t)lt * LC_LD + q];
+    }
+    if (tid == 0) {
+      bd[0] = cl.map_shared_rank(dg, orr)[lr];
+      bd[1] = cl.map_shared_rank(dg, ort)[lt];
+    }
+    cl.sync();  // B: rows r, t read everywhere; their owners may overwrite them
+    for (int li = tid; li < R; li += LC_THREADS) {
+      const int64_t i = (int64_t)li * LC + c;
+      if (i <= r || i >= n) continue;
+      const double* Ci = Cs + (size_t)li * LC_LD;
+      const double* Wi = Ws + (size_t)li * LC_LD;
+      double v;
+      if (t == r) {
+        v = upd(i, r, Ci, bWr, k);
+      } else if (i < t) {
+        v = upd(t, i, bCt, Wi, k);            // (t, i) -> (i, r)
+        A[i * ld + t] = upd(i, r, Ci, bWr, k);  // (i, r) -> (t, i): brought up to date, tagged
+        tag[i * ld + t] = (uint8_t)k;
+      } else if (i == t) {
+        v = upd(t, r, bCt, bWr, k);           // (t, r) stays
+      } else {
+        v = upd(i, t, Ci, bWt, k);            // (i, t) -> (i, r)
+        A[t * ld + i] = __ldcg(A + r * ld + i);  // (i, r) -> (i, t) with its tag
+        tag[t * ld + i] = __ldcg(tag + r * ld + i);
+      }
+      col[li] = v;
+    }
+    if (t != r)
+      for (int64_t j = (int64_t)c * LC_THREADS + tid; j < r0; j += (int64_t)LC * LC_THREADS) {
+        const double x = __ldcg(A + j * ld + r);
+        A[j * ld + r] = __ldcg(A + j * ld + t);
+        A[j * ld + t] = x;
+      }
+    __syncthreads();
+    if (t != r) {
+      if (c == orr) {
+        for (int q = tid; q < k; q += LC_THREADS) {
+          Cs[(size_t)lr * LC_LD + q] = bCt[q];
+          Ws[(size_t)lr * LC_LD + q] = bWt[q];
+        }
+        if (tid == 0) dg[lr] = bd[1];
+      }
+      if (c == ort) {
+        for (int q = tid; q < k; q += LC_THREADS) {
+          Cs[(size_t)lt * LC_LD + q] = bCr[q];
+          Ws[(size_t)lt * LC_LD + q] = bWr[q];
+        }
+        if (tid == 0) {
+          dg[lt] = bd[0];
+          A[t * ld + t] = __ldcg(A + r * ld + r);  // (r, r) -> (t, t) with its pending terms
+          tag[t * ld + t] = __ldcg(tag + r * ld + r);
+        }
+      }
+    }
+    const double p = t == r ? bd[0] : bd[1];
+    if (!(fabs(p) >= tol)) {
+      if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
+      return;  // uniform across the cluster: every thread read the same p
+    }
+    if (c == 0 && tid == 0) {
+      g.d[r] = p;
+      g.swaps[r] = t;
+    }
+    const double invp = 1.0 / p;
+    __syncthreads();
+    for (int li = tid; li < R; li += LC_THREADS) {
+      const int64_t i = (int64_t)li * LC + c;
+      if (i <= r || i >= n) continue;
+      const double cv = col[li];
+      const double w = __dmul_rn(cv, invp);  // work[i] = a_ir * (1/p)
+      Cs[(size_t)li * LC_LD + k] = cv;
+      Ws[(size_t)li * LC_LD + k] = w;
+      dg[li] = __dsub_rn(dg[li], __dmul_rn(cv, w));
+    }
+    __syncthreads();
+  }
+  // C, W and the diagonal back to global memory for the bulk update and the next panel
+  for (int li = tid; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    if (i >= n || i <= r0) continue;
+    for (int q = 0; q < nbk; ++q) {
+      g.C[q * ld + i] = Cs[(size_t)li * LC_LD + q];
+      g.W[q * ld + i] = Ws[(size_t)li * LC_LD + q];
+    }
+    g.diag[i] = dg[li];
   }
 }
 

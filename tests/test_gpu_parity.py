@@ -318,12 +318,16 @@ def _ldl_block_input(m, kind):
     raise ValueError(kind)
 
 
+@pytest.mark.parametrize("panel", ["cluster", "single_cta"])
 @pytest.mark.parametrize("m,kind", [(31, "sym"), (33, "sym"), (100, "sym"), (257, "sym"), (700, "sym"),
                                     (600, "rbf"), (320, "blocks"), (400, "int")])
-def test_pivoted_ldl_diagonal_block_bit_identical_to_reference_kernel(m, kind):
+def test_pivoted_ldl_diagonal_block_bit_identical_to_reference_kernel(m, kind, panel, monkeypatch):
     """One diagonal block (num_blocks=1): the blocked panel / delayed-update kernels reproduce the
     reference's unblocked loop (_ldl.pyx:21-61, restated in oracle/ldl_tile.c) bit for bit:
-    the same interchanges and the same pivots d, across panel boundaries and exact ties."""
+    the same interchanges and the same pivots d, across panel boundaries and exact ties; both
+    panel kernels (16-CTA cluster, and the one-CTA kernel used above 6144 rows)."""
+    if panel == "single_cta":
+        monkeypatch.setenv("B2D_LDL_SINGLE_CTA", "1")
     a = _ldl_block_input(m, kind)
     ctx = _native.Context(m, _native.MODE_LDL_PIV, num_blocks=1)
     ctx.factor_host_async(a.ctypes.data, m, _native.B2D_F64, 0)
