@@ -159,6 +159,8 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(LDL_FINISH_SMEM_MAX * 8)));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
@@ -1009,12 +1011,12 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
     if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256, 0, s>>>(g, r0, nbk);
     c->launches += mt > 0 ? 3 : 2;
   }
-  ldl_finish_kernel<<<std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
-                                                                         o.perm_global, c->ell, c->diag);
+  ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
+                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
+                                                                        o.perm_global, c->ell, c->diag);
   pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
-  for (int q = 0; q < nt; ++q)
-    tile_inv_unit_kernel<<<1, T, T * 129 * 8, s>>>(o.map(sa).tile(q, q), c->inv + (int64_t)q * TILE_ELEMS);
-  c->launches += 6 + nt;
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), c->inv);
+  c->launches += 7;
   cudaEventRecord(o.ev_used[sa], s);
   return B2D_OK;
 }

@@ -432,21 +432,37 @@ __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, in
 }
 
 // swaps -> block permutation (kernels/dense.py:25-30), global perm (memdet.py:352-353),
-// ell = log|d| (memdet.py:406) and the D values; one thread walks the swaps, all fill the rest.
+// ell = log|d| (memdet.py:406) and the D values.  One thread walks the swaps (sequential by
+// definition) on a shared-memory copy of the permutation when it fits (LDL_FINISH_SMEM_MAX rows).
+constexpr int64_t LDL_FINISH_SMEM_MAX = 24576;
 __global__ void ldl_finish_kernel(const int64_t* __restrict__ swaps, const double* __restrict__ d, int64_t n,
                                   int64_t g0, int64_t* __restrict__ perm_local, int64_t* __restrict__ perm_global,
                                   double* __restrict__ ell, double* __restrict__ dout) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int64_t i = 0; i < n; ++i) perm_local[i] = i;
-    for (int64_t r = 0; r < n; ++r) {
-      const int64_t t = swaps[r];
-      if (t != r) {
-        const int64_t x = perm_local[r];
-        perm_local[r] = perm_local[t];
-        perm_local[t] = x;
+  extern __shared__ int64_t sperm[];
+  if (blockIdx.x == 0) {
+    const bool sm = n <= LDL_FINISH_SMEM_MAX;
+    int64_t* pl = sm ? sperm : perm_local;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) pl[i] = i;
+    __syncthreads();
+    auto walk = [&](int64_t* __restrict__ q) {
+      for (int64_t r = 0; r < n; ++r) {
+        const int64_t t = __ldg(swaps + r);
+        if (t != r) {
+          const int64_t x = q[r];
+          q[r] = q[t];
+          q[t] = x;
+        }
       }
+    };
+    if (threadIdx.x == 0) {
+      if (sm) walk(sperm);
+      else walk(perm_local);
     }
-    for (int64_t i = 0; i < n; ++i) perm_global[g0 + i] = g0 + perm_local[i];
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      if (sm) perm_local[i] = pl[i];
+      perm_global[g0 + i] = g0 + pl[i];
+    }
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     ell[g0 + i] = log(fabs(d[i]));
@@ -475,8 +491,11 @@ __global__ void __launch_bounds__(256) pack_unit_lower_kernel(const double* __re
 
 // X = L^{-1} of a unit-lower 128 x 128 tile: one thread per column, forward substitution in
 // 8-row blocks; X[r][c] (r > c) kept transposed in the upper triangle of the staging array.
-__global__ void __launch_bounds__(128) tile_inv_unit_kernel(const double* __restrict__ tile, double* __restrict__ inv) {
+// One CTA per diagonal tile q of `map` (blockIdx.x = q): inv + q * TILE_ELEMS = L_qq^{-1}.
+__global__ void __launch_bounds__(128) tile_inv_unit_kernel(TileMap map, double* __restrict__ inv_base) {
   extern __shared__ double M[];  // [T][129]
+  const double* __restrict__ tile = map.tile(blockIdx.x, blockIdx.x);
+  double* __restrict__ inv = inv_base + (int64_t)blockIdx.x * TILE_ELEMS;
   const int c = threadIdx.x;
   for (int o = c; o < TILE_ELEMS; o += T) {
     const int r = (o >> 3) & 127;
