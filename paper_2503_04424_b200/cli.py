@@ -3,10 +3,14 @@
     python -m paper_2503_04424_b200 memdet --in K.mdm --assume spd --num-blocks 8 --json
     python -m paper_2503_04424_b200 gen --kind rbf --n 4096 --out K.mdm
     python -m paper_2503_04424_b200 cost --m 4096 --nb 4 --case sym --json
+    python -m paper_2503_04424_b200 flodance --prefix K.pfx --d 1 --n0 5 --ns 3000 --q 1 --predict 4096
+    python -m paper_2503_04424_b200 pipeline --kind rbf --n 4096 --out K.mdm --assume spd --ns 3000 --json
 
 Same flags, JSON payload (schema_version 1) and exit codes as the reference: 0 success,
-2 usage error, 3 numerical failure, 4 I/O failure.  `--assume gen` (the LU path) and the
-FLODANCE / SLQ / block-diagonal subcommands are outside this engine's scope.
+2 usage error, 3 numerical failure, 4 I/O failure.  `--assume gen` (the LU path) and the SLQ /
+block-diagonal baselines are outside this engine's scope; `gen` / `pipeline` generate the
+BASELINE families (one output per datapoint, so FLODANCE runs with d = 1 in `pipeline`) instead
+of the reference's Matern-LMC generator.
 """
 
 from __future__ import annotations
@@ -14,11 +18,16 @@ from __future__ import annotations
 import argparse
 import json
 import sys
+import time
+
+import numpy as np
 
 from . import __version__, gen
 from .cost import predicted_cost
 from .errors import NumericalError, OocdetError, StorageError
+from .flodance import fit_prefix, predict, predict_interval, scaling_ratio_trace
 from .memdet import memdet_cholesky, memdet_ldl
+from .prefixio import read_prefix
 from .storage import write_matrix
 
 SCHEMA_VERSION = 1
@@ -75,7 +84,7 @@ def cmd_memdet(args) -> int:
     return 0
 
 
-def cmd_gen(args) -> int:
+def _generate(args):
     kinds = {
         "wishart": lambda: (gen.spd_wishart(args.n, args.k or args.n, args.seed, args.jitter or 1e-3), "spd"),
         "rbf": lambda: (gen.rbf(args.n, args.d, args.ell, args.jitter or 1e-6, args.seed), "spd"),
@@ -85,7 +94,11 @@ def cmd_gen(args) -> int:
         "sym-random": lambda: (gen.random_symmetric(args.n, args.seed), "symmetric"),
     }
     a, sym = kinds[args.kind]()
-    mf = write_matrix(args.out, a, sym)
+    return write_matrix(args.out, a, sym)
+
+
+def cmd_gen(args) -> int:
+    mf = _generate(args)
     _emit(args, {"schema_version": SCHEMA_VERSION, "path": mf.path, "m": mf.m, "dtype": str(mf.dtype),
                  "symmetry": mf.symmetry, "kind": args.kind, "seed": args.seed},
           [f"wrote {mf.symmetry} {mf.m}x{mf.m} matrix to {mf.path}"])
@@ -108,6 +121,71 @@ def cmd_cost(args) -> int:
     return 0
 
 
+def cmd_flodance(args) -> int:
+    """Fit and extrapolate a prefix sidecar (reference cli.py:107-135)."""
+    ell, _ = read_prefix(args.prefix)
+    fit = fit_prefix(ell, args.d, args.n0, args.ns, args.q)
+    L_hat, ell_hat = predict(fit, args.predict)
+    payload = {"schema_version": SCHEMA_VERSION, **fit.to_json_dict(), "n": args.predict,
+               "L_hat": float(L_hat), "logdet_hat": float(ell_hat)}
+    lines = [f"fit on [{args.n0}, {args.ns}], q = {args.q}: c0 = {fit.c0:.6g}, "
+             f"nu = {np.array2string(fit.nu, precision=6)}, sigma_hat = {fit.sigma_hat:.6g}",
+             f"L_hat({args.predict}) = {float(L_hat):.12e}",
+             f"logdet_hat({args.predict}) = {float(ell_hat):.12e}"]
+    if args.interval is not None:
+        lo, hi = predict_interval(fit, args.predict, args.interval)
+        payload["interval"] = {"level": args.interval, "lower": lo, "upper": hi}
+        lines.append(f"{args.interval:.0%} interval [{lo:.12e}, {hi:.12e}]")
+    if args.trace_out:
+        trace = scaling_ratio_trace(ell, args.d)
+        with open(args.trace_out, "w") as f:
+            f.write("n,log_ratio\n")
+            for n, v in enumerate(trace, start=2):
+                f.write(f"{n},{v!r}\n")
+        lines.append(f"wrote ratio trace to {args.trace_out}")
+    _emit(args, payload, lines)
+    return 0
+
+
+def cmd_pipeline(args) -> int:
+    """Generate, factor on the B200 engine, fit and extrapolate (reference cli.py:169-199)."""
+    started = time.perf_counter()
+    inputs = {"kind": args.kind, "n": args.n, "k": args.k, "d": args.d, "ell": args.ell, "alpha": args.alpha,
+              "seed": args.seed, "jitter": args.jitter}
+    mf = _generate(args)
+    driver = memdet_cholesky if args.assume == "spd" else memdet_ldl
+    res = driver(mf, max_mem=args.max_mem, num_blocks=args.num_blocks, scratch_dir=args.scratch_dir)
+    truth = res.logabsdet
+    fit = fit_prefix(res.prefix, 1, args.n0, args.ns, args.q)
+    _, ell_hat = predict(fit, args.n)
+    rel_error = abs(float(ell_hat) - truth) / max(1.0, abs(truth))
+    outputs = {
+        "matrix": {"path": mf.path, "m": mf.m, "symmetry": mf.symmetry},
+        "memdet": {"logabsdet": truth, "sign": res.sign, **res.info.to_json_dict()},
+        "flodance": {**fit.to_json_dict(), "n": args.n, "logdet_hat": float(ell_hat)},
+        "rel_error": rel_error,
+    }
+    payload = {"schema_version": SCHEMA_VERSION, "command": "pipeline", "inputs": inputs, "outputs": outputs,
+               "timing": {"wall_seconds": time.perf_counter() - started}}
+    _emit(args, payload, [f"generated {mf.m}x{mf.m} {args.kind} matrix",
+                          f"memdet logabsdet = {truth:.12e}",
+                          f"extrapolated logdet_hat({args.n}) = {float(ell_hat):.12e}",
+                          f"relative error = {rel_error:.3e}"])
+    return 0
+
+
+def _add_gen_args(p):
+    p.add_argument("--kind", default="rbf", choices=("wishart", "rbf", "ntk-like", "spd-random", "sym-random"))
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--k", type=int, default=None, help="inner dimension (wishart / ntk-like)")
+    p.add_argument("--d", type=int, default=16, help="RBF point dimension")
+    p.add_argument("--ell", type=float, default=4.0, help="RBF length scale")
+    p.add_argument("--alpha", type=float, default=0.75, help="NTK-like power-law exponent")
+    p.add_argument("--jitter", type=float, default=None)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--out", required=True)
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2503_04424_b200",
                                      description="B200 MEMDET log-determinants (drop-in for oocdet memdet)")
@@ -125,15 +203,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.set_defaults(func=cmd_memdet)
 
     p = sub.add_parser("gen", help="write a seeded BASELINE-family matrix (MEMDET01)")
-    p.add_argument("--kind", default="rbf", choices=("wishart", "rbf", "ntk-like", "spd-random", "sym-random"))
-    p.add_argument("--n", type=int, required=True)
-    p.add_argument("--k", type=int, default=None, help="inner dimension (wishart / ntk-like)")
-    p.add_argument("--d", type=int, default=16, help="RBF point dimension")
-    p.add_argument("--ell", type=float, default=4.0, help="RBF length scale")
-    p.add_argument("--alpha", type=float, default=0.75, help="NTK-like power-law exponent")
-    p.add_argument("--jitter", type=float, default=None)
-    p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--out", required=True)
+    _add_gen_args(p)
     p.add_argument("--json", action="store_true")
     p.set_defaults(func=cmd_gen)
 
@@ -143,6 +213,30 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--case", choices=("gen", "sym"), default="sym")
     p.add_argument("--json", action="store_true")
     p.set_defaults(func=cmd_cost)
+
+    p = sub.add_parser("flodance", help="fit and extrapolate a prefix sequence")
+    p.add_argument("--prefix", required=True, help="prefix sidecar file")
+    p.add_argument("--d", type=int, required=True)
+    p.add_argument("--n0", type=int, required=True, help="burn-in start")
+    p.add_argument("--ns", type=int, required=True, help="fit window end")
+    p.add_argument("--q", type=int, required=True, help="exponent correction order")
+    p.add_argument("--predict", type=int, required=True, metavar="N")
+    p.add_argument("--interval", type=float, default=None, metavar="LEVEL")
+    p.add_argument("--trace-out", default=None, help="write the determinant-ratio trace as CSV")
+    p.add_argument("--json", action="store_true")
+    p.set_defaults(func=cmd_flodance)
+
+    p = sub.add_parser("pipeline", help="generate, factorize on the B200 engine, fit, and extrapolate")
+    _add_gen_args(p)
+    p.add_argument("--assume", choices=("sym", "spd"), default="sym")
+    p.add_argument("--max-mem", type=parse_size, default=None)
+    p.add_argument("--num-blocks", type=int, default=None)
+    p.add_argument("--scratch-dir", default=None)
+    p.add_argument("--n0", type=int, default=1)
+    p.add_argument("--ns", type=int, required=True)
+    p.add_argument("--q", type=int, default=0)
+    p.add_argument("--json", action="store_true")
+    p.set_defaults(func=cmd_pipeline)
     return parser
 
 

@@ -59,3 +59,21 @@ def test_memdet_json_on_gpu(tmp_path, capsys):
     bad = tmp_path / "ind.mdm"
     write_matrix(bad, gen.random_symmetric(50, seed=2), "symmetric")
     assert main(["memdet", "--in", str(bad), "--assume", "spd", "--num-blocks", "2"]) == 3  # NotSpd
+
+
+@pytest.mark.gpu
+def test_pipeline_json_on_gpu(tmp_path, capsys):
+    """`pipeline` (reference cli.py:169-199): generate, factor on the engine, fit, extrapolate."""
+    from oracle import memdet_oracle as O
+    from paper_2503_04424_b200 import fit_prefix, predict
+
+    out_path = tmp_path / "k.mdm"
+    assert main(["pipeline", "--kind", "rbf", "--n", "400", "--seed", "3", "--out", str(out_path),
+                 "--assume", "spd", "--num-blocks", "2", "--n0", "5", "--ns", "300", "--q", "1", "--json"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["command"] == "pipeline" and {"matrix", "memdet", "flodance", "rel_error"} <= set(out["outputs"])
+    ref, _ = O.memdet_cholesky(gen.rbf(400, seed=3), 2)
+    assert out["outputs"]["memdet"]["logabsdet"] == pytest.approx(float(ref[-1]), rel=1e-10)
+    fit = fit_prefix(ref, 1, 5, 300, 1)
+    assert out["outputs"]["flodance"]["logdet_hat"] == pytest.approx(float(predict(fit, 400)[1]), rel=1e-8)
+    assert out["outputs"]["rel_error"] >= 0.0
