@@ -328,8 +328,10 @@ def run_engine(args):
 
 
 def run_engine_multi(args):
-    """N > 1: one C2 logdet per step, factored across all ranks (row-cyclic tile rows, NCCL
-    broadcasts / all-reduces / all-gathers of the panels over NVLink) -> strong scaling."""
+    """N > 1: one C2 logdet per step, factored across all ranks (row-cyclic tile rows; per panel
+    an NCCL all-reduce of the diagonal block and a stream-ordered barrier, after which every
+    rank's Schur-update kernels read the solved panel tiles in place from their owners' grids
+    over NVLink peer memory) -> strong scaling."""
     import torch
     import torch.distributed as dist
 
@@ -350,7 +352,9 @@ def run_engine_multi(args):
     a = generate_rbf_device(torch, dev_x, n)
     torch.cuda.synchronize()
     peak = _native.probe_fp64_peak(local, 0.3)
-    runner = DistributedMemdet(n, None, 8, torch.device("cuda", local))
+    peer_env = os.environ.get("B2D_DIST_PEER")  # default: peer mode with NCCL, gather with gloo
+    runner = DistributedMemdet(n, None, 8, torch.device("cuda", local),
+                               peer=None if peer_env is None else peer_env == "1")
     for _ in range(args.warmup):
         prefix, fail = runner.run(a)
         if fail != -1:
@@ -399,7 +403,9 @@ def run_engine_multi(args):
             "data": "synthetic: C2 RBF Gram generated on device (seeded), not the paper's NTKs",
             "config": {"workload": "C2", "n": n, "num_blocks": C2["num_blocks"], "kind": "rbf d=16 l=4 jitter=1e-6",
                        "engine_tile": 128, "l2": "inputs (8.6 GB) larger than L2 (126 MB)",
-                       "parallelism": f"row-cyclic tile rows x{ws}, {backend} panel collectives"},
+                       "parallelism": f"row-cyclic tile rows x{ws}, " + (
+                           f"panels read in place over NVLink peer memory (CUDA IPC) after a {backend} barrier"
+                           if runner.shared is not None else f"{backend} panel all-gather")},
             "matrices_per_s": args.steps / (ms_max * 1e-3),
             "frac_of_fp64_peak": value / (ws * peak),
             "logdet": logdet,
@@ -415,6 +421,7 @@ def run_engine_multi(args):
             "gpu_launches": launches * args.steps,
             "clocks": clocks.summary(),
         }
+    runner.close()
     dist.barrier()
     dist.destroy_process_group()
     return out

@@ -135,16 +135,21 @@ int b2d_ctx_update_stats(b2d_ctx *ctx, double *flops, double *ms, int64_t *launc
  * waited for.  Tiles are 128 x 128 doubles in the engine's octet layout.
  *   b2d_tilemap: tile (i, j) lives at base + r*ld + j tiles, r = i, or with rmod > 0
  *                r = (i % rmod) * rstride + i / rmod (row-cyclic blocks gathered from ranks);
+ *                with npeer = rmod > 0 at peer[i % rmod] + (i / rmod)*ld + j tiles instead
+ *                (each rank's own grid, read in place over NVLink peer memory);
  *                packed_nt > 0 selects the packed lower triangle instead.
  *   b2d_tileset: columns [j0, j1), rows [lo(j), i1), lo = i0, or with lower = 1
  *                lo(j) = max(i0, ceil((j + row_off - off) / stride)) (rows may be local indices
  *                of a row-cyclic distribution, global row = i * stride + off). */
+#define B2D_MAX_PEERS 8
 typedef struct b2d_tilemap {
   double *base;
   int64_t ld;
   int32_t packed_nt;
   int32_t rmod;
   int64_t rstride;
+  int32_t npeer;
+  double *peer[B2D_MAX_PEERS];
 } b2d_tilemap;
 typedef struct b2d_tileset {
   int32_t i0, i1, j0, j1, lower, row_off, stride, off;
@@ -164,6 +169,15 @@ int b2d_pack_tiles(const void *src, int64_t lda, int dtype, int64_t row_base, in
                    const b2d_tilemap *out, const b2d_tileset *set, void *stream);
 /* prefix[q] = sum_{g <= q} ell[g] (double-double, rounded once), q < m. */
 int b2d_prefix_scan(const double *ell, int64_t m, double *prefix, void *stream);
+/* Peer-shared device buffers for the multi-GPU driver (replaces the panel all-gather: every rank
+ * reads the owners' solved panel tiles in place).  b2d_dev_alloc is a plain cudaMalloc on
+ * `device`; b2d_ipc_get_handle writes the 64-byte cudaIpcMemHandle of such a buffer;
+ * b2d_ipc_open_handle maps a peer's buffer into this process (peer access enabled). */
+int b2d_dev_alloc(int device, int64_t bytes, void **out);
+int b2d_dev_free(void *p);
+int b2d_ipc_get_handle(void *p, void *handle_out);
+int b2d_ipc_open_handle(int device, const void *handle, void **out);
+int b2d_ipc_close_handle(void *p);
 
 /* FP64 roofline calibration (off the timed path): sustained DMMA m8n8k4 rate over every SM for
  * about `seconds`, in TFLOP/s (2 flops per FMA). */

@@ -40,9 +40,21 @@ class OptionsC(ctypes.Structure):
                 ("host_scratch", ctypes.c_int32)]
 
 
+MAX_PEERS = 8
+
+
 class TileMapC(ctypes.Structure):
     _fields_ = [("base", ctypes.c_void_p), ("ld", ctypes.c_int64), ("packed_nt", ctypes.c_int32),
-                ("rmod", ctypes.c_int32), ("rstride", ctypes.c_int64)]
+                ("rmod", ctypes.c_int32), ("rstride", ctypes.c_int64), ("npeer", ctypes.c_int32),
+                ("peer", ctypes.c_void_p * MAX_PEERS)]
+
+
+def peer_map(peers, ld: int) -> TileMapC:
+    """Row-cyclic map over the ranks' own grids: tile (i, j) at peers[i % P] + (i // P, j)."""
+    m = TileMapC(None, ld, 0, len(peers), 0, len(peers))
+    for r, p in enumerate(peers):
+        m.peer[r] = p
+    return m
 
 
 class TileSetC(ctypes.Structure):
@@ -84,6 +96,11 @@ SIGNATURES = {
     "b2d_pack_tiles": (_I, [_P, _I64, _I, _I64, _I64, ctypes.POINTER(TileMapC),
                             ctypes.POINTER(TileSetC), _P]),
     "b2d_prefix_scan": (_I, [_P, _I64, _P, _P]),
+    "b2d_dev_alloc": (_I, [_I, _I64, ctypes.POINTER(_P)]),
+    "b2d_dev_free": (_I, [_P]),
+    "b2d_ipc_get_handle": (_I, [_P, _P]),
+    "b2d_ipc_open_handle": (_I, [_I, _P, ctypes.POINTER(_P)]),
+    "b2d_ipc_close_handle": (_I, [_P]),
 }
 
 _lib = None

@@ -1368,7 +1368,16 @@ extern "C" int b2d_probe_fp64_peak(int device, double seconds, double* tflops) {
 }
 
 static TileMap to_map(const b2d_tilemap* m) {
-  return m ? TileMap{m->base, m->ld, m->packed_nt, m->rmod, m->rstride} : TileMap{nullptr, 0, 0, 0, 0};
+  TileMap t{};
+  if (!m) return t;
+  t.base = m->base;
+  t.ld = m->ld;
+  t.packed_nt = m->packed_nt;
+  t.rmod = m->rmod;
+  t.rstride = m->rstride;
+  t.npeer = std::max(0, std::min<int>(m->npeer, MAX_PEERS));
+  for (int r = 0; r < t.npeer; ++r) t.peer[r] = m->peer[r];
+  return t;
 }
 static TileSet to_set(const b2d_tileset* t) {
   return TileSet{t->i0, t->i1, t->j0, t->j1, t->lower, t->row_off, t->stride, t->off};
@@ -1409,6 +1418,46 @@ extern "C" int b2d_tile_gemm(int mode, const b2d_tilemap* a, const b2d_tilemap* 
   else
     gemm_kernel<MODE_TRSM><<<(unsigned)n, GEMM_THREADS, GEMM_SMEM, (cudaStream_t)stream>>>(t);
   CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+// Device memory shared with peer ranks (multi-GPU driver: each rank's tile grid is read in place
+// by the others over NVLink).  Plain cudaMalloc allocations, so an IPC handle covers exactly one
+// buffer and opens at offset 0.
+extern "C" int b2d_dev_alloc(int device, int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return set_err(B2D_ERR_USAGE, "bad b2d_dev_alloc arguments");
+  CUDA_TRY(cudaSetDevice(device));
+  if (cudaMalloc(out, (size_t)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(B2D_ERR_NOMEM, "cudaMalloc of %lld bytes failed", (long long)bytes);
+  }
+  return B2D_OK;
+}
+
+extern "C" int b2d_dev_free(void* p) {
+  if (p) CUDA_TRY(cudaFree(p));
+  return B2D_OK;
+}
+
+extern "C" int b2d_ipc_get_handle(void* p, void* handle_out) {
+  if (!p || !handle_out) return set_err(B2D_ERR_USAGE, "bad b2d_ipc_get_handle arguments");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p));
+  memcpy(handle_out, &h, sizeof(h));
+  return B2D_OK;
+}
+
+extern "C" int b2d_ipc_open_handle(int device, const void* handle, void** out) {
+  if (!handle || !out) return set_err(B2D_ERR_USAGE, "bad b2d_ipc_open_handle arguments");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return B2D_OK;
+}
+
+extern "C" int b2d_ipc_close_handle(void* p) {
+  if (p) CUDA_TRY(cudaIpcCloseMemHandle(p));
   return B2D_OK;
 }
 

@@ -38,18 +38,25 @@ __host__ __device__ __forceinline__ int64_t n_packed_tiles(int nt) {
   return (int64_t)nt * (nt + 1) / 2;
 }
 
+constexpr int MAX_PEERS = 8;  // ranks whose tile grids one map can address (one NVLink domain)
+
 // Where a tile lives: the packed lower triangle (packed_nt > 0) or a row-major grid of tiles
 // with `ld` tiles per row (out-of-core blocks).
-// A third form serves row-cyclic storage gathered from several ranks: with rmod > 0, tile row
-// i lives at grid row (i % rmod) * rstride + i / rmod (rank-major blocks of rstride rows).
+// Row-cyclic storage over several ranks (rmod = ranks): tile row i belongs to rank i % rmod at
+// local row i / rmod, either gathered into one buffer of rank-major blocks of rstride rows
+// (base, npeer = 0), or read in place from each rank's own grid over NVLink peer memory
+// (npeer = rmod, peer[r] = rank r's grid as mapped into this process).
 struct TileMap {
   double* base;
   int64_t ld;
   int packed_nt;
   int rmod;
   int64_t rstride;
+  int npeer;
+  double* peer[MAX_PEERS];
   __host__ __device__ __forceinline__ double* tile(int i, int j) const {
     if (packed_nt > 0) return base + tile_index(i, j, packed_nt) * TILE_ELEMS;
+    if (npeer > 0) return peer[i % rmod] + ((int64_t)(i / rmod) * ld + j) * TILE_ELEMS;
     const int64_t r = rmod > 0 ? (int64_t)(i % rmod) * rstride + i / rmod : (int64_t)i;
     return base + (r * ld + j) * TILE_ELEMS;
   }

@@ -10,11 +10,19 @@ Step s (outer panel of W tile-columns [k0, ke)), two collectives per panel:
      exact) and every rank factors it redundantly (potrf + inverse per tile, intra-block
      solves and updates) -> identical L_blk, L_pp^{-1} and 2 log L_ii everywhere;
   2. every rank solves its own panel rows i >= ke against L_blk (DMMA TRSM + updates);
-  3. all-gather of the solved panel (each rank's rows x W tiles, double-buffered);
+  3. the solved panel is exchanged.  Peer mode (default with NCCL): a stream-ordered barrier
+     (an all-reduce of one word), after which the Schur-update kernels of every rank read the
+     owners' panel tiles in place from their tile grids over NVLink peer memory (the grids are
+     cudaMalloc'd and mapped into every rank with CUDA IPC; the kernel's producer warp bulk-
+     copies remote tiles straight into shared memory), so the exchange overlaps the DMMA work
+     tile by tile and no panel copy exists.  Gather mode: all-gather of the solved panel
+     (each rank's rows x W tiles, double-buffered) into a local buffer;
   4. next-cols: every rank updates its tiles in the next panel's columns [ke, ke+W) (main
      stream, the critical path), then the rest [ke+W, nt) on a side stream that overlaps the
      next panel's steps 1-3 (one-panel look-ahead, as the single-GPU driver).
-Every rank holds every 2 log L_ii at the end and scans the prefix itself.
+A solved panel column is final on its owner (later steps touch only columns to its right), so
+peers may read it any time after the barrier.  Every rank holds every 2 log L_ii at the end
+and scans the prefix itself.
 
 The driver is written against a small tile-ops interface so the same host logic runs on the
 GPUs (`CudaTileOps`, the C ABI's tile-level entry points on device buffers, NCCL) and in the
@@ -78,7 +86,10 @@ def factor_distributed(ops, comm, dist: RowCyclic, panel_tiles: int = 8):
         if ke >= nt:
             break
         ops.solve_panel(k0, ke)
-        comm.all_gather_into_tensor(ops.panel_buffer(s), ops.local_panel(k0, ke))
+        if getattr(ops, "peers", None):
+            comm.barrier()  # every rank's panel rows are solved: read in place from here on
+        else:
+            comm.all_gather_into_tensor(ops.panel_buffer(s), ops.local_panel(k0, ke))
         ops.update_trailing(s, k0, ke, ke, ne)                 # next panel's columns (main)
         ops.mark_panel(s)
         with ops.side():
@@ -96,7 +107,7 @@ class CudaTileOps:
     the rest updates on a side stream).  Local grid [maxloc][nt] tiles; W x W diagonal block;
     gathered panels [P][maxloc][W] tiles, double-buffered."""
 
-    def __init__(self, dist: RowCyclic, m: int, panel_tiles: int = 8, device=None):
+    def __init__(self, dist: RowCyclic, m: int, panel_tiles: int = 8, device=None, grid=None):
         import torch
 
         self.torch = torch
@@ -106,11 +117,13 @@ class CudaTileOps:
         self.dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         f64 = dict(dtype=torch.float64, device=self.dev)
         nt, ml, W = dist.nt, dist.maxloc, self.W
-        self.grid = torch.empty(ml * nt * TILE_ELEMS, **f64)
+        # the local tile grid (a peer-shareable buffer in peer mode, see DistributedMemdet)
+        self.grid = grid if grid is not None else torch.empty(ml * nt * TILE_ELEMS, **f64)
+        self.peers = None  # peer mode: every rank's grid address in this process, by rank
         self.diag_block = torch.empty(W * W * TILE_ELEMS, **f64)
         self.inv = torch.empty(W * TILE_ELEMS, **f64)
-        self.panel_loc = torch.empty(ml * W * TILE_ELEMS, **f64)
-        self.panels = [torch.empty(dist.world * ml * W * TILE_ELEMS, **f64) for _ in range(2)]
+        self._panel_loc = None  # gather mode only (allocated on first use)
+        self._panels = None
         npad = nt * T
         self.ell = torch.zeros(npad, **f64)
         self.diag = torch.zeros(npad, **f64)
@@ -204,23 +217,42 @@ class CudaTileOps:
             if p + 1 < ke:
                 self._gemm(0, g, bm, g, None, _native.TileSetC(i0, d.nloc, p + 1, ke, 0, 0, 0, 0), p, p + 1, 0)
 
+    def _gather_buffers(self):
+        if self._panels is None:
+            f64 = dict(dtype=self.torch.float64, device=self.dev)
+            ml, W = self.dist.maxloc, self.W
+            self._panel_loc = self.torch.empty(ml * W * TILE_ELEMS, **f64)
+            self._panels = [self.torch.empty(self.dist.world * ml * W * TILE_ELEMS, **f64) for _ in range(2)]
+        return self._panel_loc, self._panels
+
     def local_panel(self, k0: int, ke: int):
+        panel_loc, _ = self._gather_buffers()
         grid = self.grid.view(self.dist.maxloc, self.dist.nt, TILE_ELEMS)
-        loc = self.panel_loc.view(self.dist.maxloc, self.W, TILE_ELEMS)
+        loc = panel_loc.view(self.dist.maxloc, self.W, TILE_ELEMS)
         loc[:, : ke - k0].copy_(grid[:, k0:ke])
-        return self.panel_loc
+        return panel_loc
 
     def panel_buffer(self, s):
-        return self.panels[s % 2]
+        return self._gather_buffers()[1][s % 2]
+
+    def set_peers(self, ptrs):
+        """Peer mode: `ptrs[r]` = rank r's tile grid as addressable from this process."""
+        if len(ptrs) != self.dist.world or len(ptrs) > _native.MAX_PEERS:
+            raise ValueError(f"need {self.dist.world} peer grids (at most {_native.MAX_PEERS})")
+        self.peers = [int(p) for p in ptrs]
 
     def update_trailing(self, s, k0, ke, j0, j1):
-        """Own tiles in columns [j0, j1) -= L(i, panel) L(j, panel)^T; the gathered panel
-        [P][maxloc][W] is read through a row-cyclic tile map."""
+        """Own tiles in columns [j0, j1) -= L(i, panel) L(j, panel)^T.  The panel rows L(j, .)
+        are read in place from their owners' grids (peer mode) or from the gathered panel
+        [P][maxloc][W] (gather mode), both through a row-cyclic tile map."""
         if j1 <= j0:
             return
         d = self.dist
-        base = self.panels[s % 2].data_ptr() - k0 * TILE_BYTES
-        bmap = _native.TileMapC(base, self.W, 0, d.world, d.maxloc)
+        if self.peers:
+            bmap = _native.peer_map(self.peers, d.nt)
+        else:
+            base = self._gather_buffers()[1][s % 2].data_ptr() - k0 * TILE_BYTES
+            bmap = _native.TileMapC(base, self.W, 0, d.world, d.maxloc)
         g = self._grid_map()
         self._gemm(0, g, bmap, g, None, _native.TileSetC(0, d.nloc, j0, j1, 1, 0, d.world, d.rank), k0, ke, 0)
 
@@ -291,19 +323,105 @@ class TorchComm:
             self.d.all_gather(chunks, i, group=self.group)
         self._run(gather, out, inp)
 
+    def barrier(self):
+        """Stream-ordered barrier: an all-reduce of one word on the current CUDA stream (NCCL),
+        so work enqueued after it starts only once every rank's earlier work has finished."""
+        import torch
+
+        if self.staged:  # host barrier: finish this rank's enqueued work first
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                torch.cuda.current_stream().synchronize()
+            self.d.barrier(group=self.group)
+            return
+        if getattr(self, "_token", None) is None:
+            self._token = torch.zeros(1, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+        self.d.all_reduce(self._token, group=self.group)
+
+
+class _DeviceArray:
+    """A raw device allocation seen by torch through __cuda_array_interface__ (zero copy)."""
+
+    def __init__(self, ptr: int, nelem: int):
+        self.__cuda_array_interface__ = {"shape": (nelem,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerGrids:
+    """Tile grids shared across the ranks of one node: this rank's grid is a cudaMalloc'd
+    buffer; the others' are mapped in through CUDA IPC handles exchanged with
+    all_gather_object.  `ptrs[r]` is rank r's grid in this process."""
+
+    def __init__(self, nelem: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist_mod
+
+        self.lib = _native.load()
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev.index if dev.index is not None else torch.cuda.current_device()
+        p = ctypes.c_void_p()
+        _native.check(self.lib.b2d_dev_alloc(self.device, nelem * 8, ctypes.byref(p)), "b2d_dev_alloc")
+        self.own = p.value
+        self.tensor = torch.as_tensor(_DeviceArray(self.own, nelem), device=dev)
+        h = ctypes.create_string_buffer(64)
+        _native.check(self.lib.b2d_ipc_get_handle(ctypes.c_void_p(self.own), h), "b2d_ipc_get_handle")
+        world, rank = dist_mod.get_world_size(group), dist_mod.get_rank(group)
+        handles = [None] * world
+        dist_mod.all_gather_object(handles, h.raw, group=group)
+        self.opened, self.ptrs = [], []
+        for r, hr in enumerate(handles):
+            if r == rank:
+                self.ptrs.append(self.own)
+                continue
+            q = ctypes.c_void_p()
+            _native.check(self.lib.b2d_ipc_open_handle(self.device, ctypes.create_string_buffer(hr, 64),
+                                                       ctypes.byref(q)), "b2d_ipc_open_handle")
+            self.opened.append(q.value)
+            self.ptrs.append(q.value)
+
+    def close(self):
+        for q in self.opened:
+            self.lib.b2d_ipc_close_handle(ctypes.c_void_p(q))
+        self.opened = []
+        if self.own:
+            self.tensor = None
+            self.lib.b2d_dev_free(ctypes.c_void_p(self.own))
+            self.own = None
+
 
 class DistributedMemdet:
-    """Reusable per-rank workspace for repeated distributed factorisations of order m."""
+    """Reusable per-rank workspace for repeated distributed factorisations of order m.
+    `peer` (default: with NCCL) reads the solved panels in place over NVLink peer memory
+    instead of all-gathering them."""
 
-    def __init__(self, m: int, group=None, panel_tiles: int = 8, device=None):
+    def __init__(self, m: int, group=None, panel_tiles: int = 8, device=None, peer=None):
         import torch.distributed as dist_mod
 
         self.group = group
         self.m = m
         self.panel_tiles = panel_tiles
         self.dist = RowCyclic(-(-m // T), dist_mod.get_world_size(group), dist_mod.get_rank(group))
-        self.ops = CudaTileOps(self.dist, m, panel_tiles, device)
         self.comm = TorchComm(group)
+        if peer is None:
+            peer = not self.comm.staged and self.dist.world <= _native.MAX_PEERS
+        self.shared = None
+        grid = None
+        if peer:
+            self.shared = PeerGrids(self.dist.maxloc * self.dist.nt * TILE_ELEMS, group, device)
+            grid = self.shared.tensor
+        self.ops = CudaTileOps(self.dist, m, panel_tiles, device, grid=grid)
+        if peer:
+            self.ops.set_peers(self.shared.ptrs)
+
+    def close(self):
+        """Unmap the peers' grids and free this rank's (after every rank is done with it)."""
+        if self.shared is not None:
+            import torch
+
+            torch.cuda.synchronize()
+            self.comm.barrier()
+            torch.cuda.synchronize()
+            self.shared.close()
+            self.shared = None
 
     def run(self, a):
         """Enqueue pack + factorisation of the CUDA row-major matrix `a` (every rank passes the
@@ -312,12 +430,14 @@ class DistributedMemdet:
         return factor_distributed(self.ops, self.comm, self.dist, self.panel_tiles)
 
 
-def memdet_cholesky_distributed(a, group=None, panel_tiles: int = 8):
+def memdet_cholesky_distributed(a, group=None, panel_tiles: int = 8, peer=None):
     """Distributed logdet of a CUDA row-major SPD matrix visible to every rank (each rank packs
     only its own tile rows).  Returns (prefix as a NumPy array, fail index) on every rank."""
     import torch
 
-    runner = DistributedMemdet(int(a.shape[0]), group, panel_tiles, a.device)
+    runner = DistributedMemdet(int(a.shape[0]), group, panel_tiles, a.device, peer=peer)
     prefix, fail = runner.run(a)
     torch.cuda.synchronize(a.device)
-    return prefix.cpu().numpy(), fail
+    out = prefix.cpu().numpy()
+    runner.close()
+    return out, fail

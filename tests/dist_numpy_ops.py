@@ -24,6 +24,10 @@ class NumpyTileOps:
         self.panels = [torch.zeros((dist.world * ml, W, T, T), dtype=torch.float64) for _ in range(2)]
         self.ell = torch.zeros(nt * T, dtype=torch.float64)
         self.fail = INT64_MAX
+        self.peers = None  # peer mode: every rank's NumpyTileOps (ranks as threads of one process)
+
+    def set_peers(self, ops_by_rank):
+        self.peers = list(ops_by_rank)
 
     def load(self, a: np.ndarray):
         m, nt = self.m, self.dist.nt
@@ -89,9 +93,14 @@ class NumpyTileOps:
         for i in self.dist.rows:
             li = self.dist.local(i)
             for j in range(j0, min(j1, i + 1)):
-                gj = g[(j % P) * ml + j // P]
-                for p in range(k0, ke):
-                    self.grid[li, j] -= self.grid[li, p] @ gj[p - k0].T
+                if self.peers:  # the owner's grid, read in place
+                    row = self.peers[j % P].grid[j // P]
+                    for p in range(k0, ke):
+                        self.grid[li, j] -= self.grid[li, p] @ row[p].T
+                else:
+                    gj = g[(j % P) * ml + j // P]
+                    for p in range(k0, ke):
+                        self.grid[li, j] -= self.grid[li, p] @ gj[p - k0].T
 
     def mark_panel(self, s):
         pass
@@ -117,3 +126,89 @@ class NumpyTileOps:
 
     def prefix(self):
         return torch.cumsum(self.ell[: self.m], 0)
+
+
+class ThreadComm:
+    """TEST INFRASTRUCTURE: the collectives of paper_2503_04424_b200.distributed.TorchComm for
+    ranks run as threads of one process (CPU tensors, or CUDA tensors on one GPU with one stream
+    per thread).  Host barriers only: no kernel ever waits on another rank's kernel."""
+
+    class Group:
+        def __init__(self, world):
+            import threading
+
+            self.world = world
+            self.bar = threading.Barrier(world)
+            self.slots = [None] * world
+            self.result = None
+
+    ReduceOp = torch.distributed.ReduceOp
+
+    def __init__(self, group, rank):
+        self.g, self.rank = group, rank
+
+    @staticmethod
+    def _sync(t):
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+
+    def _exchange(self, t, combine):
+        g = self.g
+        self._sync(t)
+        g.slots[self.rank] = t
+        g.bar.wait()
+        if self.rank == 0:
+            g.result = combine(g.slots)
+            self._sync(g.result)
+        g.bar.wait()
+        return g.result
+
+    def all_reduce(self, t, op=None):
+        if op is None or op == self.ReduceOp.SUM:
+            r = self._exchange(t, lambda xs: torch.stack([x.to(xs[0].device) for x in xs]).sum(0))
+        elif op == self.ReduceOp.MIN:
+            r = self._exchange(t, lambda xs: torch.stack([x.to(xs[0].device) for x in xs]).min(0).values)
+        else:
+            raise ValueError(op)
+        t.copy_(r)
+        self._sync(t)
+        self.g.bar.wait()
+
+    def broadcast(self, t, src):
+        r = self._exchange(t, lambda xs: xs[src].clone())
+        t.copy_(r)
+        self._sync(t)
+        self.g.bar.wait()
+
+    def all_gather_into_tensor(self, out, inp):
+        r = self._exchange(inp, lambda xs: torch.cat([x.reshape(-1) for x in xs]))
+        out.copy_(r.reshape(out.shape))
+        self._sync(out)
+        self.g.bar.wait()
+
+    def barrier(self):
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+        self.g.bar.wait()
+
+
+def run_threads(world, fn):
+    """Run fn(rank) for every rank in its own thread; returns the results by rank (re-raises)."""
+    import threading
+
+    out, err = [None] * world, []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            err.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(600)
+    if err:
+        raise err[0]
+    return out

@@ -76,3 +76,32 @@ def test_row_cyclic_layout():
     # every tile row has exactly one owner and the lower triangle is balanced within one row
     loads = [sum(i + 1 for i in RowCyclic(64, 4, r).rows) for r in range(4)]
     assert max(loads) - min(loads) <= 64
+
+
+@pytest.mark.parametrize("world,m,panel", [(2, 700, 2), (3, 1000, 3), (4, 900, 2)])
+def test_peer_mode_driver_matches_oracle(world, m, panel):
+    """Peer mode (the NVLink product path: solved panels read in place from their owners' grids
+    after a barrier, no all-gather): ranks as threads sharing memory, NumPy tile math."""
+    from dist_numpy_ops import NumpyTileOps, ThreadComm, run_threads
+    from oracle import memdet_oracle as O
+
+    from paper_2503_04424_b200 import gen
+    from paper_2503_04424_b200.distributed import RowCyclic, factor_distributed
+
+    a = gen.spd_wishart(m, m, seed=9, shift=1e-2)
+    nt = -(-m // 128)
+    group = ThreadComm.Group(world)
+    ops = [NumpyTileOps(RowCyclic(nt, world, r), m, panel) for r in range(world)]
+    for o in ops:
+        o.load(a)
+        o.set_peers(ops)
+
+    def rank(r):
+        return factor_distributed(ops[r], ThreadComm(group, r), ops[r].dist, panel)
+
+    res = run_threads(world, rank)
+    ref, _ = O.memdet_cholesky(a, 1)
+    for r, (prefix, fail) in enumerate(res):
+        assert fail == -1
+        assert rel_err(prefix.numpy(), ref) <= 1e-10, (r, rel_err(prefix.numpy(), ref))
+        assert all(o.panels[0].abs().sum() == 0 for o in ops)  # no panel was ever gathered

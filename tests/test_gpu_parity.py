@@ -217,7 +217,7 @@ def test_out_of_core_not_spd():
 # ------------------------------------------------------------------ multi-rank driver on the GPU
 
 
-def _dist_worker(rank, world, port, backend, m, panel, q):
+def _dist_worker(rank, world, port, backend, m, panel, peer, q):
     import os
     import sys
 
@@ -234,18 +234,21 @@ def _dist_worker(rank, world, port, backend, m, panel, q):
     from paper_2503_04424_b200.distributed import memdet_cholesky_distributed
 
     a = torch.from_numpy(gen.spd_wishart(m, m, seed=11, shift=1e-2)).cuda()
-    prefix, fail = memdet_cholesky_distributed(a, panel_tiles=panel)
+    prefix, fail = memdet_cholesky_distributed(a, panel_tiles=panel, peer=peer)
     q.put((rank, prefix, fail))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,backend,m,panel", [(1, "nccl", 1000, 4), (2, "gloo", 1000, 3),
-                                                   (3, "gloo", 777, 2)])
-def test_distributed_driver_cuda_tile_ops(world, backend, m, panel):
+@pytest.mark.parametrize("world,backend,m,panel,peer", [(1, "nccl", 1000, 4, None), (2, "gloo", 1000, 3, False),
+                                                        (3, "gloo", 777, 2, False), (2, "gloo", 1000, 3, True),
+                                                        (3, "gloo", 900, 2, True)])
+def test_distributed_driver_cuda_tile_ops(world, backend, m, panel, peer):
     """The row-cyclic multi-GPU driver with the real CUDA tile kernels.  One GPU is available,
-    so world > 1 runs several ranks on cuda:0 with gloo (collectives are host-side, no rank
-    waits on another's kernels); world = 1 exercises the NCCL path."""
+    so world > 1 runs several ranks on cuda:0 with gloo (collectives and barriers are host-side,
+    no rank waits on another's kernels); world = 1 exercises the NCCL path.  peer=True is the
+    product exchange: every rank's grid is cudaMalloc'd, mapped into the other ranks with CUDA
+    IPC, and the Schur-update kernels read the owners' solved panel tiles in place."""
     import socket
 
     import torch.multiprocessing as mp
@@ -256,7 +259,8 @@ def test_distributed_driver_cuda_tile_ops(world, backend, m, panel):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, backend, m, panel, q)) for r in range(world)]
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, backend, m, panel, peer, q))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=600) for _ in range(world)]
