@@ -119,8 +119,14 @@ def ntk_like_device(n: int, p: int, alpha: float, jitter: float = 1e-8, seed: in
         del z
     k.div_(p)
     k.diagonal().add_(jitter)
-    # bit-symmetric: mirror the lower triangle onto the upper (kernelgen.py:136-149 precedent)
-    k.copy_(torch.tril(k) + torch.tril(k, -1).T)
+    # bit-symmetric: mirror the lower triangle onto the upper (kernelgen.py:136-149 precedent),
+    # block column by block column so no n x n temporary is needed
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        blk = k[c0:c1, c0:c1]
+        blk.copy_(torch.tril(blk) + torch.tril(blk, -1).T)
+        if c1 < n:
+            k[c0:c1, c1:].copy_(k[c1:, c0:c1].T)
     return k
 
 
