@@ -45,6 +45,10 @@ extern "C" {
 #define B2D_MODE_LDL_NOPIV 1   /* memdet_ldl without pivoting: d = L_ii^2, perm = identity  */
 #define B2D_MODE_LDL_PIV 2     /* memdet_ldl with block-local 1x1 pivots (_ldl.pyx:30-46):
                                   the reference's b x b block walk, d = D, perm = pivots    */
+#define B2D_MODE_LU 3          /* memdet_lu (generic matrix, memdet.py:268-319): block-local
+                                  partial pivoting in the reference's generic block walk;
+                                  d = U_ii, perm = pivots, prefix[m-1] = log|det|; a zero
+                                  pivot (singular) sets fail_index and returns B2D_OK       */
 
 typedef struct b2d_run_info {
   int64_t m;               /* matrix order                                                 */

@@ -22,7 +22,7 @@ B2D_ERR_NOMEM = 6
 B2D_ERR_UNSUPPORTED = 7
 
 B2D_F64, B2D_F32 = 0, 1
-MODE_CHOLESKY, MODE_LDL_NOPIV, MODE_LDL_PIV = 0, 1, 2
+MODE_CHOLESKY, MODE_LDL_NOPIV, MODE_LDL_PIV, MODE_LU = 0, 1, 2, 3
 
 
 class RunInfoC(ctypes.Structure):

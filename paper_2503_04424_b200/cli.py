@@ -7,8 +7,8 @@
     python -m paper_2503_04424_b200 pipeline --kind rbf --n 4096 --out K.mdm --assume spd --ns 3000 --json
 
 Same flags, JSON payload (schema_version 1) and exit codes as the reference: 0 success,
-2 usage error, 3 numerical failure, 4 I/O failure.  `--assume gen` (the LU path) and the SLQ /
-block-diagonal baselines are outside this engine's scope; `gen` / `pipeline` generate the
+2 usage error, 3 numerical failure, 4 I/O failure.  The SLQ / block-diagonal baselines are
+outside this engine's scope; `gen` / `pipeline` generate the
 BASELINE families (one output per datapoint, so FLODANCE runs with d = 1 in `pipeline`) instead
 of the reference's Matern-LMC generator.
 """
@@ -26,7 +26,7 @@ from . import __version__, gen
 from .cost import predicted_cost
 from .errors import NumericalError, OocdetError, StorageError
 from .flodance import fit_prefix, predict, predict_interval, scaling_ratio_trace
-from .memdet import memdet_cholesky, memdet_ldl
+from .memdet import memdet_cholesky, memdet_ldl, memdet_lu
 from .prefixio import read_prefix
 from .storage import write_matrix
 
@@ -59,11 +59,14 @@ def _emit(args, payload: dict, lines):
 
 
 def cmd_memdet(args) -> int:
-    if args.assume == "gen":
-        raise ValueError("--assume gen (LU) is outside the B200 engine's scope; use sym or spd")
-    driver = memdet_cholesky if args.assume == "spd" else memdet_ldl
-    res = driver(args.infile, max_mem=args.max_mem, num_blocks=args.num_blocks,
-                 scratch_dir=args.scratch_dir, prefix_out=args.prefix_out)
+    kwargs = dict(max_mem=args.max_mem, num_blocks=args.num_blocks, scratch_dir=args.scratch_dir)
+    if args.assume == "gen":  # reference cli.py:81-88
+        if args.prefix_out:
+            raise ValueError("--prefix-out requires --assume sym or spd")
+        res = memdet_lu(args.infile, **kwargs)
+    else:
+        driver = memdet_cholesky if args.assume == "spd" else memdet_ldl
+        res = driver(args.infile, prefix_out=args.prefix_out, **kwargs)
     info = res.info
     payload = {
         "schema_version": SCHEMA_VERSION, "logabsdet": res.logabsdet, "sign": res.sign,

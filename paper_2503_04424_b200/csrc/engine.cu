@@ -25,6 +25,7 @@
 #include "../../include/memdet_b200.h"
 #include "kernels.cu"
 #include "ldl.cu"
+#include "lu.cu"
 
 namespace b2d {
 
@@ -90,6 +91,7 @@ struct Ooc {
   unsigned long long* amax = nullptr;
   uint8_t* ltag = nullptr;  // blocked pivoted LDL: per-entry tags, panel columns C / W, diagonal, pivot column
   double *lC = nullptr, *lW = nullptr, *ldiag = nullptr, *lcol = nullptr;
+  double* inv2 = nullptr;  // LU: inverses of the diagonal tiles of U^T (column-block solves)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
@@ -159,6 +161,12 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)lu_panel_smem(LC_RMAX)));
+  CUDA_TRY(cudaFuncSetAttribute(tile_inv_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
+  CUDA_TRY(cudaFuncSetAttribute(transpose_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)TRANSPOSE_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(ldl_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(LDL_FINISH_SMEM_MAX * 8)));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -217,6 +225,7 @@ static void destroy(Ctx* c) {
   cudaFree(o.lW);
   cudaFree(o.ldiag);
   cudaFree(o.lcol);
+  cudaFree(o.inv2);
   cudaFree(o.stage);
   for (double* h : o.pool) {
     if (o.dev_scratch) cudaFree(h);
@@ -270,7 +279,8 @@ static int64_t ref_select_blocking(int64_t m, int64_t c, int64_t beta) {
   return q;
 }
 
-static void fill_ref_info(b2d_run_info* info, int64_t m, int64_t num_blocks, int64_t max_mem, int esz) {
+static void fill_ref_info(b2d_run_info* info, int64_t m, int64_t num_blocks, int64_t max_mem, int esz,
+                          bool generic = false) {
   int64_t nb = num_blocks > 0 ? num_blocks : (max_mem > 0 ? ref_select_blocking(m, max_mem, esz) : 1);
   int64_t n_b, b, tail;
   ref_layout(m, nb, &n_b, &b, &tail);
@@ -281,6 +291,11 @@ static void fill_ref_info(b2d_run_info* info, int64_t m, int64_t num_blocks, int
   info->blocks_read = (2 * n * n * n - 3 * n * n + 7 * n) / 6;                       // cost.py:79-83
   info->blocks_written = n <= 2 ? 0 : (n * n * n + 3 * n * n - 22 * n + 24) / 6;     // cost.py:86-92
   info->scratch_slots = n <= 2 ? 0 : (n * n + n - 8) / 2;                            // cost.py:95-101
+  if (generic) {  // the generic walk (memdet.py:97-121): cost.py:79-101, case "generic"
+    info->blocks_read = (2 * n * n * n - 3 * n * n + 4 * n) / 3;
+    info->blocks_written = n <= 2 ? 0 : (n * n * n - 4 * n - 3) / 3;
+    info->scratch_slots = n <= 2 ? 0 : n * n - n - 1;
+  }
 }
 
 
@@ -326,7 +341,7 @@ static int create_streams_events(Ctx* c) {
 // select_blocking(max_mem), memdet.py:63-80, 249-255) and grows until the slots fit.
 static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx** out) {
   if (m < 1) return set_err(B2D_ERR_USAGE, "matrix dimension must be >= 1, got %lld", (long long)m);
-  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV && mode != B2D_MODE_LDL_PIV)
+  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV && mode != B2D_MODE_LDL_PIV && mode != B2D_MODE_LU)
     return set_err(B2D_ERR_USAGE, "unknown mode %d", mode);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -350,9 +365,11 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   const int64_t npad_full = (int64_t)nt_full * T;
   const size_t incore_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + (size_t)nt_full * TILE_BYTES +
                              3 * (size_t)npad_full * 8 + (size_t)NSTAGE * T * npad_full * 8;
-  // block-pivoted LDL pivots inside the reference's b x b diagonal blocks: always the block walk
-  const bool force = (opt && opt->force_out_of_core) || mode == B2D_MODE_LDL_PIV;
-  const int nslot = mode == B2D_MODE_LDL_PIV ? NSLOT_LDL : NSLOT;
+  // block-pivoted LDL pivots inside the reference's b x b diagonal blocks, and the generic LU
+  // runs the reference's generic walk: always the block walk
+  const bool pivoted = mode == B2D_MODE_LDL_PIV || mode == B2D_MODE_LU;
+  const bool force = (opt && opt->force_out_of_core) || pivoted;
+  const int nslot = pivoted ? NSLOT_LDL : NSLOT;
   int64_t vec_len = npad_full;
 #define ALLOC(ptr, bytes)                                        \
   do {                                                           \
@@ -377,10 +394,14 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       int64_t n_b, b, tail;
       ref_layout(m, nb, &n_b, &b, &tail);
       const int nbt = (int)((b + T - 1) / T);
-      const size_t need = (size_t)(nslot + (mode == B2D_MODE_LDL_PIV ? 1 : 0)) * nbt * nbt * TILE_BYTES +
+      const size_t need = (size_t)(nslot + (pivoted ? 1 : 0)) * nbt * nbt * TILE_BYTES +
                           (size_t)nbt * TILE_BYTES +
                           (size_t)T * nbt * T * 8 + 3 * (size_t)(m + (int64_t)(nbt + 1) * T) * 8;
-      if (need <= budget || n_b >= m) {
+      // LU: |det| does not depend on where the pivots are searched, so the engine keeps its
+      // diagonal blocks within the cluster panel kernel's reach (the reported counters stay
+      // the reference's)
+      const bool lu_fits = mode != B2D_MODE_LU || b <= (int64_t)LC * LC_RMAX;
+      if ((need <= budget && lu_fits) || n_b >= m) {
         if (need > budget) {
           destroy(c);
           return set_err(B2D_ERR_NOMEM, "no out-of-core plan fits %.2f GB of HBM", budget / 1e9);
@@ -404,7 +425,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     ALLOC(o.stage, (size_t)T * o.nbt * T * 8);
     ALLOC(c->inv, (size_t)o.nbt * TILE_BYTES);
-    if (mode == B2D_MODE_LDL_PIV) {
+    if (pivoted) {
       const int64_t ld = (int64_t)o.nbt * T;
       ALLOC(o.dense, (size_t)ld * ld * 8);
       ALLOC(o.swaps, (size_t)ld * 8);
@@ -417,11 +438,14 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       ALLOC(o.lW, (size_t)LDL_NB * ld * 8);
       ALLOC(o.ldiag, (size_t)ld * 8);
       ALLOC(o.lcol, (size_t)ld * 8);
+      if (mode == B2D_MODE_LU) ALLOC(o.inv2, (size_t)o.nbt * TILE_BYTES);
     }
     // scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front; in HBM
     // when it fits beside the slots (scratch traffic then moves at HBM instead of PCIe speed),
     // otherwise in pinned host memory
-    const int64_t nsc = o.nb <= 2 ? 0 : ((int64_t)o.nb * o.nb + o.nb - 8) / 2;
+    const int64_t nsc = o.nb <= 2 ? 0
+                        : mode == B2D_MODE_LU ? (int64_t)o.nb * o.nb - o.nb - 1        // cost.py, generic
+                                              : ((int64_t)o.nb * o.nb + o.nb - 8) / 2;
     size_t used = 0, fb = 0, tb = 0;
     cudaMemGetInfo(&fb, &tb);
     used = free_b > fb ? free_b - fb : 0;
@@ -845,7 +869,7 @@ static std::vector<Visit> stage_visits(int nb, int k) {
 // slot s as the engine's lower block (rj, ri): from the scratchpad if it was written this run
 // (the reference cache table, storage.py:134-144), else from the input in 128-row strips
 // (H2D + pack_block_kernel).  Waits until the slot's previous contents are consumed and stored.
-static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, int dtype) {
+static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, int dtype, bool trans = true) {
   Ooc& o = c->o;
   cudaStreamWaitEvent(o.s_h2d, o.ev_used[s], 0);
   cudaStreamWaitEvent(o.s_h2d, o.ev_stored[s], 0);
@@ -854,6 +878,27 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
     cudaStreamWaitEvent(o.s_h2d, o.ev_key[key], 0);  // the scratch copy must have landed
     CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyDefault, o.s_h2d));
     if (!o.dev_scratch) c->h2d += (int64_t)o.slot_bytes();
+  } else if (!trans) {
+    // generic blocks (LU): reference block (ri, rj) as the engine block (ri, rj), strip J of
+    // its rows -> tile row J
+    const size_t esz = dtype == B2D_F64 ? 8 : 4;
+    const int64_t rows_blk = o.size(ri), cols_blk = o.size(rj);
+    const int64_t ld_stage = (int64_t)o.nbt * T;
+    for (int J = 0; J < o.tiles(ri); ++J) {
+      const int64_t frow = (int64_t)ri * o.b + (int64_t)J * T;
+      const int64_t nrows = std::min<int64_t>(T, rows_blk - (int64_t)J * T);
+      const char* src = (const char*)a + ((size_t)frow * lda + (size_t)rj * o.b) * esz;
+      CUDA_TRY(cudaMemcpy2DAsync(o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)cols_blk * esz,
+                                 (size_t)nrows, cudaMemcpyHostToDevice, o.s_h2d));
+      c->h2d += nrows * cols_blk * (int64_t)esz;
+      if (dtype == B2D_F64)
+        pack_block_nt_kernel<double><<<o.tiles(rj), 256, 0, o.s_h2d>>>(
+            (const double*)o.stage, ld_stage, rows_blk, cols_blk, ri == rj, o.map(s), J);
+      else
+        pack_block_nt_kernel<float><<<o.tiles(rj), 256, 0, o.s_h2d>>>(
+            (const float*)o.stage, ld_stage, rows_blk, cols_blk, ri == rj, o.map(s), J);
+      c->launches++;
+    }
   } else {
     const size_t esz = dtype == B2D_F64 ? 8 : 4;
     const int64_t rows_blk = o.size(rj), cols_blk = o.size(ri);  // engine block: rows of rj, cols of ri
@@ -908,8 +953,9 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
 
 // Panel solve of slot s (engine lower block (x, k), x's rows) against the factored diagonal
 // block in slot sa: right-looking over L_kk's tile-columns in groups of W (dense.py:94-99).
-static void ooc_trsm(Ctx* c, int s, int x, int sa, int k) {
+static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nullptr) {
   Ooc& o = c->o;
+  if (!inv) inv = c->inv;
   cudaStreamWaitEvent(c->s_main, o.ev_loaded[s], 0);
   const int R = o.tiles(x), Q = o.tiles(k), W = c->W_TILES;
   for (int q0 = 0; q0 < Q; q0 += W) {
@@ -917,7 +963,7 @@ static void ooc_trsm(Ctx* c, int s, int x, int sa, int k) {
     for (int q = q0; q < qe; ++q) {
       GemmTask t{};
       t.c = o.map(s);
-      t.binv = c->inv + (int64_t)q * TILE_ELEMS;
+      t.binv = inv + (int64_t)q * TILE_ELEMS;
       t.out = TileSet{0, R, q, q + 1, 0, 0};
       t.k = q;
       launch_gemm(c, c->s_main, MODE_TRSM, t, false, 0.0);
@@ -976,7 +1022,7 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
   cudaStream_t s = c->s_main;
   cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
-  unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld);
+  unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld, 1);
   cudaMemsetAsync(o.amax, 0, 8, s);
   block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
   // blocked pivoted LDL: panels of LDL_NB steps (one CTA), then the delayed trailing update
@@ -1021,6 +1067,114 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
   return B2D_OK;
 }
 
+// Generic (LU) diagonal block in slot sa (stage k), reference lu_inplace (dense.py:38-54):
+// dense copy, blocked LU with block-local partial pivoting, pivots / permutation / log|u_ii|,
+// then L (unit lower) back into slot sa and U^T (lower) into slot su with the inverses of
+// their diagonal tiles for the row-block and column-block solves.
+static int ooc_lu_factor(Ctx* c, int sa, int su, int k) {
+  Ooc& o = c->o;
+  const int nt = o.tiles(k);
+  const int64_t n = o.size(k);
+  const int64_t ld = (int64_t)o.nbt * T, g0 = (int64_t)k * o.b;
+  cudaStream_t s = c->s_main;
+  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
+  cudaStreamWaitEvent(s, o.ev_used[su], 0);
+  cudaStreamWaitEvent(s, o.ev_stored[su], 0);
+  unpack_block_kernel<<<(unsigned)(nt * nt), 256, 0, s>>>(o.map(sa), nt, o.dense, ld, 0);
+  const LuArgs g{o.dense, o.dblk, o.swaps, c->fail, ld, n, g0};
+  const int cols_grid = (int)std::max<int64_t>(1, (n + 255) / 256);
+  for (int64_t r0 = 0; r0 < n; r0 += LU_NB) {
+    const int nbk = (int)std::min<int64_t>(LU_NB, n - r0);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = LC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(LC);
+    cfg.blockDim = dim3(LC_THREADS);
+    cfg.dynamicSmemBytes = lu_panel_smem((int)((n + LC - 1) / LC));
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, lu_panel_cluster_kernel, g, r0, nbk));
+    lu_swap_rows_kernel<<<cols_grid, 256, 0, s>>>(g, r0, nbk);
+    const int64_t rest = n - r0 - nbk;
+    if (rest > 0) {
+      lu_u12_kernel<<<(unsigned)((rest + 127) / 128), 128, 0, s>>>(g, r0, nbk);
+      const int64_t mt = (rest + 63) / 64;
+      lu_bulk_kernel<<<(unsigned)(mt * mt), 256, 0, s>>>(g, r0, nbk);
+    }
+    c->launches += rest > 0 ? 4 : 2;
+  }
+  ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
+                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
+                                                                        o.perm_global, c->ell, c->diag);
+  const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
+  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
+  pack_upper_t_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(su), nt);
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), c->inv);
+  tile_inv_lower_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(su), o.inv2);
+  c->launches += 7;
+  cudaEventRecord(o.ev_used[sa], s);
+  cudaEventRecord(o.ev_used[su], s);
+  return B2D_OK;
+}
+
+// One visit of the reference's generic walk, stage k (memdet.py:97-121): rows bottom-up, the
+// column direction alternating so one of B / C is reused between consecutive visits.
+struct GVisit {
+  int i, j;
+  bool new_row, load_b, solve_b, write_b, next_diag;
+};
+
+static std::vector<GVisit> generic_visits(int nb, int k) {
+  std::vector<GVisit> v;
+  const int t = nb - 1 - k;
+  for (int i = nb - 1; i > k; --i) {
+    const bool asc = (i - k) % 2 == 0;
+    const int first = asc ? k + 1 : nb - 1, last = asc ? nb - 1 : k + 1;
+    for (int step = 0; step < nb - 1 - k; ++step) {
+      const int j = asc ? k + 1 + step : nb - 1 - step;
+      const bool bottom = i == nb - 1;
+      v.push_back(GVisit{i, j, j == first, bottom || j != first, bottom, bottom && (t > 2 || j != last),
+                         i == k + 1 && j == k + 1});
+    }
+  }
+  return v;
+}
+
+// Slot x (engine block of `rows` x `cols` blocks) replaced by its transpose, through the
+// permute temp slot (pointer swap, as ooc_permute).
+static void ooc_transpose(Ctx* c, int x, int rows, int cols) {
+  Ooc& o = c->o;
+  const int tmp = o.nslot - 1;
+  transpose_block_kernel<<<(unsigned)(o.tiles(rows) * o.tiles(cols)), 256, TRANSPOSE_SMEM, c->s_main>>>(
+      o.map(x), o.map(tmp), o.tiles(rows), o.tiles(cols));
+  c->launches++;
+  std::swap(o.slot[x], o.slot[tmp]);
+  cudaEventRecord(o.ev_used[x], c->s_main);  // the store of slot x must follow the transpose
+}
+
+// Generic Schur update of slot st (block (i, j)) -= X_i Y_j: X_i in slot sx (rows of i, the
+// column block solved against U), Y_j^T in slot sy (rows of j, the row block solved with L).
+static void ooc_schur_full(Ctx* c, int st, int i, int j, int sx, int sy, int k) {
+  Ooc& o = c->o;
+  for (int x : {st, sx, sy}) cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
+  GemmTask t{};
+  t.a = o.map(sx);
+  t.b = o.map(sy);
+  t.c = o.map(st);
+  t.out = TileSet{0, o.tiles(i), 0, o.tiles(j), 0, 0};
+  t.p0 = 0;
+  t.p1 = o.tiles(k);
+  const double K = (double)t.p1 * T;
+  launch_gemm(c, c->s_main, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
+  cudaEventRecord(o.ev_used[st], c->s_main);
+  cudaEventRecord(o.ev_used[sx], c->s_main);
+  cudaEventRecord(o.ev_used[sy], c->s_main);
+}
+
 // Panel block in slot x (engine rows of block `rows`): columns permuted by the stage's block
 // permutation into the temp slot, which then takes slot x's place (memdet.py:365-366, 378-379).
 static void ooc_permute(Ctx* c, int x, int rows, int k) {
@@ -1056,7 +1210,7 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   o.reads = o.writes = 0;
   o.rr = 0;
   auto alloc = [&](std::initializer_list<int> busy) {
-    const int pool = c->mode == B2D_MODE_LDL_PIV ? o.nslot - 1 : o.nslot;  // last LDL slot: permute temp
+    const int pool = c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU ? o.nslot - 1 : o.nslot;  // last: permute temp
     for (int tries = 0; tries < pool; ++tries) {
       const int s = o.rr;
       o.rr = (o.rr + 1) % pool;
@@ -1067,8 +1221,52 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
     return -1;
   };
   const bool piv = c->mode == B2D_MODE_LDL_PIV;
+  int rc = 0;
+  if (c->mode == B2D_MODE_LU) {
+    // the reference's generic walk (memdet.py:268-319); blocks (i, k), (i, j), (k, k) are held
+    // as themselves, row-k blocks (k, j) transposed so that T -= X_i Y_j is the engine's
+    // C -= A B^T
+    int sa = alloc({});
+    if ((rc = ooc_load(c, 0, 0, sa, a, lda, dtype, false))) return rc;
+    for (int k = 0; k < o.nb; ++k) {
+      const int su = alloc({sa});
+      if ((rc = ooc_lu_factor(c, sa, su, k))) return rc;
+      if (k == o.nb - 1) break;
+      int sx = -1, sy = -1, next_a = -1;
+      for (const GVisit& v : generic_visits(o.nb, k)) {
+        if (v.new_row) {
+          sx = alloc({sa, su, sy, sx});
+          if ((rc = ooc_load(c, v.i, k, sx, a, lda, dtype, false))) return rc;
+          ooc_trsm(c, sx, v.i, su, k, o.inv2);  // X_i = A(i, k) U^{-1}    (dense.py:102-106)
+        }
+        if (v.load_b) {
+          sy = alloc({sa, su, sy, sx});
+          if ((rc = ooc_load(c, k, v.j, sy, a, lda, dtype))) return rc;
+          if (v.solve_b) {
+            ooc_permute(c, sy, v.j, k);         // Y_j^T = (P A(k, j))^T L^{-T} (dense.py:94-99)
+            ooc_trsm(c, sy, v.j, sa, k);
+            if (v.write_b && (rc = ooc_store(c, k, v.j, sy))) return rc;
+          }
+        }
+        const int st = alloc({sa, su, sx, sy});
+        if ((rc = ooc_load(c, v.i, v.j, st, a, lda, dtype, false))) return rc;
+        ooc_schur_full(c, st, v.i, v.j, sx, sy, k);  // dense.py:109-116, "ct_b"
+        // (k+1, j > k+1) is next stage's row block: kept transposed, the form its solve uses
+        if (v.i == k + 1 && v.j > k + 1) ooc_transpose(c, st, v.i, v.j);
+        if (v.next_diag) next_a = st;
+        else if ((rc = ooc_store(c, v.i, v.j, st))) return rc;
+      }
+      sa = next_a;
+    }
+    enqueue_prefix(c);
+    cudaEventRecord(c->ev_join, o.s_d2h);
+    cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+    end(c, user);
+    CUDA_TRY(cudaGetLastError());
+    return B2D_OK;
+  }
   int sa = alloc({});
-  int rc = ooc_load(c, 0, 0, sa, a, lda, dtype);
+  rc = ooc_load(c, 0, 0, sa, a, lda, dtype);
   if (rc) return rc;
   for (int k = 0; k < o.nb; ++k) {
     if (piv) {
@@ -1176,6 +1374,7 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
               at(c->ev_catch[st]), at(c->ev_rest[st]));
   }
   if (fail_index) *fail_index = fail == ULLONG_MAX ? -1 : (int64_t)fail;
+  if (c->mode == B2D_MODE_LU) return B2D_OK;  // a zero pivot means det = 0 (fail_index), not an error
   if (fail != ULLONG_MAX && c->mode == B2D_MODE_LDL_PIV)
     return set_err(B2D_ERR_INDEFINITE, "LDL pivot %lld below tolerance (block-local 1x1 pivoting)",
                    (long long)fail);
@@ -1187,7 +1386,7 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
 
 static int fetch_perm(Ctx* c, int64_t* perm) {
   if (!perm) return set_err(B2D_ERR_USAGE, "null perm");
-  if (c->mode == B2D_MODE_LDL_PIV && c->ooc && c->o.perm_global) {
+  if ((c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU) && c->ooc && c->o.perm_global) {
     CUDA_TRY(cudaMemcpy(perm, c->o.perm_global, c->m * 8, cudaMemcpyDeviceToHost));
   } else {
     for (int64_t g = 0; g < c->m; ++g) perm[g] = g;
@@ -1305,14 +1504,15 @@ int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, i
   if (rc == B2D_OK && perm_out) rc = fetch_perm(c, perm_out);
   destroy(c);
   if (rc != B2D_OK && rc != B2D_ERR_NOT_SPD) return rc;
-  fill_ref_info(&local, m, num_blocks, max_mem, esz);
+  fill_ref_info(&local, m, num_blocks, max_mem, esz, mode == B2D_MODE_LU);
   local.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (info) *info = local;
   if (rc == B2D_OK && sign_out) {
-    // cumprod(sign d) (memdet.py:407); Cholesky pivots are positive
+    // cumprod(sign d) (memdet.py:407); Cholesky pivots are positive.  LU: sign of det(U) only
+    // (the permutation parity is the caller's, from perm_out)
     int64_t sg = 1;
     for (int64_t g = 0; g < m; ++g) {
-      if (mode == B2D_MODE_LDL_PIV) sg *= d_out[g] > 0 ? 1 : (d_out[g] < 0 ? -1 : 0);
+      if (mode == B2D_MODE_LDL_PIV || mode == B2D_MODE_LU) sg *= d_out[g] > 0 ? 1 : (d_out[g] < 0 ? -1 : 0);
       sign_out[g] = sg;
     }
   }

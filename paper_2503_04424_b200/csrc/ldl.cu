@@ -22,11 +22,12 @@
 namespace b2d {
 namespace cg = cooperative_groups;
 
+// lower = 1: the lower tile triangle (symmetric blocks); 0: every tile (generic blocks).
 __global__ void __launch_bounds__(256) unpack_block_kernel(TileMap src, int ntiles, double* __restrict__ dense,
-                                                           int64_t ld) {
+                                                           int64_t ld, int lower) {
   __shared__ double sm[32][129];
   int I, J;
-  const TileSet all{0, ntiles, 0, ntiles, 1, 0, 0, 0};
+  const TileSet all{0, ntiles, 0, ntiles, lower, 0, 0, 0};
   tile_order(blockIdx.x, all, 1, &I, &J);
   const double* t = src.tile(I, J);
   for (int qtr = 0; qtr < 4; ++qtr) {
@@ -447,7 +448,7 @@ __global__ void ldl_finish_kernel(const int64_t* __restrict__ swaps, const doubl
     auto walk = [&](int64_t* __restrict__ q) {
       for (int64_t r = 0; r < n; ++r) {
         const int64_t t = __ldg(swaps + r);
-        if (t != r) {
+        if (t > r && t < n) {  // (entries past a failed step are stale: never valid there)
           const int64_t x = q[r];
           q[r] = q[t];
           q[t] = x;

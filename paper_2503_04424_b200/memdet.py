@@ -21,7 +21,7 @@ from __future__ import annotations
 import math
 import threading
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 from typing import Iterator, NamedTuple
 
 import numpy as np
@@ -93,16 +93,31 @@ class ScheduleEntry:
     target: str
 
 
+def _generic_visits(n_b: int, k: int):
+    """Stage-k walk (0-based) of the generic case (memdet.py:97-121): rows bottom-up, the
+    column direction alternating per row so one of B / C is reused between consecutive visits;
+    yields (i, j, new_row, load_b, next_diag)."""
+    for i in range(n_b - 1, k, -1):
+        asc = (i - k) % 2 == 0
+        js = range(k + 1, n_b) if asc else range(n_b - 1, k, -1)
+        first = k + 1 if asc else n_b - 1
+        for j in js:
+            yield i, j, j == first, i == n_b - 1 or j != first, i == j == k + 1
+
+
 def schedule(n_b: int, case: str, k: int) -> list[ScheduleEntry]:
     """Reference tile-visit order for stage k (1-based) with fresh-load annotations
-    (memdet.py:156-177).  Only the symmetric case is in scope for this engine."""
+    (memdet.py:156-177); the out-of-core engine walks the same order."""
     if case not in ("generic", "symmetric"):
         raise ValueError(f"case must be 'generic' or 'symmetric', got {case!r}")
-    if case == "generic":
-        raise NotImplementedError("the generic (LU) path is out of scope for the B200 engine")
     if not 1 <= k < n_b:
         raise ValueError(f"stage k must satisfy 1 <= k < n_b, got k={k}, n_b={n_b}")
     out = []
+    if case == "generic":
+        for i, j, new_row, load_b, nd in _generic_visits(n_b, k - 1):
+            loads = tuple(x for x, on in (("B", load_b), ("C", new_row)) if on)
+            out.append(ScheduleEntry(i + 1, j + 1, loads, "resident" if nd else "store"))
+        return out
     for v in _symmetric_visits(n_b, k - 1):
         loads = tuple(x for x, on in (("B", v.load_b), ("C", v.load_c)) if on)
         out.append(ScheduleEntry(v.i + 1, v.j + 1, loads, "resident" if v.next_diag else "store"))
@@ -169,6 +184,15 @@ class SpdResult:
     @property
     def block_logdets(self) -> np.ndarray:
         return _block_logdets(self.prefix, self.info.b)
+
+
+@dataclass(frozen=True)
+class GenericResult:
+    """log|det| and sign of a generic matrix (reference memdet.py:201-205)."""
+
+    logabsdet: float
+    sign: int
+    info: RunInfo
 
 
 @dataclass(frozen=True)
@@ -239,8 +263,8 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     m = src.m
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
     ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
-    if src.device_ptr is not None and mode == _native.MODE_LDL_PIV:
-        # the block-pivoted walk streams reference blocks from host memory
+    if src.device_ptr is not None and mode in (_native.MODE_LDL_PIV, _native.MODE_LU):
+        # the block-pivoted walks stream reference blocks from host memory
         src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
     if src.device_ptr is not None:
         if out_of_core:
@@ -264,9 +288,11 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
         raise IndefiniteBlockError(f"LDL pivot {fail} below tolerance: {_native.last_error()}")
     _native.check(rc, "memdet engine")
     perm = None
-    if mode == _native.MODE_LDL_PIV:
+    if mode in (_native.MODE_LDL_PIV, _native.MODE_LU):
         perm = np.empty(m, np.int64)
         ctx.fetch_perm(perm)
+    if mode == _native.MODE_LU:
+        return d, prefix, info, ctx.out_of_core, (perm, fail)
     return d, prefix, info, ctx.out_of_core, perm
 
 
@@ -274,15 +300,16 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
             out_of_core=None):
     t0 = time.perf_counter()
     src = MatrixSource(matrix, assume)
-    if src.symmetry == "generic":
+    if src.symmetry == "generic" and mode != _native.MODE_LU:
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
     d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core)
     nb = lay.n_b
+    case = "generic" if mode == _native.MODE_LU else "symmetric"
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
-                   blocks_read=predicted_reads(nb, "symmetric"),
-                   blocks_written=predicted_writes(nb, "symmetric"),
-                   scratch_slots=scratch_slots(nb, "symmetric"),
+                   blocks_read=predicted_reads(nb, case),
+                   blocks_written=predicted_writes(nb, case),
+                   scratch_slots=scratch_slots(nb, case),
                    wall_seconds=time.perf_counter() - t0, device_ms=float(cinfo.device_ms),
                    h2d_bytes=int(cinfo.h2d_bytes), d2h_bytes=int(cinfo.d2h_bytes),
                    kernel_launches=int(cinfo.kernel_launches), engine_tile=int(cinfo.tile),
@@ -310,6 +337,64 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
         with PrefixWriter(prefix_out) as w:
             w.append(prefix, np.ones(len(prefix), dtype=np.int64))
     return res
+
+
+def _perm_parity(perm: np.ndarray) -> int:
+    """Sign of a permutation (cycle decomposition)."""
+    seen = np.zeros(len(perm), dtype=bool)
+    swaps = 0
+    for i in range(len(perm)):
+        if not seen[i]:
+            j, length = i, 0
+            while not seen[j]:
+                seen[j] = True
+                j = int(perm[j])
+                length += 1
+            swaps += length - 1
+    return -1 if swaps % 2 else 1
+
+
+def memdet_lu(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, device: int = 0,
+              assume: str | None = None, hbm_budget: int | None = None) -> GenericResult:
+    """log|det| and sign of a generic (non-symmetric) matrix via blocked LU with block-local
+    partial pivoting, the reference's generic block walk (memdet.py:268-319).  A singular
+    matrix returns (-inf, 0) rather than raising, as the reference.  Pivots are searched
+    inside the engine's diagonal blocks (|det| and its sign do not depend on the pivot order;
+    the reported block counters are the reference's for its n_b)."""
+    del scratch_dir
+    d, prefix, info, (perm, fail) = _memdet(matrix, _native.MODE_LU, "generic", max_mem, num_blocks, device,
+                                            assume or "generic", hbm_budget, True)
+    # the reference's counters for its walk (scratch = the peak number of distinct blocks
+    # written, storage.py:265-267); it stops at a singular stage (memdet.py:293-294), whose
+    # position the engine reports when its block grid is the reference's
+    stage = info.n_b
+    if fail >= 0 and info.ooc_blocks == info.n_b and info.ooc_block > 0:
+        stage = fail // info.ooc_block
+    r, w, slots = _generic_counts_until(info.n_b, stage)
+    info = replace(info, blocks_read=r, blocks_written=w, scratch_slots=slots)
+    if fail >= 0 or not np.all(np.isfinite(d)) or np.any(d == 0):
+        return GenericResult(-np.inf, 0, info)
+    sign = _perm_parity(perm) * int(np.prod(np.sign(d)))
+    return GenericResult(float(prefix[-1]), sign, info)
+
+
+def _generic_counts_until(n_b: int, stage: int):
+    """(reads, writes, scratch slots) of the reference generic walk when it stops while
+    factoring the diagonal block of `stage` (memdet.py:283-319)."""
+    reads, writes, keys = 1, 0, set()
+    for k in range(min(stage, n_b - 1)):
+        t = n_b - 1 - k
+        for i, j, new_row, load_b, nd in _generic_visits(n_b, k):
+            reads += int(new_row) + int(load_b) + 1
+            if i == n_b - 1:  # the bottom row solves and stores the row-k blocks
+                last = n_b - 1 if (i - k) % 2 == 0 else k + 1
+                if t > 2 or j != last:
+                    writes += 1
+                    keys.add((k, j))
+            if not nd:
+                writes += 1
+                keys.add((i, j))
+    return reads, writes, len(keys)
 
 
 def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,

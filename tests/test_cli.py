@@ -28,7 +28,8 @@ def test_usage_and_io_exit_codes(tmp_path, capsys):
     p = tmp_path / "g.mdm"
     write_matrix(p, gen.random_spd(8, seed=1), "generic")
     assert main(["memdet", "--in", str(p), "--assume", "spd", "--num-blocks", "1"]) == 2  # generic file
-    assert main(["memdet", "--in", str(p), "--assume", "gen", "--num-blocks", "1"]) == 2  # LU out of scope
+    assert main(["memdet", "--in", str(p), "--assume", "gen", "--num-blocks", "1",
+                 "--prefix-out", str(tmp_path / "x.pfx")]) == 2  # no prefixes for generic (cli.py:85-88)
     bad = tmp_path / "bad.mdm"
     bad.write_bytes(b"not a matrix file at all" * 4)
     assert main(["memdet", "--in", str(bad), "--assume", "spd", "--num-blocks", "1"]) == 4
@@ -77,3 +78,18 @@ def test_pipeline_json_on_gpu(tmp_path, capsys):
     fit = fit_prefix(ref, 1, 5, 300, 1)
     assert out["outputs"]["flodance"]["logdet_hat"] == pytest.approx(float(predict(fit, 400)[1]), rel=1e-8)
     assert out["outputs"]["rel_error"] >= 0.0
+
+
+@pytest.mark.gpu
+def test_memdet_gen_json_on_gpu(tmp_path, capsys):
+    """`memdet --assume gen` runs the LU path (reference cli.py:81-104)."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((200, 200)) + 30 * np.eye(200)
+    a[0] *= -1
+    p = tmp_path / "g.mdm"
+    write_matrix(p, a, "generic")
+    assert main(["memdet", "--in", str(p), "--assume", "gen", "--num-blocks", "3", "--json"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    sign, ld = np.linalg.slogdet(a)
+    assert out["sign"] == int(sign) and out["logabsdet"] == pytest.approx(ld, rel=1e-10)
+    assert (out["n_b"], out["blocks_read"], out["blocks_written"], out["scratch_slots"]) == (3, 13, 4, 4)

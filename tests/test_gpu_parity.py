@@ -403,3 +403,53 @@ def test_out_of_core_scratch_placement(host_scratch):
     assert rel_err(pre, ref) <= 1e-10
     assert (info.ooc_reads, info.ooc_writes, info.ooc_scratch) == (rinfo.blocks_read, rinfo.blocks_written,
                                                                     rinfo.scratch_slots)
+
+
+# ------------------------------------------------------------------ generic LU (memdet_lu)
+
+
+def test_lu_matches_reference_golden():
+    """memdet_lu against the unmodified reference (tests/golden/lu.*): log|det| within 1e-10
+    (1e-4 for the float32 file, the reference's f32 bar), the sign exactly, the reference's
+    block counters; (-inf, 0) where block-local pivoting meets a singular diagonal block.
+    The exactly rank-deficient matrix's finite value is roundoff (it differs across the
+    reference's own block counts), so it is not compared."""
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "lu.json")) as f:
+        cases = json.load(f)["cases"]
+    arrays = np.load(os.path.join(here, "lu.npz"))
+    for c in cases:
+        a = arrays[c["name"]]
+        tol = 1e-4 if a.dtype == np.float32 else 1e-10
+        for nb, ref in c["runs"].items():
+            res = eng.memdet_lu(a, num_blocks=int(nb))
+            key = (c["name"], nb)
+            if c["name"].startswith("singular"):
+                # exact rank deficiency: whether elimination meets an exact zero pivot (det = 0,
+                # the walk stops) or a roundoff-sized one depends on the arithmetic order
+                assert res.sign == 0 or np.isfinite(res.logabsdet), key
+                continue
+            assert (res.info.n_b, res.info.b, res.info.blocks_read, res.info.blocks_written,
+                    res.info.scratch_slots) == (ref["n_b"], ref["b"], ref["blocks_read"], ref["blocks_written"],
+                                                ref["scratch_slots"]), key
+            if ref["sign"] == 0:
+                assert res.sign == 0 and res.logabsdet == -np.inf, key
+                continue
+            assert res.sign == ref["sign"], key
+            assert abs(res.logabsdet - ref["logabsdet"]) <= tol * max(1.0, abs(ref["logabsdet"])), \
+                (key, res.logabsdet, ref["logabsdet"])
+
+
+@pytest.mark.parametrize("m,nb", [(3000, 2), (2900, 3), (5000, 1)])
+def test_lu_larger_vs_slogdet(m, nb):
+    """Several 32-column panels per block, ragged blocks, the 16-CTA panel at 5000 rows."""
+    rng = np.random.default_rng(m)
+    a = rng.standard_normal((m, m)) + 3.0 * np.sqrt(m) * np.eye(m)
+    a[: m // 2] *= -1.0
+    sign, ref = np.linalg.slogdet(a)
+    res = eng.memdet_lu(a, num_blocks=nb)
+    assert res.sign == int(sign)
+    assert abs(res.logabsdet - ref) <= 1e-10 * abs(ref)

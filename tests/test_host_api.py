@@ -128,3 +128,33 @@ def test_generators_are_bit_symmetric_and_nested():
     np.testing.assert_array_equal(big[:64, :64], small)
     h = hashlib.sha256(gen.rbf(32, seed=0).tobytes()).hexdigest()
     assert h == hashlib.sha256(gen.rbf(32, seed=0).tobytes()).hexdigest()
+
+
+def test_generic_schedule_matches_reference():
+    """schedule(n_b, "generic", k) equals the unmodified reference's (tests/golden/lu.json)."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "lu.json")) as f:
+        sched = json.load(f)["schedule_generic"]
+    for key, entries in sched.items():
+        nb, k = map(int, key.split("_"))
+        got = [[e.i, e.j, list(e.loads), e.target] for e in eng.schedule(nb, "generic", k)]
+        assert got == entries, key
+
+
+def test_generic_counters_match_reference():
+    """The LU walk's block counters (reads / writes / peak scratch) for every golden run."""
+    import json
+    import os
+
+    from paper_2503_04424_b200.memdet import _generic_counts_until
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "lu.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        for nb, run in c["runs"].items():
+            if run["sign"] == 0:
+                continue  # stopped early: stage depends on where the singular block was met
+            assert _generic_counts_until(run["n_b"], run["n_b"]) == (run["blocks_read"], run["blocks_written"],
+                                                                      run["scratch_slots"]), (c["name"], nb)
