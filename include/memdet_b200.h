@@ -9,12 +9,14 @@
  *   b2d_memdet_sym          <- memdet_cholesky   memdet.py:415-433  (mode B2D_MODE_CHOLESKY)
  *                              memdet_ldl        memdet.py:392-412  (mode B2D_MODE_LDL_*)
  *                              driver body       memdet.py:322-389  (_memdet_symmetric)
+ *                              memdet_lu         memdet.py:268-319  (mode B2D_MODE_LU, the
+ *                                                generic walk; reads every block)
  *   b2d_ctx_*               <- the same driver, split so inputs can stay resident in HBM
  *   return codes            <- oocdet.errors                 errors.py:8-51
  *
  * Matrices are row-major (the MEMDET01 data region, storage.py:3-16) with a leading dimension
- * in elements.  Only the row-major upper tile triangle is read (the (i <= j) tiles the
- * reference reads); inputs are borrowed read-only and never modified.
+ * in elements.  The symmetric modes read only the row-major upper tile triangle (the (i <= j)
+ * tiles the reference reads); inputs are borrowed read-only and never modified.
  * Every call blocks until the device work it issued has finished, except
  * b2d_ctx_factor_device_async, which only enqueues on the caller's stream.
  */
