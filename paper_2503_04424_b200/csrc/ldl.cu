@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
     dg[li] = i < n ? g.diag[i] : 0.0;
   }
   // (row, col) up to date with steps [tag, k): cr = C row of `row`, wc = W row of `col`
-  auto upd = [&](int64_t row, int64_t col_, const double* cr, const double* wc, int k) {
-    double v = __ldcg(A + col_ * ld + row);
-    for (int q = __ldcg(tag + col_ * ld + row); q < k; ++q) v = __dsub_rn(v, __dmul_rn(cr[q], wc[q]));
+  // raw entry v with pending steps [tg, k) applied: cr = C row of its row, wc = W row of its column
+  auto chain = [&](double v, int tg, const double* cr, const double* wc, int k) {
+    for (int q = tg; q < k; ++q) v = __dsub_rn(v, __dmul_rn(cr[q], wc[q]));
     return v;
   };
   for (int k = 0; k < nbk; ++k) {
@@ -289,19 +289,30 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
       if (i <= r || i >= n) continue;
       const double* Ci = Cs + (size_t)li * LC_LD;
       const double* Wi = Ws + (size_t)li * LC_LD;
+      // every raw entry and tag this row needs is loaded before any chain runs (one L2 round)
       double v;
       if (t == r) {
-        v = upd(i, r, Ci, bWr, k);
+        const double a0 = __ldcg(A + r * ld + i);
+        const int g0 = __ldcg(tag + r * ld + i);
+        v = chain(a0, g0, Ci, bWr, k);
       } else if (i < t) {
-        v = upd(t, i, bCt, Wi, k);            // (t, i) -> (i, r)
-        A[i * ld + t] = upd(i, r, Ci, bWr, k);  // (i, r) -> (t, i): brought up to date, tagged
+        const double a0 = __ldcg(A + i * ld + t), a1 = __ldcg(A + r * ld + i);
+        const int g0 = __ldcg(tag + i * ld + t), g1 = __ldcg(tag + r * ld + i);
+        v = chain(a0, g0, bCt, Wi, k);        // (t, i) -> (i, r)
+        A[i * ld + t] = chain(a1, g1, Ci, bWr, k);  // (i, r) -> (t, i): brought up to date, tagged
         tag[i * ld + t] = (uint8_t)k;
       } else if (i == t) {
-        v = upd(t, r, bCt, bWr, k);           // (t, r) stays
+        const double a0 = __ldcg(A + r * ld + t), ad = __ldcg(A + r * ld + r);
+        const int g0 = __ldcg(tag + r * ld + t), gd = __ldcg(tag + r * ld + r);
+        v = chain(a0, g0, bCt, bWr, k);       // (t, r) stays
+        A[t * ld + t] = ad;                   // (r, r) -> (t, t) with its pending terms
+        tag[t * ld + t] = (uint8_t)gd;
       } else {
-        v = upd(i, t, Ci, bWt, k);            // (i, t) -> (i, r)
-        A[t * ld + i] = __ldcg(A + r * ld + i);  // (i, r) -> (i, t) with its tag
-        tag[t * ld + i] = __ldcg(tag + r * ld + i);
+        const double a0 = __ldcg(A + t * ld + i), a1 = __ldcg(A + r * ld + i);
+        const int g0 = __ldcg(tag + t * ld + i), g1 = __ldcg(tag + r * ld + i);
+        v = chain(a0, g0, Ci, bWt, k);        // (i, t) -> (i, r)
+        A[t * ld + i] = a1;                   // (i, r) -> (i, t) with its tag
+        tag[t * ld + i] = (uint8_t)g1;
       }
       col[li] = v;
     }
@@ -325,11 +336,7 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
           Cs[(size_t)lt * LC_LD + q] = bCr[q];
           Ws[(size_t)lt * LC_LD + q] = bWr[q];
         }
-        if (tid == 0) {
-          dg[lt] = bd[0];
-          A[t * ld + t] = __ldcg(A + r * ld + r);  // (r, r) -> (t, t) with its pending terms
-          tag[t * ld + t] = __ldcg(tag + r * ld + r);
-        }
+        if (tid == 0) dg[lt] = bd[0];  // (the raw (r, r) -> (t, t) move is in the row loop above)
       }
     }
     const double p = t == r ? bd[0] : bd[1];
