@@ -80,6 +80,9 @@ typedef struct b2d_options {
   int32_t force_out_of_core; /* 1: stream blocks through HBM even if the matrix fits          */
   int32_t host_scratch;    /* 1: keep the out-of-core scratchpad in pinned host memory even when
                               it fits in HBM next to the block slots (default: HBM if it fits) */
+  int32_t emulation;       /* trailing Schur updates of the in-core driver: 0 FP64 DMMA tensor
+                              cores (default); 1 FP64 emulated on the int8 tcgen05 tensor cores
+                              (Ozaki scheme, 8 slices, error ~13 u relative to sum |a b|)      */
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;

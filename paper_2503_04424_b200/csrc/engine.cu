@@ -26,6 +26,7 @@
 #include "kernels.cu"
 #include "ldl.cu"
 #include "lu.cu"
+#include "ozaki.cu"
 
 namespace b2d {
 
@@ -133,7 +134,11 @@ struct Ctx {
   // right-looking updates at outer step act[b] (-1: from the start) after one catch-up update
   std::vector<int> act;
   bool trace = false;  // B2D_TRACE: print a per-step event timeline on fetch
-  int profiling = 0;  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
+  int profiling = 0;
+  // Ozaki (int8 tcgen05) trailing updates: panel slices and row exponents
+  bool oz = false;
+  int8_t *oz_sa = nullptr, *oz_sb = nullptr;
+  int* oz_expo = nullptr;  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
   int64_t launches = 0;
@@ -161,6 +166,7 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(oz_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)lu_panel_smem(LC_RMAX)));
@@ -192,6 +198,9 @@ static void destroy(Ctx* c) {
   for (auto* p : c->strip) cudaFree(p);
   cudaFree(c->gram_neg);
   cudaFree(c->gram_pos);
+  cudaFree(c->oz_sa);
+  cudaFree(c->oz_sb);
+  cudaFree(c->oz_expo);
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
   for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
                   &c->prof_ev})
@@ -379,10 +388,21 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       return set_err(B2D_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", (size_t)(bytes), cudaGetErrorString(e_)); \
     }                                                            \
   } while (0)
-  if (!force && incore_need <= budget) {
+  // Schur-update arithmetic: FP64 DMMA (default) or the Ozaki int8 emulation (opt->emulation = 1,
+  // or B2D_SCHUR=ozaki / dmma to override)
+  bool oz = opt && opt->emulation == 1;
+  if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
+  const size_t oz_need = oz ? 2 * (size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4 : 0;
+  if (!force && incore_need + oz_need <= budget) {
     c->nt = nt_full;
     ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
     ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
+    if (oz) {  // slices of one outer panel (rows <= n_pad, K <= 16 tiles), A and B layouts
+      c->oz = true;
+      ALLOC(c->oz_sa, (size_t)OZ_S * npad_full * (16 * T));
+      ALLOC(c->oz_sb, (size_t)OZ_S * npad_full * (16 * T));
+      ALLOC(c->oz_expo, (size_t)npad_full * 4);
+    }
   } else {
     Ooc& o = c->o;
     c->ooc = true;
@@ -516,6 +536,35 @@ static void launch_update_set(Ctx* c, cudaStream_t s, const FactorTarget& ft, co
   int64_t ndiag = 0;
   for (int j = out.j0; j < out.j1; ++j) ndiag += j >= out.lo(j) && j < out.i1;
   launch_gemm(c, s, MODE_UPDATE, t, prof, (double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
+}
+
+// The same update emulated on the int8 tensor cores (ozaki.cu): slices of panel rows
+// [min row of `out`, nt) x K tile-columns [p0, p1), then one CTA per output half-tile.
+static void launch_update_oz(Ctx* c, cudaStream_t s, const FactorTarget& ft, const TileSet& out, int p0, int p1,
+                             bool prof) {
+  const int64_t ntile = out.count();
+  if (ntile <= 0 || p1 <= p0) return;
+  const int r0 = out.lo(out.j0);
+  OzPanel P{ft.map, r0, ft.nt - r0, p0, p1 - p0, c->oz_sa, c->oz_sb, c->oz_expo};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof && c->profiling) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  oz_expo_kernel<<<P.rt, 256, 0, s>>>(P);
+  oz_slice_kernel<<<dim3(P.rt, P.kt), 256, 0, s>>>(P);
+  oz_update_kernel<<<(unsigned)(2 * ntile), OZ_THREADS, OZ_SMEM, s>>>(P, ft.map, out);
+  c->launches += 3;
+  if (e0) {
+    const double K = (double)(p1 - p0) * T;
+    int64_t ndiag = 0;
+    for (int j = out.j0; j < out.j1; ++j) ndiag += j >= out.lo(j) && j < out.i1;
+    cudaEventRecord(e1, s);
+    c->prof_ev.push_back(e0);
+    c->prof_ev.push_back(e1);
+    c->prof_flops.push_back((double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
+  }
 }
 
 // Schur update of the target's lower tiles in tile-columns [j0, j1) with K tile-columns [p0, p1)
@@ -658,7 +707,10 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
     if (ne < nt) launch_update_set(c, c->s_mid, ft, TileSet{ne, nt, ke, ne, 0, 0}, k0, ke, false);
     // rest(k0): active columns right of the next panel, overlapping the next panel
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
-    launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
+    if (c->oz && ft.map.packed_nt > 0 && (ke - k0) <= 16)
+      launch_update_oz(c, c->s_side, ft, TileSet{0, nt, ne, std::max(ne, end_active), 1, 0}, k0, ke, true);
+    else
+      launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
   }
   // join the side streams
