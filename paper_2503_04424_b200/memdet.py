@@ -234,10 +234,10 @@ _ctx_lock = threading.Lock()
 
 
 def _context(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
-             out_of_core=None) -> _native.Context:
+             out_of_core=None, emulation=False) -> _native.Context:
     kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
-              max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core))
-    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"])
+              max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation))
+    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"])
     with _ctx_lock:
         ctx = _ctx_cache.get(base)
         # an in-core plan ignores the reference tiling; an out-of-core one is built from it
@@ -258,7 +258,7 @@ def release_engine_cache():
 
 
 def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max_mem, hbm_budget,
-                out_of_core):
+                out_of_core, emulation=False):
     dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
     m = src.m
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
@@ -269,13 +269,13 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     if src.device_ptr is not None:
         if out_of_core:
             raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
-        ctx = _context(m, mode, src.device_index)
+        ctx = _context(m, mode, src.device_index, emulation=emulation)
         import torch
 
         stream = torch.cuda.current_stream(src.device_index).cuda_stream
         ctx.factor_device_async(src.device_ptr, src.lda, dcode, stream)
     else:
-        ctx = _context(m, mode, device, **ooc_kw)
+        ctx = _context(m, mode, device, emulation=emulation, **ooc_kw)
         a, lda = src.host_rowmajor()
         ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
     d = np.empty(m, np.float64)
@@ -297,13 +297,16 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
 
 
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
-            out_of_core=None):
+            out_of_core=None, schur="dmma"):
+    if schur not in ("dmma", "ozaki"):
+        raise ValueError(f"schur must be 'dmma' or 'ozaki', got {schur!r}")
     t0 = time.perf_counter()
     src = MatrixSource(matrix, assume)
     if src.symmetry == "generic" and mode != _native.MODE_LU:
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
-    d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core)
+    d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core,
+                                              schur == "ozaki")
     nb = lay.n_b
     case = "generic" if mode == _native.MODE_LU else "symmetric"
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
@@ -321,17 +324,20 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
 
 def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
                     device: int = 0, assume: str | None = None, hbm_budget: int | None = None,
-                    out_of_core: bool | None = None) -> SpdResult:
+                    out_of_core: bool | None = None, schur: str = "dmma") -> SpdResult:
     """Prefix log-determinants of an SPD matrix (blocked Cholesky, no pivoting).
 
     prefix[q-1] = logdet of the leading q x q principal submatrix, summed from 2 log L_ii;
     NotSpdError on the first non-positive leading minor.  A matrix whose packed lower triangle
     exceeds `hbm_budget` (default: free HBM) — or any host matrix with out_of_core=True — runs
     the reference's out-of-core tile walk, blocks streamed between host memory and HBM (the
-    scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity)."""
+    scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity).
+    schur="ozaki" runs the in-core trailing Schur updates as FP64 emulated on the int8 tcgen05
+    tensor cores (8-slice Ozaki scheme, error ~13 u relative to sum |a b|); the
+    default "dmma" uses the FP64 tensor cores."""
     del scratch_dir
     d, prefix, info, _ = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
-                                 hbm_budget, out_of_core)
+                                 hbm_budget, out_of_core, schur)
     res = SpdResult(prefix=prefix, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:
@@ -399,20 +405,21 @@ def _generic_counts_until(n_b: int, stage: int):
 
 def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
                device: int = 0, assume: str | None = None, pivoting: str = "block",
-               hbm_budget: int | None = None, out_of_core: bool | None = None) -> SymmetricResult:
+               hbm_budget: int | None = None, out_of_core: bool | None = None,
+               schur: str = "dmma") -> SymmetricResult:
     """Prefix log-determinants of a symmetric matrix via blocked LDL^T.
 
     pivoting="block" reproduces the reference's block-local 1x1 diagonal pivoting
     (_ldl.pyx:30-46; perm and prefixes of the permuted minors).  pivoting="none" is the
     unpivoted LDL^T (D = L_ii^2 of the Cholesky factor, perm = identity): its prefixes are
     the natural-order leading minors and coincide with the pivoted ones at every block
-    boundary q = k*b and at q = m."""
+    boundary q = k*b and at q = m.  schur as memdet_cholesky (in-core trailing updates)."""
     del scratch_dir
     if pivoting not in ("block", "none"):
         raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
     mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
     d, prefix, info, perm = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
-                                    out_of_core)
+                                    out_of_core, schur)
     m = len(prefix)
     if mode == _native.MODE_LDL_NOPIV:
         perm = np.arange(m, dtype=np.int64)
