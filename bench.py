@@ -281,9 +281,9 @@ def run_engine(args):
         oz_ach = oz_flops / (oz_ms * 1e-3) / 1e12 if oz_ms > 0 else None
         ozaki = {"value": flops / (oms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": oms,
                  "max_prefix_rel_diff_vs_fp64_dmma": diff, "logdet": float(oprefix[-1]),
-                 "schur": "trailing updates as FP64 emulated on int8 tcgen05 MMAs: 8 signed 7-bit slices per "
+                 "schur": "trailing updates as FP64 emulated on int8 tcgen05 MMAs: 8 balanced signed slices per "
                           "row-scaled operand, the 36 slice products with s+t <= 9 accumulated exactly in int32 "
-                          "TMEM, FP64 reconstruction (error ~13 u relative to sum |a b|)",
+                          "TMEM, FP64 reconstruction (error ~3 u relative to sum |a b|)",
                  "roofline": {"bound": "tensor (int8)", "kernel": "oz_expo + oz_slice + oz_update (rest updates)",
                               "achieved": oz_ach, "peak": oz_peak, "unit": UNIT,
                               "frac": (oz_ach / oz_peak) if oz_ach else None,

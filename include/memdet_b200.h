@@ -82,7 +82,7 @@ typedef struct b2d_options {
                               it fits in HBM next to the block slots (default: HBM if it fits) */
   int32_t emulation;       /* trailing Schur updates of the in-core driver: 0 FP64 DMMA tensor
                               cores (default); 1 FP64 emulated on the int8 tcgen05 tensor cores
-                              (Ozaki scheme, 8 slices, error ~13 u relative to sum |a b|)      */
+                              (Ozaki scheme, 8 slices, error ~3 u relative to sum |a b|)      */
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;

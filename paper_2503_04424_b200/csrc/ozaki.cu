@@ -3,17 +3,18 @@
 // The trailing update C(i, j) -= sum_p L(i, p) L(j, p)^T of one outer panel (K = 128 W) is
 // the dominant kernel.  sm_100a has no FP64 tcgen05 kind; its DMMA (mma.sync m8n8k4 f64) peaks
 // at 37 TFLOP/s, while the int8 tcgen05 path peaks at 4.5 POPS.  The panel rows are split into
-// 8 signed 7-bit slices each, after scaling every row by a power of two 2^-e_r (|L(r, :)| <
-// 2^e_r):
-//     L(r, k) 2^-e_r = sum_{s=1..8} d_s(r, k) 2^-7s + delta,   |d_s| <= 127, |delta| < 2^-56
-// (exact in FP64: each digit is the truncation of an exact power-of-two rescaling), and
+// 8 signed slices each, after scaling every row by a power of two 2^-e_r (|L(r, :)| < 2^(e_r - 1)):
+//     L(r, k) 2^-e_r = sum_{s=1..8} d_s(r, k) 2^-7s + delta,   |d_s| <= 64, |delta| <= 2^-57
+// with balanced digits (each d_s the nearest integer of an exact power-of-two rescaling of the
+// remainder, so every step is exact in FP64; balanced digits make the dropped products 4x
+// smaller than truncated ones and of random sign), and
 //     sum_k L(i, k) L(j, k) = 2^(e_i + e_j) sum_{g=2..9} 2^-7g acc_g + O(2^-53 K 2^(e_i + e_j)),
 //     acc_g = sum_{s + t = g} sum_k d_s(i, k) d_t(j, k)                       (int32, exact)
 // The 36 slice products with s + t <= 9 are tcgen05 MMAs (M = 128, N = 64, K = 32) into 8 TMEM
 // accumulators of 64 columns (all 512 TMEM columns); the epilogue reconstructs in FP64 from the
 // smallest group up and subtracts from C.  Measured error relative to sum_k |L(i,k) L(j,k)|:
-// ~1.4e-15 (13 u) at K = 2048, DGEMM-class.  int32 exactness needs 8 * 127^2 * K < 2^31, i.e.
-// K <= 16384 (OZ_KMAX; longer contractions are split).
+// ~3.3e-16 (3 u) at K = 2048 (tools/ozaki_probe.cu), DGEMM-class.  int32 exactness needs
+// 8 * 64^2 * K < 2^31 (K <= 65536); OZ_KMAX keeps a margin.
 //
 //   oz_expo_kernel    per-row exponents e_r of the panel rows
 //   oz_slice_kernel   the 8 slices in the UMMA K-major SWIZZLE_NONE layout, once as 128-row A
@@ -30,7 +31,7 @@ constexpr int OZ_STAGES = 4;
 constexpr int OZ_A_STAGE = OZ_S * OZ_BM * OZ_KSTEP;  // 32 KB
 constexpr int OZ_B_STAGE = OZ_S * OZ_BN * OZ_KSTEP;  // 16 KB
 constexpr int OZ_THREADS = 192;              // warp 0 producer, warp 1 MMA, warps 2-5 epilogue
-constexpr int OZ_KMAX = 16384;               // int32 exactness bound on K
+constexpr int OZ_KMAX = 32768;               // K bound (int32 exactness holds to 65536)
 constexpr size_t OZ_SMEM = (size_t)OZ_STAGES * (OZ_A_STAGE + OZ_B_STAGE) + (2 * OZ_STAGES + 1) * 8 + 16;
 // kind::i8 instruction descriptor: D s32 (bits 4-5 = 2), A and B signed (bits 7, 10), K-major,
 // N >> 3 at bit 17, M >> 4 at bit 24
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(256) oz_expo_kernel(OzPanel P) {
   __syncthreads();
   if (half == 0) {
     const double mm = fmax(smax[0][r], smax[1][r]);
-    P.expo[it * T + r] = mm > 0.0 ? ilogb(mm) + 1 : 0;
+    P.expo[it * T + r] = mm > 0.0 ? ilogb(mm) + 2 : 0;  // |row| < 2^(e - 1): balanced digits fit
   }
 }
 
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzPanel P) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const double y = x[u] * 128.0;
-        const double q = trunc(y);
+        const double q = rint(y);  // |y| <= 64: a balanced digit, y - q exact
         d[u] = (int8_t)q;
         x[u] = y - q;
       }

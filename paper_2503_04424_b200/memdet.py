@@ -333,7 +333,7 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
     the reference's out-of-core tile walk, blocks streamed between host memory and HBM (the
     scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity).
     schur="ozaki" runs the in-core trailing Schur updates as FP64 emulated on the int8 tcgen05
-    tensor cores (8-slice Ozaki scheme, error ~13 u relative to sum |a b|); the
+    tensor cores (8-slice Ozaki scheme, error ~3 u relative to sum |a b|); the
     default "dmma" uses the FP64 tensor cores."""
     del scratch_dir
     d, prefix, info, _ = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,

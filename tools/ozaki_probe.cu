@@ -1,5 +1,5 @@
 // Probe: FP64 Schur update C -= P_I P_J^T emulated on the int8 tensor cores (tcgen05 kind::i8,
-// Ozaki scheme: 8 signed 7-bit slices per row-scaled operand, the 36 slice products with
+// Ozaki scheme: 8 balanced signed slices per row-scaled operand, the 36 slice products with
 // s + t <= 9 accumulated exactly in int32 TMEM, one accumulator per s + t, reconstructed in
 // FP64).  Standalone: checks the result against a CPU long-double reference and measures the
 // throughput against the DMMA path's 35 TFLOP/s.
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ P
   __syncthreads();
   if (half == 0) {
     const double mm = fmax(smax[0][r], smax[1][r]);
-    se[r] = mm > 0.0 ? ilogb(mm) + 1 : 0;
+    se[r] = mm > 0.0 ? ilogb(mm) + 2 : 0;
     expo[it * T + r] = se[r];
   }
   __syncthreads();
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) slice_kernel(const double* __restrict__ P
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const double y = x[u] * 128.0;
-        const double q = trunc(y);
+        const double q = rint(y);
         d[u] = (int8_t)q;
         x[u] = y - q;
       }
