@@ -137,7 +137,7 @@ struct Ctx {
   int profiling = 0;
   // Ozaki (int8 tcgen05) trailing updates: panel slices and row exponents
   bool oz = false;
-  int8_t *oz_sa = nullptr, *oz_sb = nullptr;
+  int8_t* oz_sa = nullptr;
   int* oz_expo = nullptr;  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
@@ -199,7 +199,6 @@ static void destroy(Ctx* c) {
   cudaFree(c->gram_neg);
   cudaFree(c->gram_pos);
   cudaFree(c->oz_sa);
-  cudaFree(c->oz_sb);
   cudaFree(c->oz_expo);
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
   for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
@@ -392,15 +391,14 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   // or B2D_SCHUR=ozaki / dmma to override)
   bool oz = opt && opt->emulation == 1;
   if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
-  const size_t oz_need = oz ? 2 * (size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4 : 0;
+  const size_t oz_need = oz ? (size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4 : 0;
   if (!force && incore_need + oz_need <= budget) {
     c->nt = nt_full;
     ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
     ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
-    if (oz) {  // slices of one outer panel (rows <= n_pad, K <= 16 tiles), A and B layouts
+    if (oz) {  // slices of one outer panel (rows <= n_pad, K <= 16 tiles)
       c->oz = true;
       ALLOC(c->oz_sa, (size_t)OZ_S * npad_full * (16 * T));
-      ALLOC(c->oz_sb, (size_t)OZ_S * npad_full * (16 * T));
       ALLOC(c->oz_expo, (size_t)npad_full * 4);
     }
   } else {
@@ -545,7 +543,7 @@ static void launch_update_oz(Ctx* c, cudaStream_t s, const FactorTarget& ft, con
   const int64_t ntile = out.count();
   if (ntile <= 0 || p1 <= p0) return;
   const int r0 = out.lo(out.j0);
-  OzPanel P{ft.map, r0, ft.nt - r0, p0, p1 - p0, c->oz_sa, c->oz_sb, c->oz_expo};
+  OzPanel P{ft.map, r0, ft.nt - r0, p0, p1 - p0, c->oz_sa, c->oz_expo};
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof && c->profiling) {
     cudaEventCreate(&e0);
@@ -554,7 +552,7 @@ static void launch_update_oz(Ctx* c, cudaStream_t s, const FactorTarget& ft, con
   }
   oz_expo_kernel<<<P.rt, 256, 0, s>>>(P);
   oz_slice_kernel<<<dim3(P.rt, P.kt), 256, 0, s>>>(P);
-  oz_update_kernel<<<(unsigned)(2 * ntile), OZ_THREADS, OZ_SMEM, s>>>(P, ft.map, out);
+  oz_update_kernel<<<(unsigned)ntile, OZ_THREADS, OZ_SMEM, s>>>(P, ft.map, out);
   c->launches += 3;
   if (e0) {
     const double K = (double)(p1 - p0) * T;
