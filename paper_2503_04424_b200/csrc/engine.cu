@@ -137,8 +137,8 @@ struct Ctx {
   int profiling = 0;
   // Ozaki (int8 tcgen05) trailing updates: panel slices and row exponents
   bool oz = false;
-  int8_t* oz_sa = nullptr;
-  int* oz_expo = nullptr;  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
+  int8_t* oz_sa[2] = {};  // double-buffered by outer step
+  int* oz_expo[2] = {};  // events on the rest updates: 1 in a normal step, 2 in a serialised replay
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
   int64_t launches = 0;
@@ -198,8 +198,10 @@ static void destroy(Ctx* c) {
   for (auto* p : c->strip) cudaFree(p);
   cudaFree(c->gram_neg);
   cudaFree(c->gram_pos);
-  cudaFree(c->oz_sa);
-  cudaFree(c->oz_expo);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->oz_sa[b]);
+    cudaFree(c->oz_expo[b]);
+  }
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
   for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
                   &c->prof_ev})
@@ -391,15 +393,17 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   // or B2D_SCHUR=ozaki / dmma to override)
   bool oz = opt && opt->emulation == 1;
   if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
-  const size_t oz_need = oz ? (size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4 : 0;
+  const size_t oz_need = oz ? 2 * ((size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4) : 0;
   if (!force && incore_need + oz_need <= budget) {
     c->nt = nt_full;
     ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
     ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
-    if (oz) {  // slices of one outer panel (rows <= n_pad, K <= 16 tiles)
+    if (oz) {  // slices of an outer panel (rows <= n_pad, K <= 16 tiles), two in flight
       c->oz = true;
-      ALLOC(c->oz_sa, (size_t)OZ_S * npad_full * (16 * T));
-      ALLOC(c->oz_expo, (size_t)npad_full * 4);
+      for (int b = 0; b < 2; ++b) {
+        ALLOC(c->oz_sa[b], (size_t)OZ_S * npad_full * (16 * T));
+        ALLOC(c->oz_expo[b], (size_t)npad_full * 4);
+      }
     }
   } else {
     Ooc& o = c->o;
@@ -536,26 +540,29 @@ static void launch_update_set(Ctx* c, cudaStream_t s, const FactorTarget& ft, co
   launch_gemm(c, s, MODE_UPDATE, t, prof, (double)(ntile - ndiag) * 2.0 * T * T * K + (double)ndiag * T * (T + 1.0) * K);
 }
 
-// The same update emulated on the int8 tensor cores (ozaki.cu): slices of panel rows
-// [min row of `out`, nt) x K tile-columns [p0, p1), then one CTA per output half-tile.
-static void launch_update_oz(Ctx* c, cudaStream_t s, const FactorTarget& ft, const TileSet& out, int p0, int p1,
+// Slices of panel rows [P.r0, P.r0 + P.rt) over K tiles [P.p0, P.p0 + P.kt) (ozaki.cu).
+static void launch_oz_slices(Ctx* c, cudaStream_t s, const OzPanel& P) {
+  oz_expo_kernel<<<P.rt, 256, 0, s>>>(P);
+  oz_slice_kernel<<<dim3(P.rt, P.kt), 256, 0, s>>>(P);
+  c->launches += 2;
+}
+
+// The Schur update of `out` emulated on the int8 tensor cores from the slices P (ozaki.cu):
+// one CTA per output tile.
+static void launch_update_oz(Ctx* c, cudaStream_t s, const FactorTarget& ft, const OzPanel& P, const TileSet& out,
                              bool prof) {
   const int64_t ntile = out.count();
-  if (ntile <= 0 || p1 <= p0) return;
-  const int r0 = out.lo(out.j0);
-  OzPanel P{ft.map, r0, ft.nt - r0, p0, p1 - p0, c->oz_sa, c->oz_expo};
+  if (ntile <= 0) return;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof && c->profiling) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  oz_expo_kernel<<<P.rt, 256, 0, s>>>(P);
-  oz_slice_kernel<<<dim3(P.rt, P.kt), 256, 0, s>>>(P);
   oz_update_kernel<<<(unsigned)ntile, OZ_THREADS, OZ_SMEM, s>>>(P, ft.map, out);
-  c->launches += 3;
+  c->launches++;
   if (e0) {
-    const double K = (double)(p1 - p0) * T;
+    const double K = (double)P.kt * T;
     int64_t ndiag = 0;
     for (int j = out.j0; j < out.j1; ++j) ndiag += j >= out.lo(j) && j < out.i1;
     cudaEventRecord(e1, s);
@@ -678,7 +685,15 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
         if (ke < nt) launch_update_set(c, c->s_mid, ft, TileSet{ke, nt, p + 1, ke, 0, 0}, p, p + 1, false);
       }
     }
-    // the whole panel is solved once s_mid gets here (s_mid waited for every in-block solve)
+    // the whole panel is solved once s_mid gets here (s_mid waited for every in-block solve).
+    // Ozaki mode: slice its rows [ke, nt) once for the next-cols remainder and the rest update
+    // (buffer st % 2: the step that used it last, st - 2, finished before this panel started)
+    const bool ozs = c->oz && ft.map.packed_nt > 0 && (ke - k0) <= 16 && ke < nt;
+    OzPanel P{};
+    if (ozs) {
+      P = OzPanel{ft.map, ke, nt - ke, k0, ke - k0, c->oz_sa[st & 1], c->oz_expo[st & 1]};
+      launch_oz_slices(c, c->s_mid, P);
+    }
     cudaEventRecord(c->ev_panel[st], c->s_mid);
     if (ke >= nt) break;
     const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
@@ -702,11 +717,14 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
     cudaStreamWaitEvent(c->s_main, c->ev_panel[st], 0);
     launch_update_set(c, c->s_main, ft, TileSet{ke, ne, ke, ne, 1, 0}, k0, ke, false);
     cudaStreamWaitEvent(c->s_mid, c->ev_catch[st], 0);
-    if (ne < nt) launch_update_set(c, c->s_mid, ft, TileSet{ne, nt, ke, ne, 0, 0}, k0, ke, false);
+    if (ne < nt) {
+      if (ozs) launch_update_oz(c, c->s_mid, ft, P, TileSet{ne, nt, ke, ne, 0, 0}, false);
+      else launch_update_set(c, c->s_mid, ft, TileSet{ne, nt, ke, ne, 0, 0}, k0, ke, false);
+    }
     // rest(k0): active columns right of the next panel, overlapping the next panel
     cudaStreamWaitEvent(c->s_side, c->ev_panel[st], 0);
-    if (c->oz && ft.map.packed_nt > 0 && (ke - k0) <= 16)
-      launch_update_oz(c, c->s_side, ft, TileSet{0, nt, ne, std::max(ne, end_active), 1, 0}, k0, ke, true);
+    if (ozs)
+      launch_update_oz(c, c->s_side, ft, P, TileSet{0, nt, ne, std::max(ne, end_active), 1, 0}, true);
     else
       launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
