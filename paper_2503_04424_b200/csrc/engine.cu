@@ -697,19 +697,25 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
     cudaEventRecord(c->ev_panel[st], c->s_mid);
     if (ke >= nt) break;
     const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
-    // catch-up of the bands that join at this step (panels of steps < st, already factored)
+    // catch-up of the bands that join at this step (panels of steps < st, already factored).
+    // Bands the next-cols update reads (deadline st) go before ev_catch; the others after it,
+    // so the next panel's chain does not wait for bands it does not touch yet.
     int end_active = nt;
     if (wait_bands) {
       end_active = 0;
-      for (int b = 0; b < nbands; ++b) {
-        if (c->act[b] == st) {
+      for (int b = 0; b < nbands; ++b)
+        if (c->act[b] <= st) end_active = std::min(nt, (b + 1) * BAND);
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) cudaEventRecord(c->ev_catch[st], c->s_side);
+        for (int b = 0; b < nbands; ++b) {
+          if (c->act[b] != st || (band_deadline(c, b * BAND) <= st) != (pass == 0)) continue;
           cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
           launch_update(c, c->s_side, ft, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
         }
-        if (c->act[b] <= st) end_active = std::min(nt, (b + 1) * BAND);
       }
+    } else {
+      cudaEventRecord(c->ev_catch[st], c->s_side);
     }
-    cudaEventRecord(c->ev_catch[st], c->s_side);
     // next-cols(k0): the next panel's columns [ke, ne); its diagonal block on s_main (the next
     // potrf chain starts as soon as it is done), the rows below on s_mid.  Both follow rest(st-1)
     // and the catch-ups (ev_catch) and the whole panel solve (ev_panel).
