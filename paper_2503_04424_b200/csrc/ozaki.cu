@@ -26,6 +26,8 @@
 //                     tcgen05.mma issuer, 8 epilogue warps (tcgen05.ld, 4 lane quadrants x 2
 //                     column halves)
 
+#include <type_traits>
+
 namespace b2d {
 
 constexpr int OZ_S = 8;                      // slices per operand
@@ -106,6 +108,9 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzPanel P) {
 
 // C(i, j) -= L(i, .) L(j, .)^T over the tile set `out` (panel row tile = tile index - P.r0),
 // one CTA per output tile (tile_order).
+// Two passes: the products with s + t <= 9.  (A third pass for s + t = 10 would cut the
+// truncation error ~64x but streams every slice again for only 7 MMAs per K step: ~50% slower.)
+constexpr int NPASS = 2;
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_update_kernel(OzPanel P, TileMap C, TileSet out) {
   extern __shared__ __align__(1024) double oz_smem[];
   uint8_t* sm8 = reinterpret_cast<uint8_t*>(oz_smem);
@@ -141,40 +146,45 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_update_kernel(OzPanel P, Til
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  // pass p (compile time): groups g = G0(p) .. G0(p) + 3 from slices 1 .. NS(p)
+  constexpr int G0[2] = {2, 6}, NGR[2] = {4, 4}, NSL[2] = {4, OZ_S};
   if (warp == 0 && lane == 0) {
     // stage = slices [0, ns) of A (rows I) at slot s, of B (rows J) at slot 8 + s
     int it = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      const int ns = pass == 0 ? 4 : OZ_S;
+    auto produce = [&](auto pass_c) {
+      constexpr int ns = NSL[decltype(pass_c)::value];
       for (int ks = 0; ks < nks; ++ks, ++it) {
         const int st = it % OZ_STAGES;
         if (it >= OZ_STAGES) mbar_wait(&empty[st], ((it / OZ_STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[st], 2 * ns * OZ_SLICE);
         uint8_t* base = sm8 + st * OZ_STAGE;
         const int kk = ks + rot < nks ? ks + rot : ks + rot - nks;
+#pragma unroll
         for (int s = 0; s < ns; ++s) {
           bulk_g2s(base + s * OZ_SLICE, P.sa + (((size_t)s * P.rt + ia) * nks + kk) * OZ_SLICE, OZ_SLICE, &full[st]);
           bulk_g2s(base + (OZ_S + s) * OZ_SLICE, P.sa + (((size_t)s * P.rt + ja) * nks + kk) * OZ_SLICE, OZ_SLICE,
                    &full[st]);
         }
       }
-    }
+    };
+    produce(std::integral_constant<int, 0>{});
+    produce(std::integral_constant<int, 1>{});
   } else if (warp == 1 && lane == 0) {
     int it = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {  // the accumulators are reused: pass 0's must have been read
-        mbar_wait(drained, 0);
+    auto mma = [&](auto pass_c) {
+      constexpr int pass = decltype(pass_c)::value;
+      if (pass > 0) {  // the accumulators are reused: the previous pass's must have been read
+        mbar_wait(drained, (pass - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
       }
-      const int g0 = pass == 0 ? 2 : 6;
       for (int ks = 0; ks < nks; ++ks, ++it) {
         const int st = it % OZ_STAGES;
         mbar_wait(&full[st], (it / OZ_STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t base = smem_u32(sm8 + st * OZ_STAGE);
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          const int g = g0 + gg;
+        for (int gg = 0; gg < NGR[pass]; ++gg) {
+          const int g = G0[pass] + gg;
           const int s_first = g - OZ_S > 1 ? g - OZ_S : 1;
 #pragma unroll
           for (int s = 1; s <= OZ_S; ++s) {
@@ -194,24 +204,27 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_update_kernel(OzPanel P, Til
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                    ::"r"(smem_u32(&done[pass])) : "memory");
-    }
+    };
+    mma(std::integral_constant<int, 0>{});
+    mma(std::integral_constant<int, 1>{});
   } else if (warp >= 2) {
     const int q = warp & 3, hh = (warp - 2) >> 2;  // TMEM lane quadrant, column half
     const int r = q * 32 + lane;                   // row of the output tile
     const int ei = P.expo[ia * T + r];
     const int* ej = P.expo + ja * T + 64 * hh;
     double* ct = C.tile(I, J);
-    for (int pass = 0; pass < 2; ++pass) {
+    auto drain = [&](auto pass_c) {
+      constexpr int pass = decltype(pass_c)::value;
       mbar_wait(&done[pass], 0);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int g0 = pass == 0 ? 2 : 6;
       double part[2][32];
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) part[ch][j] = 0.0;
-        for (int gg = 3; gg >= 0; --gg) {  // smallest contributions first
-          const double w = ldexp(1.0, -7 * (g0 + gg));
+#pragma unroll 1
+        for (int gg = NGR[pass] - 1; gg >= 0; --gg) {  // smallest contributions first
+          const double w = ldexp(1.0, -7 * (G0[pass] + gg));
           uint32_t v[32];
           const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(gg * OZ_BN + 64 * hh + 32 * ch);
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_update_kernel(OzPanel P, Til
           for (int j = 0; j < 32; ++j) part[ch][j] = fma((double)(int32_t)v[j], w, part[ch][j]);
         }
       }
-      if (pass == 0) {  // TMEM read: pass 1 may overwrite the accumulators while C is updated
+      if (pass + 1 < NPASS) {  // TMEM read: the next pass may overwrite it while C is updated
         asm volatile("tcgen05.fence::before_thread_sync;");
         mbar_arrive(drained);
       }
@@ -239,7 +252,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_update_kernel(OzPanel P, Til
           // explicit global accesses (a TileMap pointer is generic to the compiler)
           __stcg(ct + o, __ldg(ct + o) - ldexp(part[ch][j], ei + __ldg(ej + c)));
         }
-    }
+    };
+    drain(std::integral_constant<int, 0>{});
+    drain(std::integral_constant<int, 1>{});
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
