@@ -1126,7 +1126,8 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
     } else {
       ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
     }
-    ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, ((n - r0) * nbk + 255) / 256)), 256, 0, s>>>(g, r0, nbk);
+    const int64_t st_ctas = std::max<int64_t>(((n - r0) * nbk + 255) / 256, (r0 + 7) / 8);
+    ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, st_ctas)), 256, 0, s>>>(g, r0, nbk);
     const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT;
     if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256, 0, s>>>(g, r0, nbk);
     c->launches += mt > 0 ? 3 : 2;

@@ -169,12 +169,6 @@ __global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs
       }
       g.col[i] = v;
     }
-    if (t != r)
-      for (int64_t j = tid; j < r0; j += LDL_PANEL_THREADS) {  // rows r, t of the finished L columns
-        const double x = A[j * ld + r];
-        A[j * ld + r] = A[j * ld + t];
-        A[j * ld + t] = x;
-      }
     __syncthreads();
     if (t != r) {
       for (int q = tid; q < 2 * k; q += LDL_PANEL_THREADS) {  // rows r, t of this panel's C / W
@@ -218,12 +212,102 @@ __global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs
 // every CTA reads rows r and t (C, W, diag) from their owners -> barrier -> local rows of the
 // new column, interchange, update.  Entry arithmetic is the single-CTA kernel's exactly.
 // Raw entries and tags stay in global memory (read through L2: other CTAs wrote them).
+#ifdef LDL_PROF  // tools/ldl_prof.cu: per-phase cycle counts of the cluster panel (CTA 0, thread 0)
+__device__ long long ldl_prof[16];
+#define LDL_MARK(slot)                                   \
+  if (c == 0 && tid == 0) {                              \
+    const long long now = clock64();                     \
+    prof_acc[slot] += now - prof_t;                      \
+    prof_t = now;                                        \
+  }
+#else
+#define LDL_MARK(slot)
+#endif
 constexpr int LC = 16;                 // CTAs per cluster (non-portable size)
 constexpr int LC_THREADS = 256;
 constexpr int LC_LD = LDL_NB + 1;      // padded smem row (conflict-free column access)
 constexpr int LC_RMAX = 384;           // local rows per CTA (n <= LC * LC_RMAX)
 __host__ __device__ constexpr size_t ldl_cluster_smem(int rows) { return (size_t)rows * (2 * LC_LD + 2) * 8; }
 
+// Cluster-panel helpers.  Candidates: (|d| bits as hi + 1 : lo, index); hi = 0 marks "none"
+// (outside the trailing range, or NaN: a NaN never beats anything, as `better`).
+struct Cand {
+  uint32_t hi, lo, idx, pad;
+};
+__device__ __forceinline__ bool cand_better(const Cand& b, const Cand& a) {
+  return b.hi > a.hi || (b.hi == a.hi && (b.lo > a.lo || (b.lo == a.lo && b.idx < a.idx)));
+}
+__device__ __forceinline__ Cand warp_best(const Cand& a) {
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, a.hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, a.hi == mh ? a.lo : 0u);
+  const uint32_t mi = __reduce_min_sync(0xffffffffu, a.hi == mh && a.lo == ml ? a.idx : 0xffffffffu);
+  return Cand{mh, ml, mi, 0};
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// 8-byte store into a cluster CTA's shared memory completing 8 tx bytes on its mbarrier.
+__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// v with the pending steps [tg, k) applied in order, each as fl(v - fl(c_q w_q)) (the reference's
+// two roundings): the products are independent, so only the subtractions form the chain.
+// Blocks of 8 terms: 8 independent products, then 8 subtractions.
+__device__ __forceinline__ double chain_terms(double v, int tg, int k, const double* cr, const double* wc) {
+  for (int q0 = tg & ~7; q0 < k; q0 += 8) {
+    double p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = __dmul_rn(cr[q0 + u], wc[q0 + u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (q0 + u >= tg && q0 + u < k) v = __dsub_rn(v, p[u]);
+  }
+  return v;
+}
+// Two independent chains over the same steps (interleaved).
+__device__ __forceinline__ void chain_terms2(double& v, int tv, const double* cv, const double* wv, double& x, int tx,
+                                             const double* cx, const double* wx, int k) {
+  for (int q0 = min(tv, tx) & ~7; q0 < k; q0 += 8) {
+    double p[8], s[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      p[u] = __dmul_rn(cv[q0 + u], wv[q0 + u]);
+      s[u] = __dmul_rn(cx[q0 + u], wx[q0 + u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (q0 + u >= tv && q0 + u < k) v = __dsub_rn(v, p[u]);
+      if (q0 + u >= tx && q0 + u < k) x = __dsub_rn(x, s[u]);
+    }
+  }
+}
+
+// The panel on a cluster of LC CTAs (one per SM), row i in CTA i % LC at local row i / LC, the
+// panel's C / W rows and the eager diagonal in shared memory.  One cluster barrier per step:
+//   1. each warp's argmax candidate is stored into every CTA; cluster barrier (it also orders
+//      the previous step's global writes: raw entries moved between CTAs' rows);
+//   2. every warp reduces the candidates -> pivot t; the owners of rows r and t push those rows
+//      (C, W, diagonal) into every CTA with st.async, completing on each CTA's mbarrier;
+//   3. each thread forms the new column entry of its rows (the interchange, as the single-CTA
+//      kernel), scales it and updates its C / W row and diagonal, and takes its candidate for the
+//      next step.  A thread only touches its own rows' diagonal entries, so no CTA barrier.
+// Rows r, t of the finished L columns (j < r0) are interchanged after the panel
+// (ldl_store_l_kernel).  Entry arithmetic is the single-CTA kernel's exactly.
 __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
   cg::cluster_group cl = cg::this_cluster();
@@ -234,133 +318,192 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
   double* Cs = sm;                      // [R][LC_LD]
   double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
   double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal
-  double* col = dg + R;                 // [R] pivot column being formed
-  __shared__ ArgMax cand[2][LC];
-  __shared__ ArgMax sred[LC_THREADS / 32];
-  __shared__ double bCr[LDL_NB], bWr[LDL_NB], bCt[LDL_NB], bWt[LDL_NB], bd[2];
+  constexpr int NW = LC_THREADS / 32;
+  constexpr int ROW = 2 * LDL_NB + 2;   // pushed row: C[0, NB), W[0, NB), diagonal, 1 / diagonal
+  __shared__ Cand cand[2][LC * NW];
+  __shared__ double rows[2][2][ROW];    // [step parity][0: row r, 1: row t]
+  __shared__ uint64_t bar[2];
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   double* __restrict__ A = g.A;
   uint8_t* __restrict__ tag = g.tag;
   const double tol = 64.0 * 2.220446049250313e-16 * __longlong_as_double((long long)*g.amax_bits);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  const uint32_t rows_u32 = smem_u32(&rows[0][0][0]), bar_u32 = smem_u32(&bar[0]);
   for (int li = tid; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
     dg[li] = i < n ? g.diag[i] : 0.0;
   }
-  // (row, col) up to date with steps [tag, k): cr = C row of `row`, wc = W row of `col`
-  // raw entry v with pending steps [tg, k) applied: cr = C row of its row, wc = W row of its column
-  auto chain = [&](double v, int tg, const double* cr, const double* wc, int k) {
-    for (int q = tg; q < k; ++q) v = __dsub_rn(v, __dmul_rn(cr[q], wc[q]));
-    return v;
+  auto cand_of = [&](int64_t i, double v) {
+    Cand x{0u, 0u, 0xffffffffu, 0u};
+    if (!isnan(v)) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v));
+      x = Cand{(uint32_t)(bits >> 32) + 1u, (uint32_t)bits, (uint32_t)i, 0u};
+    }
+    return x;
   };
+  // step 0's candidate (later steps take theirs in the update)
+  Cand my{0u, 0u, 0xffffffffu, 0u};
+  for (int li = tid; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    if (i >= r0 && i < n) {
+      const Cand x = cand_of(i, dg[li]);
+      if (cand_better(x, my)) my = x;
+    }
+  }
+  __syncthreads();  // dg loaded, barriers initialised
+  cl.sync();        // every CTA's barriers initialised before any remote arrive
+#ifdef LDL_PROF
+  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_t = clock64();
+#endif
   for (int k = 0; k < nbk; ++k) {
     const int64_t r = r0 + k;
-    ArgMax a{-1.0, INT64_MAX};
-    for (int li = tid; li < R; li += LC_THREADS) {
+    const int buf = k & 1;
+    LDL_MARK(0);
+    {
+      const Cand w = warp_best(my);
+      if (lane < LC) *cl.map_shared_rank(&cand[buf][c * NW + wib], lane) = w;
+    }
+    if (tid == 0) mbar_arrive_expect_tx(&bar[buf], (2u * (2u * k + 1u) + 1u) * 8u);
+    LDL_MARK(1);
+    cl.sync();  // candidates and the previous step's writes visible cluster-wide
+    LDL_MARK(2);
+    // raw entries (i, r) of this thread's rows and their tags: every case needs them, and r is
+    // known before the pivot (the loads overlap the reduction and the row exchange)
+    constexpr int MR = (LC_RMAX + LC_THREADS - 1) / LC_THREADS;
+    double ar[MR], a2[MR];
+    int gr[MR], g2[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int li = tid + m * LC_THREADS;
       const int64_t i = (int64_t)li * LC + c;
-      if (i >= r && i < n) a = better(a, ArgMax{fabs(dg[li]), i});
+      ar[m] = 0.0;
+      gr[m] = 0;
+      if (li < R && i > r && i < n) {
+        ar[m] = __ldcg(A + r * ld + i);
+        gr[m] = __ldcg(tag + r * ld + i);
+      }
     }
-    a = warp_argmax(a);
-    if (lane == 0) sred[wib] = a;
-    __syncthreads();
-    if (wib == 0) {
-      ArgMax b = lane < LC_THREADS / 32 ? sred[lane] : ArgMax{-1.0, INT64_MAX};
-      b = warp_argmax(b);
-      if (lane < LC) *cl.map_shared_rank(&cand[k & 1][c], lane) = b;  // push to every CTA
+    Cand b = cand[buf][lane];
+#pragma unroll
+    for (int m = 1; m < LC * NW / 32; ++m) {
+      const Cand x = cand[buf][lane + 32 * m];
+      if (cand_better(x, b)) b = x;
     }
-    cl.sync();  // A: candidates (and the previous step's rows) visible cluster-wide
-    ArgMax b{-1.0, INT64_MAX};
-    for (int q = 0; q < LC; ++q) b = better(b, cand[k & 1][q]);
-    const int64_t t = b.i;
+    b = warp_best(b);
+    if (b.hi == 0) {  // no finite diagonal left: the step fails (uniform)
+      if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
+      cl.sync();
+      return;
+    }
+    const int64_t t = b.idx;
     const int orr = (int)(r % LC), ort = (int)(t % LC);
     const int lr = (int)(r / LC), lt = (int)(t / LC);
-    for (int q = tid; q < k; q += LC_THREADS) {
-      bCr[q] = cl.map_shared_rank(Cs, orr)[(size_t)lr * LC_LD + q];
-      bWr[q] = cl.map_shared_rank(Ws, orr)[(size_t)lr * LC_LD + q];
-      bCt[q] = cl.map_shared_rank(Cs, ort)[(size_t)lt * LC_LD + q];
-      bWt[q] = cl.map_shared_rank(Ws, ort)[(size_t)lt * LC_LD + q];
-    }
-    if (tid == 0) {
-      bd[0] = cl.map_shared_rank(dg, orr)[lr];
-      bd[1] = cl.map_shared_rank(dg, ort)[lt];
-    }
-    cl.sync();  // B: rows r, t read everywhere; their owners may overwrite them
-    for (int li = tid; li < R; li += LC_THREADS) {
+    // the pivot-dependent raw entries: (t, i) for i < t, (r, r) for i = t, (i, t) for i > t
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int li = tid + m * LC_THREADS;
       const int64_t i = (int64_t)li * LC + c;
-      if (i <= r || i >= n) continue;
-      const double* Ci = Cs + (size_t)li * LC_LD;
-      const double* Wi = Ws + (size_t)li * LC_LD;
-      // every raw entry and tag this row needs is loaded before any chain runs (one L2 round)
-      double v;
-      if (t == r) {
-        const double a0 = __ldcg(A + r * ld + i);
-        const int g0 = __ldcg(tag + r * ld + i);
-        v = chain(a0, g0, Ci, bWr, k);
-      } else if (i < t) {
-        const double a0 = __ldcg(A + i * ld + t), a1 = __ldcg(A + r * ld + i);
-        const int g0 = __ldcg(tag + i * ld + t), g1 = __ldcg(tag + r * ld + i);
-        v = chain(a0, g0, bCt, Wi, k);        // (t, i) -> (i, r)
-        A[i * ld + t] = chain(a1, g1, Ci, bWr, k);  // (i, r) -> (t, i): brought up to date, tagged
-        tag[i * ld + t] = (uint8_t)k;
-      } else if (i == t) {
-        const double a0 = __ldcg(A + r * ld + t), ad = __ldcg(A + r * ld + r);
-        const int g0 = __ldcg(tag + r * ld + t), gd = __ldcg(tag + r * ld + r);
-        v = chain(a0, g0, bCt, bWr, k);       // (t, r) stays
-        A[t * ld + t] = ad;                   // (r, r) -> (t, t) with its pending terms
-        tag[t * ld + t] = (uint8_t)gd;
-      } else {
-        const double a0 = __ldcg(A + t * ld + i), a1 = __ldcg(A + r * ld + i);
-        const int g0 = __ldcg(tag + t * ld + i), g1 = __ldcg(tag + r * ld + i);
-        v = chain(a0, g0, Ci, bWt, k);        // (i, t) -> (i, r)
-        A[t * ld + i] = a1;                   // (i, r) -> (i, t) with its tag
-        tag[t * ld + i] = (uint8_t)g1;
-      }
-      col[li] = v;
-    }
-    if (t != r)
-      for (int64_t j = (int64_t)c * LC_THREADS + tid; j < r0; j += (int64_t)LC * LC_THREADS) {
-        const double x = __ldcg(A + j * ld + r);
-        A[j * ld + r] = __ldcg(A + j * ld + t);
-        A[j * ld + t] = x;
-      }
-    __syncthreads();
-    if (t != r) {
-      if (c == orr) {
-        for (int q = tid; q < k; q += LC_THREADS) {
-          Cs[(size_t)lr * LC_LD + q] = bCt[q];
-          Ws[(size_t)lr * LC_LD + q] = bWt[q];
-        }
-        if (tid == 0) dg[lr] = bd[1];
-      }
-      if (c == ort) {
-        for (int q = tid; q < k; q += LC_THREADS) {
-          Cs[(size_t)lt * LC_LD + q] = bCr[q];
-          Ws[(size_t)lt * LC_LD + q] = bWr[q];
-        }
-        if (tid == 0) dg[lt] = bd[0];  // (the raw (r, r) -> (t, t) move is in the row loop above)
+      a2[m] = 0.0;
+      g2[m] = 0;
+      if (li < R && i > r && i < n && t != r) {
+        const int64_t o = i < t ? i * ld + t : i == t ? r * ld + r : t * ld + i;
+        a2[m] = __ldcg(A + o);
+        g2[m] = __ldcg(tag + o);
       }
     }
-    const double p = t == r ? bd[0] : bd[1];
+    // owners push rows r (slot 0) and t (slot 1): thread 128 * slot + e pushes element e
+    {
+      const int slot = tid >> 7, e = tid & 127;
+      const int owner = slot ? ort : orr, lrow = slot ? lt : lr;
+      if (slot < 2 && c == owner &&
+          (e < k || (e >= LDL_NB && e < LDL_NB + k) || e == 2 * LDL_NB || (slot == 1 && e == 2 * LDL_NB + 1))) {
+        const double v = e < LDL_NB       ? Cs[(size_t)lrow * LC_LD + e]
+                         : e < 2 * LDL_NB ? Ws[(size_t)lrow * LC_LD + e - LDL_NB]
+                         : e == 2 * LDL_NB ? dg[lrow]
+                                           : 1.0 / dg[lrow];
+        const uint32_t off = rows_u32 + (uint32_t)(((buf * 2 + slot) * ROW + e) * 8);
+        const uint32_t bo = bar_u32 + (uint32_t)(buf * 8);
+#pragma unroll 4
+        for (int d = 0; d < LC; ++d) st_async_f64(dsmem_map(off, d), v, dsmem_map(bo, d));
+      }
+    }
+    LDL_MARK(3);
+    mbar_wait_acq_cluster(&bar[buf], (uint32_t)((k >> 1) & 1));
+    LDL_MARK(4);
+    const double* rr = rows[buf][0];
+    const double* rt = rows[buf][1];
+    const double p = rt[2 * LDL_NB];  // row t's eager diagonal: the pivot
     if (!(fabs(p) >= tol)) {
       if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
+      cl.sync();
       return;  // uniform across the cluster: every thread read the same p
     }
     if (c == 0 && tid == 0) {
       g.d[r] = p;
       g.swaps[r] = t;
     }
-    const double invp = 1.0 / p;
-    __syncthreads();
-    for (int li = tid; li < R; li += LC_THREADS) {
-      const int64_t i = (int64_t)li * LC + c;
-      if (i <= r || i >= n) continue;
-      const double cv = col[li];
-      const double w = __dmul_rn(cv, invp);  // work[i] = a_ir * (1/p)
-      Cs[(size_t)li * LC_LD + k] = cv;
-      Ws[(size_t)li * LC_LD + k] = w;
-      dg[li] = __dsub_rn(dg[li], __dmul_rn(cv, w));
+    const double invp = rt[2 * LDL_NB + 1];
+    // interchange in shared memory: row r's slot takes row t's C / W (row t's slot is rewritten
+    // below with row r's, as its owner's row loop forms the new entry of position t)
+    if (t != r) {
+      if (c == orr && tid < k) {
+        Cs[(size_t)lr * LC_LD + tid] = rt[tid];
+        Ws[(size_t)lr * LC_LD + tid] = rt[LDL_NB + tid];
+      }
+      if (c == ort && tid >= 128 && tid < 128 + k) {
+        Cs[(size_t)lt * LC_LD + tid - 128] = rr[tid - 128];
+        Ws[(size_t)lt * LC_LD + tid - 128] = rr[LDL_NB + tid - 128];
+      }
     }
-    __syncthreads();
+    if (c == orr && tid == (lr % LC_THREADS)) dg[lr] = p;
+    my = Cand{0u, 0u, 0xffffffffu, 0u};
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int li = tid + m * LC_THREADS;
+      const int64_t i = (int64_t)li * LC + c;
+      if (li >= R || i <= r || i >= n) continue;
+      const double* Ci = Cs + (size_t)li * LC_LD;
+      const double* Wi = Ws + (size_t)li * LC_LD;
+      double v, dnew = dg[li];
+      if (t == r) {
+        v = chain_terms(ar[m], gr[m], k, Ci, rr + LDL_NB);
+      } else if (i < t) {
+        // (t, i) -> (i, r); (i, r) -> (t, i): brought up to date, tagged
+        v = a2[m];
+        double x = ar[m];
+        chain_terms2(v, g2[m], rt, Wi, x, gr[m], Ci, rr + LDL_NB, k);
+        A[i * ld + t] = x;
+        tag[i * ld + t] = (uint8_t)k;
+      } else if (i == t) {
+        v = chain_terms(ar[m], gr[m], k, rt, rr + LDL_NB);           // (t, r) stays
+        A[t * ld + t] = a2[m];                                     // (r, r) -> (t, t) with its pending terms
+        tag[t * ld + t] = (uint8_t)g2[m];
+        dnew = rr[2 * LDL_NB];                                     // row r's diagonal moves to position t
+      } else {
+        v = chain_terms(a2[m], g2[m], k, Ci, rt + LDL_NB);           // (i, t) -> (i, r)
+        A[t * ld + i] = ar[m];                                     // (i, r) -> (i, t) with its tag
+        tag[t * ld + i] = (uint8_t)gr[m];
+      }
+      const double w = __dmul_rn(v, invp);  // work[i] = a_ir * (1/p)
+      Cs[(size_t)li * LC_LD + k] = v;
+      Ws[(size_t)li * LC_LD + k] = w;
+      const double dn = __dsub_rn(dnew, __dmul_rn(v, w));
+      dg[li] = dn;
+      const Cand x = cand_of(i, dn);
+      if (cand_better(x, my)) my = x;
+    }
+    LDL_MARK(5);
   }
+  cl.sync();  // every push landed; C / W rows final
+#ifdef LDL_PROF
+  if (c == 0 && tid == 0)
+    for (int q = 0; q < 8; ++q) ldl_prof[q] += prof_acc[q];
+#endif
   // C, W and the diagonal back to global memory for the bulk update and the next panel
   for (int li = tid; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
@@ -373,9 +516,61 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
   }
 }
 
-// Finished columns [r0, r0 + nbk): L = W below the diagonal (_ldl.pyx:59-60).
-__global__ void ldl_store_l_kernel(LdlArgs g, int64_t r0, int nbk) {
+// Finished columns [r0, r0 + nbk): L = W below the diagonal (_ldl.pyx:59-60); and the panel's
+// interchanges applied to rows of the finished columns j < r0 (the reference swaps rows r, t of
+// those columns at every step, _ldl.pyx:38-46): warp 0 of each CTA folds the panel's swaps into
+// one permutation of at most 2 * NB rows, then one warp per column gathers and scatters them.
+__global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;
+  __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (r0 > 0 && tid < 32) {
+    int64_t dcur = r0 + lane;        // row whose value ends at position r0 + lane
+    int64_t xpos = -1, xcur = -1;    // extra position `lane` (beyond the panel) and its row
+    int nx = 0;
+    for (int k = 0; k < nbk; ++k) {
+      const int64_t a = r0 + k, b = g.swaps[a];
+      if (b == a) continue;
+      const bool direct = b < r0 + nbk;
+      int hb;
+      if (direct) {
+        hb = (int)(b - r0);
+      } else {
+        const unsigned m = __ballot_sync(0xffffffffu, xpos == b);
+        if (m) {
+          hb = __ffs(m) - 1;
+        } else {
+          hb = nx++;
+          if (lane == hb) xpos = xcur = b;
+        }
+      }
+      const int64_t va = __shfl_sync(0xffffffffu, dcur, k);
+      const int64_t vb = direct ? __shfl_sync(0xffffffffu, dcur, hb) : __shfl_sync(0xffffffffu, xcur, hb);
+      if (lane == k) dcur = vb;
+      if (lane == hb) {
+        if (direct) dcur = va;
+        else xcur = va;
+      }
+    }
+    const bool dv = lane < nbk && dcur != r0 + lane, xv = lane < nx && xcur != xpos;
+    spos[lane] = dv ? r0 + lane : -1;
+    ssrc[lane] = dcur;
+    spos[32 + lane] = xv ? xpos : -1;
+    ssrc[32 + lane] = xcur;
+  }
+  __syncthreads();
+  if (r0 > 0) {
+    const int64_t p0 = spos[lane], p1 = spos[32 + lane], s0 = ssrc[lane], s1 = ssrc[32 + lane];
+    const int64_t ld = g.ld;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; j < r0; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+      double* colj = g.A + j * ld;
+      const double v0 = p0 >= 0 ? __ldcg(colj + s0) : 0.0;
+      const double v1 = p1 >= 0 ? __ldcg(colj + s1) : 0.0;
+      __syncwarp();
+      if (p0 >= 0) colj[p0] = v0;
+      if (p1 >= 0) colj[p1] = v1;
+    }
+  }
   const int64_t rows = g.n - r0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * nbk; e += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(e / rows);
@@ -391,8 +586,9 @@ __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, in
   if (*g.fail != ~0ull) return;
   __shared__ double sC[LDL_NB][LDL_BT], sW[LDL_NB][LDL_BT];
   const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld;
-  // lower-triangular tile (bi >= bj) of blockIdx.x
-  int64_t b = blockIdx.x, bj = 0;
+  // lower-triangular tile (bi >= bj), the first tile-column (the next panel's columns) last so
+  // that it is L2-resident when the next panel kernel reads it
+  int64_t b = (int64_t)gridDim.x - 1 - blockIdx.x, bj = 0;
   const int64_t nbt = (m + LDL_BT - 1) / LDL_BT;
   while (b >= nbt - bj) { b -= nbt - bj; ++bj; }
   const int64_t bi = bj + b;
