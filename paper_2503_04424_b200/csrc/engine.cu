@@ -62,8 +62,8 @@ static int panel_tiles_default() {
 constexpr int NSTAGE = 8;   // host-ingest staging strips in flight
 constexpr int BAND = 4;     // tile-columns per ingest band
 constexpr int NSLOT = 6;      // out-of-core: HBM block slots (A, B, C, T + two for prefetch)
-constexpr int NSLOT_LDL = 8;  // pivoted LDL: A, B (scaled), B (unscaled), C, T, two spare, permute temp
-constexpr int MAXSLOT = 8;
+constexpr int NSLOT_LDL = 9;  // pivoted LDL: A, B (scaled), B (unscaled), C, T, next A, two spare, permute temp
+constexpr int MAXSLOT = 9;
 
 // The lower tile triangle of an nt x nt tile matrix to factor in place: the whole packed
 // matrix (in-core) or one diagonal block slot (out-of-core).  g0 = global index of its row 0.
@@ -93,6 +93,14 @@ struct Ooc {
   uint8_t* ltag = nullptr;  // blocked pivoted LDL: per-entry tags, panel columns C / W, diagonal, pivot column
   double *lC = nullptr, *lW = nullptr, *ldiag = nullptr, *lcol = nullptr;
   double* inv2 = nullptr;  // LU: inverses of the diagonal tiles of U^T (column-block solves)
+  // pivoted LDL look-ahead: the next stage's diagonal block is factored (on s_main) while the
+  // current stage's solves and Schur updates run on s_work, so the per-stage outputs of the
+  // factor (tile inverses, block permutation, D) are double-buffered by stage parity
+  double* inv_odd = nullptr;
+  int64_t* perm_odd = nullptr;
+  double* dblk_odd = nullptr;
+  cudaStream_t s_work = nullptr;  // block-walk solves / updates: s_main, or s_mid under look-ahead
+  cudaEvent_t ev_fac = nullptr, ev_diag = nullptr, ev_work = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
@@ -106,6 +114,8 @@ struct Ooc {
   int tiles(int k) const { return (int)((size(k) + T - 1) / T); }
   TileMap map(int s) const { return TileMap{slot[s], nbt, 0}; }
   size_t slot_bytes() const { return (size_t)nbt * nbt * TILE_BYTES; }
+  int64_t* perm_of(int k) const { return (k & 1) && perm_odd ? perm_odd : perm_local; }
+  double* dblk_of(int k) const { return (k & 1) && dblk_odd ? dblk_odd : dblk; }
 };
 
 struct Ctx {
@@ -236,6 +246,11 @@ static void destroy(Ctx* c) {
   cudaFree(o.ldiag);
   cudaFree(o.lcol);
   cudaFree(o.inv2);
+  cudaFree(o.inv_odd);
+  cudaFree(o.perm_odd);
+  cudaFree(o.dblk_odd);
+  for (cudaEvent_t e : {o.ev_fac, o.ev_diag, o.ev_work})
+    if (e) cudaEventDestroy(e);
   cudaFree(o.stage);
   for (double* h : o.pool) {
     if (o.dev_scratch) cudaFree(h);
@@ -461,6 +476,11 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       ALLOC(o.ldiag, (size_t)ld * 8);
       ALLOC(o.lcol, (size_t)ld * 8);
       if (mode == B2D_MODE_LU) ALLOC(o.inv2, (size_t)o.nbt * TILE_BYTES);
+      if (mode == B2D_MODE_LDL_PIV) {
+        ALLOC(o.inv_odd, (size_t)o.nbt * TILE_BYTES);
+        ALLOC(o.perm_odd, (size_t)ld * 8);
+        ALLOC(o.dblk_odd, (size_t)ld * 8);
+      }
     }
     // scratchpad: exactly the reference capacity (cost.py:95-101), allocated up front; in HBM
     // when it fits beside the slots (scratch traffic then moves at HBM instead of PCIe speed),
@@ -486,6 +506,9 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&o.s_h2d, cudaStreamNonBlocking, hi);
     cudaStreamCreateWithPriority(&o.s_d2h, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&o.ev_fac, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_diag, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_work, cudaEventDisableTiming);
   }
   ALLOC(c->ell, vec_len * 8);
   ALLOC(c->diag, vec_len * 8);
@@ -1030,7 +1053,7 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
 static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nullptr) {
   Ooc& o = c->o;
   if (!inv) inv = c->inv;
-  cudaStreamWaitEvent(c->s_main, o.ev_loaded[s], 0);
+  cudaStreamWaitEvent(o.s_work, o.ev_loaded[s], 0);
   const int R = o.tiles(x), Q = o.tiles(k), W = c->W_TILES;
   for (int q0 = 0; q0 < Q; q0 += W) {
     const int qe = std::min(q0 + W, Q);
@@ -1040,7 +1063,7 @@ static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nu
       t.binv = inv + (int64_t)q * TILE_ELEMS;
       t.out = TileSet{0, R, q, q + 1, 0, 0};
       t.k = q;
-      launch_gemm(c, c->s_main, MODE_TRSM, t, false, 0.0);
+      launch_gemm(c, o.s_work, MODE_TRSM, t, false, 0.0);
       if (q + 1 < qe) {
         GemmTask u{};
         u.a = o.map(s);
@@ -1049,7 +1072,7 @@ static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nu
         u.out = TileSet{0, R, q + 1, qe, 0, 0};
         u.p0 = q;
         u.p1 = q + 1;
-        launch_gemm(c, c->s_main, MODE_UPDATE, u, false, 0.0);
+        launch_gemm(c, o.s_work, MODE_UPDATE, u, false, 0.0);
       }
     }
     if (qe < Q) {
@@ -1060,17 +1083,17 @@ static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nu
       u.out = TileSet{0, R, qe, Q, 0, 0};
       u.p0 = q0;
       u.p1 = qe;
-      launch_gemm(c, c->s_main, MODE_UPDATE, u, false, 0.0);
+      launch_gemm(c, o.s_work, MODE_UPDATE, u, false, 0.0);
     }
   }
-  cudaEventRecord(o.ev_used[s], c->s_main);
-  cudaEventRecord(o.ev_used[sa], c->s_main);
+  cudaEventRecord(o.ev_used[s], o.s_work);
+  cudaEventRecord(o.ev_used[sa], o.s_work);
 }
 
 // Schur update of slot st (engine block (j, i)) -= L(j,k) L(i,k)^T (dense.py:109-116).
 static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
   Ooc& o = c->o;
-  for (int x : {st, sbj, sci}) cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
+  for (int x : {st, sbj, sci}) cudaStreamWaitEvent(o.s_work, o.ev_loaded[x], 0);
   GemmTask t{};
   t.a = o.map(sbj);
   t.b = o.map(sci);
@@ -1079,28 +1102,30 @@ static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
   t.p0 = 0;
   t.p1 = o.tiles(k);
   const double K = (double)t.p1 * T;
-  launch_gemm(c, c->s_main, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
-  cudaEventRecord(o.ev_used[st], c->s_main);
-  cudaEventRecord(o.ev_used[sbj], c->s_main);
-  cudaEventRecord(o.ev_used[sci], c->s_main);
+  launch_gemm(c, o.s_work, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
+  cudaEventRecord(o.ev_used[st], o.s_work);
+  cudaEventRecord(o.ev_used[sbj], o.s_work);
+  cudaEventRecord(o.ev_used[sci], o.s_work);
 }
 
 // Pivoted LDL^T of the diagonal block in slot sa (stage k): dense copy, tolerance scale, the
 // cooperative 1x1-pivot factorisation, permutation / log|d| bookkeeping, then the unit factor
 // back into the slot and the inverses of its diagonal tiles for the panel solves.
-static int ooc_ldl_factor(Ctx* c, int sa, int k) {
+static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
   Ooc& o = c->o;
   const int nt = o.tiles(k);
   int64_t n = o.size(k);
   const int64_t ld = (int64_t)o.nbt * T, g0 = (int64_t)k * o.b;
-  cudaStream_t s = c->s_main;
+  double* dblk = o.dblk_of(k);
+  int64_t* perm = o.perm_of(k);
+  double* inv = (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
   cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
   unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld, 1);
   cudaMemsetAsync(o.amax, 0, 8, s);
   block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
   // blocked pivoted LDL: panels of LDL_NB steps (one CTA), then the delayed trailing update
-  const LdlArgs g{o.dense, o.ltag, o.lC, o.lW, o.ldiag, o.lcol, o.dblk, o.swaps, c->fail, o.amax, ld, n, g0};
+  const LdlArgs g{o.dense, o.ltag, o.lC, o.lW, o.ldiag, o.lcol, dblk, o.swaps, c->fail, o.amax, ld, n, g0};
   cudaMemsetAsync(o.ltag, 0, (size_t)ld * ld, s);
   ldl_diag_init_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256, 0, s>>>(g);
   c->launches += 1;
@@ -1133,10 +1158,10 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k) {
     c->launches += mt > 0 ? 3 : 2;
   }
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
-                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
+                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,
                                                                         o.perm_global, c->ell, c->diag);
   pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
-  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), c->inv);
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), inv);
   c->launches += 7;
   cudaEventRecord(o.ev_used[sa], s);
   return B2D_OK;
@@ -1224,18 +1249,18 @@ static std::vector<GVisit> generic_visits(int nb, int k) {
 static void ooc_transpose(Ctx* c, int x, int rows, int cols) {
   Ooc& o = c->o;
   const int tmp = o.nslot - 1;
-  transpose_block_kernel<<<(unsigned)(o.tiles(rows) * o.tiles(cols)), 256, TRANSPOSE_SMEM, c->s_main>>>(
+  transpose_block_kernel<<<(unsigned)(o.tiles(rows) * o.tiles(cols)), 256, TRANSPOSE_SMEM, o.s_work>>>(
       o.map(x), o.map(tmp), o.tiles(rows), o.tiles(cols));
   c->launches++;
   std::swap(o.slot[x], o.slot[tmp]);
-  cudaEventRecord(o.ev_used[x], c->s_main);  // the store of slot x must follow the transpose
+  cudaEventRecord(o.ev_used[x], o.s_work);  // the store of slot x must follow the transpose
 }
 
 // Generic Schur update of slot st (block (i, j)) -= X_i Y_j: X_i in slot sx (rows of i, the
 // column block solved against U), Y_j^T in slot sy (rows of j, the row block solved with L).
 static void ooc_schur_full(Ctx* c, int st, int i, int j, int sx, int sy, int k) {
   Ooc& o = c->o;
-  for (int x : {st, sx, sy}) cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
+  for (int x : {st, sx, sy}) cudaStreamWaitEvent(o.s_work, o.ev_loaded[x], 0);
   GemmTask t{};
   t.a = o.map(sx);
   t.b = o.map(sy);
@@ -1244,10 +1269,10 @@ static void ooc_schur_full(Ctx* c, int st, int i, int j, int sx, int sy, int k) 
   t.p0 = 0;
   t.p1 = o.tiles(k);
   const double K = (double)t.p1 * T;
-  launch_gemm(c, c->s_main, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
-  cudaEventRecord(o.ev_used[st], c->s_main);
-  cudaEventRecord(o.ev_used[sx], c->s_main);
-  cudaEventRecord(o.ev_used[sy], c->s_main);
+  launch_gemm(c, o.s_work, MODE_UPDATE, t, true, (double)t.out.count() * 2.0 * T * T * K);
+  cudaEventRecord(o.ev_used[st], o.s_work);
+  cudaEventRecord(o.ev_used[sx], o.s_work);
+  cudaEventRecord(o.ev_used[sy], o.s_work);
 }
 
 // Panel block in slot x (engine rows of block `rows`): columns permuted by the stage's block
@@ -1255,9 +1280,9 @@ static void ooc_schur_full(Ctx* c, int st, int i, int j, int sx, int sy, int k) 
 static void ooc_permute(Ctx* c, int x, int rows, int k) {
   Ooc& o = c->o;
   const int tmp = o.nslot - 1;
-  cudaStreamWaitEvent(c->s_main, o.ev_loaded[x], 0);
-  permute_cols_kernel<<<2048, 256, 0, c->s_main>>>(o.map(x), o.map(tmp), o.tiles(rows), o.tiles(k), o.size(k),
-                                                   o.perm_local);
+  cudaStreamWaitEvent(o.s_work, o.ev_loaded[x], 0);
+  permute_cols_kernel<<<2048, 256, 0, o.s_work>>>(o.map(x), o.map(tmp), o.tiles(rows), o.tiles(k), o.size(k),
+                                                   o.perm_of(k));
   c->launches++;
   std::swap(o.slot[x], o.slot[tmp]);
 }
@@ -1265,11 +1290,12 @@ static void ooc_permute(Ctx* c, int x, int rows, int k) {
 // dst = src * D^{-1} over the stage's columns (memdet.py:368-371: B /= d, the unscaled copy kept).
 static void ooc_scale(Ctx* c, int src, int dst, int rows, int k) {
   Ooc& o = c->o;
-  cudaStreamWaitEvent(c->s_main, o.ev_stored[dst], 0);
-  scale_cols_kernel<<<2048, 256, 0, c->s_main>>>(o.map(src), o.map(dst), o.tiles(rows), o.tiles(k), o.size(k), o.dblk);
+  cudaStreamWaitEvent(o.s_work, o.ev_stored[dst], 0);
+  scale_cols_kernel<<<2048, 256, 0, o.s_work>>>(o.map(src), o.map(dst), o.tiles(rows), o.tiles(k), o.size(k),
+                                                 o.dblk_of(k));
   c->launches++;
-  cudaEventRecord(o.ev_used[src], c->s_main);
-  cudaEventRecord(o.ev_used[dst], c->s_main);
+  cudaEventRecord(o.ev_used[src], o.s_work);
+  cudaEventRecord(o.ev_used[dst], o.s_work);
 }
 
 // The reference driver (memdet.py:322-389) with HBM slots for its A/B/C/S buffers: every read
@@ -1284,6 +1310,9 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   o.written.clear();
   o.reads = o.writes = 0;
   o.rr = 0;
+  // pivoted LDL: factors on s_main (high priority), the walk's solves / updates on s_mid
+  const bool look = c->mode == B2D_MODE_LDL_PIV && getenv("B2D_LDL_NO_LOOKAHEAD") == nullptr;
+  o.s_work = look ? c->s_mid : c->s_main;
   auto alloc = [&](std::initializer_list<int> busy) {
     const int pool = c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU ? o.nslot - 1 : o.nslot;  // last: permute temp
     for (int tries = 0; tries < pool; ++tries) {
@@ -1343,9 +1372,32 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   int sa = alloc({});
   rc = ooc_load(c, 0, 0, sa, a, lda, dtype);
   if (rc) return rc;
+  // pivoted LDL: factor the stage's diagonal block on s_main; s_work waits for it
+  // B2D_LDL_TRACE: per-stage factor start / end and walk progress (timing events, printed here)
+  const bool ltrace = piv && getenv("B2D_LDL_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!ltrace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  auto factor_ldl = [&](int slot, int k) -> int {
+    if (o.s_work != c->s_main) {
+      cudaEventRecord(o.ev_diag, o.s_work);  // the block's last Schur update
+      cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+    }
+    tmark(c->s_main);
+    int r = ooc_ldl_factor(c, slot, k, c->s_main);
+    tmark(c->s_main);
+    cudaEventRecord(o.ev_fac, c->s_main);
+    return r;
+  };
+  if (piv && (rc = factor_ldl(sa, 0))) return rc;
   for (int k = 0; k < o.nb; ++k) {
     if (piv) {
-      if ((rc = ooc_ldl_factor(c, sa, k))) return rc;
+      cudaStreamWaitEvent(o.s_work, o.ev_fac, 0);  // stage k's factor (issued ahead)
     } else {
       cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
       make_bounds(c, o.tiles(k), false);
@@ -1353,42 +1405,73 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
       cudaEventRecord(o.ev_used[sa], c->s_main);
     }
     if (k == o.nb - 1) break;
+    const double* inv_k = piv && (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
     // bx: the column's solved row-k block (unscaled); by: its D^{-1}-scaled copy (LDL) or bx
     int bx = -1, by = -1, sc = -1, next_a = -1;
+    bool early = false;  // look-ahead: block (k+1, k+1) updated and its factor issued
     for (const Visit& v : stage_visits(o.nb, k)) {
+      if (early && v.next_diag) continue;  // done ahead (one update per stage: same result)
       if (v.col_start) {
         if (v.load_b) {
-          bx = alloc({sa, bx, by, sc});
+          bx = alloc({sa, bx, by, sc, next_a});
           if ((rc = ooc_load(c, k, v.j, bx, a, lda, dtype))) return rc;
           if (piv) ooc_permute(c, bx, v.j, k);
-          ooc_trsm(c, bx, v.j, sa, k);
+          ooc_trsm(c, bx, v.j, sa, k, inv_k);
         } else {
           bx = sc;  // the previous visit's C is this column's row-k block (memdet.py:359-360)
         }
         if (piv) {
-          by = alloc({sa, bx, sc});
+          by = alloc({sa, bx, sc, next_a});
           ooc_scale(c, bx, by, v.j, k);
         } else {
           by = bx;
         }
       }
       if (v.load_c) {
-        sc = alloc({sa, bx, by, sc});
+        sc = alloc({sa, bx, by, sc, next_a});
         if ((rc = ooc_load(c, k, v.i, sc, a, lda, dtype))) return rc;
         if (v.solve_c) {
           if (piv) ooc_permute(c, sc, v.i, k);
-          ooc_trsm(c, sc, v.i, sa, k);
+          ooc_trsm(c, sc, v.i, sa, k, inv_k);
         }
         if (v.write_c && (rc = ooc_store(c, k, v.i, sc))) return rc;
       }
-      const int st = alloc({sa, bx, by, sc});
+      const int st = alloc({sa, bx, by, sc, next_a});
       if ((rc = ooc_load(c, v.i, v.j, st, a, lda, dtype))) return rc;
       // T(j, i) -= [D^{-1}] L(j, k) * L(i, k)^T (the unscaled copy on the diagonal visit)
       ooc_schur(c, st, v.j, v.i, by, v.i == v.j ? bx : sc, k);
       if (v.next_diag) next_a = st;
       else if ((rc = ooc_store(c, v.i, v.j, st))) return rc;
+      if (look && !early && v.j == o.nb - 1 && v.i == k + 1 && v.i != v.j) {
+        // L(k+1, k) was just solved (slot sc): update block (k+1, k+1) now, the walk's last
+        // visit, and factor it on s_main while the rest of the stage runs on s_work
+        const int by2 = alloc({sa, bx, by, sc});
+        ooc_scale(c, sc, by2, k + 1, k);
+        const int sd = alloc({sa, bx, by, sc, by2});
+        if ((rc = ooc_load(c, k + 1, k + 1, sd, a, lda, dtype))) return rc;
+        ooc_schur(c, sd, k + 1, k + 1, by2, sc, k);
+        next_a = sd;
+        early = true;
+        if ((rc = factor_ldl(next_a, k + 1))) return rc;
+      }
     }
+    if (piv && !early && (rc = factor_ldl(next_a, k + 1))) return rc;
+    tmark(o.s_work);  // end of stage k's walk
     sa = next_a;
+  }
+  if (ltrace) {
+    cudaDeviceSynchronize();
+    // events: f0s f0e, then per stage k < nb-1: f(k+1)s f(k+1)e walk_end(k)
+    float ms = 0;
+    for (size_t q = 1; q < tev.size(); ++q) {
+      cudaEventElapsedTime(&ms, tev[0], tev[q]);
+      fprintf(stderr, "[ldl trace] event %zu at %.2f ms\n", q, ms);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+  if (o.s_work != c->s_main) {
+    cudaEventRecord(o.ev_work, o.s_work);
+    cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
   }
   enqueue_prefix(c);
   cudaEventRecord(c->ev_join, o.s_d2h);
