@@ -157,6 +157,11 @@ struct Ctx {
   std::chrono::steady_clock::time_point t0;
   bool ooc = false;
   Ooc o;
+  // block-pivoted LDL in core (reference block size a multiple of the tile): the packed
+  // triangle holds the matrix, o.* the block factor state; the stage's solved panel lives in
+  // full-height grids of nt x nbt tiles, unscaled and D^{-1}-scaled, double-buffered by stage
+  bool ldl_ic = false;
+  double* pan[2][2] = {};  // [stage parity][0: unscaled, 1: scaled]
 };
 
 static int configure_kernels() {
@@ -176,6 +181,9 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ldl_factor_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(oz_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CUDA_TRY(cudaFuncSetAttribute(lu_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -246,6 +254,8 @@ static void destroy(Ctx* c) {
   cudaFree(o.ldiag);
   cudaFree(o.lcol);
   cudaFree(o.inv2);
+  for (auto& pp : c->pan)
+    for (double* q : pp) cudaFree(q);
   cudaFree(o.inv_odd);
   cudaFree(o.perm_odd);
   cudaFree(o.dblk_odd);
@@ -393,7 +403,22 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   // block-pivoted LDL pivots inside the reference's b x b diagonal blocks, and the generic LU
   // runs the reference's generic walk: always the block walk
   const bool pivoted = mode == B2D_MODE_LDL_PIV || mode == B2D_MODE_LU;
-  const bool force = (opt && opt->force_out_of_core) || pivoted;
+  bool force = (opt && opt->force_out_of_core) || pivoted;
+  // block-pivoted LDL in core: the reference's blocks (num_blocks, else select_blocking(max_mem))
+  // must start on tile boundaries; needs the packed triangle plus four nt x nbt panel grids and
+  // the dense block state
+  int64_t ic_nb = 0, ic_b = 0, ic_tail = 0;
+  if (mode == B2D_MODE_LDL_PIV && !(opt && opt->force_out_of_core)) {
+    int64_t nb0 = 1;
+    if (opt && opt->num_blocks > 0) nb0 = opt->num_blocks;
+    else if (opt && opt->max_mem > 0) nb0 = ref_select_blocking(m, opt->max_mem, 8);
+    ref_layout(m, std::max<int64_t>(1, nb0), &ic_nb, &ic_b, &ic_tail);
+    const int64_t bt = (ic_b + T - 1) / T, ldb = bt * T;
+    const size_t ic_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + 4 * (size_t)nt_full * bt * TILE_BYTES +
+                           (size_t)(nt_full + bt) * TILE_BYTES + (size_t)ldb * ldb * 9 + 3 * (size_t)npad_full * 8 +
+                           (size_t)NSTAGE * T * npad_full * 8 + (size_t)(m + 8 * ldb) * 8;
+    if ((ic_b % T == 0 || ic_nb == 1) && ic_need <= budget) force = false;
+  }
   const int nslot = pivoted ? NSLOT_LDL : NSLOT;
   int64_t vec_len = npad_full;
 #define ALLOC(ptr, bytes)                                        \
@@ -409,7 +434,37 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   bool oz = opt && opt->emulation == 1;
   if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
   const size_t oz_need = oz ? 2 * ((size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4) : 0;
-  if (!force && incore_need + oz_need <= budget) {
+  if (!force && mode == B2D_MODE_LDL_PIV) {
+    Ooc& o = c->o;
+    c->ldl_ic = true;
+    c->nt = nt_full;
+    o.nb = (int)ic_nb;
+    o.b = ic_b;
+    o.tail = ic_tail;
+    o.nbt = (int)((ic_b + T - 1) / T);
+    const int64_t ld = (int64_t)o.nbt * T;
+    ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
+    ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
+    for (auto& pp : c->pan)
+      for (double*& q : pp) ALLOC(q, (size_t)c->nt * o.nbt * TILE_BYTES);
+    ALLOC(o.dense, (size_t)ld * ld * 8);
+    ALLOC(o.swaps, (size_t)ld * 8);
+    ALLOC(o.perm_local, (size_t)ld * 8);
+    ALLOC(o.perm_global, (size_t)(m + ld) * 8);
+    ALLOC(o.dblk, (size_t)ld * 8);
+    ALLOC(o.amax, 8);
+    ALLOC(o.ltag, (size_t)ld * ld);
+    ALLOC(o.lC, (size_t)LDL_NB * ld * 8);
+    ALLOC(o.lW, (size_t)LDL_NB * ld * 8);
+    ALLOC(o.ldiag, (size_t)ld * 8);
+    ALLOC(o.lcol, (size_t)ld * 8);
+    ALLOC(o.inv_odd, (size_t)o.nbt * TILE_BYTES);
+    ALLOC(o.perm_odd, (size_t)ld * 8);
+    ALLOC(o.dblk_odd, (size_t)ld * 8);
+    cudaEventCreateWithFlags(&o.ev_fac, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_diag, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_work, cudaEventDisableTiming);
+  } else if (!force && incore_need + oz_need <= budget) {
     c->nt = nt_full;
     ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
     ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
@@ -793,11 +848,14 @@ static void end(Ctx* c, cudaStream_t user) {
   c->pending = true;
 }
 
+static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
+
 static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   if (c->ooc)
     return set_err(B2D_ERR_UNSUPPORTED, "out-of-core contexts take host inputs (the matrix exceeds the HBM budget)");
+  if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, false, user);
   CUDA_TRY(cudaSetDevice(c->device));
   begin(c, user);
   const unsigned ntiles = (unsigned)n_packed_tiles(c->nt);
@@ -892,17 +950,11 @@ static void plan_bands(Ctx* c, size_t esz) {
 // records an event, and the factorisation waits per band, so PCIe overlaps the DMMA work.
 static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
 
-static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
-  if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
-  if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
-  if (c->ooc) return run_ooc(c, a, lda, dtype, user);
-  CUDA_TRY(cudaSetDevice(c->device));
+// The strips of a host matrix into the packed triangle (s_copy / s_pack); ev_band[b] is recorded
+// on s_pack once tile-columns [b * BAND, (b + 1) * BAND) are packed.
+static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype) {
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
-  for (int b = 0; b < NSTAGE; ++b)
-    if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
-  begin(c, user);
-  plan_bands(c, esz);
   for (int J = 0; J < c->nt; ++J) {
     const int b = J % NSTAGE;
     const int64_t r0 = (int64_t)J * T;
@@ -929,6 +981,23 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
     cudaEventRecord(c->ev_stage[b], c->s_pack);
     if ((J + 1) % BAND == 0 || J + 1 == c->nt) cudaEventRecord(c->ev_band[J / BAND], c->s_pack);
   }
+  return B2D_OK;
+}
+
+static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
+  if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
+  if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  if (c->ooc) return run_ooc(c, a, lda, dtype, user);
+  if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, true, user);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t npad = (int64_t)c->nt * T;
+  const size_t esz = dtype == B2D_F64 ? 8 : 4;
+  for (int b = 0; b < NSTAGE; ++b)
+    if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
+  begin(c, user);
+  plan_bands(c, esz);
+  int rc = ingest_host_strips(c, a, lda, dtype);
+  if (rc) return rc;
   enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, true);
   enqueue_prefix(c);
   cudaEventRecord(c->ev_join, c->s_pack);
@@ -1048,44 +1117,51 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
   return B2D_OK;
 }
 
-// Panel solve of slot s (engine lower block (x, k), x's rows) against the factored diagonal
-// block in slot sa: right-looking over L_kk's tile-columns in groups of W (dense.py:94-99).
-static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nullptr) {
-  Ooc& o = c->o;
-  if (!inv) inv = c->inv;
-  cudaStreamWaitEvent(o.s_work, o.ev_loaded[s], 0);
-  const int R = o.tiles(x), Q = o.tiles(k), W = c->W_TILES;
+// Panel solve X <- X L^{-T} of R x Q tiles against the factored diagonal block lkk (Q x Q tiles,
+// unit or not per inv): right-looking over L's tile-columns in groups of W (dense.py:94-99).
+static void trsm_panel(Ctx* c, cudaStream_t s, const TileMap& x, int R, const TileMap& lkk, int Q,
+                       const double* inv) {
+  const int W = c->W_TILES;
   for (int q0 = 0; q0 < Q; q0 += W) {
     const int qe = std::min(q0 + W, Q);
     for (int q = q0; q < qe; ++q) {
       GemmTask t{};
-      t.c = o.map(s);
+      t.c = x;
       t.binv = inv + (int64_t)q * TILE_ELEMS;
       t.out = TileSet{0, R, q, q + 1, 0, 0};
       t.k = q;
-      launch_gemm(c, o.s_work, MODE_TRSM, t, false, 0.0);
+      launch_gemm(c, s, MODE_TRSM, t, false, 0.0);
       if (q + 1 < qe) {
         GemmTask u{};
-        u.a = o.map(s);
-        u.b = o.map(sa);
-        u.c = o.map(s);
+        u.a = x;
+        u.b = lkk;
+        u.c = x;
         u.out = TileSet{0, R, q + 1, qe, 0, 0};
         u.p0 = q;
         u.p1 = q + 1;
-        launch_gemm(c, o.s_work, MODE_UPDATE, u, false, 0.0);
+        launch_gemm(c, s, MODE_UPDATE, u, false, 0.0);
       }
     }
     if (qe < Q) {
       GemmTask u{};
-      u.a = o.map(s);
-      u.b = o.map(sa);
-      u.c = o.map(s);
+      u.a = x;
+      u.b = lkk;
+      u.c = x;
       u.out = TileSet{0, R, qe, Q, 0, 0};
       u.p0 = q0;
       u.p1 = qe;
-      launch_gemm(c, o.s_work, MODE_UPDATE, u, false, 0.0);
+      launch_gemm(c, s, MODE_UPDATE, u, false, 0.0);
     }
   }
+}
+
+// Panel solve of slot s (engine lower block (x, k), x's rows) against the factored diagonal
+// block in slot sa.
+static void ooc_trsm(Ctx* c, int s, int x, int sa, int k, const double* inv = nullptr) {
+  Ooc& o = c->o;
+  if (!inv) inv = c->inv;
+  cudaStreamWaitEvent(o.s_work, o.ev_loaded[s], 0);
+  trsm_panel(c, o.s_work, o.map(s), o.tiles(x), o.map(sa), o.tiles(k), inv);
   cudaEventRecord(o.ev_used[s], o.s_work);
   cudaEventRecord(o.ev_used[sa], o.s_work);
 }
@@ -1111,7 +1187,7 @@ static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
 // Pivoted LDL^T of the diagonal block in slot sa (stage k): dense copy, tolerance scale, the
 // cooperative 1x1-pivot factorisation, permutation / log|d| bookkeeping, then the unit factor
 // back into the slot and the inverses of its diagonal tiles for the panel solves.
-static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
+static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, bool overlapped = false) {
   Ooc& o = c->o;
   const int nt = o.tiles(k);
   int64_t n = o.size(k);
@@ -1119,9 +1195,8 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
   double* dblk = o.dblk_of(k);
   int64_t* perm = o.perm_of(k);
   double* inv = (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
-  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
-  unpack_block_kernel<<<ntri, 256, 0, s>>>(o.map(sa), nt, o.dense, ld, 1);
+  unpack_block_kernel<<<ntri, 256, 0, s>>>(blk, nt, o.dense, ld, 1);
   cudaMemsetAsync(o.amax, 0, 8, s);
   block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
   // blocked pivoted LDL: panels of LDL_NB steps (one CTA), then the delayed trailing update
@@ -1131,6 +1206,26 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
   c->launches += 1;
   // B2D_LDL_SINGLE_CTA forces the one-CTA panel kernel (the path for blocks above 16*384 rows)
   const bool single_cta = getenv("B2D_LDL_SINGLE_CTA") != nullptr;
+  // B2D_LDL_PERSIST: 0 = per-panel kernels always; 1 (default) = the one-launch cluster factor
+  // when the factor runs beside other work (it holds its SMs); 2 = always
+  const char* pe = getenv("B2D_LDL_PERSIST");
+  const int persist = pe ? atoi(pe) : 1;
+  if (n <= (int64_t)LC * LC_RMAX && !single_cta && (persist == 2 || (persist == 1 && overlapped))) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = LC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(LC);
+    cfg.blockDim = dim3(LC_THREADS);
+    cfg.dynamicSmemBytes = ldl_factor_smem((int)((n + LC - 1) / LC));
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_factor_cluster_kernel, g));
+    c->launches += 1;
+  } else
   for (int64_t r0 = 0; r0 < n; r0 += LDL_NB) {
     const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
     if (n <= (int64_t)LC * LC_RMAX && !single_cta) {
@@ -1160,11 +1255,18 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
                       n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,
                                                                         o.perm_global, c->ell, c->diag);
-  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
-  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), inv);
+  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, blk, nt);
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv);
   c->launches += 7;
-  cudaEventRecord(o.ev_used[sa], s);
   return B2D_OK;
+}
+
+static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
+  Ooc& o = c->o;
+  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
+  const int rc = ldl_factor_block(c, o.map(sa), k, s);
+  cudaEventRecord(o.ev_used[sa], s);
+  return rc;
 }
 
 // Generic (LU) diagonal block in slot sa (stage k), reference lu_inplace (dense.py:38-54):
@@ -1481,6 +1583,143 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   return B2D_OK;
 }
 
+// Block-pivoted LDL^T in core (memdet_ldl; memdet.py:322-389, kernels/_ldl.pyx:21-61): the
+// reference's stages over its b x b blocks with the matrix resident in the packed triangle.
+// Stage k: the diagonal block is factored with block-local pivoting (s_main); the panel below
+// it is permuted, solved and D^{-1}-scaled into the stage's panel grids (s_mid); block column
+// k+1 is updated first (s_mid) so that the next factor starts at once, and the rest of the
+// trailing triangle takes one large DMMA update (s_side) while it runs.  Every tile receives
+// the walk's updates with the same operands and K, so the results equal the block walk's.
+static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user) {
+  if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
+  if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  Ooc& o = c->o;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int nt = c->nt, nb = o.nb;
+  const int64_t npad = (int64_t)nt * T;
+  if (host)
+    for (int b = 0; b < NSTAGE; ++b)
+      if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
+  begin(c, user);
+  if (host) {
+    int rc = ingest_host_strips(c, a, lda, dtype);
+    if (rc) return rc;
+  } else {
+    const unsigned ntiles = (unsigned)n_packed_tiles(nt);
+    if (dtype == B2D_F64)
+      pack_tiles_kernel<double, 32><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_pack>>>((const double*)a, lda, 0, c->m,
+                                                                                  c->tiles, nt, 0);
+    else
+      pack_tiles_kernel<float, 32><<<ntiles, PACK_THREADS, PACK_SMEM, c->s_pack>>>((const float*)a, lda, 0, c->m,
+                                                                                 c->tiles, nt, 0);
+    c->launches++;
+    for (auto& e : c->ev_band) cudaEventRecord(e, c->s_pack);
+  }
+  auto wait_cols = [&](cudaStream_t st, int j1) {  // tile-columns [0, j1) packed
+    const int b = std::min((int)c->ev_band.size(), (j1 + BAND - 1) / BAND) - 1;
+    if (b >= 0) cudaStreamWaitEvent(st, c->ev_band[b], 0);
+  };
+  auto col0 = [&](int k) { return (int)((int64_t)k * o.b / T); };
+  const TileMap packed{c->tiles, 0, nt};
+  auto diag_map = [&](int k) {
+    TileMap t = packed;
+    t.roff = t.coff = col0(k);
+    return t;
+  };
+  int rc = 0;
+  // B2D_LDL_TRACE: timing events (name, stage) printed after the run
+  const bool ltrace = getenv("B2D_LDL_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tev;
+  auto tmark = [&](const char* what, int k, cudaStream_t st) {
+    if (!ltrace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.emplace_back(std::string(what) + " " + std::to_string(k), e);
+  };
+  tmark("start", 0, c->s_main);
+  wait_cols(c->s_main, col0(0) + o.tiles(0));
+  tmark("factor-begin", 0, c->s_main);
+  if ((rc = ldl_factor_block(c, diag_map(0), 0, c->s_main))) return rc;
+  tmark("factor-end", 0, c->s_main);
+  cudaEventRecord(c->ev_catch[0], c->s_main);
+  for (int k = 0; k + 1 < nb; ++k) {
+    const int par = k & 1;
+    const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb, R = nt - i0, kb1 = o.tiles(k + 1);
+    const double* inv_k = par && o.inv_odd ? o.inv_odd : c->inv;
+    // panel: rows [i0, nt) of block column k, permuted by the stage's pivots (memdet.py:365-366),
+    // solved with the unit factor (dense.py:94-99), and its D^{-1}-scaled copy (memdet.py:368-371)
+    cudaStreamWaitEvent(c->s_mid, c->ev_catch[k], 0);
+    if (k >= 2) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 2], 0);  // last reader of pan[par]
+    wait_cols(c->s_mid, i0);
+    TileMap src = packed;
+    src.roff = i0;
+    src.coff = k0;
+    const TileMap pu{c->pan[par][0] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+    const TileMap ps{c->pan[par][1] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+    permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(src, pu, R, kb, o.size(k), o.perm_of(k));
+    trsm_panel(c, c->s_mid, pu, R, diag_map(k), kb, inv_k);
+    scale_cols_kernel<<<2048, 256, 0, c->s_mid>>>(pu, ps, R, kb, o.size(k), o.dblk_of(k));
+    c->launches += 2;
+    tmark("panel-end", k, c->s_mid);
+    cudaEventRecord(c->ev_panel[k], c->s_mid);
+    // T -= (L D^{-1})_rows L_cols^T (dense.py:109-116) over block column k+1 first
+    GemmTask u{};
+    u.a = TileMap{c->pan[par][1], o.nbt, 0};  // rows indexed by global tile row
+    u.b = TileMap{c->pan[par][0], o.nbt, 0};
+    u.c = packed;
+    u.p0 = 0;
+    u.p1 = kb;
+    const double K = (double)kb * T;
+    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 1], 0);
+    wait_cols(c->s_mid, i0 + kb1);
+    u.out = TileSet{i0, nt, i0, i0 + kb1, 1, 0};
+    launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+    tmark("next-col-end", k, c->s_mid);
+    cudaEventRecord(o.ev_diag, c->s_mid);
+    cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+    tmark("factor-begin", k + 1, c->s_main);
+    // B2D_LDL_SCHED: 1 (default) = the next factor alone on the GPU (per-panel kernels), then the
+    // rest update beside the next panel solve; 0 = the factor beside the rest update (one-launch
+    // cluster factor)
+    const char* se = getenv("B2D_LDL_SCHED");
+    const bool serial = se ? atoi(se) != 0 : true;
+    if ((rc = ldl_factor_block(c, diag_map(k + 1), k + 1, c->s_main, !serial && i0 + kb1 < nt))) return rc;
+    tmark("factor-end", k + 1, c->s_main);
+    cudaEventRecord(c->ev_catch[k + 1], c->s_main);
+    if (i0 + kb1 < nt) {
+      // after the next-col update, i.e. issued with the next factor, which takes its SMs first
+      cudaStreamWaitEvent(c->s_side, o.ev_diag, 0);
+      if (serial) cudaStreamWaitEvent(c->s_side, c->ev_catch[k + 1], 0);
+      wait_cols(c->s_side, nt);
+      u.out = TileSet{i0 + kb1, nt, i0 + kb1, nt, 1, 0};
+      launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+    }
+    tmark("rest-end", k, c->s_side);
+    cudaEventRecord(c->ev_rest[k], c->s_side);
+  }
+  cudaEventRecord(o.ev_work, c->s_mid);
+  cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
+  cudaEventRecord(o.ev_diag, c->s_side);
+  cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+  cudaEventRecord(c->ev_join, c->s_pack);
+  cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+  enqueue_prefix(c);
+  tmark("end", nb, c->s_main);
+  end(c, user);
+  if (ltrace) {
+    cudaDeviceSynchronize();
+    for (size_t q = 1; q < tev.size(); ++q) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0].second, tev[q].second);
+      fprintf(stderr, "[ldl trace] %-14s %8.2f ms\n", tev[q].first.c_str(), ms);
+    }
+    for (auto& e : tev) cudaEventDestroy(e.second);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
 static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index, b2d_run_info* info) {
   if (!c->pending) return set_err(B2D_ERR_USAGE, "no factorisation enqueued");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1544,7 +1783,7 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
 
 static int fetch_perm(Ctx* c, int64_t* perm) {
   if (!perm) return set_err(B2D_ERR_USAGE, "null perm");
-  if ((c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU) && c->ooc && c->o.perm_global) {
+  if ((c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU) && c->o.perm_global) {
     CUDA_TRY(cudaMemcpy(perm, c->o.perm_global, c->m * 8, cudaMemcpyDeviceToHost));
   } else {
     for (int64_t g = 0; g < c->m; ++g) perm[g] = g;

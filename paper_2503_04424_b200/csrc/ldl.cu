@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs
 // new column, interchange, update.  Entry arithmetic is the single-CTA kernel's exactly.
 // Raw entries and tags stay in global memory (read through L2: other CTAs wrote them).
 #ifdef LDL_PROF  // tools/ldl_prof.cu: per-phase cycle counts of the cluster panel (CTA 0, thread 0)
-__device__ long long ldl_prof[16];
+__device__ long long ldl_prof[16];  // [0, 8): panel steps; [8, 16): one-launch factor phases
 #define LDL_MARK(slot)                                   \
   if (c == 0 && tid == 0) {                              \
     const long long now = clock64();                     \
@@ -306,45 +306,47 @@ __device__ __forceinline__ void chain_terms2(double& v, int tv, const double* cv
 //   3. each thread forms the new column entry of its rows (the interchange, as the single-CTA
 //      kernel), scales it and updates its C / W row and diagonal, and takes its candidate for the
 //      next step.  A thread only touches its own rows' diagonal entries, so no CTA barrier.
-// Rows r, t of the finished L columns (j < r0) are interchanged after the panel
-// (ldl_store_l_kernel).  Entry arithmetic is the single-CTA kernel's exactly.
-__global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
-  if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
+// Rows r, t of the finished L columns (j < r0) are interchanged after the panel (ldl_store_part).
+// Entry arithmetic is the single-CTA kernel's exactly.
+constexpr int LC_NW = LC_THREADS / 32;
+constexpr int LC_ROW = 2 * LDL_NB + 2;  // pushed row: C[0, NB), W[0, NB), diagonal, 1 / diagonal
+struct ClusterShared {
+  Cand cand[2][LC * LC_NW];
+  double rows[2][2][LC_ROW];  // [step parity][0: row r, 1: row t]
+  uint64_t bar[2];
+  int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
+};
+
+__device__ __forceinline__ void cluster_shared_init(ClusterShared& sh) {
+  if (threadIdx.x == 0) {
+    mbar_init(&sh.bar[0], 1);
+    mbar_init(&sh.bar[1], 1);
+    fence_mbar_init();
+  }
+}
+
+__device__ __forceinline__ Cand cand_of(int64_t i, double v) {
+  Cand x{0u, 0u, 0xffffffffu, 0u};
+  if (!isnan(v)) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v));
+    x = Cand{(uint32_t)(bits >> 32) + 1u, (uint32_t)bits, (uint32_t)i, 0u};
+  }
+  return x;
+}
+
+// The nbk steps of the panel at r0; gs0 = steps this kernel ran before (mbarrier phases and
+// buffer parity).  Returns false if a step failed (uniform across the cluster, after a cluster
+// barrier).  On return the C / W rows of the panel are final in shared memory.
+__device__ __forceinline__ bool cluster_panel_steps(const LdlArgs& g, int64_t r0, int nbk, double* Cs, double* Ws,
+                                                    double* dg, int R, ClusterShared& sh, int gs0) {
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
-  extern __shared__ double sm[];
   const int64_t n = g.n, ld = g.ld;
-  const int R = (int)((n + LC - 1) / LC);
-  double* Cs = sm;                      // [R][LC_LD]
-  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
-  double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal
-  constexpr int NW = LC_THREADS / 32;
-  constexpr int ROW = 2 * LDL_NB + 2;   // pushed row: C[0, NB), W[0, NB), diagonal, 1 / diagonal
-  __shared__ Cand cand[2][LC * NW];
-  __shared__ double rows[2][2][ROW];    // [step parity][0: row r, 1: row t]
-  __shared__ uint64_t bar[2];
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   double* __restrict__ A = g.A;
   uint8_t* __restrict__ tag = g.tag;
   const double tol = 64.0 * 2.220446049250313e-16 * __longlong_as_double((long long)*g.amax_bits);
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  const uint32_t rows_u32 = smem_u32(&rows[0][0][0]), bar_u32 = smem_u32(&bar[0]);
-  for (int li = tid; li < R; li += LC_THREADS) {
-    const int64_t i = (int64_t)li * LC + c;
-    dg[li] = i < n ? g.diag[i] : 0.0;
-  }
-  auto cand_of = [&](int64_t i, double v) {
-    Cand x{0u, 0u, 0xffffffffu, 0u};
-    if (!isnan(v)) {
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(v));
-      x = Cand{(uint32_t)(bits >> 32) + 1u, (uint32_t)bits, (uint32_t)i, 0u};
-    }
-    return x;
-  };
+  const uint32_t rows_u32 = smem_u32(&sh.rows[0][0][0]), bar_u32 = smem_u32(&sh.bar[0]);
   // step 0's candidate (later steps take theirs in the update)
   Cand my{0u, 0u, 0xffffffffu, 0u};
   for (int li = tid; li < R; li += LC_THREADS) {
@@ -354,21 +356,19 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
       if (cand_better(x, my)) my = x;
     }
   }
-  __syncthreads();  // dg loaded, barriers initialised
-  cl.sync();        // every CTA's barriers initialised before any remote arrive
 #ifdef LDL_PROF
   long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long prof_t = clock64();
 #endif
   for (int k = 0; k < nbk; ++k) {
     const int64_t r = r0 + k;
-    const int buf = k & 1;
+    const int gs = gs0 + k, buf = gs & 1;
     LDL_MARK(0);
     {
       const Cand w = warp_best(my);
-      if (lane < LC) *cl.map_shared_rank(&cand[buf][c * NW + wib], lane) = w;
+      if (lane < LC) *cl.map_shared_rank(&sh.cand[buf][c * LC_NW + wib], lane) = w;
     }
-    if (tid == 0) mbar_arrive_expect_tx(&bar[buf], (2u * (2u * k + 1u) + 1u) * 8u);
+    if (tid == 0) mbar_arrive_expect_tx(&sh.bar[buf], (2u * (2u * k + 1u) + 1u) * 8u);
     LDL_MARK(1);
     cl.sync();  // candidates and the previous step's writes visible cluster-wide
     LDL_MARK(2);
@@ -388,17 +388,17 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
         gr[m] = __ldcg(tag + r * ld + i);
       }
     }
-    Cand b = cand[buf][lane];
+    Cand b = sh.cand[buf][lane];
 #pragma unroll
-    for (int m = 1; m < LC * NW / 32; ++m) {
-      const Cand x = cand[buf][lane + 32 * m];
+    for (int m = 1; m < LC * LC_NW / 32; ++m) {
+      const Cand x = sh.cand[buf][lane + 32 * m];
       if (cand_better(x, b)) b = x;
     }
     b = warp_best(b);
     if (b.hi == 0) {  // no finite diagonal left: the step fails (uniform)
       if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
       cl.sync();
-      return;
+      return false;
     }
     const int64_t t = b.idx;
     const int orr = (int)(r % LC), ort = (int)(t % LC);
@@ -426,22 +426,22 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
                          : e < 2 * LDL_NB ? Ws[(size_t)lrow * LC_LD + e - LDL_NB]
                          : e == 2 * LDL_NB ? dg[lrow]
                                            : 1.0 / dg[lrow];
-        const uint32_t off = rows_u32 + (uint32_t)(((buf * 2 + slot) * ROW + e) * 8);
+        const uint32_t off = rows_u32 + (uint32_t)(((buf * 2 + slot) * LC_ROW + e) * 8);
         const uint32_t bo = bar_u32 + (uint32_t)(buf * 8);
 #pragma unroll 4
         for (int d = 0; d < LC; ++d) st_async_f64(dsmem_map(off, d), v, dsmem_map(bo, d));
       }
     }
     LDL_MARK(3);
-    mbar_wait_acq_cluster(&bar[buf], (uint32_t)((k >> 1) & 1));
+    mbar_wait_acq_cluster(&sh.bar[buf], (uint32_t)((gs >> 1) & 1));
     LDL_MARK(4);
-    const double* rr = rows[buf][0];
-    const double* rt = rows[buf][1];
+    const double* rr = sh.rows[buf][0];
+    const double* rt = sh.rows[buf][1];
     const double p = rt[2 * LDL_NB];  // row t's eager diagonal: the pivot
     if (!(fabs(p) >= tol)) {
       if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
       cl.sync();
-      return;  // uniform across the cluster: every thread read the same p
+      return false;  // uniform across the cluster: every thread read the same p
     }
     if (c == 0 && tid == 0) {
       g.d[r] = p;
@@ -504,32 +504,62 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
   if (c == 0 && tid == 0)
     for (int q = 0; q < 8; ++q) ldl_prof[q] += prof_acc[q];
 #endif
-  // C, W and the diagonal back to global memory for the bulk update and the next panel
-  for (int li = tid; li < R; li += LC_THREADS) {
+  return true;
+}
+
+// C and W rows of the panel (rows > r0) back to global memory for the store and bulk phases.
+__device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_t r0, int nbk, const double* Cs,
+                                                        const double* Ws, int R, int c) {
+  for (int li = threadIdx.x; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
-    if (i >= n || i <= r0) continue;
+    if (i >= g.n || i <= r0) continue;
     for (int q = 0; q < nbk; ++q) {
-      g.C[q * ld + i] = Cs[(size_t)li * LC_LD + q];
-      g.W[q * ld + i] = Ws[(size_t)li * LC_LD + q];
+      g.C[q * g.ld + i] = Cs[(size_t)li * LC_LD + q];
+      g.W[q * g.ld + i] = Ws[(size_t)li * LC_LD + q];
     }
-    g.diag[i] = dg[li];
+  }
+}
+
+__global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  extern __shared__ double sm[];
+  const int R = (int)((g.n + LC - 1) / LC);
+  double* Cs = sm;                      // [R][LC_LD]
+  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
+  double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal
+  __shared__ ClusterShared sh;
+  cluster_shared_init(sh);
+  for (int li = threadIdx.x; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    dg[li] = i < g.n ? g.diag[i] : 0.0;
+  }
+  __syncthreads();  // dg loaded, barriers initialised
+  cl.sync();        // every CTA's barriers initialised before any remote arrive
+  if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) return;
+  cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c);
+  for (int li = threadIdx.x; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    if (i < g.n && i > r0) g.diag[i] = dg[li];
   }
 }
 
 // Finished columns [r0, r0 + nbk): L = W below the diagonal (_ldl.pyx:59-60); and the panel's
 // interchanges applied to rows of the finished columns j < r0 (the reference swaps rows r, t of
-// those columns at every step, _ldl.pyx:38-46): warp 0 of each CTA folds the panel's swaps into
-// one permutation of at most 2 * NB rows, then one warp per column gathers and scatters them.
-__global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0, int nbk) {
-  if (*g.fail != ~0ull) return;
-  __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
+// those columns at every step, _ldl.pyx:38-46): warp 0 folds the panel's swaps into one
+// permutation of at most 2 * NB rows (spos / ssrc, in shared memory), then one warp per column
+// gathers and scatters them.  Work item w of nw (CTA-granular).
+__device__ __forceinline__ void ldl_store_part(const LdlArgs& g, int64_t r0, int nbk, int64_t* spos, int64_t* ssrc,
+                                               int64_t w, int64_t nw) {
   const int tid = threadIdx.x, lane = tid & 31;
+  const int nthr = blockDim.x;
   if (r0 > 0 && tid < 32) {
     int64_t dcur = r0 + lane;        // row whose value ends at position r0 + lane
     int64_t xpos = -1, xcur = -1;    // extra position `lane` (beyond the panel) and its row
     int nx = 0;
     for (int k = 0; k < nbk; ++k) {
-      const int64_t a = r0 + k, b = g.swaps[a];
+      const int64_t a = r0 + k, b = __ldcg(g.swaps + a);
       if (b == a) continue;
       const bool direct = b < r0 + nbk;
       int hb;
@@ -562,7 +592,7 @@ __global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0,
   if (r0 > 0) {
     const int64_t p0 = spos[lane], p1 = spos[32 + lane], s0 = ssrc[lane], s1 = ssrc[32 + lane];
     const int64_t ld = g.ld;
-    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; j < r0; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t j = (w * nthr + tid) >> 5; j < r0; j += (nw * nthr) >> 5) {
       double* colj = g.A + j * ld;
       const double v0 = p0 >= 0 ? __ldcg(colj + s0) : 0.0;
       const double v1 = p1 >= 0 ? __ldcg(colj + s1) : 0.0;
@@ -572,31 +602,35 @@ __global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0,
     }
   }
   const int64_t rows = g.n - r0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * nbk; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = w * nthr + tid; e < rows * nbk; e += nw * nthr) {
     const int k = (int)(e / rows);
     const int64_t i = r0 + e % rows, r = r0 + k;
-    if (i > r) g.A[r * g.ld + i] = g.W[k * g.ld + i];
+    if (i > r) g.A[r * g.ld + i] = __ldcg(g.W + k * g.ld + i);
   }
 }
 
-// Trailing update with the panel's nbk steps: a_ij -= c_i^q w_j^q for q = tag_ij .. nbk-1, in
-// order, for j >= r0 + nbk, i >= j; tags reset.  64 x 64 entry tiles, 4 x 4 per thread.
-constexpr int LDL_BT = 64;
-__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk) {
+__global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;
-  __shared__ double sC[LDL_NB][LDL_BT], sW[LDL_NB][LDL_BT];
+  __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
+  ldl_store_part(g, r0, nbk, spos, ssrc, blockIdx.x, gridDim.x);
+}
+
+// Trailing update with the panel's nbk steps: a_ij -= c_i^q w_j^q for q = tag_ij .. nbk-1, in
+// order, for j >= r0 + nbk, i >= j; tags reset.  64 x 64 entry tiles, 4 x 4 per thread (256
+// threads); tile b of the lower tile triangle (column-major).
+constexpr int LDL_BT = 64;
+__device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int nbk, int64_t b, double* sC,
+                                              double* sW) {
   const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld;
-  // lower-triangular tile (bi >= bj), the first tile-column (the next panel's columns) last so
-  // that it is L2-resident when the next panel kernel reads it
-  int64_t b = (int64_t)gridDim.x - 1 - blockIdx.x, bj = 0;
+  int64_t bj = 0;
   const int64_t nbt = (m + LDL_BT - 1) / LDL_BT;
   while (b >= nbt - bj) { b -= nbt - bj; ++bj; }
   const int64_t bi = bj + b;
   const int64_t i0 = re + bi * LDL_BT, j0 = re + bj * LDL_BT;
   for (int e = threadIdx.x; e < nbk * LDL_BT; e += 256) {
     const int q = e / LDL_BT, x = e % LDL_BT;
-    sC[q][x] = i0 + x < g.n ? g.C[q * ld + i0 + x] : 0.0;
-    sW[q][x] = j0 + x < g.n ? g.W[q * ld + j0 + x] : 0.0;
+    sC[q * LDL_BT + x] = i0 + x < g.n ? __ldcg(g.C + q * ld + i0 + x) : 0.0;
+    sW[q * LDL_BT + x] = j0 + x < g.n ? __ldcg(g.W + q * ld + j0 + x) : 0.0;
   }
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -608,15 +642,15 @@ __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, in
     for (int c = 0; c < 4; ++c) {
       const int64_t i = i0 + tx + 16 * a, j = j0 + ty + 16 * c;
       const bool ok = i < g.n && j < g.n && i >= j;
-      v[a][c] = ok ? g.A[j * ld + i] : 0.0;
-      tg[a][c] = ok ? g.tag[j * ld + i] : 255;
+      v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
+      tg[a][c] = ok ? __ldcg(g.tag + j * ld + i) : 255;
     }
   for (int q = 0; q < nbk; ++q) {
     double cc[4], ww[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) cc[a] = sC[q][tx + 16 * a];
+    for (int a = 0; a < 4; ++a) cc[a] = sC[q * LDL_BT + tx + 16 * a];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) ww[c] = sW[q][ty + 16 * c];
+    for (int c = 0; c < 4; ++c) ww[c] = sW[q * LDL_BT + ty + 16 * c];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -633,6 +667,78 @@ __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, in
         if (tg[a][c]) g.tag[j * ld + i] = 0;
       }
     }
+  __syncthreads();  // sC / sW reused by the next tile
+}
+
+__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk) {
+  if (*g.fail != ~0ull) return;
+  __shared__ double sC[LDL_NB * LDL_BT], sW[LDL_NB * LDL_BT];
+  // the first tile-column (the next panel's columns) last, so that it is L2-resident when the
+  // next panel kernel reads it
+  ldl_bulk_tile(g, r0, nbk, (int64_t)gridDim.x - 1 - blockIdx.x, sC, sW);
+}
+
+// The whole pivoted factorisation of the block on one 16-CTA cluster (one launch): per panel
+// the cluster steps, then the store / interchange and the bulk update spread over the cluster's
+// CTAs, with cluster barriers between the phases.  It holds its 16 SMs from start to end, so it
+// runs beside the trailing DMMA updates of the previous stage at full speed (the per-panel
+// kernels would each wait for SMs there).  Same arithmetic as the per-panel kernels.
+__host__ __device__ constexpr size_t ldl_factor_smem(int rows) {
+  return ((size_t)rows + (2 * (size_t)rows * LC_LD > 2 * (size_t)LDL_NB * LDL_BT ? 2 * (size_t)rows * LC_LD
+                                                                                  : 2 * (size_t)LDL_NB * LDL_BT)) * 8;
+}
+__global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlArgs g) {
+  if (*g.fail != ~0ull) return;
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  extern __shared__ double sm[];
+  const int64_t n = g.n, ld = g.ld;
+  const int R = (int)((n + LC - 1) / LC);
+  double* dg = sm;                      // [R] eager diagonal (kept across panels)
+  double* Cs = dg + R;                  // [R][LC_LD] (panel phase) / bulk staging C
+  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
+  double* sC = Cs;                      // bulk phase: [NB][BT] x 2
+  double* sW = Cs + LDL_NB * LDL_BT;
+  __shared__ ClusterShared sh;
+  cluster_shared_init(sh);
+  for (int li = threadIdx.x; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    dg[li] = i < n ? g.A[i * ld + i] : 0.0;
+  }
+  __syncthreads();
+  cl.sync();
+#ifdef LDL_PROF
+  const int tid = threadIdx.x;
+  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_t = clock64();
+#define FMARK(slot) LDL_MARK(slot)
+#else
+#define FMARK(slot)
+#endif
+  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB) {
+    const int nbk = (int)(n - r0 < LDL_NB ? n - r0 : LDL_NB);
+    FMARK(0);
+    if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, (int)r0)) return;
+    FMARK(1);
+    cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c);
+    cl.sync();  // C / W rows and the panel's interchanges visible cluster-wide
+    FMARK(2);
+    ldl_store_part(g, r0, nbk, sh.spos, sh.ssrc, c, LC);
+    FMARK(3);
+    const int64_t m = n - r0 - nbk;
+    if (m > 0) {
+      const int64_t nbt = (m + LDL_BT - 1) / LDL_BT, ntile = nbt * (nbt + 1) / 2;
+      for (int64_t b = c; b < ntile; b += LC) ldl_bulk_tile(g, r0, nbk, ntile - 1 - b, sC, sW);
+    }
+    FMARK(4);
+    cl.sync();  // the trailing block up to date before the next panel reads it
+    FMARK(5);
+  }
+#ifdef LDL_PROF
+  if (c == 0 && tid == 0)
+    for (int q = 0; q < 8; ++q) ldl_prof[8 + q] += prof_acc[q];
+#endif
+#undef FMARK
 }
 
 // swaps -> block permutation (kernels/dense.py:25-30), global perm (memdet.py:352-353),

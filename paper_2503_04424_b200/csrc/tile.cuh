@@ -42,6 +42,8 @@ constexpr int MAX_PEERS = 8;  // ranks whose tile grids one map can address (one
 
 // Where a tile lives: the packed lower triangle (packed_nt > 0) or a row-major grid of tiles
 // with `ld` tiles per row (out-of-core blocks).
+// A sub-block of the packed triangle (a diagonal block, or the panel below it) is addressed with
+// block-local indices through (roff, coff).
 // Row-cyclic storage over several ranks (rmod = ranks): tile row i belongs to rank i % rmod at
 // local row i / rmod, either gathered into one buffer of rank-major blocks of rstride rows
 // (base, npeer = 0), or read in place from each rank's own grid over NVLink peer memory
@@ -54,8 +56,9 @@ struct TileMap {
   int64_t rstride;
   int npeer;
   double* peer[MAX_PEERS];
+  int roff = 0, coff = 0;  // packed triangle: tile (i, j) of the map is packed tile (i + roff, j + coff)
   __host__ __device__ __forceinline__ double* tile(int i, int j) const {
-    if (packed_nt > 0) return base + tile_index(i, j, packed_nt) * TILE_ELEMS;
+    if (packed_nt > 0) return base + tile_index(i + roff, j + coff, packed_nt) * TILE_ELEMS;
     if (npeer > 0) return peer[i % rmod] + ((int64_t)(i / rmod) * ld + j) * TILE_ELEMS;
     const int64_t r = rmod > 0 ? (int64_t)(i % rmod) * rstride + i / rmod : (int64_t)i;
     return base + (r * ld + j) * TILE_ELEMS;

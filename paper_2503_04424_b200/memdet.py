@@ -240,8 +240,10 @@ def _context(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, m
     base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"])
     with _ctx_lock:
         ctx = _ctx_cache.get(base)
-        # an in-core plan ignores the reference tiling; an out-of-core one is built from it
-        if ctx is not None and (not ctx.out_of_core or ctx.key[4:6] == (kw["num_blocks"], kw["max_mem"])):
+        # an in-core plan ignores the reference tiling (except the block-pivoted LDL, which pivots
+        # inside the reference's blocks); an out-of-core one is built from it
+        tiled = ctx is not None and (ctx.out_of_core or mode == _native.MODE_LDL_PIV)
+        if ctx is not None and (not tiled or ctx.key[4:6] == (kw["num_blocks"], kw["max_mem"])):
             return ctx
         for k in list(_ctx_cache):
             _ctx_cache.pop(k).close()
@@ -263,13 +265,20 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     m = src.m
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
     ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
-    if src.device_ptr is not None and mode in (_native.MODE_LDL_PIV, _native.MODE_LU):
-        # the block-pivoted walks stream reference blocks from host memory
+    if src.device_ptr is not None and mode == _native.MODE_LU:
+        # the generic walk streams reference blocks from host memory
         src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
+    if src.device_ptr is not None and mode == _native.MODE_LDL_PIV:
+        # in core when the reference's blocks are tile-aligned and fit; else the block walk,
+        # which streams reference blocks from host memory
+        ctx = _context(m, mode, src.device_index, emulation=emulation, **ooc_kw)
+        if ctx.out_of_core:
+            src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
     if src.device_ptr is not None:
         if out_of_core:
             raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
-        ctx = _context(m, mode, src.device_index, emulation=emulation)
+        kw = ooc_kw if mode == _native.MODE_LDL_PIV else {}
+        ctx = _context(m, mode, src.device_index, emulation=emulation, **kw)
         import torch
 
         stream = torch.cuda.current_stream(src.device_index).cuda_stream

@@ -301,8 +301,31 @@ def test_pivoted_ldl_matches_reference_golden(golden, name):
         np.testing.assert_array_equal(res.prefix_signs, ref["signs"], err_msg=f"{name} {key}")
         assert rel_err(res.prefix, ref["prefix"]) <= tol, (name, key, rel_err(res.prefix, ref["prefix"]))
         assert res.prefix.dtype == inp.dtype
-        assert (res.info.ooc_reads, res.info.ooc_writes, res.info.ooc_scratch) == \
+        assert (res.info.blocks_read, res.info.blocks_written, res.info.scratch_slots) == \
             (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
+        if res.info.out_of_core:  # the block walk makes exactly the reference's transfers
+            assert (res.info.ooc_reads, res.info.ooc_writes, res.info.ooc_scratch) == \
+                (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
+
+
+@pytest.mark.parametrize("m,nb", [(1024, 4), (1022, 4), (1280, 5), (768, 2), (2048, 8), (700, 1)])
+def test_pivoted_ldl_in_core_equals_block_walk(m, nb):
+    """Tile-aligned reference blocks run in core (the matrix resident, one large update per
+    stage, the next block's factor overlapped); every tile gets the walk's updates with the same
+    operands and K, so perm, D and the prefixes equal the out-of-core block walk's bit for bit,
+    and the walk makes the reference's transfers."""
+    a = gen.random_symmetric(m, seed=m + nb)
+    res = eng.memdet_ldl(a, num_blocks=nb)
+    walk = eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
+    assert not res.info.out_of_core and walk.info.out_of_core
+    np.testing.assert_array_equal(res.perm, walk.perm)
+    np.testing.assert_array_equal(res.prefix_signs, walk.prefix_signs)
+    assert np.array_equal(res.prefix.view(np.int64), walk.prefix.view(np.int64)), \
+        np.max(np.abs(res.prefix - walk.prefix))
+    ref_perm, ref_prefix, ref_signs, rinfo = O.memdet_ldl(a, nb)
+    np.testing.assert_array_equal(res.perm, ref_perm)
+    assert rel_err(res.prefix, ref_prefix) <= 1e-10
+    assert (walk.info.ooc_reads, walk.info.ooc_writes) == (rinfo.blocks_read, rinfo.blocks_written)
 
 
 def _ldl_block_input(m, kind):
@@ -322,16 +345,21 @@ def _ldl_block_input(m, kind):
     raise ValueError(kind)
 
 
-@pytest.mark.parametrize("panel", ["cluster", "single_cta"])
+@pytest.mark.parametrize("panel", ["cluster", "single_cta", "persistent"])
 @pytest.mark.parametrize("m,kind", [(31, "sym"), (33, "sym"), (100, "sym"), (257, "sym"), (700, "sym"),
                                     (600, "rbf"), (320, "blocks"), (400, "int")])
 def test_pivoted_ldl_diagonal_block_bit_identical_to_reference_kernel(m, kind, panel, monkeypatch):
     """One diagonal block (num_blocks=1): the blocked panel / delayed-update kernels reproduce the
     reference's unblocked loop (_ldl.pyx:21-61, restated in oracle/ldl_tile.c) bit for bit:
-    the same interchanges and the same pivots d, across panel boundaries and exact ties; both
-    panel kernels (16-CTA cluster, and the one-CTA kernel used above 6144 rows)."""
+    the same interchanges and the same pivots d, across panel boundaries and exact ties; all
+    three forms (per-panel 16-CTA cluster kernels, the one-launch cluster factor used beside
+    the trailing updates, and the one-CTA kernel used above 6144 rows)."""
     if panel == "single_cta":
         monkeypatch.setenv("B2D_LDL_SINGLE_CTA", "1")
+    if panel == "persistent":
+        monkeypatch.setenv("B2D_LDL_PERSIST", "2")
+    else:
+        monkeypatch.setenv("B2D_LDL_PERSIST", "0")
     a = _ldl_block_input(m, kind)
     ctx = _native.Context(m, _native.MODE_LDL_PIV, num_blocks=1)
     ctx.factor_host_async(a.ctypes.data, m, _native.B2D_F64, 0)

@@ -108,5 +108,42 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 6; ++i) printf("  %-14s %8.0f cyc/step\n", names[i], (double)prof[i] / n);
     printf("  total          %8.0f cyc/step\n", (double)tot / n);
   }
+  // the one-launch cluster factor
+  CK(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const size_t fsm = ldl_factor_smem((int)((n + LC - 1) / LC));
+  CK(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+  for (int rep = 0; rep < 2; ++rep) {
+    CK(cudaMemcpy(A, h.data(), n * n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemset(tag, 0, n * n));
+    CK(cudaMemset(fail, 0xff, 8));
+    long long zero[16] = {0};
+    CK(cudaMemcpyToSymbol(ldl_prof, zero, sizeof(zero)));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = LC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(LC);
+    cfg.blockDim = dim3(LC_THREADS);
+    cfg.dynamicSmemBytes = fsm;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaEventRecord(e0);
+    CK(cudaLaunchKernelEx(&cfg, ldl_factor_cluster_kernel, g));
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long prof[16];
+    CK(cudaMemcpyFromSymbol(prof, ldl_prof, sizeof(prof)));
+    std::vector<double> dd(n);
+    CK(cudaMemcpy(dd.data(), d, n * 8, cudaMemcpyDeviceToHost));
+    double ld_sum = 0;
+    for (double v : dd) ld_sum += log(fabs(v));
+    printf("one-launch factor n=%lld: %.2f ms  logabsdet %.10e\n", (long long)n, ms, ld_sum);
+    const char* fn[5] = {"panel steps", "writeback+sync", "store/swap", "bulk", "sync"};
+    for (int i = 0; i < 5; ++i) printf("  %-16s %8.2f ms (CTA 0 @1.9GHz)\n", fn[i], prof[9 + i] / 1.9e6);
+  }
   return 0;
 }
