@@ -1206,10 +1206,11 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   c->launches += 1;
   // B2D_LDL_SINGLE_CTA forces the one-CTA panel kernel (the path for blocks above 16*384 rows)
   const bool single_cta = getenv("B2D_LDL_SINGLE_CTA") != nullptr;
-  // B2D_LDL_PERSIST: 0 = per-panel kernels always; 1 (default) = the one-launch cluster factor
-  // when the factor runs beside other work (it holds its SMs); 2 = always
+  // B2D_LDL_PERSIST: 0 (default) = per-panel kernels; 1 = the one-launch cluster factor when
+  // the factor runs beside other work (it holds its 16 SMs, but its bulk updates run on those
+  // 16 SMs only: 58 ms vs 23 ms alone at b = 4096, so it loses at C2); 2 = always
   const char* pe = getenv("B2D_LDL_PERSIST");
-  const int persist = pe ? atoi(pe) : 1;
+  const int persist = pe ? atoi(pe) : 0;
   if (n <= (int64_t)LC * LC_RMAX && !single_cta && (persist == 2 || (persist == 1 && overlapped))) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1679,11 +1680,10 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     cudaEventRecord(o.ev_diag, c->s_mid);
     cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
     tmark("factor-begin", k + 1, c->s_main);
-    // B2D_LDL_SCHED: 1 (default) = the next factor alone on the GPU (per-panel kernels), then the
-    // rest update beside the next panel solve; 0 = the factor beside the rest update (one-launch
-    // cluster factor)
+    // B2D_LDL_SCHED: 0 (default) = the next factor beside the rest update; 1 = the factor alone
+    // on the GPU, then the rest update beside the next panel solve (measured slower at C2)
     const char* se = getenv("B2D_LDL_SCHED");
-    const bool serial = se ? atoi(se) != 0 : true;
+    const bool serial = se ? atoi(se) != 0 : false;
     if ((rc = ldl_factor_block(c, diag_map(k + 1), k + 1, c->s_main, !serial && i0 + kb1 < nt))) return rc;
     tmark("factor-end", k + 1, c->s_main);
     cudaEventRecord(c->ev_catch[k + 1], c->s_main);

@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0,
 constexpr int LDL_BT = 64;
 __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int nbk, int64_t b, double* sC,
                                               double* sW) {
-  const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld;
+  const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld, n = g.n;
   int64_t bj = 0;
   const int64_t nbt = (m + LDL_BT - 1) / LDL_BT;
   while (b >= nbt - bj) { b -= nbt - bj; ++bj; }
@@ -629,50 +629,94 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   const int64_t i0 = re + bi * LDL_BT, j0 = re + bj * LDL_BT;
   for (int e = threadIdx.x; e < nbk * LDL_BT; e += 256) {
     const int q = e / LDL_BT, x = e % LDL_BT;
-    sC[q * LDL_BT + x] = i0 + x < g.n ? __ldcg(g.C + q * ld + i0 + x) : 0.0;
-    sW[q * LDL_BT + x] = j0 + x < g.n ? __ldcg(g.W + q * ld + j0 + x) : 0.0;
+    sC[q * LDL_BT + x] = i0 + x < n ? __ldcg(g.C + q * ld + i0 + x) : 0.0;
+    sW[q * LDL_BT + x] = j0 + x < n ? __ldcg(g.W + q * ld + j0 + x) : 0.0;
   }
-  __syncthreads();
+  // thread (tx, ty): rows i0 + 4 tx + a, columns j0 + 4 ty + c (a, c < 4)
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t ib = i0 + 4 * tx, jb = j0 + 4 * ty;
+  // interior off-diagonal tiles: vector loads / stores (i0 is a multiple of 32, ld of 128)
+  const bool vec = bi > bj && i0 + LDL_BT <= n && j0 + LDL_BT <= n;
   double v[4][4];
-  int tg[4][4];
+  uint32_t tw[4];  // tags of the 4 rows of column c, one byte each
+  bool tagged = false;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int c = 0; c < 4; ++c) {
+    const int64_t j = jb + c;
+    if (vec) {
+      const double2* p = reinterpret_cast<const double2*>(g.A + j * ld + ib);
+      const double2 x0 = __ldcg(p), x1 = __ldcg(p + 1);
+      v[0][c] = x0.x;
+      v[1][c] = x0.y;
+      v[2][c] = x1.x;
+      v[3][c] = x1.y;
+      tw[c] = __ldcg(reinterpret_cast<const unsigned int*>(g.tag + j * ld + ib));
+    } else {
+      tw[c] = 0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int64_t i = i0 + tx + 16 * a, j = j0 + ty + 16 * c;
-      const bool ok = i < g.n && j < g.n && i >= j;
-      v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
-      tg[a][c] = ok ? __ldcg(g.tag + j * ld + i) : 255;
-    }
-  for (int q = 0; q < nbk; ++q) {
-    double cc[4], ww[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) cc[a] = sC[q * LDL_BT + tx + 16 * a];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) ww[c] = sW[q * LDL_BT + ty + 16 * c];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (q >= tg[a][c]) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int64_t i = i0 + tx + 16 * a, j = j0 + ty + 16 * c;
-      if (i < g.n && j < g.n && i >= j) {
-        g.A[j * ld + i] = v[a][c];
-        if (tg[a][c]) g.tag[j * ld + i] = 0;
+      for (int a = 0; a < 4; ++a) {
+        const int64_t i = ib + a;
+        const bool ok = i < n && j < n && i >= j;
+        v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
+        tw[c] |= (uint32_t)(ok ? __ldcg(g.tag + j * ld + i) : 0) << (8 * a);
       }
     }
+    tagged |= tw[c] != 0;
+  }
+  __syncthreads();
+  if (!__any_sync(0xffffffffu, tagged)) {
+    // no entry of the warp holds any of the panel's steps: every term applies
+    for (int q = 0; q < nbk; ++q) {
+      const double2 c01 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx);
+      const double2 c23 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx + 2);
+      const double2 w01 = *reinterpret_cast<const double2*>(sW + q * LDL_BT + 4 * ty);
+      const double2 w23 = *reinterpret_cast<const double2*>(sW + q * LDL_BT + 4 * ty + 2);
+      const double cc[4] = {c01.x, c01.y, c23.x, c23.y}, ww[4] = {w01.x, w01.y, w23.x, w23.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
+    }
+  } else {
+    for (int q = 0; q < nbk; ++q) {
+      double cc[4], ww[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) cc[a] = sC[q * LDL_BT + 4 * tx + a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) ww[c] = sW[q * LDL_BT + 4 * ty + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (q >= (int)((tw[c] >> (8 * a)) & 0xffu)) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int64_t j = jb + c;
+    if (vec) {
+      double2* p = reinterpret_cast<double2*>(g.A + j * ld + ib);
+      p[0] = make_double2(v[0][c], v[1][c]);
+      p[1] = make_double2(v[2][c], v[3][c]);
+      if (tw[c]) *reinterpret_cast<unsigned int*>(g.tag + j * ld + ib) = 0u;
+    } else {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t i = ib + a;
+        if (i < n && j < n && i >= j) {
+          g.A[j * ld + i] = v[a][c];
+          if ((tw[c] >> (8 * a)) & 0xffu) g.tag[j * ld + i] = 0;
+        }
+      }
+    }
+  }
   __syncthreads();  // sC / sW reused by the next tile
 }
 
 __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;
-  __shared__ double sC[LDL_NB * LDL_BT], sW[LDL_NB * LDL_BT];
+  __shared__ __align__(16) double sC[LDL_NB * LDL_BT];
+  __shared__ __align__(16) double sW[LDL_NB * LDL_BT];
   // the first tile-column (the next panel's columns) last, so that it is L2-resident when the
   // next panel kernel reads it
   ldl_bulk_tile(g, r0, nbk, (int64_t)gridDim.x - 1 - blockIdx.x, sC, sW);
@@ -684,7 +728,7 @@ __global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, in
 // runs beside the trailing DMMA updates of the previous stage at full speed (the per-panel
 // kernels would each wait for SMs there).  Same arithmetic as the per-panel kernels.
 __host__ __device__ constexpr size_t ldl_factor_smem(int rows) {
-  return ((size_t)rows + (2 * (size_t)rows * LC_LD > 2 * (size_t)LDL_NB * LDL_BT ? 2 * (size_t)rows * LC_LD
+  return ((size_t)rows + 1 + (2 * (size_t)rows * LC_LD > 2 * (size_t)LDL_NB * LDL_BT ? 2 * (size_t)rows * LC_LD
                                                                                   : 2 * (size_t)LDL_NB * LDL_BT)) * 8;
 }
 __global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlArgs g) {
@@ -695,7 +739,7 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlAr
   const int64_t n = g.n, ld = g.ld;
   const int R = (int)((n + LC - 1) / LC);
   double* dg = sm;                      // [R] eager diagonal (kept across panels)
-  double* Cs = dg + R;                  // [R][LC_LD] (panel phase) / bulk staging C
+  double* Cs = dg + ((R + 1) & ~1);     // [R][LC_LD] (panel phase) / bulk staging C (16-byte aligned)
   double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
   double* sC = Cs;                      // bulk phase: [NB][BT] x 2
   double* sW = Cs + LDL_NB * LDL_BT;
