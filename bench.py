@@ -291,6 +291,41 @@ def run_engine(args):
                                              "products per FP64 multiply-add (not measured)",
                               "launches": oz_launches, "kernel_ms": oz_ms}}
 
+    # the second entry point of the path: memdet_ldl with the reference's block-local 1x1 pivoting
+    # (num_blocks=8: b = 4096, bit-identical pivots), in core, device-resident input
+    ldl = None
+    if not args.no_ldl:
+        lctx = _native.Context(n, _native.MODE_LDL_PIV, local, num_blocks=C2["num_blocks"])
+        lprefix = np.empty(n)
+
+        def lstep():
+            lctx.factor_device_async(a.data_ptr(), n, _native.B2D_F64, sptr)
+
+        for _ in range(max(1, args.warmup)):
+            lstep()
+            rc, _, linfo = lctx.fetch(None, lprefix)
+            _native.check(rc, "ldl warmup")
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            lstep()
+        e1.record(stream)
+        barrier()
+        lms = e0.elapsed_time(e1) / args.steps
+        rc, _, linfo = lctx.fetch(None, lprefix)
+        _native.check(rc, "ldl steps")
+        lperm = np.empty(n, np.int64)
+        lctx.fetch_perm(lperm)
+        l_in_core = not lctx.out_of_core
+        lctx.close()
+        ldl = {"value": flops / (lms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": lms,
+               "frac_of_fp64_peak": flops / (lms * 1e-3) / 1e12 / peak,
+               "config": {"num_blocks": C2["num_blocks"], "pivoting": "block-local 1x1 (reference _ldl.pyx)",
+                          "in_core": l_in_core},
+               "logdet": float(lprefix[-1]), "logdet_rel_diff_vs_cholesky": abs(float(lprefix[-1]) - logdet) / abs(logdet),
+               "interchanged_rows": int(np.sum(lperm != np.arange(n))),
+               "gpu_launches": int(linfo.kernel_launches) * args.steps}
+
     # e2e through the public API from pinned host memory
     pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
     pinned.copy_(a)
@@ -323,6 +358,18 @@ def run_engine(args):
         ozaki["e2e"] = {"value": flops / osec / 1e12, "unit": UNIT, "seconds_per_step": osec, "steps": e2e_steps,
                         "api": "paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks=8, schur='ozaki')",
                         "logdet": ores.logabsdet}
+    if ldl is not None:
+        eng.memdet_ldl(host, num_blocks=C2["num_blocks"])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            lres = eng.memdet_ldl(host, num_blocks=C2["num_blocks"])
+        lsec = (time.perf_counter() - t0) / e2e_steps
+        eng.release_engine_cache()
+        ldl["e2e"] = {"value": flops / lsec / 1e12, "unit": UNIT, "seconds_per_step": lsec, "steps": e2e_steps,
+                      "h2d_bytes_per_step": int(lres.info.h2d_bytes), "d2h_bytes_per_step": int(lres.info.d2h_bytes),
+                      "api": "paper_2503_04424_b200.memdet_ldl(pinned host ndarray, num_blocks=8)",
+                      "logdet": lres.logabsdet}
 
     out = None
     if rank == 0:
@@ -376,6 +423,7 @@ def run_engine(args):
                     "logdet": e2e_logdet},
             "gpu_launches": launches_per_step * args.steps,
             "ozaki": ozaki,
+            "ldl": ldl,
             "clocks": clocks.summary(),
         }
     if ws > 1:
@@ -513,6 +561,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ozaki", action="store_true", help="skip the opt-in int8-emulated Schur line")
+    ap.add_argument("--no-ldl", action="store_true", help="skip the memdet_ldl (block-pivoted) line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
