@@ -898,7 +898,8 @@ static void plan_bands(Ctx* c, size_t esz) {
   make_bounds(c, nt, true);
   const int nbands = (nt + BAND - 1) / BAND;
   const int nsteps = (int)c->bounds.size() - 1;
-  const double m = (double)c->m, pcie = 48e9, rate = 34e12, chain_rate = 20e12;
+  const double m = (double)c->m, rate = 34e12, chain_rate = 20e12;
+  const double pcie = getenv("B2D_PCIE_GBS") ? atof(getenv("B2D_PCIE_GBS")) * 1e9 : 48e9;
   const double col_lat = getenv("B2D_COL_LAT_US") ? atof(getenv("B2D_COL_LAT_US")) * 1e-6 : 900e-6;
   const double tile_flops = 2.0 * T * T * T;
   std::vector<double> arrival(nbands);
