@@ -97,6 +97,7 @@ struct Ooc {
   // current stage's solves and Schur updates run on s_work, so the per-stage outputs of the
   // factor (tile inverses, block permutation, D) are double-buffered by stage parity
   double* inv_odd = nullptr;
+  double* inv2_odd = nullptr;
   int64_t* perm_odd = nullptr;
   double* dblk_odd = nullptr;
   cudaStream_t s_work = nullptr;  // block-walk solves / updates: s_main, or s_mid under look-ahead
@@ -162,6 +163,15 @@ struct Ctx {
   // full-height grids of nt x nbt tiles, unscaled and D^{-1}-scaled, double-buffered by stage
   bool ldl_ic = false;
   double* pan[2][2] = {};  // [stage parity][0: unscaled, 1: scaled]
+  // generic LU in core (the same conditions): the matrix as a full nt x nt tile grid; per stage
+  // parity the column panel X, the transposed row panel Y^T and a transpose buffer (nt x nbt
+  // tiles each, rows = global tile index), and the U^T factor of the diagonal block
+  bool lu_ic = false;
+  double* grid = nullptr;
+  double* lpan[2][3] = {};
+  double* ublk[2] = {};
+  double* bstage[2] = {};                     // host ingest: one reference block each
+  std::vector<cudaEvent_t> ev_bstage, ev_cross;  // staging buffer free; stage k's blocks packed
 };
 
 static int configure_kernels() {
@@ -214,6 +224,9 @@ static void destroy(Ctx* c) {
   cudaFree(c->fail);
   if (c->s_copy) cudaStreamSynchronize(c->s_copy);
   for (auto* p : c->strip) cudaFree(p);
+  for (auto* p : c->bstage) cudaFree(p);
+  for (auto* v : {&c->ev_bstage, &c->ev_cross})
+    for (auto e : *v) cudaEventDestroy(e);
   cudaFree(c->gram_neg);
   cudaFree(c->gram_pos);
   for (int b = 0; b < 2; ++b) {
@@ -256,7 +269,12 @@ static void destroy(Ctx* c) {
   cudaFree(o.inv2);
   for (auto& pp : c->pan)
     for (double* q : pp) cudaFree(q);
+  for (auto& pp : c->lpan)
+    for (double* q : pp) cudaFree(q);
+  for (double* q : c->ublk) cudaFree(q);
+  cudaFree(c->grid);
   cudaFree(o.inv_odd);
+  cudaFree(o.inv2_odd);
   cudaFree(o.perm_odd);
   cudaFree(o.dblk_odd);
   for (cudaEvent_t e : {o.ev_fac, o.ev_diag, o.ev_work})
@@ -408,6 +426,18 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   // must start on tile boundaries; needs the packed triangle plus four nt x nbt panel grids and
   // the dense block state
   int64_t ic_nb = 0, ic_b = 0, ic_tail = 0;
+  if (mode == B2D_MODE_LU && !(opt && opt->force_out_of_core)) {
+    int64_t nb0 = 1;
+    if (opt && opt->num_blocks > 0) nb0 = opt->num_blocks;
+    else if (opt && opt->max_mem > 0) nb0 = ref_select_blocking(m, opt->max_mem, 8);
+    ref_layout(m, std::max<int64_t>(1, nb0), &ic_nb, &ic_b, &ic_tail);
+    const int64_t bt = (ic_b + T - 1) / T, ldb = bt * T;
+    const size_t ic_need = (size_t)nt_full * nt_full * TILE_BYTES + 6 * (size_t)nt_full * bt * TILE_BYTES +
+                           (size_t)(nt_full + 5 * bt) * TILE_BYTES + (size_t)ldb * ldb * 8 +
+                           3 * (size_t)npad_full * 8 + (size_t)NSTAGE * T * npad_full * 8 + (size_t)(m + 8 * ldb) * 8;
+    // the cluster LU panel holds the block's rows in distributed shared memory
+    if ((ic_b % T == 0 || ic_nb == 1) && ic_b <= (int64_t)LC * LC_RMAX && ic_need <= budget) force = false;
+  }
   if (mode == B2D_MODE_LDL_PIV && !(opt && opt->force_out_of_core)) {
     int64_t nb0 = 1;
     if (opt && opt->num_blocks > 0) nb0 = opt->num_blocks;
@@ -434,7 +464,34 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   bool oz = opt && opt->emulation == 1;
   if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
   const size_t oz_need = oz ? 2 * ((size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4) : 0;
-  if (!force && mode == B2D_MODE_LDL_PIV) {
+  if (!force && mode == B2D_MODE_LU) {
+    Ooc& o = c->o;
+    c->lu_ic = true;
+    c->nt = nt_full;
+    o.nb = (int)ic_nb;
+    o.b = ic_b;
+    o.tail = ic_tail;
+    o.nbt = (int)((ic_b + T - 1) / T);
+    const int64_t ld = (int64_t)o.nbt * T;
+    ALLOC(c->grid, (size_t)c->nt * c->nt * TILE_BYTES);
+    ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
+    for (auto& pp : c->lpan)
+      for (double*& q : pp) ALLOC(q, (size_t)c->nt * o.nbt * TILE_BYTES);
+    for (double*& q : c->ublk) ALLOC(q, (size_t)o.nbt * o.nbt * TILE_BYTES);
+    ALLOC(o.dense, (size_t)ld * ld * 8);
+    ALLOC(o.swaps, (size_t)ld * 8);
+    ALLOC(o.perm_local, (size_t)ld * 8);
+    ALLOC(o.perm_global, (size_t)(m + ld) * 8);
+    ALLOC(o.dblk, (size_t)ld * 8);
+    ALLOC(o.inv2, (size_t)o.nbt * TILE_BYTES);
+    ALLOC(o.inv_odd, (size_t)o.nbt * TILE_BYTES);
+    ALLOC(o.inv2_odd, (size_t)o.nbt * TILE_BYTES);
+    ALLOC(o.perm_odd, (size_t)ld * 8);
+    ALLOC(o.dblk_odd, (size_t)ld * 8);
+    cudaEventCreateWithFlags(&o.ev_fac, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_diag, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_work, cudaEventDisableTiming);
+  } else if (!force && mode == B2D_MODE_LDL_PIV) {
     Ooc& o = c->o;
     c->ldl_ic = true;
     c->nt = nt_full;
@@ -849,6 +906,7 @@ static void end(Ctx* c, cudaStream_t user) {
 }
 
 static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
+static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
 
 static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
@@ -856,6 +914,7 @@ static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStre
   if (c->ooc)
     return set_err(B2D_ERR_UNSUPPORTED, "out-of-core contexts take host inputs (the matrix exceeds the HBM budget)");
   if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, false, user);
+  if (c->lu_ic) return run_lu_incore(c, a, lda, dtype, false, user);
   CUDA_TRY(cudaSetDevice(c->device));
   begin(c, user);
   const unsigned ntiles = (unsigned)n_packed_tiles(c->nt);
@@ -990,6 +1049,7 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   if (c->ooc) return run_ooc(c, a, lda, dtype, user);
   if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, true, user);
+  if (c->lu_ic) return run_lu_incore(c, a, lda, dtype, true, user);
   CUDA_TRY(cudaSetDevice(c->device));
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
@@ -1275,17 +1335,17 @@ static int ooc_ldl_factor(Ctx* c, int sa, int k, cudaStream_t s) {
 // dense copy, blocked LU with block-local partial pivoting, pivots / permutation / log|u_ii|,
 // then L (unit lower) back into slot sa and U^T (lower) into slot su with the inverses of
 // their diagonal tiles for the row-block and column-block solves.
-static int ooc_lu_factor(Ctx* c, int sa, int su, int k) {
+static int lu_factor_block(Ctx* c, const TileMap& blk, const TileMap& umap, int k, cudaStream_t s) {
   Ooc& o = c->o;
   const int nt = o.tiles(k);
   const int64_t n = o.size(k);
   const int64_t ld = (int64_t)o.nbt * T, g0 = (int64_t)k * o.b;
-  cudaStream_t s = c->s_main;
-  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
-  cudaStreamWaitEvent(s, o.ev_used[su], 0);
-  cudaStreamWaitEvent(s, o.ev_stored[su], 0);
-  unpack_block_kernel<<<(unsigned)(nt * nt), 256, 0, s>>>(o.map(sa), nt, o.dense, ld, 0);
-  const LuArgs g{o.dense, o.dblk, o.swaps, c->fail, ld, n, g0};
+  double* dblk = o.dblk_of(k);
+  int64_t* perm = o.perm_of(k);
+  double* inv = (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
+  double* inv2 = (k & 1) && o.inv2_odd ? o.inv2_odd : o.inv2;
+  unpack_block_kernel<<<(unsigned)(nt * nt), 256, 0, s>>>(blk, nt, o.dense, ld, 0);
+  const LuArgs g{o.dense, dblk, o.swaps, c->fail, ld, n, g0};
   const int cols_grid = (int)std::max<int64_t>(1, (n + 255) / 256);
   for (int64_t r0 = 0; r0 < n; r0 += LU_NB) {
     const int nbk = (int)std::min<int64_t>(LU_NB, n - r0);
@@ -1312,17 +1372,27 @@ static int ooc_lu_factor(Ctx* c, int sa, int su, int k) {
     c->launches += rest > 0 ? 4 : 2;
   }
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
-                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, o.dblk, n, g0, o.perm_local,
+                      n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,
                                                                         o.perm_global, c->ell, c->diag);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
-  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(sa), nt);
-  pack_upper_t_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, o.map(su), nt);
-  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(sa), c->inv);
-  tile_inv_lower_kernel<<<nt, T, T * 129 * 8, s>>>(o.map(su), o.inv2);
+  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, blk, nt);
+  pack_upper_t_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, umap, nt);
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv);
+  tile_inv_lower_kernel<<<nt, T, T * 129 * 8, s>>>(umap, inv2);
   c->launches += 7;
+  return B2D_OK;
+}
+
+static int ooc_lu_factor(Ctx* c, int sa, int su, int k) {
+  Ooc& o = c->o;
+  cudaStream_t s = c->s_main;
+  cudaStreamWaitEvent(s, o.ev_loaded[sa], 0);
+  cudaStreamWaitEvent(s, o.ev_used[su], 0);
+  cudaStreamWaitEvent(s, o.ev_stored[su], 0);
+  const int rc = lu_factor_block(c, o.map(sa), o.map(su), k, s);
   cudaEventRecord(o.ev_used[sa], s);
   cudaEventRecord(o.ev_used[su], s);
-  return B2D_OK;
+  return rc;
 }
 
 // One visit of the reference's generic walk, stage k (memdet.py:97-121): rows bottom-up, the
@@ -1717,6 +1787,187 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     }
     for (auto& e : tev) cudaEventDestroy(e.second);
   }
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+// Generic LU in core (memdet_lu; memdet.py:268-319, kernels/dense.py:38-54, 94-106): the
+// reference's stages over its b x b blocks with the matrix resident as a full tile grid.  Stage
+// k: the diagonal block is factored P A = L U with block-local partial pivoting (s_main; L back
+// into the grid's diagonal block, U^T into a block grid); the column panel X = A(i, k) U^{-1}
+// and the transposed, permuted row panel Y^T = (P A(k, j))^T L^{-T} are formed in full-height
+// panel grids (s_mid); block column and block row k+1 are updated first so the next factor
+// starts at once, and the rest of the trailing square takes one DMMA update T -= X Y (s_side)
+// beside it.  The same kernels, operands and K per tile as the generic block walk.
+static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user) {
+  if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
+  if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  Ooc& o = c->o;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int nt = c->nt, nb = o.nb;
+  const size_t esz = dtype == B2D_F64 ? 8 : 4;
+  const TileMap full{c->grid, nt, 0};
+  begin(c, user);
+  // ingest, reference block by block in the stages' cross order -- (k, k), block row k, block
+  // column k -- so that stage k starts once its blocks are in: ev_cross[k] after the last of
+  // them; ev_diag_in = block (0, 0) (the first factor starts on it alone).  Host blocks go
+  // through two staging buffers (2D copies of b x b, then pack_block_nt per 128-row strip).
+  auto col0 = [&](int k) { return (int)((int64_t)k * o.b / T); };
+  const int64_t ldb = (int64_t)o.nbt * T;
+  if (host) {
+    for (auto*& q : c->bstage)
+      if (!q) CUDA_TRY(cudaMalloc(&q, (size_t)ldb * ldb * 8));
+  }
+  if ((int)c->ev_cross.size() < nb) {
+    while ((int)c->ev_cross.size() < nb) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      c->ev_cross.push_back(e);
+    }
+    while (c->ev_bstage.size() < 2) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      c->ev_bstage.push_back(e);
+    }
+  }
+  int nblk = 0;
+  auto ingest = [&](int I, int J) -> int {
+    const int64_t rows = o.size(I), cols = o.size(J);
+    const TileMap dst{c->grid + ((size_t)col0(I) * nt + col0(J)) * TILE_ELEMS, nt, 0};
+    const char* src;
+    int64_t sld;
+    if (host) {
+      const int sb = nblk & 1;
+      if (nblk >= 2) cudaStreamWaitEvent(c->s_copy, c->ev_bstage[sb], 0);
+      CUDA_TRY(cudaMemcpy2DAsync(c->bstage[sb], (size_t)ldb * esz,
+                                 (const char*)a + ((size_t)I * o.b * lda + (size_t)J * o.b) * esz, (size_t)lda * esz,
+                                 (size_t)cols * esz, (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+      cudaEventRecord(c->ev_copied[sb], c->s_copy);
+      cudaStreamWaitEvent(c->s_pack, c->ev_copied[sb], 0);
+      c->h2d += rows * cols * (int64_t)esz;
+      src = (const char*)c->bstage[sb];
+      sld = ldb;
+    } else {
+      src = (const char*)a + ((size_t)I * o.b * lda + (size_t)J * o.b) * esz;
+      sld = lda;
+    }
+    for (int r = 0; r < o.tiles(I); ++r) {
+      const char* sr = src + (size_t)r * T * sld * esz;
+      if (dtype == B2D_F64)
+        pack_block_nt_kernel<double><<<o.tiles(J), 256, 0, c->s_pack>>>((const double*)sr, sld, rows, cols, I == J,
+                                                                         dst, r);
+      else
+        pack_block_nt_kernel<float><<<o.tiles(J), 256, 0, c->s_pack>>>((const float*)sr, sld, rows, cols, I == J,
+                                                                        dst, r);
+      c->launches++;
+    }
+    if (host) cudaEventRecord(c->ev_bstage[nblk & 1], c->s_pack);
+    ++nblk;
+    return B2D_OK;
+  };
+  int rc = 0;
+  if (host) {
+    for (int k = 0; k < nb; ++k) {
+      if ((rc = ingest(k, k))) return rc;
+      if (k == 0) cudaEventRecord(o.ev_fac, c->s_pack);  // block (0, 0)
+      for (int j = k + 1; j < nb; ++j)
+        if ((rc = ingest(k, j))) return rc;
+      for (int i = k + 1; i < nb; ++i)
+        if ((rc = ingest(i, k))) return rc;
+      cudaEventRecord(c->ev_cross[k], c->s_pack);
+    }
+  } else {  // resident: one pack launch per 128-row strip
+    for (int J = 0; J < nt; ++J) {
+      const char* sr = (const char*)a + (size_t)J * T * lda * esz;
+      if (dtype == B2D_F64)
+        pack_block_nt_kernel<double><<<nt, 256, 0, c->s_pack>>>((const double*)sr, lda, c->m, c->m, 1, full, J);
+      else
+        pack_block_nt_kernel<float><<<nt, 256, 0, c->s_pack>>>((const float*)sr, lda, c->m, c->m, 1, full, J);
+      c->launches++;
+    }
+    cudaEventRecord(o.ev_fac, c->s_pack);
+    for (int k = 0; k < nb; ++k) cudaEventRecord(c->ev_cross[k], c->s_pack);
+  }
+  auto blk = [&](int k) { return TileMap{c->grid + ((size_t)col0(k) * nt + col0(k)) * TILE_ELEMS, nt, 0}; };
+  auto umap = [&](int k) { return TileMap{c->ublk[k & 1], o.nbt, 0}; };
+  cudaStreamWaitEvent(c->s_main, o.ev_fac, 0);
+  if ((rc = lu_factor_block(c, blk(0), umap(0), 0, c->s_main))) return rc;
+  cudaEventRecord(c->ev_catch[0], c->s_main);
+  for (int k = 0; k + 1 < nb; ++k) {
+    const int par = k & 1;
+    const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb, R = nt - i0, kb1 = o.tiles(k + 1);
+    const double* inv_l = par && o.inv_odd ? o.inv_odd : c->inv;
+    const double* inv_u = par && o.inv2_odd ? o.inv2_odd : o.inv2;
+    cudaStreamWaitEvent(c->s_mid, c->ev_catch[k], 0);
+    if (k >= 2) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 2], 0);  // last reader of lpan[par]
+    cudaStreamWaitEvent(c->s_mid, c->ev_cross[k], 0);                 // block row / column k in
+    const size_t poff = (size_t)i0 * o.nbt * TILE_ELEMS;
+    const TileMap X{c->lpan[par][0] + poff, o.nbt, 0}, Yt{c->lpan[par][1] + poff, o.nbt, 0},
+        Tt{c->lpan[par][2] + poff, o.nbt, 0};
+    // X = A(i, k) U^{-1} (dense.py:102-106): tile rows [i0, nt) of block column k
+    CUDA_TRY(cudaMemcpy2DAsync(c->lpan[par][0] + poff, (size_t)o.nbt * TILE_BYTES,
+                               c->grid + ((size_t)i0 * nt + k0) * TILE_ELEMS, (size_t)nt * TILE_BYTES,
+                               (size_t)kb * TILE_BYTES, (size_t)R, cudaMemcpyDeviceToDevice, c->s_mid));
+    trsm_panel(c, c->s_mid, X, R, umap(k), kb, inv_u);
+    // Y^T = (P A(k, j))^T L^{-T} (dense.py:94-99, memdet.py:365-366): block row k transposed,
+    // its (block-local) rows permuted, solved with the unit L
+    transpose_block_kernel<<<(unsigned)(kb * R), 256, TRANSPOSE_SMEM, c->s_mid>>>(
+        TileMap{c->grid + ((size_t)k0 * nt + i0) * TILE_ELEMS, nt, 0}, Tt, kb, R);
+    permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(Tt, Yt, R, kb, o.size(k), o.perm_of(k));
+    trsm_panel(c, c->s_mid, Yt, R, blk(k), kb, inv_l);
+    c->launches += 2;
+    cudaEventRecord(c->ev_panel[k], c->s_mid);
+    // T(i, j) -= X_i Y_j (dense.py:109-116, "ct_b"): block column and block row k+1 first
+    GemmTask u{};
+    u.a = TileMap{c->lpan[par][0], o.nbt, 0};  // rows indexed by global tile row
+    u.b = TileMap{c->lpan[par][1], o.nbt, 0};  // rows indexed by global tile column
+    u.c = full;
+    u.p0 = 0;
+    u.p1 = kb;
+    const double K = (double)kb * T;
+    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 1], 0);
+    cudaStreamWaitEvent(c->s_mid, c->ev_cross[k + 1], 0);
+    u.out = TileSet{i0, nt, i0, i0 + kb1, 0, 0};
+    launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+    if (i0 + kb1 < nt) {
+      u.out = TileSet{i0, i0 + kb1, i0 + kb1, nt, 0, 0};
+      launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+    }
+    cudaEventRecord(o.ev_diag, c->s_mid);
+    cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+    if ((rc = lu_factor_block(c, blk(k + 1), umap(k + 1), k + 1, c->s_main))) return rc;
+    cudaEventRecord(c->ev_catch[k + 1], c->s_main);
+    if (i0 + kb1 < nt) {
+      cudaStreamWaitEvent(c->s_side, o.ev_diag, 0);
+      if (k > 0 || !host) {
+        cudaStreamWaitEvent(c->s_side, c->ev_cross[nb - 1], 0);
+        u.out = TileSet{i0 + kb1, nt, i0 + kb1, nt, 0, 0};
+        launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+      } else {
+        // stage 0 runs while the matrix streams in: the rest of the trailing square in the
+        // cross sets of the later stages (block (s, s), row s, column s), each as it arrives
+        for (int st = 2; st < nb; ++st) {
+          const int s0 = col0(st), s1 = s0 + o.tiles(st);
+          cudaStreamWaitEvent(c->s_side, c->ev_cross[st], 0);
+          u.out = TileSet{s0, s1, s0, nt, 0, 0};
+          launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+          if (s1 < nt) {
+            u.out = TileSet{s1, nt, s0, s1, 0, 0};
+            launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+          }
+        }
+      }
+    }
+    cudaEventRecord(c->ev_rest[k], c->s_side);
+  }
+  cudaEventRecord(o.ev_work, c->s_mid);
+  cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
+  cudaEventRecord(o.ev_diag, c->s_side);
+  cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+  cudaEventRecord(c->ev_join, c->s_pack);
+  cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+  enqueue_prefix(c);
+  end(c, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
 }

@@ -240,9 +240,9 @@ def _context(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, m
     base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"])
     with _ctx_lock:
         ctx = _ctx_cache.get(base)
-        # an in-core plan ignores the reference tiling (except the block-pivoted LDL, which pivots
-        # inside the reference's blocks); an out-of-core one is built from it
-        tiled = ctx is not None and (ctx.out_of_core or mode == _native.MODE_LDL_PIV)
+        # an in-core plan ignores the reference tiling (except the block-pivoted LDL and LU, which
+        # pivot inside the reference's blocks); an out-of-core one is built from it
+        tiled = ctx is not None and (ctx.out_of_core or mode in (_native.MODE_LDL_PIV, _native.MODE_LU))
         if ctx is not None and (not tiled or ctx.key[4:6] == (kw["num_blocks"], kw["max_mem"])):
             return ctx
         for k in list(_ctx_cache):
@@ -370,21 +370,26 @@ def _perm_parity(perm: np.ndarray) -> int:
 
 
 def memdet_lu(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, device: int = 0,
-              assume: str | None = None, hbm_budget: int | None = None) -> GenericResult:
+              assume: str | None = None, hbm_budget: int | None = None,
+              out_of_core: bool | None = None) -> GenericResult:
     """log|det| and sign of a generic (non-symmetric) matrix via blocked LU with block-local
-    partial pivoting, the reference's generic block walk (memdet.py:268-319).  A singular
-    matrix returns (-inf, 0) rather than raising, as the reference.  Pivots are searched
-    inside the engine's diagonal blocks (|det| and its sign do not depend on the pivot order;
-    the reported block counters are the reference's for its n_b)."""
+    partial pivoting over the reference's blocks (memdet.py:268-319): in core when its blocks
+    start on tile boundaries and the matrix fits (the stages with the matrix resident), else
+    the reference's generic block walk out of core.  A singular matrix returns (-inf, 0)
+    rather than raising, as the reference.  Pivots are searched inside the engine's diagonal
+    blocks (|det| and its sign do not depend on the pivot order; the reported block counters
+    are the reference's for its n_b)."""
     del scratch_dir
     d, prefix, info, (perm, fail) = _memdet(matrix, _native.MODE_LU, "generic", max_mem, num_blocks, device,
-                                            assume or "generic", hbm_budget, True)
+                                            assume or "generic", hbm_budget, out_of_core)
     # the reference's counters for its walk (scratch = the peak number of distinct blocks
     # written, storage.py:265-267); it stops at a singular stage (memdet.py:293-294), whose
     # position the engine reports when its block grid is the reference's
     stage = info.n_b
     if fail >= 0 and info.ooc_blocks == info.n_b and info.ooc_block > 0:
         stage = fail // info.ooc_block
+    elif fail >= 0 and not info.out_of_core:  # in core: the engine's blocks are the reference's
+        stage = fail // info.b
     r, w, slots = _generic_counts_until(info.n_b, stage)
     info = replace(info, blocks_read=r, blocks_written=w, scratch_slots=slots)
     if fail >= 0 or not np.all(np.isfinite(d)) or np.any(d == 0):
