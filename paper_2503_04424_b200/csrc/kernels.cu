@@ -452,15 +452,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(GemmTask t) {
   const int nchunks = (MODE == MODE_TRSM) ? (T / KC) : (t.p1 - t.p0) * (T / KC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // B read in place from other ranks' grids (multi-GPU peer mode): those k-chunks move with
+  // 16-byte cp.async by the whole producer warp (plain global loads through the peer aperture),
+  // each lane's completion counted on the stage barrier; A (own rows) keeps the bulk copy
+  const bool bpeer = MODE == MODE_UPDATE && t.b.npeer > 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], bpeer ? 33 : 1);
       mbar_init(&empty[s], 8);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
+  if (warp == 8 && bpeer) {
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % STAGES;
+      if (c >= STAGES) mbar_wait(&empty[s], ((c / STAGES) - 1) & 1);
+      const int p = t.p0 + c / (T / KC);
+      const int off = (c % (T / KC)) * STAGE_ELEMS;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], STAGE_ELEMS * 8);
+        bulk_g2s(sA + s * STAGE_ELEMS, t.a.tile(i, p) + off, STAGE_ELEMS * 8, &full[s]);
+      }
+      const double* gb = t.b.tile(j, p) + off;
+      const uint32_t sb = smem_u32(sB + s * STAGE_ELEMS);
+#pragma unroll 8
+      for (int q = lane; q < STAGE_ELEMS / 2; q += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + q * 16), "l"(gb + 2 * q) : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[s])) : "memory");
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    return;
+  }
   if (warp == 8) {
     // ---------------- producer: one elected lane streams K-chunks with the bulk-copy engine
     if (lane == 0) {

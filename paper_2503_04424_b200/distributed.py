@@ -388,6 +388,20 @@ class PeerGrids:
             self.own = None
 
 
+def _peers_reachable(group=None, device=None) -> bool:
+    """Every rank's device can map every other rank's memory (P2P over NVLink / NVSwitch)."""
+    import torch
+    import torch.distributed as dist_mod
+
+    dev = device.index if device is not None and device.index is not None else torch.cuda.current_device()
+    devs = [None] * dist_mod.get_world_size(group)
+    dist_mod.all_gather_object(devs, dev, group=group)
+    ok = all(a == b or torch.cuda.can_device_access_peer(dev, b) for a in [dev] for b in devs)
+    flags = [None] * len(devs)
+    dist_mod.all_gather_object(flags, ok, group=group)
+    return all(flags)
+
+
 class DistributedMemdet:
     """Reusable per-rank workspace for repeated distributed factorisations of order m.
     `peer` (default: with NCCL) reads the solved panels in place over NVLink peer memory
@@ -402,7 +416,7 @@ class DistributedMemdet:
         self.dist = RowCyclic(-(-m // T), dist_mod.get_world_size(group), dist_mod.get_rank(group))
         self.comm = TorchComm(group)
         if peer is None:
-            peer = not self.comm.staged and self.dist.world <= _native.MAX_PEERS
+            peer = not self.comm.staged and self.dist.world <= _native.MAX_PEERS and _peers_reachable(group, device)
         self.shared = None
         grid = None
         if peer:
