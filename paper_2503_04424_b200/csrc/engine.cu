@@ -1305,14 +1305,23 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk));
-    } else {
-      ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
+      // the cluster kernel stored the panel's L; the row interchanges of the finished columns
+      // ride along the bulk update as extra blocks
+      const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
+      const int64_t nswap = r0 > 0 ? std::min<int64_t>(148, (r0 + 63) / 64) : 0;
+      if (ntile + nswap > 0) {
+        ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256, 0, s>>>(g, r0, nbk, ntile);
+        c->launches += 1;
+      }
+      c->launches += 1;
+      continue;
     }
+    ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
     const int64_t st_ctas = std::max<int64_t>(((n - r0) * nbk + 255) / 256, (r0 + 7) / 8);
     ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, st_ctas)), 256, 0, s>>>(g, r0, nbk);
-    const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT;
-    if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256, 0, s>>>(g, r0, nbk);
-    c->launches += mt > 0 ? 3 : 2;
+    const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
+    if (ntile > 0) ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, s>>>(g, r0, nbk, ntile);
+    c->launches += ntile > 0 ? 3 : 2;
   }
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
                       n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,

@@ -507,15 +507,18 @@ __device__ __forceinline__ bool cluster_panel_steps(const LdlArgs& g, int64_t r0
   return true;
 }
 
-// C and W rows of the panel (rows > r0) back to global memory for the store and bulk phases.
+// C and W rows of the panel (rows > r0) back to global memory for the store and bulk phases;
+// with store_l also the finished L columns (L = W below the diagonal, _ldl.pyx:59-60).
 __device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_t r0, int nbk, const double* Cs,
-                                                        const double* Ws, int R, int c) {
+                                                        const double* Ws, int R, int c, bool store_l) {
   for (int li = threadIdx.x; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
     if (i >= g.n || i <= r0) continue;
     for (int q = 0; q < nbk; ++q) {
+      const double w = Ws[(size_t)li * LC_LD + q];
       g.C[q * g.ld + i] = Cs[(size_t)li * LC_LD + q];
-      g.W[q * g.ld + i] = Ws[(size_t)li * LC_LD + q];
+      g.W[q * g.ld + i] = w;
+      if (store_l && i > r0 + q) g.A[(r0 + q) * g.ld + i] = w;
     }
   }
 }
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
   __syncthreads();  // dg loaded, barriers initialised
   cl.sync();        // every CTA's barriers initialised before any remote arrive
   if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) return;
-  cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c);
+  cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c, true);
   for (int li = threadIdx.x; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
     if (i < g.n && i > r0) g.diag[i] = dg[li];
@@ -550,8 +553,8 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArg
 // those columns at every step, _ldl.pyx:38-46): warp 0 folds the panel's swaps into one
 // permutation of at most 2 * NB rows (spos / ssrc, in shared memory), then one warp per column
 // gathers and scatters them.  Work item w of nw (CTA-granular).
-__device__ __forceinline__ void ldl_store_part(const LdlArgs& g, int64_t r0, int nbk, int64_t* spos, int64_t* ssrc,
-                                               int64_t w, int64_t nw) {
+__device__ __forceinline__ void ldl_swap_part(const LdlArgs& g, int64_t r0, int nbk, int64_t* spos, int64_t* ssrc,
+                                              int64_t w, int64_t nw) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int nthr = blockDim.x;
   if (r0 > 0 && tid < 32) {
@@ -601,6 +604,12 @@ __device__ __forceinline__ void ldl_store_part(const LdlArgs& g, int64_t r0, int
       if (p1 >= 0) colj[p1] = v1;
     }
   }
+}
+
+__device__ __forceinline__ void ldl_store_part(const LdlArgs& g, int64_t r0, int nbk, int64_t* spos, int64_t* ssrc,
+                                               int64_t w, int64_t nw) {
+  ldl_swap_part(g, r0, nbk, spos, ssrc, w, nw);
+  const int tid = threadIdx.x, nthr = blockDim.x;
   const int64_t rows = g.n - r0;
   for (int64_t e = w * nthr + tid; e < rows * nbk; e += nw * nthr) {
     const int k = (int)(e / rows);
@@ -713,13 +722,20 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   __syncthreads();  // sC / sW reused by the next tile
 }
 
-__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk) {
+// Blocks [0, ntile): the bulk tiles; blocks [ntile, gridDim.x): the panel's row interchanges on
+// the finished L columns (after the cluster panel kernel, which stores the panel's L itself).
+__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile) {
   if (*g.fail != ~0ull) return;
   __shared__ __align__(16) double sC[LDL_NB * LDL_BT];
   __shared__ __align__(16) double sW[LDL_NB * LDL_BT];
+  if ((int64_t)blockIdx.x >= ntile) {
+    __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
+    ldl_swap_part(g, r0, nbk, spos, ssrc, (int64_t)blockIdx.x - ntile, (int64_t)gridDim.x - ntile);
+    return;
+  }
   // the first tile-column (the next panel's columns) last, so that it is L2-resident when the
   // next panel kernel reads it
-  ldl_bulk_tile(g, r0, nbk, (int64_t)gridDim.x - 1 - blockIdx.x, sC, sW);
+  ldl_bulk_tile(g, r0, nbk, ntile - 1 - blockIdx.x, sC, sW);
 }
 
 // The whole pivoted factorisation of the block on one 16-CTA cluster (one launch): per panel
@@ -764,7 +780,7 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlAr
     FMARK(0);
     if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, (int)r0)) return;
     FMARK(1);
-    cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c);
+    cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c, false);
     cl.sync();  // C / W rows and the panel's interchanges visible cluster-wide
     FMARK(2);
     ldl_store_part(g, r0, nbk, sh.spos, sh.ssrc, c, LC);

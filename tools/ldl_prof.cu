@@ -76,16 +76,10 @@ int main(int argc, char** argv) {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       tp += ms;
-      const int64_t st_ctas = std::max<int64_t>(((n - r0) * nbk + 255) / 256, (r0 + 7) / 8);
+      const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
+      const int64_t nswap = r0 > 0 ? std::min<int64_t>(148, (r0 + 63) / 64) : 0;
       cudaEventRecord(e0);
-      ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, st_ctas)), 256>>>(g, r0, nbk);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      cudaEventElapsedTime(&ms, e0, e1);
-      ts += ms;
-      const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT;
-      cudaEventRecord(e0);
-      if (mt > 0) ldl_bulk_kernel<<<(unsigned)(mt * (mt + 1) / 2), 256>>>(g, r0, nbk);
+      if (ntile + nswap > 0) ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256>>>(g, r0, nbk, ntile);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
