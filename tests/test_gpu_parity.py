@@ -116,6 +116,23 @@ def test_device_tensor_path_equals_host_path():
     assert torch.equal(t.cpu(), torch.from_numpy(a))  # input untouched
 
 
+@pytest.mark.parametrize("nb,dtype", [(4, np.float64), (2, np.float32), (3, np.float64)])
+def test_pivoted_ldl_device_tensor_equals_host(nb, dtype):
+    """memdet_ldl on a CUDA tensor: tile-aligned blocks run in core straight from the device
+    copy (nb = 4, 2); the others move it to host for the block walk (nb = 3); the result is the
+    host path's bit for bit and the input is untouched."""
+    torch = pytest.importorskip("torch")
+    a = gen.random_symmetric(1024, seed=nb).astype(dtype)
+    host = eng.memdet_ldl(a, num_blocks=nb)
+    t = torch.from_numpy(a).cuda()
+    dev = eng.memdet_ldl(t, num_blocks=nb)
+    np.testing.assert_array_equal(host.perm, dev.perm)
+    np.testing.assert_array_equal(host.prefix, dev.prefix)
+    np.testing.assert_array_equal(host.prefix_signs, dev.prefix_signs)
+    assert dev.info.out_of_core == (nb == 3)
+    assert torch.equal(t.cpu(), torch.from_numpy(a))
+
+
 def test_f32_matrix_file(tmp_path):
     a = gen.random_spd(200, seed=12).astype(np.float32)
     p = tmp_path / "f.mdm"
