@@ -13,10 +13,10 @@ int main() {
   int cases[] = {0};
   for (int dbg : cases) {
     cudaMemcpy(t, h.data(), TILE_BYTES, cudaMemcpyHostToDevice);
-    potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, 1, 0, inv, ell, dg, f, T);
+    potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, inv, ell, dg, f, 0, T);
     cudaEventRecord(e0);
     for (int i = 0; i < 20; ++i) {
-      potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, 1, 0, inv, ell, dg, f, T);
+      potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, inv, ell, dg, f, 0, T);
     }
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -24,7 +24,7 @@ int main() {
   }
   long long* pr; cudaMalloc(&pr, 16 * 8); cudaMemset(pr, 0, 128);
   cudaMemcpy(t, h.data(), TILE_BYTES, cudaMemcpyHostToDevice);
-  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, 1, 0, inv, ell, dg, f, T, pr);
+  potrf_inv_kernel<<<1, POTRF_THREADS, POTRF_SMEM>>>(t, inv, ell, dg, f, 0, T, pr);
   long long hp[16]; cudaMemcpy(hp, pr, 128, cudaMemcpyDeviceToHost);
   const char* names[] = {"start", "loaded", "diag0", "A2(c0=0)", "A3 diag upd", "diag8", "A3(c0=0) end", "phaseA", "phaseB", "stored"};
   for (int i = 1; i < 10; ++i) printf("%-14s %8lld cycles (cum %8lld)\n", names[i], hp[i] - hp[i - 1], hp[i] - hp[0]);
