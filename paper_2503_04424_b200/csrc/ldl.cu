@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(LDL_PANEL_THREADS, 1) ldl_panel_kernel(LdlArgs
     if (tid == 0) g.swaps[r] = t;
     __syncthreads();
     const double p = g.diag[r];
-    if (!(fabs(p) >= tol)) {
+    if (!(fabs(p) >= tol) || tol == 0.0) {  // (tol = 0: an all-zero block, which the reference rejects)
       if (tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
       return;  // uniform: every thread read the same p
     }
@@ -438,7 +438,7 @@ __device__ __forceinline__ bool cluster_panel_steps(const LdlArgs& g, int64_t r0
     const double* rr = sh.rows[buf][0];
     const double* rt = sh.rows[buf][1];
     const double p = rt[2 * LDL_NB];  // row t's eager diagonal: the pivot
-    if (!(fabs(p) >= tol)) {
+    if (!(fabs(p) >= tol) || tol == 0.0) {  // (tol = 0: an all-zero block, which the reference rejects)
       if (c == 0 && tid == 0) atomicMin(g.fail, (unsigned long long)(g.g0 + r));
       cl.sync();
       return false;  // uniform across the cluster: every thread read the same p

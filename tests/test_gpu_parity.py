@@ -345,6 +345,39 @@ def test_pivoted_ldl_in_core_equals_block_walk(m, nb):
     assert (walk.info.ooc_reads, walk.info.ooc_writes) == (rinfo.blocks_read, rinfo.blocks_written)
 
 
+def test_pivoted_ldl_in_core_failing_block_matches_walk():
+    """A zero diagonal block at stage 2 (the Schur complement of a block-diagonal matrix):
+    in core and the block walk raise IndefiniteBlockError at the same global pivot, as the
+    reference's block-local pivoting does."""
+    m, nb = 1024, 4
+    a = gen.random_symmetric(m, seed=9)
+    a[512:768, :] = 0.0
+    a[:, 512:768] = 0.0
+    msgs = []
+    for ooc in (None, True):
+        with pytest.raises(eng.IndefiniteBlockError) as e:
+            eng.memdet_ldl(a, num_blocks=nb, out_of_core=ooc)
+        msgs.append(str(e.value).split(":")[0])
+    assert msgs[0] == msgs[1] and msgs[0] == "LDL pivot 512 below tolerance", msgs
+
+
+def test_lu_in_core_singular_block_matches_walk():
+    """A zero diagonal block at stage 2: (-inf, 0) in core and through the walk, with the
+    reference's counters of a walk that stops at stage 2 (memdet.py:293-294)."""
+    m, nb = 1024, 4
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((m, m)) + 2.0 * np.sqrt(m) * np.eye(m)
+    a[512:768, 512:768] = 0.0
+    a[512:768, :512] = 0.0
+    a[:512, 512:768] = 0.0
+    r1 = eng.memdet_lu(a, num_blocks=nb)
+    r2 = eng.memdet_lu(a, num_blocks=nb, out_of_core=True)
+    assert not r1.info.out_of_core and r2.info.out_of_core
+    assert (r1.sign, r1.logabsdet) == (0, -np.inf) == (r2.sign, r2.logabsdet)
+    assert (r1.info.blocks_read, r1.info.blocks_written, r1.info.scratch_slots) == \
+        (r2.info.blocks_read, r2.info.blocks_written, r2.info.scratch_slots)
+
+
 def _ldl_block_input(m, kind):
     rng = np.random.default_rng(m)
     if kind == "sym":
