@@ -1011,32 +1011,39 @@ static void plan_bands(Ctx* c, size_t esz) {
 static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
 
 // The strips of a host matrix into the packed triangle (s_copy / s_pack); ev_band[b] is recorded
-// on s_pack once tile-columns [b * BAND, (b + 1) * BAND) are packed.
-static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype) {
+// on s_pack once tile-columns [b * BAND, (b + 1) * BAND) are packed.  skip > 0: the leading
+// skip x skip tiles are already in (their strips bring only the columns from skip * 128 on).
+static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype, int skip = 0) {
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
   for (int J = 0; J < c->nt; ++J) {
     const int b = J % NSTAGE;
     const int64_t r0 = (int64_t)J * T;
     const int64_t rows = std::min<int64_t>(T, c->m - r0);
-    const int64_t cols = c->m - r0;  // columns [r0, m): the upper triangle of this strip
+    const int i_lo = J < skip ? skip : 0;
+    const int64_t c0 = std::max<int64_t>(r0, (int64_t)i_lo * T);
+    const int64_t cols = c->m - c0;  // columns [c0, m): the upper triangle of this strip
     // staging buffer b is free once the pack of strip J - NSTAGE has run
     if (J >= NSTAGE) cudaStreamWaitEvent(c->s_copy, c->ev_stage[b], 0);
-    const char* src = (const char*)a + (size_t)(r0 * lda + r0) * esz;
-    // staged with leading dimension npad, offset so that column r0 lands at index r0
-    char* dst = (char*)c->strip[b] + (size_t)r0 * esz;
-    CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)npad * esz, src, (size_t)lda * esz, (size_t)cols * esz,
-                               (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+    if (cols > 0) {
+      const char* src = (const char*)a + (size_t)(r0 * lda + c0) * esz;
+      // staged with leading dimension npad, offset so that column c0 lands at index c0
+      char* dst = (char*)c->strip[b] + (size_t)c0 * esz;
+      CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)npad * esz, src, (size_t)lda * esz, (size_t)cols * esz,
+                                 (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+      c->h2d += rows * cols * (int64_t)esz;
+    }
     cudaEventRecord(c->ev_copied[b], c->s_copy);
-    c->h2d += rows * cols * (int64_t)esz;
     cudaStreamWaitEvent(c->s_pack, c->ev_copied[b], 0);
-    const unsigned ntile = (unsigned)(c->nt - J);
-    if (dtype == B2D_F64)
-      pack_tiles_kernel<double, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
-          (const double*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
-    else
-      pack_tiles_kernel<float, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
-          (const float*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J);
+    const unsigned ntile = (unsigned)(c->nt - std::max(J, i_lo));
+    if (ntile > 0) {
+      if (dtype == B2D_F64)
+        pack_tiles_kernel<double, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+            (const double*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J, i_lo);
+      else
+        pack_tiles_kernel<float, 8><<<ntile, PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+            (const float*)c->strip[b], npad, r0, c->m, c->tiles, c->nt, J, i_lo);
+    }
     c->launches++;
     cudaEventRecord(c->ev_stage[b], c->s_pack);
     if ((J + 1) % BAND == 0 || J + 1 == c->nt) cudaEventRecord(c->ev_band[J / BAND], c->s_pack);
@@ -1682,8 +1689,32 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     for (int b = 0; b < NSTAGE; ++b)
       if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
   begin(c, user);
+  const int skip = host && nb > 1 ? o.tiles(0) : 0;
   if (host) {
-    int rc = ingest_host_strips(c, a, lda, dtype);
+    // the first diagonal block ahead of the strips (factor 0 starts on it alone): one b x b 2D
+    // copy, packed strip by strip into its lower tiles
+    if (skip > 0) {
+      const int64_t ldb = (int64_t)o.nbt * T, b0 = o.size(0);
+      const size_t esz = dtype == B2D_F64 ? 8 : 4;
+      if (!c->bstage[0]) CUDA_TRY(cudaMalloc(&c->bstage[0], (size_t)ldb * ldb * 8));
+      cudaStreamWaitEvent(c->s_copy, c->ev_start, 0);
+      CUDA_TRY(cudaMemcpy2DAsync(c->bstage[0], (size_t)ldb * esz, a, (size_t)lda * esz, (size_t)b0 * esz, (size_t)b0,
+                                 cudaMemcpyHostToDevice, c->s_copy));
+      c->h2d += b0 * b0 * (int64_t)esz;
+      cudaEventRecord(c->ev_copied[0], c->s_copy);
+      cudaStreamWaitEvent(c->s_pack, c->ev_copied[0], 0);
+      for (int J = 0; J < skip; ++J) {
+        if (dtype == B2D_F64)
+          pack_tiles_kernel<double, 8><<<(unsigned)(skip - J), PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+              (const double*)c->bstage[0], ldb, 0, c->m, c->tiles, nt, J);
+        else
+          pack_tiles_kernel<float, 8><<<(unsigned)(skip - J), PACK_THREADS, PACK_SMEM, c->s_pack>>>(
+              (const float*)c->bstage[0], ldb, 0, c->m, c->tiles, nt, J);
+        c->launches++;
+      }
+      cudaEventRecord(o.ev_fac, c->s_pack);
+    }
+    int rc = ingest_host_strips(c, a, lda, dtype, skip);
     if (rc) return rc;
   } else {
     const unsigned ntiles = (unsigned)n_packed_tiles(nt);
@@ -1719,7 +1750,8 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     tev.emplace_back(std::string(what) + " " + std::to_string(k), e);
   };
   tmark("start", 0, c->s_main);
-  wait_cols(c->s_main, col0(0) + o.tiles(0));
+  if (skip > 0) cudaStreamWaitEvent(c->s_main, o.ev_fac, 0);
+  else wait_cols(c->s_main, col0(0) + o.tiles(0));
   tmark("factor-begin", 0, c->s_main);
   if ((rc = ldl_factor_block(c, diag_map(0), 0, c->s_main))) return rc;
   tmark("factor-end", 0, c->s_main);

@@ -66,12 +66,13 @@ __device__ __forceinline__ void pack_tile_body(double* sm, double* __restrict__ 
 template <typename Tin, int NLOAD>
 __global__ void __launch_bounds__(PACK_THREADS, NLOAD >= 32 ? 2 : 4)
     pack_tiles_kernel(const Tin* __restrict__ src, int64_t lda, int64_t row_base, int64_t m,
-                      double* __restrict__ tiles, int nt, int j_lo) {
+                      double* __restrict__ tiles, int nt, int j_lo, int i_lo = 0) {
   extern __shared__ double sm[];  // [64][PACK_LD]: sm[c*PACK_LD + r] for the current 64 columns
+  // tiles (I, J), J >= j_lo, I >= max(J, i_lo), column by column
   int64_t b = blockIdx.x;
   int J = j_lo;
-  while (b >= nt - J) { b -= nt - J; ++J; }
-  const int I = J + (int)b;
+  while (b >= nt - max(J, i_lo)) { b -= nt - max(J, i_lo); ++J; }
+  const int I = max(J, i_lo) + (int)b;
   const int64_t R0 = (int64_t)I * T, C0 = (int64_t)J * T;
   pack_tile_body<NLOAD>(sm, tiles + tile_index(I, J, nt) * TILE_ELEMS, [&](int r, int c) {
     const int64_t R = R0 + r, C = C0 + c;
