@@ -345,6 +345,22 @@ def test_pivoted_ldl_in_core_equals_block_walk(m, nb):
     assert (walk.info.ooc_reads, walk.info.ooc_writes) == (rinfo.blocks_read, rinfo.blocks_written)
 
 
+@pytest.mark.parametrize("m,nb", [(1022, 4), (768, 3)])
+def test_in_core_f32_inputs_equal_block_walk(m, nb):
+    """float32 inputs (converted on the device) through the in-core LDL and LU equal the block
+    walks bit for bit."""
+    a = gen.random_symmetric(m, seed=m).astype(np.float32)
+    r1, r2 = eng.memdet_ldl(a, num_blocks=nb), eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
+    assert not r1.info.out_of_core and r2.info.out_of_core
+    np.testing.assert_array_equal(r1.perm, r2.perm)
+    np.testing.assert_array_equal(r1.prefix, r2.prefix)
+    assert r1.prefix.dtype == np.float32
+    g = (np.random.default_rng(m).standard_normal((m, m)) + 2.0 * np.sqrt(m) * np.eye(m)).astype(np.float32)
+    u1, u2 = eng.memdet_lu(g, num_blocks=nb), eng.memdet_lu(g, num_blocks=nb, out_of_core=True)
+    assert not u1.info.out_of_core and u2.info.out_of_core
+    assert (u1.sign, u1.logabsdet) == (u2.sign, u2.logabsdet)
+
+
 def test_pivoted_ldl_in_core_failing_block_matches_walk():
     """A zero diagonal block at stage 2 (the Schur complement of a block-diagonal matrix):
     in core and the block walk raise IndefiniteBlockError at the same global pivot, as the
