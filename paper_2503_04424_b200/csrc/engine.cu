@@ -140,7 +140,7 @@ struct Ctx {
   cudaStream_t s_mid = nullptr;  // panel work off the potrf chain (rows below the panel block)
   cudaEvent_t ev_m2s = nullptr;  // s_main -> s_mid hand-off (potrf + in-block solve of a column)
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_join = nullptr;
-  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_catch, ev_stage, ev_copied, ev_band;
+  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_resta, ev_catch, ev_stage, ev_copied, ev_band;
   // band activation (host ingest): band b = tile-columns [b*BAND, (b+1)*BAND) joins the
   // right-looking updates at outer step act[b] (-1: from the start) after one catch-up update
   std::vector<int> act;
@@ -162,7 +162,7 @@ struct Ctx {
   // triangle holds the matrix, o.* the block factor state; the stage's solved panel lives in
   // full-height grids of nt x nbt tiles, unscaled and D^{-1}-scaled, double-buffered by stage
   bool ldl_ic = false;
-  double* pan[2][2] = {};  // [stage parity][0: unscaled, 1: scaled]
+  double* pan[3][2] = {};  // [stage % 3][0: unscaled, 1: scaled]
   // generic LU in core (the same conditions): the matrix as a full nt x nt tile grid; per stage
   // parity the column panel X, the transposed row panel Y^T and a transpose buffer (nt x nbt
   // tiles each, rows = global tile index), and the U^T factor of the diagonal block
@@ -234,7 +234,7 @@ static void destroy(Ctx* c) {
     cudaFree(c->oz_expo[b]);
   }
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
-  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
+  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_resta, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
                   &c->prof_ev})
     for (auto e : *v) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
@@ -369,12 +369,14 @@ static int create_streams_events(Ctx* c) {
   const int nsteps = c->nt;  // enough for any panel-width schedule
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
+  c->ev_resta.resize(nsteps);
   c->ev_catch.resize(nsteps);
   c->trace = getenv("B2D_TRACE") != nullptr;
   const unsigned evf = c->trace ? cudaEventDefault : cudaEventDisableTiming;
   for (int s = 0; s < nsteps; ++s) {
     cudaEventCreateWithFlags(&c->ev_panel[s], evf);
     cudaEventCreateWithFlags(&c->ev_rest[s], evf);
+    cudaEventCreateWithFlags(&c->ev_resta[s], evf);
     cudaEventCreateWithFlags(&c->ev_catch[s], evf);
   }
   const int nbands = (c->nt + BAND - 1) / BAND;
@@ -444,7 +446,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     else if (opt && opt->max_mem > 0) nb0 = ref_select_blocking(m, opt->max_mem, 8);
     ref_layout(m, std::max<int64_t>(1, nb0), &ic_nb, &ic_b, &ic_tail);
     const int64_t bt = (ic_b + T - 1) / T, ldb = bt * T;
-    const size_t ic_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + 4 * (size_t)nt_full * bt * TILE_BYTES +
+    const size_t ic_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + 6 * (size_t)nt_full * bt * TILE_BYTES +
                            (size_t)(nt_full + bt) * TILE_BYTES + (size_t)ldb * ldb * 9 + 3 * (size_t)npad_full * 8 +
                            (size_t)NSTAGE * T * npad_full * 8 + (size_t)(m + 8 * ldb) * 8;
     if ((ic_b % T == 0 || ic_nb == 1) && ic_need <= budget) force = false;
@@ -656,6 +658,24 @@ static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, boo
     c->prof_ev.push_back(e0);
     c->prof_ev.push_back(e1);
     c->prof_flops.push_back(flops);
+  }
+}
+
+// The trailing ("rest") update of a stage that runs beside the next diagonal factor, issued as
+// sequential launches over K chunks of `rest_kchunk()` tile-columns: each CTA then holds its SM
+// for K = 128 * chunk instead of the whole block width, so the factor's cluster and bulk
+// launches find free SMs sooner.  Exact: the accumulators start from C and the chunks continue
+// the same k order, and a stored FP64 accumulator reloads unchanged.
+static int rest_kchunk() {
+  const char* e = getenv("B2D_REST_KCHUNK");
+  return e ? atoi(e) : 8;
+}
+static void launch_update_kchunked(Ctx* c, cudaStream_t s, GemmTask u) {
+  const int p0 = u.p0, p1 = u.p1, kc = rest_kchunk() > 0 ? rest_kchunk() : p1 - p0;
+  for (int q = p0; q < p1; q += kc) {
+    u.p0 = q;
+    u.p1 = std::min(p1, q + kc);
+    launch_gemm(c, s, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * (double)(u.p1 - u.p0) * T);
   }
 }
 
@@ -1763,30 +1783,38 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     // panel: rows [i0, nt) of block column k, permuted by the stage's pivots (memdet.py:365-366),
     // solved with the unit factor (dense.py:94-99), and its D^{-1}-scaled copy (memdet.py:368-371)
     cudaStreamWaitEvent(c->s_mid, c->ev_catch[k], 0);
-    if (k >= 2) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 2], 0);  // last reader of pan[par]
+    const int pb = k % 3;  // panel buffers: three, so panel k waits only for rest k-3
+    if (k >= 3) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 3], 0);  // last reader of pan[pb]
     wait_cols(c->s_mid, i0);
-    TileMap src = packed;
-    src.roff = i0;
-    src.coff = k0;
-    const TileMap pu{c->pan[par][0] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
-    const TileMap ps{c->pan[par][1] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
-    permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(src, pu, R, kb, o.size(k), o.perm_of(k));
-    trsm_panel(c, c->s_mid, pu, R, diag_map(k), kb, inv_k);
-    scale_cols_kernel<<<2048, 256, 0, c->s_mid>>>(pu, ps, R, kb, o.size(k), o.dblk_of(k));
-    c->launches += 2;
+    // B2D_LDL_SPLIT (default 1): the rows of block k+1 are solved and its diagonal block
+    // updated first, so the next factor starts on them while the rows below are solved
+    const char* spe = getenv("B2D_LDL_SPLIT");
+    const int r_split = (spe ? atoi(spe) != 0 : true) ? i0 + kb1 : nt;
+    auto panel_rows = [&](int r0, int r1) {  // global tile rows [r0, r1) of the panel
+      TileMap src = packed;
+      src.roff = r0;
+      src.coff = k0;
+      const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+      const TileMap ps{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+      permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(src, pu, r1 - r0, kb, o.size(k), o.perm_of(k));
+      trsm_panel(c, c->s_mid, pu, r1 - r0, diag_map(k), kb, inv_k);
+      scale_cols_kernel<<<2048, 256, 0, c->s_mid>>>(pu, ps, r1 - r0, kb, o.size(k), o.dblk_of(k));
+      c->launches += 2;
+    };
+    panel_rows(i0, r_split);
     tmark("panel-end", k, c->s_mid);
-    cudaEventRecord(c->ev_panel[k], c->s_mid);
-    // T -= (L D^{-1})_rows L_cols^T (dense.py:109-116) over block column k+1 first
+    // T -= (L D^{-1})_rows L_cols^T (dense.py:109-116) over block column k+1 first (its
+    // diagonal block first of all)
     GemmTask u{};
-    u.a = TileMap{c->pan[par][1], o.nbt, 0};  // rows indexed by global tile row
-    u.b = TileMap{c->pan[par][0], o.nbt, 0};
+    u.a = TileMap{c->pan[pb][1], o.nbt, 0};  // rows indexed by global tile row
+    u.b = TileMap{c->pan[pb][0], o.nbt, 0};
     u.c = packed;
     u.p0 = 0;
     u.p1 = kb;
     const double K = (double)kb * T;
-    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 1], 0);
+    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // block column k+1 current
     wait_cols(c->s_mid, i0 + kb1);
-    u.out = TileSet{i0, nt, i0, i0 + kb1, 1, 0};
+    u.out = TileSet{i0, r_split, i0, i0 + kb1, 1, 0};
     launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
     tmark("next-col-end", k, c->s_mid);
     cudaEventRecord(o.ev_diag, c->s_mid);
@@ -1799,13 +1827,30 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     if ((rc = ldl_factor_block(c, diag_map(k + 1), k + 1, c->s_main, !serial && i0 + kb1 < nt))) return rc;
     tmark("factor-end", k + 1, c->s_main);
     cudaEventRecord(c->ev_catch[k + 1], c->s_main);
+    if (r_split < nt) {  // the rows below block k+1: solve, then their block-column k+1 update
+      panel_rows(r_split, nt);
+      u.out = TileSet{r_split, nt, i0, i0 + kb1, 1, 0};
+      launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+      tmark("below-end", k, c->s_mid);
+    }
+    cudaEventRecord(c->ev_panel[k], c->s_mid);
     if (i0 + kb1 < nt) {
-      // after the next-col update, i.e. issued with the next factor, which takes its SMs first
-      cudaStreamWaitEvent(c->s_side, o.ev_diag, 0);
+      // after the whole panel (issued after the next factor, which takes its SMs first)
+      cudaStreamWaitEvent(c->s_side, c->ev_panel[k], 0);
       if (serial) cudaStreamWaitEvent(c->s_side, c->ev_catch[k + 1], 0);
       wait_cols(c->s_side, nt);
-      u.out = TileSet{i0 + kb1, nt, i0 + kb1, nt, 1, 0};
-      launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+      // block column k+2 first (the next stage's next-col update waits for it alone), then the
+      // rest: two launches over disjoint tiles, each tile's operands and K unchanged
+      const int i2 = k + 2 < nb ? std::min(nt, i0 + kb1 + o.tiles(k + 2)) : nt;
+      u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 1, 0};
+      launch_update_kchunked(c, c->s_side, u);
+      cudaEventRecord(c->ev_resta[k], c->s_side);
+      if (i2 < nt) {
+        u.out = TileSet{i2, nt, i2, nt, 1, 0};
+        launch_update_kchunked(c, c->s_side, u);
+      }
+    } else {
+      cudaEventRecord(c->ev_resta[k], c->s_side);
     }
     tmark("rest-end", k, c->s_side);
     cudaEventRecord(c->ev_rest[k], c->s_side);
@@ -1966,7 +2011,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
     u.p0 = 0;
     u.p1 = kb;
     const double K = (double)kb * T;
-    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 1], 0);
+    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // cross k+1 current
     cudaStreamWaitEvent(c->s_mid, c->ev_cross[k + 1], 0);
     u.out = TileSet{i0, nt, i0, i0 + kb1, 0, 0};
     launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
@@ -1982,8 +2027,20 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
       cudaStreamWaitEvent(c->s_side, o.ev_diag, 0);
       if (k > 0 || !host) {
         cudaStreamWaitEvent(c->s_side, c->ev_cross[nb - 1], 0);
-        u.out = TileSet{i0 + kb1, nt, i0 + kb1, nt, 0, 0};
-        launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+        // block column and block row k+2 first (the next stage's cross update waits for them
+        // alone), then the rest of the square: disjoint tiles, operands and K unchanged
+        const int i2 = k + 2 < nb ? std::min(nt, i0 + kb1 + o.tiles(k + 2)) : nt;
+        u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 0, 0};
+        launch_update_kchunked(c, c->s_side, u);
+        if (i2 < nt) {
+          u.out = TileSet{i0 + kb1, i2, i2, nt, 0, 0};
+          launch_update_kchunked(c, c->s_side, u);
+        }
+        cudaEventRecord(c->ev_resta[k], c->s_side);
+        if (i2 < nt) {
+          u.out = TileSet{i2, nt, i2, nt, 0, 0};
+          launch_update_kchunked(c, c->s_side, u);
+        }
       } else {
         // stage 0 runs while the matrix streams in: the rest of the trailing square in the
         // cross sets of the later stages (block (s, s), row s, column s), each as it arrives
@@ -2000,6 +2057,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
       }
     }
     cudaEventRecord(c->ev_rest[k], c->s_side);
+    if (!(i0 + kb1 < nt && (k > 0 || !host))) cudaEventRecord(c->ev_resta[k], c->s_side);
   }
   cudaEventRecord(o.ev_work, c->s_mid);
   cudaStreamWaitEvent(c->s_main, o.ev_work, 0);

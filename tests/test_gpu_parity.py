@@ -326,11 +326,15 @@ def test_pivoted_ldl_matches_reference_golden(golden, name):
 
 
 @pytest.mark.parametrize("m,nb", [(1024, 4), (1022, 4), (1280, 5), (768, 2), (2048, 8), (700, 1)])
-def test_pivoted_ldl_in_core_equals_block_walk(m, nb):
-    """Tile-aligned reference blocks run in core (the matrix resident, one large update per
+@pytest.mark.parametrize("kchunk", ["8", "1"])
+def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, monkeypatch):
+    """B2D_REST_KCHUNK splits the trailing update over K into sequential launches (1 = one
+    tile-column each), which must not change a bit.
+    Tile-aligned reference blocks run in core (the matrix resident, one large update per
     stage, the next block's factor overlapped); every tile gets the walk's updates with the same
     operands and K, so perm, D and the prefixes equal the out-of-core block walk's bit for bit,
     and the walk makes the reference's transfers."""
+    monkeypatch.setenv("B2D_REST_KCHUNK", kchunk)
     a = gen.random_symmetric(m, seed=m + nb)
     res = eng.memdet_ldl(a, num_blocks=nb)
     walk = eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
@@ -538,11 +542,14 @@ def test_lu_matches_reference_golden():
 
 
 @pytest.mark.parametrize("m,nb", [(1024, 4), (1022, 4), (1280, 5), (2048, 2), (700, 1)])
-def test_lu_in_core_equals_block_walk(m, nb):
-    """Tile-aligned reference blocks run in core (full tile grid resident, one large update per
+@pytest.mark.parametrize("kchunk", ["8", "1"])
+def test_lu_in_core_equals_block_walk(m, nb, kchunk, monkeypatch):
+    """B2D_REST_KCHUNK = 1 splits the trailing update over K into one launch per tile-column.
+    Tile-aligned reference blocks run in core (full tile grid resident, one large update per
     stage, the next block's factor overlapped): every tile gets the walk's updates with the
     same operands and K, so log|det|, the sign and the pivots equal the generic walk's bit for
     bit, and agree with numpy's slogdet."""
+    monkeypatch.setenv("B2D_REST_KCHUNK", kchunk)
     rng = np.random.default_rng(m + nb)
     a = rng.standard_normal((m, m)) + 2.0 * np.sqrt(m) * np.eye(m)
     a[::3] *= -1.0
