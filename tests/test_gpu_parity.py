@@ -9,6 +9,8 @@ well-conditioned inputs, 1e-6 on the power-law (NTK-like) spectra, 1e-4 for floa
 (the reference's own f32 bar, tests/test_memdet.py:247-256)."""
 
 import hashlib
+import os
+import json
 
 import numpy as np
 import pytest
@@ -182,6 +184,37 @@ def test_c2_full_size_vs_independent_gpu_factorisation():
     assert rel_err(res.prefix, ref) <= 1e-10, rel_err(res.prefix, ref)
     small = eng.memdet_cholesky(a[:4096, :4096].contiguous(), num_blocks=1)
     assert rel_err(res.prefix[:4096], small.prefix) <= 1e-12
+
+
+@pytest.mark.slow
+def test_c2_full_size_matches_reference_golden():
+    """C2 at full size against the UNMODIFIED reference's own outputs on the same bytes
+    (tests/golden/c2.*, made by make_c2_golden.py): the host input is regenerated here and its
+    SHA-256 must equal the one the reference factored; then every memdet_cholesky prefix and
+    every memdet_ldl prefix within 1e-10 (north star), and the LDL pivots and signs."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "c2.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/c2.json not generated")
+    with open(path) as f:
+        meta = json.load(f)
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2.npz"))
+    a = gen.rbf(meta["m"], seed=0, threads=os.cpu_count() or 1)
+    h = hashlib.sha256()
+    for r0 in range(0, a.shape[0], 1024):
+        h.update(np.ascontiguousarray(a[r0:r0 + 1024]).tobytes())
+    assert h.hexdigest() == meta["input_sha256"]
+    chol = eng.memdet_cholesky(a, num_blocks=meta["num_blocks"])
+    assert rel_err(chol.prefix, ref["chol__prefix"]) <= 1e-10, rel_err(chol.prefix, ref["chol__prefix"])
+    ldl = eng.memdet_ldl(a, num_blocks=meta["num_blocks"])
+    eng.release_engine_cache()
+    assert rel_err(ldl.prefix, ref["ldl__prefix"]) <= 1e-10, rel_err(ldl.prefix, ref["ldl__prefix"])
+    np.testing.assert_array_equal(ldl.perm, ref["ldl__perm"])
+    np.testing.assert_array_equal(ldl.prefix_signs, ref["ldl__signs"])
+    for r, res in (("chol", chol), ("ldl", ldl)):
+        info = meta["runs"][r]
+        assert (res.info.n_b, res.info.b) == (info["n_b"], info["b"])
+        assert (res.info.blocks_read, res.info.blocks_written, res.info.scratch_slots) == \
+            (info["blocks_read"], info["blocks_written"], info["scratch_slots"])
 
 
 # ------------------------------------------------------------------ out-of-core block streamer
