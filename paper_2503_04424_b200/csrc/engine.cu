@@ -1778,7 +1778,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   cudaEventRecord(c->ev_catch[0], c->s_main);
   for (int k = 0; k + 1 < nb; ++k) {
     const int par = k & 1;
-    const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb, R = nt - i0, kb1 = o.tiles(k + 1);
+    const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb, kb1 = o.tiles(k + 1);
     const double* inv_k = par && o.inv_odd ? o.inv_odd : c->inv;
     // panel: rows [i0, nt) of block column k, permuted by the stage's pivots (memdet.py:365-366),
     // solved with the unit factor (dense.py:94-99), and its D^{-1}-scaled copy (memdet.py:368-371)
