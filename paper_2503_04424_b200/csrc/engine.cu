@@ -103,6 +103,7 @@ struct Ooc {
   cudaStream_t s_work = nullptr;  // block-walk solves / updates: s_main, or s_mid under look-ahead
   cudaEvent_t ev_fac = nullptr, ev_diag = nullptr, ev_work = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaStream_t s_walk = nullptr;  // Cholesky walk under look-ahead (low priority)
   double* stage = nullptr;                         // one 128-row file strip
   std::map<std::pair<int, int>, double*> scratch;  // pinned host blocks (kept across runs)
   std::map<std::pair<int, int>, cudaEvent_t> ev_key;  // last store of each scratch block
@@ -286,6 +287,7 @@ static void destroy(Ctx* c) {
   }
   for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
   if (o.s_h2d) cudaStreamDestroy(o.s_h2d);
+  if (o.s_walk) cudaStreamDestroy(o.s_walk);
   if (o.s_d2h) cudaStreamDestroy(o.s_d2h);
   delete c;
 }
@@ -576,6 +578,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     ALLOC(o.stage, (size_t)T * o.nbt * T * 8);
     ALLOC(c->inv, (size_t)o.nbt * TILE_BYTES);
+    if (!pivoted) ALLOC(o.inv_odd, (size_t)o.nbt * TILE_BYTES);  // stage parity (walk look-ahead)
     if (pivoted) {
       const int64_t ld = (int64_t)o.nbt * T;
       ALLOC(o.dense, (size_t)ld * ld * 8);
@@ -620,6 +623,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&o.s_h2d, cudaStreamNonBlocking, hi);
     cudaStreamCreateWithPriority(&o.s_d2h, cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&o.s_walk, cudaStreamNonBlocking, lo);
     cudaEventCreateWithFlags(&o.ev_fac, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&o.ev_diag, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&o.ev_work, cudaEventDisableTiming);
@@ -1522,7 +1526,11 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
   o.rr = 0;
   // pivoted LDL: factors on s_main (high priority), the walk's solves / updates on s_mid
   const bool look = c->mode == B2D_MODE_LDL_PIV && getenv("B2D_LDL_NO_LOOKAHEAD") == nullptr;
-  o.s_work = look ? c->s_mid : c->s_main;
+  // Cholesky: the same look-ahead with the walk on its own stream (the diagonal factor is the
+  // in-core multi-stream driver on s_main / s_mid / s_side); B2D_OOC_NO_LOOKAHEAD disables it
+  const bool clook = c->mode != B2D_MODE_LDL_PIV && c->mode != B2D_MODE_LU && o.s_walk && o.inv_odd &&
+                     getenv("B2D_OOC_NO_LOOKAHEAD") == nullptr;
+  o.s_work = look ? c->s_mid : clook ? o.s_walk : c->s_main;
   auto alloc = [&](std::initializer_list<int> busy) {
     const int pool = c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU ? o.nslot - 1 : o.nslot;  // last: permute temp
     for (int tries = 0; tries < pool; ++tries) {
@@ -1604,9 +1612,24 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
     cudaEventRecord(o.ev_fac, c->s_main);
     return r;
   };
+  // Cholesky under look-ahead: the in-core driver on the block's tile grid, tile inverses in the
+  // stage-parity buffer (the walk of stage k still reads stage k's while k+1 is factored)
+  auto factor_chol = [&](int slot, int k) {
+    cudaEventRecord(o.ev_diag, o.s_work);  // the block's last Schur update
+    cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+    cudaStreamWaitEvent(c->s_main, o.ev_loaded[slot], 0);
+    make_bounds(c, o.tiles(k), false);
+    double* inv0 = c->inv;
+    if (k & 1) c->inv = o.inv_odd;
+    enqueue_factor(c, FactorTarget{o.map(slot), o.tiles(k), (int64_t)k * o.b}, false);
+    c->inv = inv0;
+    cudaEventRecord(o.ev_used[slot], c->s_main);
+    cudaEventRecord(o.ev_fac, c->s_main);
+  };
   if (piv && (rc = factor_ldl(sa, 0))) return rc;
+  if (clook) factor_chol(sa, 0);
   for (int k = 0; k < o.nb; ++k) {
-    if (piv) {
+    if (piv || clook) {
       cudaStreamWaitEvent(o.s_work, o.ev_fac, 0);  // stage k's factor (issued ahead)
     } else {
       cudaStreamWaitEvent(c->s_main, o.ev_loaded[sa], 0);
@@ -1615,7 +1638,7 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
       cudaEventRecord(o.ev_used[sa], c->s_main);
     }
     if (k == o.nb - 1) break;
-    const double* inv_k = piv && (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
+    const double* inv_k = (piv || clook) && (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
     // bx: the column's solved row-k block (unscaled); by: its D^{-1}-scaled copy (LDL) or bx
     int bx = -1, by = -1, sc = -1, next_a = -1;
     bool early = false;  // look-ahead: block (k+1, k+1) updated and its factor issued
@@ -1652,6 +1675,15 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
       ooc_schur(c, st, v.j, v.i, by, v.i == v.j ? bx : sc, k);
       if (v.next_diag) next_a = st;
       else if ((rc = ooc_store(c, v.i, v.j, st))) return rc;
+      if (clook && !early && v.j == o.nb - 1 && v.i == k + 1 && v.i != v.j) {
+        // as below, unscaled: T(k+1, k+1) -= L(k+1, k) L(k+1, k)^T, the diagonal visit's operands
+        const int sd = alloc({sa, bx, by, sc});
+        if ((rc = ooc_load(c, k + 1, k + 1, sd, a, lda, dtype))) return rc;
+        ooc_schur(c, sd, k + 1, k + 1, sc, sc, k);
+        next_a = sd;
+        early = true;
+        factor_chol(next_a, k + 1);
+      }
       if (look && !early && v.j == o.nb - 1 && v.i == k + 1 && v.i != v.j) {
         // L(k+1, k) was just solved (slot sc): update block (k+1, k+1) now, the walk's last
         // visit, and factor it on s_main while the rest of the stage runs on s_work
@@ -1666,6 +1698,7 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
       }
     }
     if (piv && !early && (rc = factor_ldl(next_a, k + 1))) return rc;
+    if (clook && !early) factor_chol(next_a, k + 1);
     tmark(o.s_work);  // end of stage k's walk
     sa = next_a;
   }
