@@ -38,6 +38,7 @@ METRIC = "FP64 logdet TFLOP/s (n^3/3)"
 UNIT = "TFLOP/s"
 INT8_PEAK_TOPS = 4500.0  # nominal B200 dense int8 tensor throughput (TOPS), for the opt-in Ozaki line
 C2 = dict(n=32768, num_blocks=8, d=16, ell=4.0, jitter=1e-6, seed=0)
+OOC = dict(n=65536, num_blocks=4, hbm_budget=int(24e9))  # out-of-core line: C3-sized RBF, forced walk
 SAMPLE_N = 16384  # CPU baseline sample: leading principal 16384 submatrix of C2, b = 4096
 PROFILE_SUMMARY = os.path.join(REPO, "profiles", "r01_gemm_update_ncu.json")
 
@@ -160,6 +161,25 @@ def generate_rbf_device(torch, dev_x, n):
                                              C2["jitter"], ctypes.c_void_p(a.data_ptr()),
                                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return a
+
+
+def measure_pcie(torch, nbytes=1 << 30, reps=3):
+    """Pinned host <-> HBM copy rates (GB/s) for the out-of-core roofline."""
+    h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
+    d = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    rates = []
+    for src, dst in ((h, d), (d, h)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        rates.append(reps * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del h, d
+    return rates[0], rates[1]
 
 
 def traffic_from_profile():
@@ -371,6 +391,49 @@ def run_engine(args):
                       "api": "paper_2503_04424_b200.memdet_ldl(pinned host ndarray, num_blocks=8)",
                       "logdet": lres.logabsdet}
 
+    # out-of-core (the north star's configs[4] schedule): the reference's tile walk on a C3-sized
+    # RBF Gram (n = 65536, 34 GB in pinned host memory; the C2 points extended, nested) with
+    # num_blocks=4 (b = 16384) under a 24 GB HBM budget -- 6 block slots in HBM, the 17 GB
+    # scratchpad in pinned host memory -- against its roofline max(flops/peak, H2D/PCIe, D2H/PCIe)
+    ooc = None
+    if not args.no_ooc:
+        h2d_gbs, d2h_gbs = measure_pcie(torch)
+        del pinned, host
+        on = OOC["n"]
+        oflops = on ** 3 / 3.0
+        ox = torch.from_numpy(gen.rbf_points(on, C2["d"], C2["seed"])).cuda()
+        oa = generate_rbf_device(torch, ox, on)
+        ohost_t = torch.empty((on, on), dtype=torch.float64, pin_memory=True)
+        ohost_t.copy_(oa)
+        del oa, ox
+        torch.cuda.empty_cache()
+        ohost = ohost_t.numpy()
+        budget = OOC["hbm_budget"]
+        eng.memdet_cholesky(ohost, num_blocks=OOC["num_blocks"], hbm_budget=budget, out_of_core=True)  # warm: pins the scratchpad
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ores2 = eng.memdet_cholesky(ohost, num_blocks=OOC["num_blocks"], hbm_budget=budget, out_of_core=True)
+        osec2 = (time.perf_counter() - t0) / e2e_steps
+        eng.release_engine_cache()
+        oi = ores2.info
+        roof = max(oflops / (peak * 1e12), oi.h2d_bytes / (h2d_gbs * 1e9), oi.d2h_bytes / (d2h_gbs * 1e9))
+        ooc = {"value": oflops / osec2 / 1e12, "unit": UNIT, "seconds_per_step": osec2, "steps": e2e_steps,
+               "config": {"workload": "RBF Gram n=65536 (C3 size; C2's recipe and points, nested)",
+                          "n": on, "num_blocks": OOC["num_blocks"], "b": int(oi.b), "hbm_budget_bytes": budget,
+                          "out_of_core": bool(oi.out_of_core), "scratchpad": "pinned host"},
+               "blocks_read": int(oi.blocks_read), "blocks_written": int(oi.blocks_written),
+               "scratch_slots": int(oi.scratch_slots), "engine_reads": int(oi.ooc_reads),
+               "engine_writes": int(oi.ooc_writes),
+               "h2d_bytes_per_step": int(oi.h2d_bytes), "d2h_bytes_per_step": int(oi.d2h_bytes),
+               "roofline": {"bound": "max(FP64 tensor, PCIe H2D, PCIe D2H)", "time_s": roof, "frac": roof / osec2,
+                            "peak_tflops": peak, "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                            "pcie_source": "pinned 1 GiB cudaMemcpy each way, this run"},
+               "logdet": ores2.logabsdet,
+               "nested_prefix_rel_diff_vs_c2": float(np.max(np.abs(ores2.prefix[:n] - res.prefix)
+                                                            / np.maximum(1.0, np.abs(res.prefix)))),
+               "api": "paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks=4, hbm_budget=24e9, out_of_core=True)"}
+
     out = None
     if rank == 0:
         cpu = None
@@ -424,6 +487,7 @@ def run_engine(args):
             "gpu_launches": launches_per_step * args.steps,
             "ozaki": ozaki,
             "ldl": ldl,
+            "out_of_core": ooc,
             "clocks": clocks.summary(),
         }
     if ws > 1:
@@ -562,6 +626,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ozaki", action="store_true", help="skip the opt-in int8-emulated Schur line")
     ap.add_argument("--no-ldl", action="store_true", help="skip the memdet_ldl (block-pivoted) line")
+    ap.add_argument("--no-ooc", action="store_true", help="skip the out-of-core line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
