@@ -817,6 +817,9 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
       if (c->act[b] < 0) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
   }
   int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel)
+  // B2D_LEFT_BELOW (default 1): the rows below each panel are updated left-looking per column
+  const char* lbe = getenv("B2D_LEFT_BELOW");
+  const bool left_below = lbe ? atoi(lbe) != 0 : true;
   for (int st = 0; st < nsteps; ++st) {
     const int k0 = c->bounds[st];
     const int ke = c->bounds[st + 1];
@@ -838,6 +841,16 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
       launch_trsm(c, c->s_main, ft, p, p + 1, ke);
       cudaEventRecord(c->ev_m2s, c->s_main);
       cudaStreamWaitEvent(c->s_mid, c->ev_m2s, 0);
+      if (left_below) {
+        // rows below, left-looking inside the panel: column p takes the panel's columns
+        // [k0, p) in ONE launch (K = 128 (p - k0)) right before its solve -- each tile is read
+        // and written once per panel instead of once per column, with the same k order (the
+        // FP64 accumulators start from C), so the result is bit-identical
+        if (ke < nt && p > k0) launch_update_set(c, c->s_mid, ft, TileSet{ke, nt, p, p + 1, 0, 0}, k0, p, false);
+        launch_trsm(c, c->s_mid, ft, p, ke, nt);
+        if (p + 1 < ke) launch_update_set(c, c->s_main, ft, TileSet{p + 1, ke, p + 1, ke, 1, 0}, p, p + 1, false);
+        continue;
+      }
       launch_trsm(c, c->s_mid, ft, p, ke, nt);
       if (p + 1 < ke) {
         launch_update_set(c, c->s_main, ft, TileSet{p + 1, ke, p + 1, ke, 1, 0}, p, p + 1, false);
