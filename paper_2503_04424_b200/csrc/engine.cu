@@ -1227,16 +1227,30 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
 static void trsm_panel(Ctx* c, cudaStream_t s, const TileMap& x, int R, const TileMap& lkk, int Q,
                        const double* inv) {
   const int W = c->W_TILES;
+  const char* lbe = getenv("B2D_LEFT_BELOW");
+  const bool left = lbe ? atoi(lbe) != 0 : true;
   for (int q0 = 0; q0 < Q; q0 += W) {
     const int qe = std::min(q0 + W, Q);
     for (int q = q0; q < qe; ++q) {
+      if (left && q > q0) {
+        // left-looking inside the group: column q takes columns [q0, q) in one launch right
+        // before its solve (same k order as the right-looking K = 128 updates: bit-identical)
+        GemmTask u{};
+        u.a = x;
+        u.b = lkk;
+        u.c = x;
+        u.out = TileSet{0, R, q, q + 1, 0, 0};
+        u.p0 = q0;
+        u.p1 = q;
+        launch_gemm(c, s, MODE_UPDATE, u, false, 0.0);
+      }
       GemmTask t{};
       t.c = x;
       t.binv = inv + (int64_t)q * TILE_ELEMS;
       t.out = TileSet{0, R, q, q + 1, 0, 0};
       t.k = q;
       launch_gemm(c, s, MODE_TRSM, t, false, 0.0);
-      if (q + 1 < qe) {
+      if (!left && q + 1 < qe) {
         GemmTask u{};
         u.a = x;
         u.b = lkk;
