@@ -673,8 +673,11 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
     tagged |= tw[c] != 0;
   }
   __syncthreads();
-  if (!__any_sync(0xffffffffu, tagged)) {
-    // no entry of the warp holds any of the panel's steps: every term applies
+  {
+    // every term on every entry (the fast path); entries that already hold some of the panel's
+    // steps (tag > 0, rare: rows / columns moved by the panel's interchanges) are redone below
+    // from their loaded value with the terms [tag, nbk) only -- each entry still sees exactly
+    // its terms, in order, with the reference's two roundings
     for (int q = 0; q < nbk; ++q) {
       const double2 c01 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx);
       const double2 c23 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx + 2);
@@ -686,18 +689,20 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
     }
-  } else {
-    for (int q = 0; q < nbk; ++q) {
-      double cc[4], ww[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) cc[a] = sC[q * LDL_BT + 4 * tx + a];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) ww[c] = sW[q * LDL_BT + 4 * ty + c];
+    if (tagged) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (q >= (int)((tw[c] >> (8 * a)) & 0xffu)) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
+        for (int c = 0; c < 4; ++c) {
+          const int tg = (int)((tw[c] >> (8 * a)) & 0xffu);
+          if (tg) {
+            const int64_t i = ib + a, j = jb + c;
+            double x = __ldcg(g.A + j * ld + i);
+            for (int q = tg; q < nbk; ++q)
+              x = __dsub_rn(x, __dmul_rn(sC[q * LDL_BT + 4 * tx + a], sW[q * LDL_BT + 4 * ty + c]));
+            v[a][c] = x;
+          }
+        }
     }
   }
 #pragma unroll
