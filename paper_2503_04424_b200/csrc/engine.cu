@@ -10,6 +10,12 @@
 // (dense.py:94-99), Schur-update the trailing tiles (dense.py:109-116); the prefix is the
 // running sum of 2 log L_ii (memdet.py:428).
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <climits>
 #include <cstdlib>
@@ -67,6 +73,95 @@ constexpr int MAXSLOT = 9;
 
 // The lower tile triangle of an nt x nt tile matrix to factor in place: the whole packed
 // matrix (in-core) or one diagonal block slot (out-of-core).  g0 = global index of its row 0.
+// Host worker threads for staging pageable inputs (e.g. a memory-mapped MEMDET01 file) into
+// pinned buffers: a parallel-for over task indices, run from a CUDA host callback.
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int t = 0; t < n; ++t) th_.emplace_back([this] { work(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // f(0 .. ntask-1) on the workers and the calling thread; returns when all are done
+  void run(int ntask, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> serial(run_m_);  // one parallel-for at a time (contexts share the pool)
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f;
+      ntask_ = ntask;
+      next_ = 0;
+      busy_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (int i; (i = next_.fetch_add(1)) < ntask;) f(i);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return busy_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void work() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      int n;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        f = job_;
+        n = ntask_;
+      }
+      for (int i; (i = next_.fetch_add(1)) < n;) (*f)(i);
+      std::lock_guard<std::mutex> g(m_);
+      if (--busy_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, run_m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int ntask_ = 0, busy_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+constexpr int NHBUF = 4;                       // pinned staging buffers for pageable inputs
+constexpr size_t HBUF_BYTES = (size_t)64 << 20; // (at most; sized to the input's strips)
+constexpr size_t STAGE_MIN_COPY = (size_t)2 << 20;  // smaller pageable copies go to the driver
+static HostPool* host_pool() {  // shared by all contexts, created on first pageable input
+  static HostPool* pool = [] {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return new HostPool((int)std::max(1u, std::min(16u, hw ? hw : 4u) - 1));
+  }();
+  return pool;
+}
+
+struct FillJob {
+  HostPool* pool;
+  char* dst;
+  const char* src;
+  size_t spitch, width, rows;
+};
+static void CUDART_CB fill_cb(void* p) {
+  std::unique_ptr<FillJob> j(static_cast<FillJob*>(p));
+  const size_t per = std::max<size_t>(1, ((size_t)1 << 20) / j->width);  // ~1 MB per task
+  const int ntask = (int)((j->rows + per - 1) / per);
+  j->pool->run(ntask, [&](int t) {
+    const size_t r1 = std::min(j->rows, (size_t)(t + 1) * per);
+    for (size_t r = (size_t)t * per; r < r1; ++r) memcpy(j->dst + r * j->width, j->src + r * j->spitch, j->width);
+  });
+}
+
 struct FactorTarget {
   TileMap map;
   int nt;
@@ -134,6 +229,24 @@ struct Ctx {
   double* prefix = nullptr;  // n_pad
   unsigned long long* fail = nullptr;
   double* strip[NSTAGE] = {};  // host-ingest staging strips (128 x n_pad doubles each)
+  // pageable host inputs: each 2D host->HBM copy goes through NHBUF pinned buffers, filled by
+  // host worker threads in a callback on s_fill (stream-ordered, so the enqueue never blocks)
+  bool src_pageable = false;
+  // host-strip ingest cursor: pageable inputs are enqueued band by band as the factorisation is
+  // enqueued (a deep queue of staging callbacks would block the host thread before any
+  // factorisation work is queued); pinned inputs are enqueued up front
+  struct Ingest {
+    const void* a = nullptr;
+    int64_t lda = 0;
+    int dtype = 0, skip = 0, next = 0;
+    bool active = false;
+  } ing;
+  void* hbuf[NHBUF] = {};
+  cudaEvent_t ev_hfill[NHBUF] = {}, ev_hcopy[NHBUF] = {};
+  bool hbuf_used[NHBUF] = {};
+  cudaStream_t s_fill = nullptr;
+  size_t hbuf_bytes = 0;
+  uint64_t hseq = 0;
   double* gram_neg = nullptr;   // Gram formation: -scale * G chunk as tiles
   double* gram_pos = nullptr;   //                   G chunk as tiles
   int64_t gram_cap = 0;         // tiles allocated per buffer
@@ -214,6 +327,15 @@ static int configure_kernels() {
 static void destroy(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->s_fill) {
+    cudaStreamSynchronize(c->s_fill);
+    cudaStreamDestroy(c->s_fill);
+  }
+  for (int k = 0; k < NHBUF; ++k) {
+    if (c->hbuf[k]) cudaFreeHost(c->hbuf[k]);
+    if (c->ev_hfill[k]) cudaEventDestroy(c->ev_hfill[k]);
+    if (c->ev_hcopy[k]) cudaEventDestroy(c->ev_hcopy[k]);
+  }
   if (c->s_main) cudaStreamSynchronize(c->s_main);
   if (c->s_side) cudaStreamSynchronize(c->s_side);
   if (c->s_mid) cudaStreamSynchronize(c->s_mid);
@@ -796,7 +918,8 @@ static void launch_trsm(Ctx* c, cudaStream_t s, const FactorTarget& ft, int p, i
 // steps < s (K = 128*k0, on s_side, after its band event), then joins the regular next-cols /
 // rest updates from step s on.  act[b] <= the step whose next-cols update first touches band b,
 // so every column is current before it is factored.
-static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
+static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
+                           const std::function<void(int)>* step_hook = nullptr) {
   // profiling mode 2: every launch on s_main (serialised replay: per-launch event times are the
   // kernel's own, nothing runs beside it)
   struct Restore {
@@ -821,6 +944,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
   const char* lbe = getenv("B2D_LEFT_BELOW");
   const bool left_below = lbe ? atoi(lbe) != 0 : true;
   for (int st = 0; st < nsteps; ++st) {
+    if (step_hook) (*step_hook)(st);  // host ingest of the bands this step may wait for
     const int k0 = c->bounds[st];
     const int ke = c->bounds[st + 1];
     // panel(k0): its columns were last touched by next-cols(st-1) and rest(st-2)
@@ -907,6 +1031,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands) {
       launch_update(c, c->s_side, ft, ne, std::max(ne, end_active), k0, ke, true);
     cudaEventRecord(c->ev_rest[st], c->s_side);
   }
+  if (step_hook) (*step_hook)(INT_MAX);
   // join the side streams
   cudaEventRecord(c->ev_join, c->s_side);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
@@ -995,7 +1120,10 @@ static void plan_bands(Ctx* c, size_t esz) {
   const int nbands = (nt + BAND - 1) / BAND;
   const int nsteps = (int)c->bounds.size() - 1;
   const double m = (double)c->m, rate = 34e12, chain_rate = 20e12;
-  const double pcie = getenv("B2D_PCIE_GBS") ? atof(getenv("B2D_PCIE_GBS")) * 1e9 : 48e9;
+  // ingest rate of the model: PCIe for pinned inputs; for pageable ones the host staging copies
+  // (measured ~15 GB/s from a memory-mapped file with 16 threads) are the bound
+  const char* rate_env = getenv(c->src_pageable ? "B2D_STAGE_GBS" : "B2D_PCIE_GBS");
+  const double pcie = rate_env ? atof(rate_env) * 1e9 : (c->src_pageable ? 14e9 : 48e9);
   const double col_lat = getenv("B2D_COL_LAT_US") ? atof(getenv("B2D_COL_LAT_US")) * 1e-6 : 900e-6;
   const double tile_flops = 2.0 * T * T * T;
   std::vector<double> arrival(nbands);
@@ -1050,10 +1178,53 @@ static int run_ooc(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t u
 // The strips of a host matrix into the packed triangle (s_copy / s_pack); ev_band[b] is recorded
 // on s_pack once tile-columns [b * BAND, (b + 1) * BAND) are packed.  skip > 0: the leading
 // skip x skip tiles are already in (their strips bring only the columns from skip * 128 on).
-static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype, int skip = 0) {
+// Host -> HBM 2D copy of a host input on stream s.  Pinned sources go straight to the copy
+// engine; pageable ones (a memory-mapped file, a plain ndarray) are staged: rows are copied into
+// one of NHBUF pinned buffers by the host pool in a callback on s_fill, and the DMA from that
+// buffer waits for the fill (the next fill of a buffer waits for its DMA), so host copies and
+// PCIe transfers overlap each other and the factorisation.
+static int h2d_2d(Ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                  cudaStream_t s) {
+  if (width == 0 || height == 0) return B2D_OK;
+  if (!c->src_pageable || width * height < STAGE_MIN_COPY) {
+    CUDA_TRY(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, s));
+    return B2D_OK;
+  }
+  if (!c->s_fill) {
+    // buffers of two 128-row strips of the matrix (at most HBUF_BYTES): a small input does not
+    // pin 256 MB
+    c->hbuf_bytes = std::min(HBUF_BYTES, std::max(STAGE_MIN_COPY, (size_t)2 * T * (size_t)c->m * 8));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->s_fill, cudaStreamNonBlocking));
+    for (int k = 0; k < NHBUF; ++k) {
+      CUDA_TRY(cudaHostAlloc(&c->hbuf[k], c->hbuf_bytes, cudaHostAllocDefault));
+      cudaEventCreateWithFlags(&c->ev_hfill[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->ev_hcopy[k], cudaEventDisableTiming);
+    }
+  }
+  const size_t per = std::max<size_t>(1, c->hbuf_bytes / width);
+  for (size_t r0 = 0; r0 < height; r0 += per) {
+    const size_t rows = std::min(per, height - r0);
+    const int k = (int)(c->hseq++ % NHBUF);
+    if (c->hbuf_used[k]) cudaStreamWaitEvent(c->s_fill, c->ev_hcopy[k], 0);
+    auto* job = new FillJob{host_pool(), (char*)c->hbuf[k], (const char*)src + r0 * spitch, spitch, width, rows};
+    if (cudaLaunchHostFunc(c->s_fill, fill_cb, job) != cudaSuccess) {
+      delete job;
+      return set_err(B2D_ERR_CUDA, "cudaLaunchHostFunc failed");
+    }
+    cudaEventRecord(c->ev_hfill[k], c->s_fill);
+    cudaStreamWaitEvent(s, c->ev_hfill[k], 0);
+    CUDA_TRY(cudaMemcpy2DAsync((char*)dst + r0 * dpitch, dpitch, c->hbuf[k], width, width, rows,
+                               cudaMemcpyHostToDevice, s));
+    cudaEventRecord(c->ev_hcopy[k], s);
+    c->hbuf_used[k] = true;
+  }
+  return B2D_OK;
+}
+
+static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype, int skip, int J0, int J1) {
   const int64_t npad = (int64_t)c->nt * T;
   const size_t esz = dtype == B2D_F64 ? 8 : 4;
-  for (int J = 0; J < c->nt; ++J) {
+  for (int J = J0; J < J1; ++J) {
     const int b = J % NSTAGE;
     const int64_t r0 = (int64_t)J * T;
     const int64_t rows = std::min<int64_t>(T, c->m - r0);
@@ -1066,8 +1237,9 @@ static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype, int
       const char* src = (const char*)a + (size_t)(r0 * lda + c0) * esz;
       // staged with leading dimension npad, offset so that column c0 lands at index c0
       char* dst = (char*)c->strip[b] + (size_t)c0 * esz;
-      CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)npad * esz, src, (size_t)lda * esz, (size_t)cols * esz,
-                                 (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+      if (int rc = h2d_2d(c, dst, (size_t)npad * esz, src, (size_t)lda * esz, (size_t)cols * esz, (size_t)rows,
+                          c->s_copy))
+        return rc;
       c->h2d += rows * cols * (int64_t)esz;
     }
     cudaEventRecord(c->ev_copied[b], c->s_copy);
@@ -1088,9 +1260,32 @@ static int ingest_host_strips(Ctx* c, const void* a, int64_t lda, int dtype, int
   return B2D_OK;
 }
 
+// Enqueue the host strips [ing.next, J1) (whole bands) of the run's input.
+static int ingest_upto(Ctx* c, int J1) {
+  if (!c->ing.active) return B2D_OK;
+  J1 = std::min(c->nt, ((J1 + BAND - 1) / BAND) * BAND);
+  if (J1 <= c->ing.next) return B2D_OK;
+  const int rc = ingest_host_strips(c, c->ing.a, c->ing.lda, c->ing.dtype, c->ing.skip, c->ing.next, J1);
+  c->ing.next = J1;
+  return rc;
+}
+static int ingest_start(Ctx* c, const void* a, int64_t lda, int dtype, int skip) {
+  c->ing = Ctx::Ingest{a, lda, dtype, skip, 0, true};
+  return c->src_pageable ? B2D_OK : ingest_upto(c, c->nt);
+}
+
 static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  {
+    // pageable input (not page-locked): staged through pinned buffers (h2d_2d); B2D_HOST_STAGING=0
+    // leaves it to the driver's pageable copies
+    cudaPointerAttributes pa{};
+    const bool known = cudaPointerGetAttributes(&pa, a) == cudaSuccess;
+    cudaGetLastError();
+    const char* hs = getenv("B2D_HOST_STAGING");
+    c->src_pageable = (hs ? atoi(hs) != 0 : true) && (!known || pa.type == cudaMemoryTypeUnregistered);
+  }
   if (c->ooc) return run_ooc(c, a, lda, dtype, user);
   if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, true, user);
   if (c->lu_ic) return run_lu_incore(c, a, lda, dtype, true, user);
@@ -1101,9 +1296,24 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
     if (!c->strip[b]) CUDA_TRY(cudaMalloc(&c->strip[b], (size_t)T * npad * 8));
   begin(c, user);
   plan_bands(c, esz);
-  int rc = ingest_host_strips(c, a, lda, dtype);
+  int rc = ingest_start(c, a, lda, dtype, 0);
   if (rc) return rc;
-  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, true);
+  // pageable: the bands step 0 waits for now, then each step enqueues the bands that join the
+  // updates up to two steps ahead (enqueue_factor's hook runs before the step's waits)
+  const int nbands = (c->nt + BAND - 1) / BAND;
+  auto bands_upto = [&](int st) {
+    int b = 0;
+    while (b < nbands && c->act[b] <= st) ++b;
+    return b * BAND;
+  };
+  if ((rc = ingest_upto(c, bands_upto(-1)))) return rc;
+  int hook_rc = 0;
+  const std::function<void(int)> hook = [&](int st) {
+    if (!hook_rc) hook_rc = ingest_upto(c, st == INT_MAX ? c->nt : bands_upto(st + 2));
+  };
+  enqueue_factor(c, FactorTarget{TileMap{c->tiles, 0, c->nt}, c->nt, 0}, true, &hook);
+  if (hook_rc) return hook_rc;
+  c->ing.active = false;
   enqueue_prefix(c);
   cudaEventRecord(c->ev_join, c->s_pack);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
@@ -1159,8 +1369,9 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
       const int64_t frow = (int64_t)ri * o.b + (int64_t)J * T;
       const int64_t nrows = std::min<int64_t>(T, rows_blk - (int64_t)J * T);
       const char* src = (const char*)a + ((size_t)frow * lda + (size_t)rj * o.b) * esz;
-      CUDA_TRY(cudaMemcpy2DAsync(o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)cols_blk * esz,
-                                 (size_t)nrows, cudaMemcpyHostToDevice, o.s_h2d));
+      if (int rc = h2d_2d(c, o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)cols_blk * esz,
+                          (size_t)nrows, o.s_h2d))
+        return rc;
       c->h2d += nrows * cols_blk * (int64_t)esz;
       if (dtype == B2D_F64)
         pack_block_nt_kernel<double><<<o.tiles(rj), 256, 0, o.s_h2d>>>(
@@ -1178,8 +1389,9 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
       const int64_t frow = (int64_t)ri * o.b + (int64_t)J * T;            // first file row of the strip
       const int64_t nrows = std::min<int64_t>(T, cols_blk - (int64_t)J * T);
       const char* src = (const char*)a + ((size_t)frow * lda + (size_t)rj * o.b) * esz;
-      CUDA_TRY(cudaMemcpy2DAsync(o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)rows_blk * esz,
-                                 (size_t)nrows, cudaMemcpyHostToDevice, o.s_h2d));
+      if (int rc = h2d_2d(c, o.stage, (size_t)ld_stage * esz, src, (size_t)lda * esz, (size_t)rows_blk * esz,
+                          (size_t)nrows, o.s_h2d))
+        return rc;
       c->h2d += nrows * rows_blk * (int64_t)esz;
       if (dtype == B2D_F64)
         pack_block_kernel<double><<<o.tiles(rj), PACK_THREADS, PACK_SMEM, o.s_h2d>>>(
@@ -1778,8 +1990,9 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const size_t esz = dtype == B2D_F64 ? 8 : 4;
       if (!c->bstage[0]) CUDA_TRY(cudaMalloc(&c->bstage[0], (size_t)ldb * ldb * 8));
       cudaStreamWaitEvent(c->s_copy, c->ev_start, 0);
-      CUDA_TRY(cudaMemcpy2DAsync(c->bstage[0], (size_t)ldb * esz, a, (size_t)lda * esz, (size_t)b0 * esz, (size_t)b0,
-                                 cudaMemcpyHostToDevice, c->s_copy));
+      if (int rc = h2d_2d(c, c->bstage[0], (size_t)ldb * esz, a, (size_t)lda * esz, (size_t)b0 * esz, (size_t)b0,
+                          c->s_copy))
+        return rc;
       c->h2d += b0 * b0 * (int64_t)esz;
       cudaEventRecord(c->ev_copied[0], c->s_copy);
       cudaStreamWaitEvent(c->s_pack, c->ev_copied[0], 0);
@@ -1794,7 +2007,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       }
       cudaEventRecord(o.ev_fac, c->s_pack);
     }
-    int rc = ingest_host_strips(c, a, lda, dtype, skip);
+    int rc = ingest_start(c, a, lda, dtype, skip);
     if (rc) return rc;
   } else {
     const unsigned ntiles = (unsigned)n_packed_tiles(nt);
@@ -1808,6 +2021,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     for (auto& e : c->ev_band) cudaEventRecord(e, c->s_pack);
   }
   auto wait_cols = [&](cudaStream_t st, int j1) {  // tile-columns [0, j1) packed
+    if (host) ingest_upto(c, j1);  // pageable input: enqueued as needed
     const int b = std::min((int)c->ev_band.size(), (j1 + BAND - 1) / BAND) - 1;
     if (b >= 0) cudaStreamWaitEvent(st, c->ev_band[b], 0);
   };
@@ -1985,9 +2199,10 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
     if (host) {
       const int sb = nblk & 1;
       if (nblk >= 2) cudaStreamWaitEvent(c->s_copy, c->ev_bstage[sb], 0);
-      CUDA_TRY(cudaMemcpy2DAsync(c->bstage[sb], (size_t)ldb * esz,
-                                 (const char*)a + ((size_t)I * o.b * lda + (size_t)J * o.b) * esz, (size_t)lda * esz,
-                                 (size_t)cols * esz, (size_t)rows, cudaMemcpyHostToDevice, c->s_copy));
+      if (int rc = h2d_2d(c, c->bstage[sb], (size_t)ldb * esz,
+                          (const char*)a + ((size_t)I * o.b * lda + (size_t)J * o.b) * esz, (size_t)lda * esz,
+                          (size_t)cols * esz, (size_t)rows, c->s_copy))
+        return rc;
       cudaEventRecord(c->ev_copied[sb], c->s_copy);
       cudaStreamWaitEvent(c->s_pack, c->ev_copied[sb], 0);
       c->h2d += rows * cols * (int64_t)esz;
