@@ -27,6 +27,7 @@ import os
 import subprocess
 import sys
 import threading
+import tempfile
 import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
@@ -391,6 +392,33 @@ def run_engine(args):
                       "api": "paper_2503_04424_b200.memdet_ldl(pinned host ndarray, num_blocks=8)",
                       "logdet": lres.logabsdet}
 
+    # e2e from a MEMDET01 file (the reference's own input form: memory-mapped, pageable; staged
+    # through pinned buffers by host threads), on tmpfs when there is one
+    e2e_file = None
+    if not args.no_file:
+        from paper_2503_04424_b200.storage import MatrixFile
+        fdir = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        fpath = os.path.join(fdir, f"b2d_bench_c2_{os.getpid()}.mdm")
+        try:
+            mm = MatrixFile.create(fpath, n, "f64", "spd").memmap("r+")
+            for r0 in range(0, n, 2048):
+                mm[r0:r0 + 2048] = host[r0:r0 + 2048]
+            mm.flush()
+            del mm
+            eng.memdet_cholesky(fpath, num_blocks=C2["num_blocks"])  # warm
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                fres = eng.memdet_cholesky(fpath, num_blocks=C2["num_blocks"])
+            fsec = (time.perf_counter() - t0) / e2e_steps
+            eng.release_engine_cache()
+            e2e_file = {"value": flops / fsec / 1e12, "unit": UNIT, "seconds_per_step": fsec, "steps": e2e_steps,
+                        "h2d_bytes_per_step": int(fres.info.h2d_bytes), "d2h_bytes_per_step": int(fres.info.d2h_bytes),
+                        "api": "paper_2503_04424_b200.memdet_cholesky('<file>.mdm', num_blocks=8) (MEMDET01 file "
+                               f"on {fdir}, memory-mapped)", "logdet": fres.logabsdet}
+        finally:
+            if os.path.exists(fpath):
+                os.remove(fpath)
+
     # out-of-core (the north star's configs[4] schedule): the reference's tile walk on a C3-sized
     # RBF Gram (n = 65536, 34 GB in pinned host memory; the C2 points extended, nested) with
     # num_blocks=4 (b = 16384) under a 24 GB HBM budget -- 6 block slots in HBM, the 17 GB
@@ -487,6 +515,7 @@ def run_engine(args):
             "gpu_launches": launches_per_step * args.steps,
             "ozaki": ozaki,
             "ldl": ldl,
+            "e2e_file": e2e_file,
             "out_of_core": ooc,
             "clocks": clocks.summary(),
         }
@@ -627,6 +656,7 @@ def main():
     ap.add_argument("--no-ozaki", action="store_true", help="skip the opt-in int8-emulated Schur line")
     ap.add_argument("--no-ldl", action="store_true", help="skip the memdet_ldl (block-pivoted) line")
     ap.add_argument("--no-ooc", action="store_true", help="skip the out-of-core line")
+    ap.add_argument("--no-file", action="store_true", help="skip the MEMDET01-file e2e line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

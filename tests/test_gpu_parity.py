@@ -644,3 +644,46 @@ def test_ozaki_c2_full_size_vs_independent_gpu_factorisation():
     ref = torch.cumsum(2.0 * torch.log(torch.diagonal(low)), 0).cpu().numpy()
     del low
     assert rel_err(res.prefix, ref) <= 1e-10, rel_err(res.prefix, ref)
+
+
+# ------------------------------------------------------------------ pageable (file) inputs
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_memdet01_file_input_staged_equals_pinned(tmp_path, dtype, monkeypatch):
+    """A MEMDET01 file (memory-mapped: pageable host memory, the reference's own input form)
+    goes through the pinned staging buffers filled by host threads; the bytes, hence every
+    result, must equal the pinned-input run and the driver's own pageable copies
+    (B2D_HOST_STAGING=0): Cholesky (in core and forced out of core), pivoted LDL, LU."""
+    torch = pytest.importorskip("torch")
+    from paper_2503_04424_b200.storage import write_matrix
+
+    m = 2304  # 128-row strips of 2.4 MB (f64): above the staging threshold
+    spd = gen.spd_wishart(m, m, seed=7, shift=1e-2).astype(dtype)
+    sym = gen.random_symmetric(m, seed=8).astype(dtype)
+    gen_m = (np.random.default_rng(9).standard_normal((m, m)) + 2.0 * np.sqrt(m) * np.eye(m)).astype(dtype)
+    ps, py, pg = tmp_path / "spd.mdm", tmp_path / "sym.mdm", tmp_path / "gen.mdm"
+    write_matrix(ps, spd, "spd")
+    write_matrix(py, sym, "symmetric")
+    write_matrix(pg, gen_m, "generic")
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64 if dtype == np.float64 else torch.float32, pin_memory=True)
+        t.numpy()[:] = a
+        return t.numpy()
+
+    runs = {
+        "chol": (lambda x: eng.memdet_cholesky(x, num_blocks=3).prefix, ps, spd),
+        "chol_ooc": (lambda x: eng.memdet_cholesky(x, num_blocks=3, out_of_core=True).prefix, ps, spd),
+        "ldl": (lambda x: eng.memdet_ldl(x, num_blocks=3).prefix, py, sym),
+        "lu": (lambda x: np.array([eng.memdet_lu(x, num_blocks=3).logabsdet]), pg, gen_m),
+    }
+    for name, (f, path, arr) in runs.items():
+        monkeypatch.setenv("B2D_HOST_STAGING", "1")
+        staged = f(str(path))
+        ref = f(pinned(arr))
+        monkeypatch.setenv("B2D_HOST_STAGING", "0")
+        driver = f(str(path))
+        eng.release_engine_cache()
+        assert np.array_equal(staged.view(np.uint8), ref.view(np.uint8)), name
+        assert np.array_equal(staged.view(np.uint8), driver.view(np.uint8)), name
