@@ -1274,7 +1274,15 @@ static int ingest_start(Ctx* c, const void* a, int64_t lda, int dtype, int skip)
   return c->src_pageable ? B2D_OK : ingest_upto(c, c->nt);
 }
 
+static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
+// An enqueue that fails half-way may leave staging callbacks pending on s_fill; they read the
+// caller's buffer, so they finish before the error returns (the caller may free it).
 static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
+  const int rc = factor_host_impl(c, a, lda, dtype, user);
+  if (rc != B2D_OK && c->s_fill) cudaStreamSynchronize(c->s_fill);
+  return rc;
+}
+static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   {
