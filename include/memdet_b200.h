@@ -120,7 +120,10 @@ int b2d_ctx_destroy(b2d_ctx *ctx);
  * (a cudaStream_t, 0 = legacy default).  Results stay on the device until b2d_ctx_fetch. */
 int b2d_ctx_factor_device_async(b2d_ctx *ctx, const void *dev_a, int64_t lda, int dtype,
                                 void *stream);
-/* Same, from HOST memory (pinned or pageable): streams the upper tile triangle in strips. */
+/* Same, from HOST memory (pinned or pageable): streams the upper tile triangle in strips.
+ * Pinned memory is read by DMA; pageable memory (a memory-mapped file, malloc'd memory) is
+ * copied into pinned staging buffers by the library's host threads in stream order.  Either
+ * way `host_a` is read after the call returns: keep it valid until b2d_ctx_fetch. */
 int b2d_ctx_factor_host_async(b2d_ctx *ctx, const void *host_a, int64_t lda, int dtype,
                               void *stream);
 /* Wait for the enqueued work, check for failure, copy the outputs to host (any may be NULL). */
