@@ -2120,14 +2120,24 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       // after the whole panel (issued after the next factor, which takes its SMs first)
       cudaStreamWaitEvent(c->s_side, c->ev_panel[k], 0);
       if (serial) cudaStreamWaitEvent(c->s_side, c->ev_catch[k + 1], 0);
-      wait_cols(c->s_side, nt);
       // block column k+2 first (the next stage's next-col update waits for it alone), then the
-      // rest: two launches over disjoint tiles, each tile's operands and K unchanged
+      // rest: launches over disjoint tiles, each tile's operands and K unchanged.  Host input,
+      // stage 0: the rest goes block column by block column, each as soon as its strips are in
+      // (the matrix is still streaming in)
       const int i2 = k + 2 < nb ? std::min(nt, i0 + kb1 + o.tiles(k + 2)) : nt;
+      const bool by_cols = host && k == 0;
+      wait_cols(c->s_side, by_cols ? i2 : nt);
       u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 1, 0};
       launch_update_kchunked(c, c->s_side, u);
       cudaEventRecord(c->ev_resta[k], c->s_side);
-      if (i2 < nt) {
+      if (by_cols) {
+        for (int q = k + 3, j0 = i2; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
+          const int j1 = std::min(nt, j0 + o.tiles(q));
+          wait_cols(c->s_side, j1);
+          u.out = TileSet{j0, nt, j0, j1, 1, 0};
+          launch_update_kchunked(c, c->s_side, u);
+        }
+      } else if (i2 < nt) {
         u.out = TileSet{i2, nt, i2, nt, 1, 0};
         launch_update_kchunked(c, c->s_side, u);
       }
