@@ -676,6 +676,16 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       // diagonal blocks within the cluster panel kernel's reach (the reported counters stay
       // the reference's)
       const bool lu_fits = mode != B2D_MODE_LU || b <= (int64_t)LC * LC_RMAX;
+      // pivoted LDL: the pivots are searched inside the reference's blocks (block-local 1x1
+      // pivoting, _ldl.pyx), so a finer grid would change perm and the prefixes -- never grow
+      if (mode == B2D_MODE_LDL_PIV && need > budget) {
+        destroy(c);
+        return set_err(B2D_ERR_NOMEM,
+                       "block-pivoted LDL keeps the reference's %lld blocks of %lld rows (its pivots depend on "
+                       "them): the out-of-core walk needs %.2f GB of HBM, the budget is %.2f GB (raise hbm_budget, "
+                       "or use more num_blocks / a smaller max_mem, or pivoting='none')",
+                       (long long)n_b, (long long)b, need / 1e9, budget / 1e9);
+      }
       if ((need <= budget && lu_fits) || n_b >= m) {
         if (need > budget) {
           destroy(c);

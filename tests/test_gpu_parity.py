@@ -687,3 +687,17 @@ def test_memdet01_file_input_staged_equals_pinned(tmp_path, dtype, monkeypatch):
         eng.release_engine_cache()
         assert np.array_equal(staged.view(np.uint8), ref.view(np.uint8)), name
         assert np.array_equal(staged.view(np.uint8), driver.view(np.uint8)), name
+
+
+def test_pivoted_ldl_out_of_core_keeps_reference_blocks():
+    """The out-of-core planner may refine the block grid for Cholesky (results do not depend on
+    it), never for the block-pivoted LDL, whose pivots are searched inside the reference's
+    blocks: under a budget its walk cannot meet it fails loudly instead of pivoting over other
+    blocks; with room, perm and prefixes are the reference's."""
+    a = gen.random_symmetric(1536, seed=12)
+    with pytest.raises(MemoryError, match="keeps the reference's"):
+        eng.memdet_ldl(a, num_blocks=2, hbm_budget=20 << 20, out_of_core=True)
+    res = eng.memdet_ldl(a, num_blocks=2, hbm_budget=1 << 30, out_of_core=True)
+    ref_perm, ref_prefix, _, _ = O.memdet_ldl(a, 2)
+    np.testing.assert_array_equal(res.perm, ref_perm)
+    assert rel_err(res.prefix, ref_prefix) <= 1e-10
