@@ -2255,16 +2255,26 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
     return B2D_OK;
   };
   int rc = 0;
-  if (host) {
-    for (int k = 0; k < nb; ++k) {
-      if ((rc = ingest(k, k))) return rc;
+  // host input: cross sets enqueued up to `upto` (pinned: all at once; pageable: as the stages
+  // need them, since the staging callbacks would otherwise block this thread before the first
+  // factor is queued)
+  int crosses = 0;
+  auto ingest_crosses = [&](int upto) -> int {
+    for (int k = crosses; k < std::min(upto, nb); ++k) {
+      int r;
+      if ((r = ingest(k, k))) return r;
       if (k == 0) cudaEventRecord(o.ev_fac, c->s_pack);  // block (0, 0)
       for (int j = k + 1; j < nb; ++j)
-        if ((rc = ingest(k, j))) return rc;
+        if ((r = ingest(k, j))) return r;
       for (int i = k + 1; i < nb; ++i)
-        if ((rc = ingest(i, k))) return rc;
+        if ((r = ingest(i, k))) return r;
       cudaEventRecord(c->ev_cross[k], c->s_pack);
+      crosses = k + 1;
     }
+    return B2D_OK;
+  };
+  if (host) {
+    if ((rc = ingest_crosses(getenv("B2D_LU_ALL_CROSSES") ? nb : 2))) return rc;
   } else {  // resident: one pack launch per 128-row strip
     for (int J = 0; J < nt; ++J) {
       const char* sr = (const char*)a + (size_t)J * T * lda * esz;
@@ -2315,6 +2325,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
     u.p1 = kb;
     const double K = (double)kb * T;
     if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // cross k+1 current
+    if (host && (rc = ingest_crosses(k + 2))) return rc;
     cudaStreamWaitEvent(c->s_mid, c->ev_cross[k + 1], 0);
     u.out = TileSet{i0, nt, i0, i0 + kb1, 0, 0};
     launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
@@ -2329,6 +2340,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
     if (i0 + kb1 < nt) {
       cudaStreamWaitEvent(c->s_side, o.ev_diag, 0);
       if (k > 0 || !host) {
+        if (host && (rc = ingest_crosses(nb))) return rc;
         cudaStreamWaitEvent(c->s_side, c->ev_cross[nb - 1], 0);
         // block column and block row k+2 first (the next stage's cross update waits for them
         // alone), then the rest of the square: disjoint tiles, operands and K unchanged
@@ -2349,6 +2361,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
         // cross sets of the later stages (block (s, s), row s, column s), each as it arrives
         for (int st = 2; st < nb; ++st) {
           const int s0 = col0(st), s1 = s0 + o.tiles(st);
+          if ((rc = ingest_crosses(st + 1))) return rc;
           cudaStreamWaitEvent(c->s_side, c->ev_cross[st], 0);
           u.out = TileSet{s0, s1, s0, nt, 0, 0};
           launch_gemm(c, c->s_side, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
