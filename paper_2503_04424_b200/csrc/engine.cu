@@ -1281,7 +1281,9 @@ static int ingest_upto(Ctx* c, int J1) {
 }
 static int ingest_start(Ctx* c, const void* a, int64_t lda, int dtype, int skip) {
   c->ing = Ctx::Ingest{a, lda, dtype, skip, 0, true};
-  return c->src_pageable ? B2D_OK : ingest_upto(c, c->nt);
+  const char* pe = getenv("B2D_INGEST_PROGRESSIVE");
+  const bool progressive = pe ? atoi(pe) != 0 : c->src_pageable;
+  return progressive ? B2D_OK : ingest_upto(c, c->nt);
 }
 
 static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
