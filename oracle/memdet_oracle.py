@@ -214,7 +214,7 @@ class OracleInfo:
     scratch_slots: int
 
 
-def memdet_symmetric(mat: np.ndarray, n_b: int, pivoted: bool):
+def memdet_symmetric(mat: np.ndarray, n_b: int, pivoted: bool, inplace: bool = False):
     """memdet.py:322-389 — blocked right-looking LDL^T (pivoted) or Cholesky (not).
 
     `mat` is the full symmetric matrix (row-major, as stored in a MEMDET01 file).  Tiles
@@ -222,11 +222,12 @@ def memdet_symmetric(mat: np.ndarray, n_b: int, pivoted: bool):
     each stage factors the diagonal tile, lower-solves the row-k tiles once, scales them by
     D^{-1} for LDL, and applies `T -= C^T B` to every trailing (i <= j) tile.
     Returns (d, perm, info): d = D (LDL) or diag(L) (Cholesky), perm block-local pivots.
+    inplace=True overwrites `mat` (full-size goldens whose copy would not fit host memory).
     """
     m = mat.shape[0]
     lay = from_grid(m, n_b)
     nb = lay.n_b
-    work = np.array(mat, copy=True)  # stands in for file + scratchpad
+    work = mat if inplace else np.array(mat, copy=True)  # stands in for file + scratchpad
     d_all = np.empty(m, mat.dtype)
     perm_all = np.arange(m, dtype=np.int64)
     reads = 1  # tile (0, 0) loaded before stage 0 (memdet.py:345)
@@ -279,15 +280,15 @@ def memdet_symmetric(mat: np.ndarray, n_b: int, pivoted: bool):
     return d_all, perm_all, info
 
 
-def memdet_cholesky(mat: np.ndarray, n_b: int):
+def memdet_cholesky(mat: np.ndarray, n_b: int, inplace: bool = False):
     """memdet.py:415-433 — prefix[q-1] = sum_{i<q} 2 log L_ii (sequential cumsum)."""
-    d, _, info = memdet_symmetric(mat, n_b, pivoted=False)
+    d, _, info = memdet_symmetric(mat, n_b, pivoted=False, inplace=inplace)
     return np.cumsum(2.0 * np.log(d)), info
 
 
-def memdet_ldl(mat: np.ndarray, n_b: int):
+def memdet_ldl(mat: np.ndarray, n_b: int, inplace: bool = False):
     """memdet.py:392-412 — (perm, prefix = cumsum log|d|, signs = cumprod sign d)."""
-    d, perm, info = memdet_symmetric(mat, n_b, pivoted=True)
+    d, perm, info = memdet_symmetric(mat, n_b, pivoted=True, inplace=inplace)
     prefix = np.cumsum(np.log(np.abs(d)))
     signs = np.cumprod(np.sign(d)).astype(np.int64)
     return perm, prefix, signs, info

@@ -2,7 +2,7 @@
 
     python -m paper_2503_04424_b200 memdet --in K.mdm --assume spd --num-blocks 8 --json
     python -m paper_2503_04424_b200 gen --kind rbf --n 4096 --out K.mdm
-    python -m paper_2503_04424_b200 cost --m 4096 --nb 4 --case sym --json
+    python -m paper_2503_04424_b200 cost --m 4096 --nb 4 [--case gen|sym] --json
     python -m paper_2503_04424_b200 flodance --prefix K.pfx --d 1 --n0 5 --ns 3000 --q 1 --predict 4096
     python -m paper_2503_04424_b200 pipeline --kind rbf --n 4096 --out K.mdm --assume spd --ns 3000 --json
 
@@ -111,12 +111,15 @@ def cmd_gen(args) -> int:
 def cmd_cost(args) -> int:
     case = {"gen": "generic", "sym": "symmetric"}[args.case]
     pc = predicted_cost(args.m, args.nb, case)
+    def num(x):  # exact counts stay JSON integers (reference cost.py:58-60)
+        return int(x) if x.denominator == 1 else float(x)
+
     ops = {}
     for name in ("decomposition", "lower_solve", "upper_solve", "full_multiply", "gramian_multiply"):
         op = getattr(pc, name)
-        ops[name] = {"count": float(op.count), "flops_per_op": float(op.flops_per_op), "total": float(op.total)}
+        ops[name] = {"count": num(op.count), "flops_per_op": num(op.flops_per_op), "total": num(op.total)}
     payload = {"schema_version": SCHEMA_VERSION, "m": pc.m, "n_b": pc.n_b, "b": pc.m // pc.n_b,
-               "case": pc.case, "operations": ops, "total_flops": float(pc.total_flops),
+               "case": pc.case, "operations": ops, "total_flops": num(pc.total_flops),
                "blocks_read": pc.blocks_read, "blocks_written": pc.blocks_written,
                "scratch_slots": pc.scratch_slots}
     _emit(args, payload, [f"total FMA {float(pc.total_flops):.6g}, reads {pc.blocks_read}, "
@@ -213,7 +216,7 @@ def build_parser() -> argparse.ArgumentParser:
     p = sub.add_parser("cost", help="analytical cost model query")
     p.add_argument("--m", type=int, required=True)
     p.add_argument("--nb", type=int, required=True)
-    p.add_argument("--case", choices=("gen", "sym"), default="sym")
+    p.add_argument("--case", choices=("gen", "sym"), default="gen")  # reference cli.py:276-279
     p.add_argument("--json", action="store_true")
     p.set_defaults(func=cmd_cost)
 

@@ -672,10 +672,23 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
       const size_t need = (size_t)(nslot + (pivoted ? 1 : 0)) * nbt * nbt * TILE_BYTES +
                           (size_t)nbt * TILE_BYTES +
                           (size_t)T * nbt * T * 8 + 3 * (size_t)(m + (int64_t)(nbt + 1) * T) * 8;
-      // LU: |det| does not depend on where the pivots are searched, so the engine keeps its
-      // diagonal blocks within the cluster panel kernel's reach (the reported counters stay
-      // the reference's)
-      const bool lu_fits = mode != B2D_MODE_LU || b <= (int64_t)LC * LC_RMAX;
+      // LU pivots inside the reference's diagonal blocks (block-local partial pivoting,
+      // dense.py:38-54), so a finer grid would change the result (a zero leading block of a
+      // finer grid is singular where the reference's block is not) -- never grow it either
+      if (mode == B2D_MODE_LU && b > (int64_t)LC * LC_RMAX) {
+        destroy(c);
+        return set_err(B2D_ERR_UNSUPPORTED,
+                       "generic LU factors the reference's %lld-row diagonal blocks with a cluster panel kernel "
+                       "that holds at most %d rows: use num_blocks >= %lld (or a smaller max_mem)",
+                       (long long)b, LC * LC_RMAX, (long long)ceil_div(m, (int64_t)LC * LC_RMAX));
+      }
+      if (mode == B2D_MODE_LU && need > budget) {
+        destroy(c);
+        return set_err(B2D_ERR_NOMEM,
+                       "generic LU keeps the reference's %lld blocks of %lld rows (its pivots depend on them): "
+                       "the out-of-core walk needs %.2f GB of HBM, the budget is %.2f GB",
+                       (long long)n_b, (long long)b, need / 1e9, budget / 1e9);
+      }
       // pivoted LDL: the pivots are searched inside the reference's blocks (block-local 1x1
       // pivoting, _ldl.pyx), so a finer grid would change perm and the prefixes -- never grow
       if (mode == B2D_MODE_LDL_PIV && need > budget) {
@@ -686,7 +699,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
                        "or use more num_blocks / a smaller max_mem, or pivoting='none')",
                        (long long)n_b, (long long)b, need / 1e9, budget / 1e9);
       }
-      if ((need <= budget && lu_fits) || n_b >= m) {
+      if (need <= budget || n_b >= m) {
         if (need > budget) {
           destroy(c);
           return set_err(B2D_ERR_NOMEM, "no out-of-core plan fits %.2f GB of HBM", budget / 1e9);
@@ -1276,8 +1289,12 @@ static int ingest_upto(Ctx* c, int J1) {
   J1 = std::min(c->nt, ((J1 + BAND - 1) / BAND) * BAND);
   if (J1 <= c->ing.next) return B2D_OK;
   const int rc = ingest_host_strips(c, c->ing.a, c->ing.lda, c->ing.dtype, c->ing.skip, c->ing.next, J1);
+  if (rc) {
+    c->ing.active = false;  // strips from ing.next on were not all enqueued: no later wait may pass
+    return rc;
+  }
   c->ing.next = J1;
-  return rc;
+  return B2D_OK;
 }
 static int ingest_start(Ctx* c, const void* a, int64_t lda, int dtype, int skip) {
   c->ing = Ctx::Ingest{a, lda, dtype, skip, 0, true};
@@ -1289,9 +1306,16 @@ static int ingest_start(Ctx* c, const void* a, int64_t lda, int dtype, int skip)
 static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user);
 // An enqueue that fails half-way may leave staging callbacks pending on s_fill; they read the
 // caller's buffer, so they finish before the error returns (the caller may free it).
+// DMA copies already enqueued on the ingest streams read it too (pinned inputs always, small
+// pageable copies through the driver), so every stream that may touch it is drained.
 static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   const int rc = factor_host_impl(c, a, lda, dtype, user);
-  if (rc != B2D_OK && c->s_fill) cudaStreamSynchronize(c->s_fill);
+  if (rc != B2D_OK) {
+    for (cudaStream_t s : {c->s_fill, c->s_copy, c->s_pack, c->o.s_h2d, c->s_main, c->s_mid, c->s_side, c->o.s_walk})
+      if (s) cudaStreamSynchronize(s);
+    c->ing.active = false;
+    c->pending = false;
+  }
   return rc;
 }
 static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
@@ -2040,10 +2064,12 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     c->launches++;
     for (auto& e : c->ev_band) cudaEventRecord(e, c->s_pack);
   }
-  auto wait_cols = [&](cudaStream_t st, int j1) {  // tile-columns [0, j1) packed
-    if (host) ingest_upto(c, j1);  // pageable input: enqueued as needed
+  auto wait_cols = [&](cudaStream_t st, int j1) -> int {  // tile-columns [0, j1) packed
+    if (host)
+      if (int e = ingest_upto(c, j1)) return e;  // pageable input: enqueued as needed
     const int b = std::min((int)c->ev_band.size(), (j1 + BAND - 1) / BAND) - 1;
     if (b >= 0) cudaStreamWaitEvent(st, c->ev_band[b], 0);
+    return B2D_OK;
   };
   auto col0 = [&](int k) { return (int)((int64_t)k * o.b / T); };
   const TileMap packed{c->tiles, 0, nt};
@@ -2065,7 +2091,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   };
   tmark("start", 0, c->s_main);
   if (skip > 0) cudaStreamWaitEvent(c->s_main, o.ev_fac, 0);
-  else wait_cols(c->s_main, col0(0) + o.tiles(0));
+  else if ((rc = wait_cols(c->s_main, col0(0) + o.tiles(0)))) return rc;
   tmark("factor-begin", 0, c->s_main);
   if ((rc = ldl_factor_block(c, diag_map(0), 0, c->s_main))) return rc;
   tmark("factor-end", 0, c->s_main);
@@ -2079,7 +2105,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     cudaStreamWaitEvent(c->s_mid, c->ev_catch[k], 0);
     const int pb = k % 3;  // panel buffers: three, so panel k waits only for rest k-3
     if (k >= 3) cudaStreamWaitEvent(c->s_mid, c->ev_rest[k - 3], 0);  // last reader of pan[pb]
-    wait_cols(c->s_mid, i0);
+    if ((rc = wait_cols(c->s_mid, i0))) return rc;
     // B2D_LDL_SPLIT (default 1): the rows of block k+1 are solved and its diagonal block
     // updated first, so the next factor starts on them while the rows below are solved
     const char* spe = getenv("B2D_LDL_SPLIT");
@@ -2107,7 +2133,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     u.p1 = kb;
     const double K = (double)kb * T;
     if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // block column k+1 current
-    wait_cols(c->s_mid, i0 + kb1);
+    if ((rc = wait_cols(c->s_mid, i0 + kb1))) return rc;
     u.out = TileSet{i0, r_split, i0, i0 + kb1, 1, 0};
     launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
     tmark("next-col-end", k, c->s_mid);
@@ -2138,14 +2164,14 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       // (the matrix is still streaming in)
       const int i2 = k + 2 < nb ? std::min(nt, i0 + kb1 + o.tiles(k + 2)) : nt;
       const bool by_cols = host && k == 0;
-      wait_cols(c->s_side, by_cols ? i2 : nt);
+      if ((rc = wait_cols(c->s_side, by_cols ? i2 : nt))) return rc;
       u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 1, 0};
       launch_update_kchunked(c, c->s_side, u);
       cudaEventRecord(c->ev_resta[k], c->s_side);
       if (by_cols) {
         for (int q = k + 3, j0 = i2; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
           const int j1 = std::min(nt, j0 + o.tiles(q));
-          wait_cols(c->s_side, j1);
+          if ((rc = wait_cols(c->s_side, j1))) return rc;
           u.out = TileSet{j0, nt, j0, j1, 1, 0};
           launch_update_kchunked(c, c->s_side, u);
         }

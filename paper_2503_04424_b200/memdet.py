@@ -21,6 +21,7 @@ from __future__ import annotations
 import math
 import threading
 import time
+from contextlib import contextmanager
 from dataclasses import dataclass, field, replace
 from typing import Iterator, NamedTuple
 
@@ -227,36 +228,67 @@ def _pick_layout(m: int, itemsize: int, max_mem, num_blocks) -> BlockLayout:
     return select_blocking(m, Budget(max_mem, itemsize))[1]
 
 
-# One cached engine context (HBM workspace) per (device, m, mode): repeated runs on the same
-# order reuse their allocation, as a plan cache would.
-_ctx_cache: dict = {}
+# Engine contexts (HBM workspaces) are leased, one run at a time: a run takes an idle context
+# of its (device, m, mode, plan) key or creates one, and returns it to the idle pool when it has
+# fetched its outputs, so repeated runs on the same order reuse their allocation (a plan cache)
+# while concurrent runs -- distinct files may proceed in parallel -- each own
+# their workspace.  Creating a context first frees every IDLE context (HBM); a context in use is
+# never closed, and release_engine_cache() closes those only when they come back.
+_ctx_idle: dict = {}
 _ctx_lock = threading.Lock()
+_ctx_generation = 0
 
 
-def _context(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
-             out_of_core=None, emulation=False) -> _native.Context:
+def _ctx_matches(ctx: _native.Context, mode: int, num_blocks: int, max_mem: int) -> bool:
+    # an in-core plan ignores the reference tiling (except the block-pivoted LDL and LU, which
+    # pivot inside the reference's blocks); an out-of-core one is built from it
+    tiled = ctx.out_of_core or mode in (_native.MODE_LDL_PIV, _native.MODE_LU)
+    return not tiled or ctx.key[4:6] == (num_blocks, max_mem)
+
+
+@contextmanager
+def _lease(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
+           out_of_core=None, emulation=False) -> Iterator[_native.Context]:
+    global _ctx_generation
     kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
               max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation))
     base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"])
+    ctx = None
+    stale = []
     with _ctx_lock:
-        ctx = _ctx_cache.get(base)
-        # an in-core plan ignores the reference tiling (except the block-pivoted LDL and LU, which
-        # pivot inside the reference's blocks); an out-of-core one is built from it
-        tiled = ctx is not None and (ctx.out_of_core or mode in (_native.MODE_LDL_PIV, _native.MODE_LU))
-        if ctx is not None and (not tiled or ctx.key[4:6] == (kw["num_blocks"], kw["max_mem"])):
-            return ctx
-        for k in list(_ctx_cache):
-            _ctx_cache.pop(k).close()
+        idle = _ctx_idle.get(base, [])
+        for i, c in enumerate(idle):
+            if _ctx_matches(c, mode, kw["num_blocks"], kw["max_mem"]):
+                ctx = idle.pop(i)
+                break
+        if ctx is None:  # free the idle workspaces before allocating a new one
+            for k in list(_ctx_idle):
+                stale.extend(_ctx_idle.pop(k))
+        gen = _ctx_generation
+    for c in stale:
+        c.close()
+    if ctx is None:
         ctx = _native.Context(m, mode, device, **kw)
-        _ctx_cache[base] = ctx
-        return ctx
+    try:
+        yield ctx
+    finally:
+        with _ctx_lock:
+            keep = gen == _ctx_generation
+            if keep:
+                _ctx_idle.setdefault(base, []).append(ctx)
+        if not keep:
+            ctx.close()
 
 
 def release_engine_cache():
-    """Free the cached HBM workspace."""
+    """Free the idle HBM workspaces (contexts in use are freed when their run returns them)."""
+    global _ctx_generation
     with _ctx_lock:
-        for k in list(_ctx_cache):
-            _ctx_cache.pop(k).close()
+        _ctx_generation += 1
+        stale = [c for v in _ctx_idle.values() for c in v]
+        _ctx_idle.clear()
+    for c in stale:
+        c.close()
 
 
 def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max_mem, hbm_budget,
@@ -268,41 +300,40 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     if src.device_ptr is not None and mode == _native.MODE_LU:
         # the generic walk streams reference blocks from host memory
         src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
-    if src.device_ptr is not None and mode == _native.MODE_LDL_PIV:
-        # in core when the reference's blocks are tile-aligned and fit; else the block walk,
-        # which streams reference blocks from host memory
-        ctx = _context(m, mode, src.device_index, emulation=emulation, **ooc_kw)
-        if ctx.out_of_core:
-            src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
-    if src.device_ptr is not None:
-        if out_of_core:
-            raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
-        kw = ooc_kw if mode == _native.MODE_LDL_PIV else {}
-        ctx = _context(m, mode, src.device_index, emulation=emulation, **kw)
-        import torch
+    if src.device_ptr is not None and out_of_core:
+        raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
+    on_device = src.device_ptr is not None
+    kw = ooc_kw if (not on_device or mode == _native.MODE_LDL_PIV) else {}
+    with _lease(m, mode, src.device_index if on_device else device, emulation=emulation, **kw) as ctx:
+        if on_device and mode == _native.MODE_LDL_PIV and ctx.out_of_core:
+            # the block-pivoted LDL runs in core when the reference's blocks are tile-aligned and
+            # fit; else the block walk, which streams reference blocks from host memory
+            src.host, src.device_ptr, on_device = src.keepalive.cpu().numpy(), None, False
+        if on_device:
+            import torch
 
-        stream = torch.cuda.current_stream(src.device_index).cuda_stream
-        ctx.factor_device_async(src.device_ptr, src.lda, dcode, stream)
-    else:
-        ctx = _context(m, mode, device, emulation=emulation, **ooc_kw)
-        a, lda = src.host_rowmajor()
-        ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
-    d = np.empty(m, np.float64)
-    prefix = np.empty(m, np.float64)
-    rc, fail, info = ctx.fetch(d, prefix)
-    if rc == _native.B2D_ERR_NOT_SPD:
-        raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
-                          f"(global pivot {fail})")
-    if rc == _native.B2D_ERR_INDEFINITE:
-        raise IndefiniteBlockError(f"LDL pivot {fail} below tolerance: {_native.last_error()}")
-    _native.check(rc, "memdet engine")
-    perm = None
-    if mode in (_native.MODE_LDL_PIV, _native.MODE_LU):
-        perm = np.empty(m, np.int64)
-        ctx.fetch_perm(perm)
+            stream = torch.cuda.current_stream(src.device_index).cuda_stream
+            ctx.factor_device_async(src.device_ptr, src.lda, dcode, stream)
+        else:
+            a, lda = src.host_rowmajor()
+            ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
+        d = np.empty(m, np.float64)
+        prefix = np.empty(m, np.float64)
+        rc, fail, info = ctx.fetch(d, prefix)
+        if rc == _native.B2D_ERR_NOT_SPD:
+            raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
+                              f"(global pivot {fail})")
+        if rc == _native.B2D_ERR_INDEFINITE:
+            raise IndefiniteBlockError(f"LDL pivot {fail} below tolerance: {_native.last_error()}")
+        _native.check(rc, "memdet engine")
+        perm = None
+        if mode in (_native.MODE_LDL_PIV, _native.MODE_LU):
+            perm = np.empty(m, np.int64)
+            ctx.fetch_perm(perm)
+        ooc = ctx.out_of_core
     if mode == _native.MODE_LU:
-        return d, prefix, info, ctx.out_of_core, (perm, fail)
-    return d, prefix, info, ctx.out_of_core, perm
+        return d, prefix, info, ooc, (perm, fail)
+    return d, prefix, info, ooc, perm
 
 
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
@@ -376,9 +407,10 @@ def memdet_lu(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, device
     partial pivoting over the reference's blocks (memdet.py:268-319): in core when its blocks
     start on tile boundaries and the matrix fits (the stages with the matrix resident), else
     the reference's generic block walk out of core.  A singular matrix returns (-inf, 0)
-    rather than raising, as the reference.  Pivots are searched inside the engine's diagonal
-    blocks (|det| and its sign do not depend on the pivot order; the reported block counters
-    are the reference's for its n_b)."""
+    rather than raising, as the reference.  Pivots are searched inside the reference's diagonal
+    blocks, as the reference's (a block-local pivot search sees only its block, so the grid is
+    never refined); blocks over 6144 rows raise NotImplementedError (the cluster panel kernel's
+    reach) and a walk that does not fit the HBM budget raises MemoryError."""
     del scratch_dir
     d, prefix, info, (perm, fail) = _memdet(matrix, _native.MODE_LU, "generic", max_mem, num_blocks, device,
                                             assume or "generic", hbm_budget, out_of_core)

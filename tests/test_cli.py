@@ -24,6 +24,21 @@ def test_cost_json(capsys):
     assert out["schema_version"] == 1 and (out["blocks_read"], out["blocks_written"], out["scratch_slots"]) == (18, 8, 6)
 
 
+def test_cost_defaults_to_generic_with_exact_integers(capsys):
+    """`cost --m M --nb N` without --case is the generic case, and exact counts are JSON ints
+    (reference cli.py:276-279, cost.py:58-60)."""
+    from paper_2503_04424_b200.cost import predicted_cost
+
+    assert main(["cost", "--m", "4096", "--nb", "4", "--json"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    pc = predicted_cost(4096, 4, "generic")
+    assert out["case"] == "generic"
+    assert isinstance(out["total_flops"], int) and out["total_flops"] == pc.total_flops
+    for name, op in out["operations"].items():
+        assert all(isinstance(op[k], int) for k in ("count", "flops_per_op", "total")), (name, op)
+        assert op["total"] == getattr(pc, name).total
+
+
 def test_usage_and_io_exit_codes(tmp_path, capsys):
     p = tmp_path / "g.mdm"
     write_matrix(p, gen.random_spd(8, seed=1), "generic")
