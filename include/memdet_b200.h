@@ -83,6 +83,12 @@ typedef struct b2d_options {
   int32_t emulation;       /* trailing Schur updates of the in-core driver: 0 FP64 DMMA tensor
                               cores (default); 1 FP64 emulated on the int8 tcgen05 tensor cores
                               (Ozaki scheme, 8 slices, error ~3 u relative to sum |a b|)      */
+  int32_t f32_arith;       /* B2D_MODE_LDL_PIV on float32 inputs: 1 factors in float32 with the
+                              reference's own f32 rounding sequence (memdet.py:337-338: d_all in
+                              the file dtype; _ldl.pyx `floating`; tolerance 64 eps(f32) max|A|),
+                              so perm / D / prefixes are the reference's; in core only.  The
+                              context then takes B2D_F32 inputs only.  0: f32 inputs are
+                              converted to f64 (round-1 behaviour)                             */
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;

@@ -50,14 +50,18 @@ class OracleIndefinite(Exception):
         self.step = step
 
 
+_SRCS = ("ldl_tile.c", "ldl32_model.c")
+
+
 def build_oracle_lib(force: bool = False) -> str:
-    """Compile ldl_tile.c with gcc into oracle/_build (test infrastructure)."""
-    src = os.path.join(_HERE, "ldl_tile.c")
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+    """Compile ldl_tile.c and ldl32_model.c with gcc into oracle/_build (test infrastructure).
+    -ffp-contract=off: the restated roundings are the written ones (FMA only where fmaf says)."""
+    srcs = [os.path.join(_HERE, f) for f in _SRCS]
+    if force or not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(f) for f in srcs):
         os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
-        rc = os.system(f"gcc -O2 -fPIC -shared -o {_LIB_PATH} {src} -lm")
+        rc = os.system(f"gcc -O2 -ffp-contract=off -fPIC -shared -o {_LIB_PATH} {' '.join(srcs)} -lm")
         if rc != 0:
-            raise RuntimeError("failed to build oracle ldl_tile.c")
+            raise RuntimeError("failed to build the oracle C sources")
     return _LIB_PATH
 
 
@@ -71,6 +75,10 @@ def _load():
             fn.restype = ctypes.c_int64
             fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double]
+        fn = lib.oracle_memdet_ldl32
+        fn.restype = ctypes.c_int64
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                       ctypes.c_void_p]
         _lib = lib
     return _lib
 
@@ -325,3 +333,16 @@ def run_stage0(mat: np.ndarray, n_b: int):
         tile = work[lay.span(i), lay.span(j)]
         tile -= solved[i].T @ solved[j]
     return work
+
+
+def memdet_ldl32(mat: np.ndarray, n_b: int):
+    """memdet.py:392-412 on a float32 file, with the f32 roundings of the reference's own calls on
+    the golden host (ldl32_model.c): (perm, d (float32), fail or -1).  prefix as the reference:
+    np.cumsum(np.log(np.abs(d))) in float32."""
+    m = mat.shape[0]
+    lay = from_grid(m, n_b)
+    work = np.array(mat, dtype=np.float32, order="C", copy=True)
+    d = np.zeros(m, np.float32)
+    perm = np.arange(m, dtype=np.int64)
+    fail = _load().oracle_memdet_ldl32(work.ctypes.data, m, lay.n_b, lay.b, d.ctypes.data, perm.ctypes.data)
+    return perm, d, int(fail)

@@ -37,7 +37,8 @@ class RunInfoC(ctypes.Structure):
 class OptionsC(ctypes.Structure):
     _fields_ = [("hbm_budget", ctypes.c_int64), ("num_blocks", ctypes.c_int64),
                 ("max_mem", ctypes.c_int64), ("force_out_of_core", ctypes.c_int32),
-                ("host_scratch", ctypes.c_int32), ("emulation", ctypes.c_int32)]
+                ("host_scratch", ctypes.c_int32), ("emulation", ctypes.c_int32),
+                ("f32_arith", ctypes.c_int32)]
 
 
 MAX_PEERS = 8
@@ -160,11 +161,12 @@ class Context:
 
     def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0, hbm_budget: int = 0,
                  num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False,
-                 host_scratch: bool = False, emulation: bool = False):
+                 host_scratch: bool = False, emulation: bool = False, f32_arith: bool = False):
         lib = load()
         h = ctypes.c_void_p()
         opt = OptionsC(int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                       int(bool(force_out_of_core)), int(bool(host_scratch)), int(bool(emulation)))
+                       int(bool(force_out_of_core)), int(bool(host_scratch)), int(bool(emulation)),
+                       int(bool(f32_arith)))
         check(lib.b2d_ctx_create_ex(device, m, mode, ctypes.byref(opt), ctypes.byref(h)),
               "b2d_ctx_create_ex")
         self._h = h
@@ -172,7 +174,7 @@ class Context:
         self.mode = mode
         self.device = device
         self.key = (device, m, mode, int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                    bool(force_out_of_core), bool(host_scratch), bool(emulation))
+                    bool(force_out_of_core), bool(host_scratch), bool(emulation), bool(f32_arith))
 
     @property
     def scratch_on_device(self) -> bool:

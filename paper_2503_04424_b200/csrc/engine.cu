@@ -33,6 +33,7 @@
 #include "ldl.cu"
 #include "lu.cu"
 #include "ozaki.cu"
+#include "ldl32.cu"
 
 namespace b2d {
 
@@ -286,6 +287,20 @@ struct Ctx {
   double* ublk[2] = {};
   double* bstage[2] = {};                     // host ingest: one reference block each
   std::vector<cudaEvent_t> ev_bstage, ev_cross;  // staging buffer free; stage k's blocks packed
+  // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
+  // block column-major in dense, the stage's solved row-k blocks X and their D^{-1}-scaled copy S
+  bool ldl32 = false;
+  struct F32 {
+    float* M = nullptr;
+    int64_t ldm = 0;
+    float* dense = nullptr;
+    int64_t ldd = 0;
+    float *X = nullptr, *S = nullptr;
+    int64_t ldx = 0;
+    float* work = nullptr;
+    float* d = nullptr;
+    unsigned* amax = nullptr;
+  } f;
 };
 
 static int configure_kernels() {
@@ -320,6 +335,7 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L32_TRSM_SMEM));
   done = true;
   return B2D_OK;
 }
@@ -402,6 +418,9 @@ static void destroy(Ctx* c) {
   cudaFree(o.dblk_odd);
   for (cudaEvent_t e : {o.ev_fac, o.ev_diag, o.ev_work})
     if (e) cudaEventDestroy(e);
+  for (void* q : {(void*)c->f.M, (void*)c->f.dense, (void*)c->f.X, (void*)c->f.S, (void*)c->f.work, (void*)c->f.d,
+                  (void*)c->f.amax})
+    cudaFree(q);
   cudaFree(o.stage);
   for (double* h : o.pool) {
     if (o.dev_scratch) cudaFree(h);
@@ -590,7 +609,48 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
   bool oz = opt && opt->emulation == 1;
   if (const char* e = getenv("B2D_SCHUR")) oz = strcmp(e, "ozaki") == 0 ? true : (strcmp(e, "dmma") == 0 ? false : oz);
   const size_t oz_need = oz ? 2 * ((size_t)OZ_S * npad_full * (size_t)(16 * T) + (size_t)npad_full * 4) : 0;
-  if (!force && mode == B2D_MODE_LU) {
+  const char* fa_env = getenv("B2D_F32_ARITH");
+  const bool f32a = mode == B2D_MODE_LDL_PIV && opt && opt->f32_arith && (fa_env ? atoi(fa_env) != 0 : true);
+  if (f32a) {
+    // float32 memdet_ldl in the reference's f32 arithmetic (ldl32.cu), in core: the matrix
+    // row-major, the stage's row-k blocks X and S, the dense diagonal block
+    Ooc& o = c->o;
+    c->ldl32 = true;
+    c->nt = nt_full;
+    int64_t nb0 = 1;
+    if (opt->num_blocks > 0) nb0 = opt->num_blocks;
+    else if (opt->max_mem > 0) nb0 = ref_select_blocking(m, opt->max_mem, 4);
+    int64_t n_b, b, tail;
+    ref_layout(m, std::max<int64_t>(1, nb0), &n_b, &b, &tail);
+    o.nb = (int)n_b;
+    o.b = b;
+    o.tail = tail;
+    auto r32 = [](int64_t x) { return (x + 31) / 32 * 32; };
+    Ctx::F32& f = c->f;
+    f.ldm = r32(m);
+    f.ldd = r32(b);
+    f.ldx = r32(std::max<int64_t>(1, m - b));
+    const size_t need = (size_t)m * f.ldm * 4 + (n_b > 1 ? 2 * (size_t)b * f.ldx * 4 : 0) + (size_t)b * f.ldd * 4 +
+                        (size_t)(m + 2 * b) * 16 + 3 * (size_t)npad_full * 8;
+    if (need > budget) {
+      destroy(c);
+      return set_err(B2D_ERR_NOMEM,
+                     "float32 memdet_ldl runs in core in f32 arithmetic: needs %.2f GB of HBM, the budget is %.2f GB",
+                     need / 1e9, budget / 1e9);
+    }
+    ALLOC(f.M, (size_t)m * f.ldm * 4);
+    ALLOC(f.dense, (size_t)b * f.ldd * 4);
+    if (n_b > 1) {
+      ALLOC(f.X, (size_t)b * f.ldx * 4);
+      ALLOC(f.S, (size_t)b * f.ldx * 4);
+    }
+    ALLOC(f.work, (size_t)b * 4);
+    ALLOC(f.d, (size_t)m * 4);
+    ALLOC(f.amax, 4);
+    ALLOC(o.swaps, (size_t)b * 8);
+    ALLOC(o.perm_local, (size_t)b * 8);
+    ALLOC(o.perm_global, (size_t)m * 8);
+  } else if (!force && mode == B2D_MODE_LU) {
     Ooc& o = c->o;
     c->lu_ic = true;
     c->nt = nt_full;
@@ -1091,11 +1151,15 @@ static void end(Ctx* c, cudaStream_t user) {
 }
 
 static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
+static int run_ldl32(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
+static int h2d_2d(Ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                  cudaStream_t s);
 static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
 
 static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  if (c->ldl32) return run_ldl32(c, a, lda, dtype, false, user);
   if (c->ooc)
     return set_err(B2D_ERR_UNSUPPORTED, "out-of-core contexts take host inputs (the matrix exceeds the HBM budget)");
   if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, false, user);
@@ -1330,6 +1394,7 @@ static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaS
     const char* hs = getenv("B2D_HOST_STAGING");
     c->src_pageable = (hs ? atoi(hs) != 0 : true) && (!known || pa.type == cudaMemoryTypeUnregistered);
   }
+  if (c->ldl32) return run_ldl32(c, a, lda, dtype, true, user);
   if (c->ooc) return run_ooc(c, a, lda, dtype, user);
   if (c->ldl_ic) return run_ldl_incore(c, a, lda, dtype, true, user);
   if (c->lu_ic) return run_lu_incore(c, a, lda, dtype, true, user);
@@ -2207,6 +2272,106 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   return B2D_OK;
 }
 
+// float32 memdet_ldl in the reference's f32 arithmetic (memdet.py:322-412 on a float32 file;
+// ldl32.cu, oracle/ldl32_model.c).  All on s_main, stage by stage: the diagonal block factored
+// one pivot step at a time (the reference's unblocked loop), the row-k blocks gathered in pivot
+// order, solved in STRSM's row blocks, scaled by D^{-1}, and every trailing block (i <= j) updated
+// in SGEMM's K-block order.
+static int run_ldl32(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user) {
+  if (dtype != B2D_F32)
+    return set_err(B2D_ERR_USAGE, "this context factors float32 inputs in f32 arithmetic (got dtype code %d)", dtype);
+  if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
+  CUDA_TRY(cudaSetDevice(c->device));
+  Ooc& o = c->o;
+  Ctx::F32& f = c->f;
+  const int64_t m = c->m, b = o.b;
+  const int nb = o.nb;
+  cudaStream_t s = c->s_main;
+  begin(c, user);
+  // the reference reads the (i <= j) blocks: block row i, columns [i * b, m)
+  for (int bi = 0; bi < nb; ++bi) {
+    const int64_t r0 = (int64_t)bi * b, rows = o.size(bi), cols = m - r0;
+    float* dst = f.M + r0 * f.ldm + r0;
+    const float* src = (const float*)a + r0 * lda + r0;
+    if (host) {
+      if (int rc = h2d_2d(c, dst, (size_t)f.ldm * 4, src, (size_t)lda * 4, (size_t)cols * 4, (size_t)rows, s)) return rc;
+      c->h2d += rows * cols * 4;
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)f.ldm * 4, src, (size_t)lda * 4, (size_t)cols * 4, (size_t)rows,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  int kb[L32_MAXKB + 1];
+  const int nkb = l32_kblocks(b, kb);
+  for (int k = 0; k < nb; ++k) {
+    const int64_t k0 = (int64_t)k * b, hk = o.size(k);
+    cudaMemsetAsync(f.amax, 0, 4, s);
+    const dim3 gb((unsigned)((hk + 31) / 32), (unsigned)((hk + 31) / 32));
+    l32_block_in_kernel<<<gb, 256, 0, s>>>(f.M, f.ldm, k0, hk, f.dense, f.ldd, f.amax);
+    const L32Step g{f.dense, f.ldd, hk, k0, f.work, f.d + k0, o.swaps, c->fail, f.amax};
+    for (int64_t r = 0; r < hk; ++r) {
+      l32_step_kernel<<<1, 1024, 0, s>>>(g, r);
+      if (r + 1 < hk) l32_update_kernel<<<(unsigned)(hk - r - 1), 256, 0, s>>>(g, r);
+    }
+    l32_finish_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (hk + 255) / 256)), 256, 0, s>>>(
+        o.swaps, f.d + k0, hk, k0, o.perm_local, o.perm_global, c->ell, c->diag, c->fail);
+    c->launches += 3 + 2 * hk - 1;
+    if (k == nb - 1) break;
+    const int64_t c0 = k0 + b, W = m - c0;
+    // row-k blocks in pivot order (memdet.py:365-366, 378-379), solved (dense.py:94-99)
+    l32_gather_kernel<<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)),
+                        256, 0, s>>>(f.M, f.ldm, k0, c0, o.perm_local, b, W, f.X, f.ldx);
+    for (int64_t ls = 0; ls < b; ls += L32_Q) {
+      const int64_t le = std::min<int64_t>(b, ls + L32_Q);
+      l32_trsm_diag_kernel<<<(unsigned)((W + L32_TW - 1) / L32_TW), 256, L32_TRSM_SMEM, s>>>(f.dense, f.ldd, f.X, f.ldx,
+                                                                                           W, ls, le, c->fail);
+      c->launches++;
+      if (le < b) {  // rows below the row block: X -= L(le:, ls:le) X(ls:le, :), one chain each
+        G32 u{};
+        u.A = f.dense + ls * f.ldd + le;
+        u.lda = f.ldd;
+        u.B = f.X + ls * f.ldx;
+        u.ldb = f.ldx;
+        u.C = f.X + le * f.ldx;
+        u.ldc = f.ldx;
+        u.Mr = b - le;
+        u.Nc = W;
+        u.nkb = 1;
+        u.kb[0] = 0;
+        u.kb[1] = (int)(le - ls);
+        u.blk = 1;
+        l32_gemm_kernel<<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((b - le + G32_BM - 1) / G32_BM)), 256, 0,
+                          s>>>(u, c->fail);
+        c->launches++;
+      }
+    }
+    // S = X / d (memdet.py:368-371); T(i, j) -= X_i^T S_j for every trailing block i <= j (memdet.py:385)
+    l32_scale_kernel<<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0,
+                       s>>>(f.X, f.S, f.ldx, b, W, f.d + k0);
+    G32 u{};
+    u.A = f.X;
+    u.lda = f.ldx;
+    u.B = f.S;
+    u.ldb = f.ldx;
+    u.C = f.M + c0 * f.ldm + c0;
+    u.ldc = f.ldm;
+    u.Mr = W;
+    u.Nc = W;
+    u.nkb = nkb;
+    for (int q = 0; q <= nkb; ++q) u.kb[q] = kb[q];
+    u.tri = 1;
+    u.blk = b;
+    u.roff = u.coff = c0;
+    l32_gemm_kernel<<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((W + G32_BM - 1) / G32_BM)), 256, 0, s>>>(
+        u, c->fail);
+    c->launches += 4;
+  }
+  enqueue_prefix(c);
+  end(c, user);
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
 // Generic LU in core (memdet_lu; memdet.py:268-319, kernels/dense.py:38-54, 94-106): the
 // reference's stages over its b x b blocks with the matrix resident as a full tile grid.  Stage
 // k: the diagonal block is factored P A = L U with block-local partial pivoting (s_main; L back
@@ -2581,6 +2746,7 @@ int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, i
   b2d_options opt{};
   opt.num_blocks = num_blocks;
   opt.max_mem = max_mem;
+  opt.f32_arith = dtype == B2D_F32 && mode == B2D_MODE_LDL_PIV;
   int rc = create(device, m, mode, &opt, &c);
   if (rc) return rc;
   rc = factor_host(c, a, lda, dtype, 0);

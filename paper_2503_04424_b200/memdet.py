@@ -248,11 +248,12 @@ def _ctx_matches(ctx: _native.Context, mode: int, num_blocks: int, max_mem: int)
 
 @contextmanager
 def _lease(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
-           out_of_core=None, emulation=False) -> Iterator[_native.Context]:
+           out_of_core=None, emulation=False, f32_arith=False) -> Iterator[_native.Context]:
     global _ctx_generation
     kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
-              max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation))
-    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"])
+              max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation),
+              f32_arith=bool(f32_arith))
+    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"], kw["f32_arith"])
     ctx = None
     stale = []
     with _ctx_lock:
@@ -302,9 +303,17 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
         src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
     if src.device_ptr is not None and out_of_core:
         raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
+    # float32 files under block pivoting factor in f32 with the reference's own rounding sequence
+    # (memdet.py:337-338, _ldl.pyx `floating`, dense.py:73 eps of the file dtype): in core
+    f32_arith = mode == _native.MODE_LDL_PIV and src.dtype == np.float32
+    if f32_arith and out_of_core:
+        raise ValueError("float32 memdet_ldl factors in core (f32 arithmetic); out_of_core=True is not available")
     on_device = src.device_ptr is not None
     kw = ooc_kw if (not on_device or mode == _native.MODE_LDL_PIV) else {}
-    with _lease(m, mode, src.device_index if on_device else device, emulation=emulation, **kw) as ctx:
+    if f32_arith:
+        kw = dict(kw, out_of_core=None)
+    with _lease(m, mode, src.device_index if on_device else device, emulation=emulation, f32_arith=f32_arith,
+                **kw) as ctx:
         if on_device and mode == _native.MODE_LDL_PIV and ctx.out_of_core:
             # the block-pivoted LDL runs in core when the reference's blocks are tile-aligned and
             # fit; else the block walk, which streams reference blocks from host memory

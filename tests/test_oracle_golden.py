@@ -99,3 +99,65 @@ def test_ldl_restatement_bit_exact_vs_reference_compiled_kernel(n, seed):
     np.testing.assert_array_equal(sw1, sw2)
     np.testing.assert_array_equal(d1, d2)
     np.testing.assert_array_equal(np.tril(a1, -1), np.tril(a2, -1))
+
+
+def _f32_golden():
+    import json
+    import os
+    import sys
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from make_f32_golden import CASES
+
+    with open(os.path.join(here, "f32.json")) as f:
+        meta = json.load(f)
+    return CASES, meta, np.load(os.path.join(here, "f32.npz"))
+
+
+def _f32_cases():
+    cases, meta, _ = _f32_golden()
+    return [(name, nb) for name, (_, nbs) in cases.items() for nb in nbs]
+
+
+@pytest.mark.parametrize("name,nb", _f32_cases())
+def test_f32_model_bit_exact_vs_reference_goldens(name, nb):
+    """oracle/ldl32_model.c (the reference's memdet_ldl on a float32 file with the f32 rounding
+    sequence of its LDL kernel, STRSM and SGEMM) reproduces the unmodified reference's outputs
+    bit for bit: permutation, signs and the float32 prefix (NumPy's own log / cumsum of d)."""
+    import hashlib
+
+    cases, meta, arr = _f32_golden()
+    a = cases[name][0]().astype(np.float32)
+    assert hashlib.sha256(a.tobytes()).hexdigest() == meta["cases"][name]["input_sha256"]
+    run = meta["cases"][name]["runs"][f"ldl_nb{nb}"]
+    perm, d, fail = O.memdet_ldl32(a, nb)
+    if "error" in run:
+        assert fail >= 0, run
+        return
+    assert fail == -1
+    key = f"{name}__ldl_nb{nb}"
+    np.testing.assert_array_equal(perm, arr[key + "__perm"])
+    np.testing.assert_array_equal(np.cumsum(np.log(np.abs(d))), arr[key + "__prefix"])
+    np.testing.assert_array_equal(np.cumprod(np.sign(d)).astype(np.int64), arr[key + "__signs"])
+
+
+@pytest.mark.parametrize("n,seed", [(33, 2), (200, 4)])
+def test_ldl_restatement_f32_bit_exact_vs_reference_compiled_kernel(n, seed):
+    """The float32 instance of the restated tile kernel vs the reference's compiled `floating`
+    kernel on float32 input."""
+    ref = _ref_ldl()
+    if ref is None:
+        pytest.skip("oracle/_ref not built (reference not mounted)")
+    from paper_2503_04424_b200 import gen
+
+    a0 = gen.random_symmetric(n, seed=seed).astype(np.float32)
+    tol = 64.0 * float(np.finfo(np.float32).eps) * float(np.max(np.abs(a0)))
+    a1 = a0.copy()
+    sw1, d1, w1 = np.empty(n, np.int64), np.empty(n, np.float32), np.empty(n, np.float32)
+    assert ref.ldl_factor(a1, sw1, d1, w1, tol) == -1
+    a2 = a0.copy()
+    sw2, d2 = O.ldl_tile(a2)
+    np.testing.assert_array_equal(sw1, sw2)
+    np.testing.assert_array_equal(d1, d2)
+    np.testing.assert_array_equal(np.tril(a1, -1), np.tril(a2, -1))
