@@ -89,6 +89,12 @@ typedef struct b2d_options {
                               so perm / D / prefixes are the reference's; in core only.  The
                               context then takes B2D_F32 inputs only.  0: f32 inputs are
                               converted to f64 (round-1 behaviour)                             */
+  int32_t ndev;            /* > 1: one context over several devices (devices[0 .. ndev)) in this
+                              process: Cholesky / unpivoted LDL over 1-D block-cyclic outer panels,
+                              each device ingesting only its own panels from host memory, panels
+                              exchanged by peer copies over NVLink; the `device`
+                              argument of b2d_ctx_create_ex is then ignored.  0 / 1: one device */
+  int32_t devices[8];
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;
@@ -104,10 +110,12 @@ int b2d_device_count(void);
  *                          pivoting domain by B2D_MODE_LDL_PIV
  *   d_out     (m) f64: diag(L) for CHOLESKY, D for LDL modes
  *   perm_out  (m) int64 or NULL; prefix_out (m) f64; sign_out (m) int64 or NULL
+ *   devices / ndev  the devices to run on (NULL / 0: device 0); ndev > 1 shards the
+ *            factorisation over them (modes CHOLESKY and LDL_NOPIV; b2d_options.ndev)
  *   fail_index  first failing global pivot (0-based) on B2D_ERR_NOT_SPD / _INDEFINITE
  */
 int b2d_memdet_sym(const void *a, int64_t m, int64_t lda, int dtype, int mode, int64_t num_blocks,
-                   int64_t max_mem, int device, double *d_out, int64_t *perm_out,
+                   int64_t max_mem, const int *devices, int ndev, double *d_out, int64_t *perm_out,
                    double *prefix_out, int64_t *sign_out, b2d_run_info *info,
                    int64_t *fail_index);
 

@@ -38,7 +38,8 @@ class OptionsC(ctypes.Structure):
     _fields_ = [("hbm_budget", ctypes.c_int64), ("num_blocks", ctypes.c_int64),
                 ("max_mem", ctypes.c_int64), ("force_out_of_core", ctypes.c_int32),
                 ("host_scratch", ctypes.c_int32), ("emulation", ctypes.c_int32),
-                ("f32_arith", ctypes.c_int32)]
+                ("f32_arith", ctypes.c_int32), ("ndev", ctypes.c_int32),
+                ("devices", ctypes.c_int32 * 8)]
 
 
 MAX_PEERS = 8
@@ -72,8 +73,8 @@ SIGNATURES = {
     "b2d_version": (_I, []),
     "b2d_last_error": (ctypes.c_char_p, []),
     "b2d_device_count": (_I, []),
-    "b2d_memdet_sym": (_I, [_P, _I64, _I64, _I, _I, _I64, _I64, _I, _P, _P, _P, _P,
-                            ctypes.POINTER(RunInfoC), ctypes.POINTER(_I64)]),
+    "b2d_memdet_sym": (_I, [_P, _I64, _I64, _I, _I, _I64, _I64, ctypes.POINTER(ctypes.c_int), _I, _P, _P, _P,
+                            _P, ctypes.POINTER(RunInfoC), ctypes.POINTER(_I64)]),
     "b2d_ctx_create": (_I, [_I, _I64, _I, ctypes.POINTER(_P)]),
     "b2d_ctx_create_ex": (_I, [_I, _I64, _I, ctypes.POINTER(OptionsC), ctypes.POINTER(_P)]),
     "b2d_ctx_is_out_of_core": (_I, [_P]),
@@ -161,12 +162,21 @@ class Context:
 
     def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0, hbm_budget: int = 0,
                  num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False,
-                 host_scratch: bool = False, emulation: bool = False, f32_arith: bool = False):
+                 host_scratch: bool = False, emulation: bool = False, f32_arith: bool = False,
+                 devices=None):
         lib = load()
         h = ctypes.c_void_p()
         opt = OptionsC(int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
                        int(bool(force_out_of_core)), int(bool(host_scratch)), int(bool(emulation)),
                        int(bool(f32_arith)))
+        devices = tuple(int(x) for x in devices) if devices else ()
+        if len(devices) > 8:
+            raise ValueError(f"at most 8 devices, got {len(devices)}")
+        if len(devices) > 1:
+            opt.ndev = len(devices)
+            for i, dv in enumerate(devices):
+                opt.devices[i] = dv
+            device = devices[0]
         check(lib.b2d_ctx_create_ex(device, m, mode, ctypes.byref(opt), ctypes.byref(h)),
               "b2d_ctx_create_ex")
         self._h = h
@@ -174,7 +184,8 @@ class Context:
         self.mode = mode
         self.device = device
         self.key = (device, m, mode, int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                    bool(force_out_of_core), bool(host_scratch), bool(emulation), bool(f32_arith))
+                    bool(force_out_of_core), bool(host_scratch), bool(emulation), bool(f32_arith), devices)
+        self.devices = devices or (device,)
 
     @property
     def scratch_on_device(self) -> bool:

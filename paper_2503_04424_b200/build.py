@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmemdet_b200.so")
 SOURCES = ["engine.cu"]
-DEPS = ["engine.cu", "kernels.cu", "ldl.cu", "lu.cu", "ozaki.cu", "ldl32.cu", "tile.cuh"]
+DEPS = ["engine.cu", "kernels.cu", "ldl.cu", "lu.cu", "ozaki.cu", "ldl32.cu", "mgpu.cu", "tile.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 

@@ -216,7 +216,12 @@ struct Ooc {
   double* dblk_of(int k) const { return (k & 1) && dblk_odd ? dblk_odd : dblk; }
 };
 
+struct MCtx;  // multi-device context (mgpu.cu)
+
 struct Ctx {
+  MCtx* mg = nullptr;  // set: a front for several devices (b2d_options.ndev > 1)
+  uint64_t hseq_strip = 0;       // multi-device ingest: staging strip rotation
+  bool strip_used[NSTAGE] = {};
   int device = 0;
   int64_t m = 0;
   int mode = B2D_MODE_CHOLESKY;
@@ -340,8 +345,14 @@ static int configure_kernels() {
   return B2D_OK;
 }
 
+static void mg_destroy(MCtx* M);
 static void destroy(Ctx* c) {
   if (!c) return;
+  if (c->mg) {
+    mg_destroy(c->mg);
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   if (c->s_fill) {
     cudaStreamSynchronize(c->s_fill);
@@ -537,8 +548,21 @@ static int create_streams_events(Ctx* c) {
 // n_pad vectors and NSTAGE ingest strips.  Out-of-core (budget exceeded or forced): NSLOT
 // block slots of nbt^2 tiles; the block grid starts at the reference n_b (num_blocks, else
 // select_blocking(max_mem), memdet.py:63-80, 249-255) and grows until the slots fit.
+static int mg_create(const int* devices, int ndev, int64_t m, int mode, const b2d_options* opt, MCtx** out);
 static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx** out) {
   if (m < 1) return set_err(B2D_ERR_USAGE, "matrix dimension must be >= 1, got %lld", (long long)m);
+  if (opt && opt->ndev > 1) {
+    if (opt->ndev > 8) return set_err(B2D_ERR_USAGE, "at most 8 devices (got %d)", opt->ndev);
+    MCtx* M = nullptr;
+    if (int rc = mg_create(opt->devices, opt->ndev, m, mode, opt, &M)) return rc;
+    Ctx* c = new Ctx();
+    c->mg = M;
+    c->device = opt->devices[0];
+    c->m = m;
+    c->mode = mode;
+    *out = c;
+    return B2D_OK;
+  }
   if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV && mode != B2D_MODE_LDL_PIV && mode != B2D_MODE_LU)
     return set_err(B2D_ERR_USAGE, "unknown mode %d", mode);
   int ndev = 0;
@@ -1156,7 +1180,10 @@ static int h2d_2d(Ctx* c, void* dst, size_t dpitch, const void* src, size_t spit
                   cudaStream_t s);
 static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
 
+static int mg_factor(MCtx* M, const void* a, int64_t lda, int dtype, bool host, cudaStream_t user);
+static int mg_fetch(MCtx* M, double* d_out, double* prefix_out, int64_t* fail_index, b2d_run_info* info);
 static int factor_device(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
+  if (c->mg) return mg_factor(c->mg, a, lda, dtype, false, user);
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   if (c->ldl32) return run_ldl32(c, a, lda, dtype, false, user);
@@ -1383,6 +1410,7 @@ static int factor_host(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream
   return rc;
 }
 static int factor_host_impl(Ctx* c, const void* a, int64_t lda, int dtype, cudaStream_t user) {
+  if (c->mg) return mg_factor(c->mg, a, lda, dtype, true, user);
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   if (lda < c->m) return set_err(B2D_ERR_USAGE, "lda %lld < m", (long long)lda);
   {
@@ -2581,6 +2609,7 @@ static int run_lu_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool hos
 }
 
 static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index, b2d_run_info* info) {
+  if (c->mg) return mg_fetch(c->mg, d_out, prefix_out, fail_index, info);
   if (!c->pending) return set_err(B2D_ERR_USAGE, "no factorisation enqueued");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaEventSynchronize(c->ev_stop));
@@ -2651,6 +2680,8 @@ static int fetch_perm(Ctx* c, int64_t* perm) {
   return B2D_OK;
 }
 
+#include "mgpu.cu"
+
 }  // namespace b2d
 
 using namespace b2d;
@@ -2702,7 +2733,10 @@ int b2d_ctx_fetch(b2d_ctx* ctx, double* d_out, double* prefix_out, int64_t* fail
   return fetch(ctx, d_out, prefix_out, fail_index, info);
 }
 
-const double* b2d_ctx_device_prefix(b2d_ctx* ctx) { return ctx ? ctx->prefix : nullptr; }
+const double* b2d_ctx_device_prefix(b2d_ctx* ctx) {
+  if (ctx && ctx->mg) return ctx->mg->r[0].c->prefix;
+  return ctx ? ctx->prefix : nullptr;
+}
 
 int b2d_ctx_fetch_perm(b2d_ctx* ctx, int64_t* perm_out) {
   if (!ctx) return set_err(B2D_ERR_USAGE, "null ctx");
@@ -2732,8 +2766,11 @@ int b2d_ctx_update_stats(b2d_ctx* ctx, double* flops, double* ms, int64_t* launc
 }
 
 int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, int64_t num_blocks,
-                   int64_t max_mem, int device, double* d_out, int64_t* perm_out, double* prefix_out,
-                   int64_t* sign_out, b2d_run_info* info, int64_t* fail_index) {
+                   int64_t max_mem, const int* devices, int ndev, double* d_out, int64_t* perm_out,
+                   double* prefix_out, int64_t* sign_out, b2d_run_info* info, int64_t* fail_index) {
+  if (ndev > 8) return set_err(B2D_ERR_USAGE, "at most 8 devices (got %d)", ndev);
+  if (ndev > 0 && !devices) return set_err(B2D_ERR_USAGE, "null devices with ndev %d", ndev);
+  const int device = ndev > 0 ? devices[0] : 0;
   if (!a || !prefix_out) return set_err(B2D_ERR_USAGE, "null argument");
   if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
   const int esz = dtype == B2D_F64 ? 8 : 4;
@@ -2747,6 +2784,8 @@ int b2d_memdet_sym(const void* a, int64_t m, int64_t lda, int dtype, int mode, i
   opt.num_blocks = num_blocks;
   opt.max_mem = max_mem;
   opt.f32_arith = dtype == B2D_F32 && mode == B2D_MODE_LDL_PIV;
+  opt.ndev = ndev > 1 ? ndev : 0;
+  for (int d = 0; d < ndev && ndev > 1; ++d) opt.devices[d] = devices[d];
   int rc = create(device, m, mode, &opt, &c);
   if (rc) return rc;
   rc = factor_host(c, a, lda, dtype, 0);

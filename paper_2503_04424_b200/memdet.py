@@ -248,12 +248,13 @@ def _ctx_matches(ctx: _native.Context, mode: int, num_blocks: int, max_mem: int)
 
 @contextmanager
 def _lease(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
-           out_of_core=None, emulation=False, f32_arith=False) -> Iterator[_native.Context]:
+           out_of_core=None, emulation=False, f32_arith=False, devices=()) -> Iterator[_native.Context]:
     global _ctx_generation
     kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
               max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation),
-              f32_arith=bool(f32_arith))
-    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"], kw["f32_arith"])
+              f32_arith=bool(f32_arith), devices=tuple(devices))
+    base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"], kw["f32_arith"],
+            kw["devices"])
     ctx = None
     stale = []
     with _ctx_lock:
@@ -293,9 +294,11 @@ def release_engine_cache():
 
 
 def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max_mem, hbm_budget,
-                out_of_core, emulation=False):
+                out_of_core, emulation=False, devices=()):
     dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
     m = src.m
+    if len(devices) > 1:
+        return _run_multi(src, mode, dcode, devices, hbm_budget, out_of_core)
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
     ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
     if src.device_ptr is not None and mode == _native.MODE_LU:
@@ -345,8 +348,34 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     return d, prefix, info, ooc, perm
 
 
+def _run_multi(src: MatrixSource, mode: int, dcode: int, devices, hbm_budget, out_of_core):
+    """Several devices in this process (engine multi-device context): each device
+    ingests only its own outer panels -- from host memory, or read in place from a device tensor
+    over NVLink peer access."""
+    if out_of_core:
+        raise ValueError("out_of_core=True is single-device (the multi-device plan shards the matrix in HBM)")
+    m = src.m
+    with _lease(m, mode, devices[0], hbm_budget=hbm_budget, devices=devices) as ctx:
+        if src.device_ptr is not None:
+            import torch
+
+            torch.cuda.synchronize(src.device_index)  # the engine orders its ranks after the legacy stream
+            ctx.factor_device_async(src.device_ptr, src.lda, dcode, 0)
+        else:
+            a, lda = src.host_rowmajor()
+            ctx.factor_host_async(a.ctypes.data, lda, dcode, 0)
+        d = np.empty(m, np.float64)
+        prefix = np.empty(m, np.float64)
+        rc, fail, info = ctx.fetch(d, prefix)
+        if rc == _native.B2D_ERR_NOT_SPD:
+            raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
+                              f"(global pivot {fail})")
+        _native.check(rc, "memdet engine (multi-device)")
+    return d, prefix, info, False, None
+
+
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
-            out_of_core=None, schur="dmma"):
+            out_of_core=None, schur="dmma", devices=None):
     if schur not in ("dmma", "ozaki"):
         raise ValueError(f"schur must be 'dmma' or 'ozaki', got {schur!r}")
     t0 = time.perf_counter()
@@ -354,8 +383,11 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
     if src.symmetry == "generic" and mode != _native.MODE_LU:
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
+    devices = tuple(int(x) for x in devices) if devices else ()
+    if len(devices) > 1 and schur != "dmma":
+        raise ValueError("schur='ozaki' is single-device")
     d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core,
-                                              schur == "ozaki")
+                                              schur == "ozaki", devices)
     nb = lay.n_b
     case = "generic" if mode == _native.MODE_LU else "symmetric"
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
@@ -373,7 +405,7 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
 
 def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
                     device: int = 0, assume: str | None = None, hbm_budget: int | None = None,
-                    out_of_core: bool | None = None, schur: str = "dmma") -> SpdResult:
+                    out_of_core: bool | None = None, schur: str = "dmma", devices=None) -> SpdResult:
     """Prefix log-determinants of an SPD matrix (blocked Cholesky, no pivoting).
 
     prefix[q-1] = logdet of the leading q x q principal submatrix, summed from 2 log L_ii;
@@ -383,10 +415,12 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
     scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity).
     schur="ozaki" runs the in-core trailing Schur updates as FP64 emulated on the int8 tcgen05
     tensor cores (8-slice Ozaki scheme, error ~3 u relative to sum |a b|); the
-    default "dmma" uses the FP64 tensor cores."""
+    default "dmma" uses the FP64 tensor cores.  devices=[d0, d1, ...] shards the factorisation over
+    several devices of this process (1-D block-cyclic outer panels, each device ingesting only its
+    own panels, panels exchanged over NVLink); hbm_budget is then per device."""
     del scratch_dir
     d, prefix, info, _ = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
-                                 hbm_budget, out_of_core, schur)
+                                 hbm_budget, out_of_core, schur, devices)
     res = SpdResult(prefix=prefix, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:
@@ -461,20 +495,20 @@ def _generic_counts_until(n_b: int, stage: int):
 def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefix_out=None,
                device: int = 0, assume: str | None = None, pivoting: str = "block",
                hbm_budget: int | None = None, out_of_core: bool | None = None,
-               schur: str = "dmma") -> SymmetricResult:
+               schur: str = "dmma", devices=None) -> SymmetricResult:
     """Prefix log-determinants of a symmetric matrix via blocked LDL^T.
 
     pivoting="block" reproduces the reference's block-local 1x1 diagonal pivoting
     (_ldl.pyx:30-46; perm and prefixes of the permuted minors).  pivoting="none" is the
     unpivoted LDL^T (D = L_ii^2 of the Cholesky factor, perm = identity): its prefixes are
     the natural-order leading minors and coincide with the pivoted ones at every block
-    boundary q = k*b and at q = m.  schur as memdet_cholesky (in-core trailing updates)."""
+    boundary q = k*b and at q = m.  schur and devices as memdet_cholesky."""
     del scratch_dir
     if pivoting not in ("block", "none"):
         raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
     mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
     d, prefix, info, perm = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
-                                    out_of_core, schur)
+                                    out_of_core, schur, devices)
     m = len(prefix)
     if mode == _native.MODE_LDL_NOPIV:
         perm = np.arange(m, dtype=np.int64)

@@ -88,7 +88,7 @@ def test_f32_one_shot_c_abi_matches_reference():
     signs = np.empty(m, np.int64)
     info = _native.RunInfoC()
     fail = ctypes.c_int64(-1)
-    rc = _native.load().b2d_memdet_sym(a.ctypes.data, m, m, _native.B2D_F32, _native.MODE_LDL_PIV, 2, 0, 0,
+    rc = _native.load().b2d_memdet_sym(a.ctypes.data, m, m, _native.B2D_F32, _native.MODE_LDL_PIV, 2, 0, None, 0,
                                        d.ctypes.data, perm.ctypes.data, prefix.ctypes.data, signs.ctypes.data,
                                        ctypes.byref(info), ctypes.byref(fail))
     assert rc == 0, _native.last_error()
