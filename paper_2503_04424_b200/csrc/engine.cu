@@ -2670,8 +2670,10 @@ static int fetch(Ctx* c, double* d_out, double* prefix_out, int64_t* fail_index,
   return B2D_OK;
 }
 
+static int mg_fetch_perm(MCtx* M, int64_t* perm);
 static int fetch_perm(Ctx* c, int64_t* perm) {
   if (!perm) return set_err(B2D_ERR_USAGE, "null perm");
+  if (c->mg) return mg_fetch_perm(c->mg, perm);
   if ((c->mode == B2D_MODE_LDL_PIV || c->mode == B2D_MODE_LU) && c->o.perm_global) {
     CUDA_TRY(cudaMemcpy(perm, c->o.perm_global, c->m * 8, cudaMemcpyDeviceToHost));
   } else {

@@ -25,13 +25,28 @@
 // Ranks synchronise on the host only for event ordering (a rank waits until the owner's thread
 // has RECORDED ev_ready[s] before enqueueing a wait on it); the device work is ordered by events
 // alone.  2 log L_ii land in the owners' ell vectors and are gathered into rank 0's, which runs
-// the prefix scan.  Ranks may share a device (tests run P = 2, 3 on one GPU): every dependency
+// the prefix scan.
+//
+// Block-pivoted LDL (memdet_ldl, _ldl.pyx:21-61): the outer panels are the reference's blocks
+// (b a multiple of 128, or one block), so stage k is panel k on rank k mod P: its owner factors
+// the diagonal block with block-local 1x1 pivoting (ldl_factor_block, the single-device kernels)
+// and forms the stage's row-k blocks -- permuted, solved, and D^{-1}-scaled (memdet.py:361-371) --
+// as full-height grids that the other ranks copy; every trailing tile receives the same update
+// (same operands, K and order) as on one device, so perm, D and the prefixes are bit-identical
+// to the single-device run.  Distributing whole reference blocks balances poorly when there are
+// few blocks per rank (C3: 16 blocks over 8 ranks); sub-block distribution with a gather of each
+// block column to its stage owner is the next step.  Ranks may share a device (tests run P = 2, 3 on one GPU): every dependency
 // is a stream-event wait, never a kernel spinning on another rank's kernel.
 
 struct MRank {
   Ctx* c = nullptr;
   std::map<int, double*> pan;  // owned step -> panel grid (rows [k0, nt) x W tiles)
   double* recv[2] = {};
+  // block-pivoted LDL: each owned stage's row-k blocks, unscaled / D^{-1}-scaled (rows [ke, nt) x W
+  // tiles, never overwritten, so the other ranks may copy them any time); received ones in
+  // recv_u / recv_s (full height, tile (i, p) at base + (i W + p))
+  std::map<int, double*> pu, ps;
+  double *recv_u[2] = {}, *recv_s[2] = {};
   int first_own = INT_MAX;     // first owned step
   std::vector<cudaEvent_t> ev_ready, ev_in, ev_src_done;
   cudaEvent_t ev_free[2] = {};
@@ -42,6 +57,7 @@ struct MCtx {
   int P = 0;
   int64_t m = 0;
   int nt = 0, W = 16, mode = 0;
+  bool ldl = false;  // block-pivoted LDL: panels = the reference's blocks
   std::vector<int> devs;
   std::vector<int> bounds;  // panel boundaries (tile-columns), nsteps + 1 entries
   std::vector<MRank> r;
@@ -61,6 +77,9 @@ static void mg_destroy(MCtx* M) {
     cudaDeviceSynchronize();
     for (auto& kv : R.pan) cudaFree(kv.second);
     for (double* q : R.recv) cudaFree(q);
+    for (auto* mp : {&R.pu, &R.ps})
+      for (auto& kv : *mp) cudaFree(kv.second);
+    for (double* q : {R.recv_u[0], R.recv_u[1], R.recv_s[0], R.recv_s[1]}) cudaFree(q);
     for (auto* v : {&R.ev_ready, &R.ev_in, &R.ev_src_done})
       for (auto e : *v)
         if (e) cudaEventDestroy(e);
@@ -81,6 +100,7 @@ static int create_shell(int device, int64_t m, int mode, Ctx** out) {
   c->device = device;
   c->m = m;
   c->mode = mode;
+  c->W_TILES = panel_tiles_default();
   c->nt = (int)((m + T - 1) / T);
   const int64_t npad = (int64_t)c->nt * T;
   bool ok = cudaMalloc((void**)&c->inv, (size_t)c->nt * TILE_BYTES) == cudaSuccess &&
@@ -99,8 +119,22 @@ static int create_shell(int device, int64_t m, int mode, Ctx** out) {
 }
 
 static int mg_create(const int* devices, int ndev, int64_t m, int mode, const b2d_options* opt, MCtx** out) {
-  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV)
-    return set_err(B2D_ERR_UNSUPPORTED, "multi-device runs Cholesky / unpivoted LDL (mode %d requested)", mode);
+  if (mode != B2D_MODE_CHOLESKY && mode != B2D_MODE_LDL_NOPIV && mode != B2D_MODE_LDL_PIV)
+    return set_err(B2D_ERR_UNSUPPORTED, "multi-device runs Cholesky and LDL (mode %d requested)", mode);
+  int64_t ref_nb = 1, ref_b = m, ref_tail = m;
+  if (mode == B2D_MODE_LDL_PIV) {
+    if (opt && opt->f32_arith)
+      return set_err(B2D_ERR_UNSUPPORTED, "float32 memdet_ldl (f32 arithmetic) is single-device");
+    int64_t nb0 = 1;
+    if (opt && opt->num_blocks > 0) nb0 = opt->num_blocks;
+    else if (opt && opt->max_mem > 0) nb0 = ref_select_blocking(m, opt->max_mem, 8);
+    ref_layout(m, std::max<int64_t>(1, nb0), &ref_nb, &ref_b, &ref_tail);
+    if (ref_nb > 1 && ref_b % T != 0)
+      return set_err(B2D_ERR_UNSUPPORTED,
+                     "multi-device block-pivoted LDL needs the reference's blocks on 128-row boundaries "
+                     "(b = %lld; use num_blocks with m / num_blocks a multiple of 128, or one device)",
+                     (long long)ref_b);
+  }
   int nvis = 0;
   if (cudaGetDeviceCount(&nvis) != cudaSuccess || nvis == 0)
     return set_err(B2D_ERR_CUDA, "no CUDA device visible: the B200 engine has no CPU fallback");
@@ -112,7 +146,8 @@ static int mg_create(const int* devices, int ndev, int64_t m, int mode, const b2
   M->mode = mode;
   M->devs.assign(devices, devices + ndev);
   M->nt = (int)((m + T - 1) / T);
-  M->W = std::max(1, env_int("B2D_MG_PANEL_TILES", 16));
+  M->ldl = mode == B2D_MODE_LDL_PIV;
+  M->W = M->ldl ? (int)((ref_b + T - 1) / T) : std::max(1, env_int("B2D_MG_PANEL_TILES", 16));
   for (int k = 0; k < M->nt; k += M->W) M->bounds.push_back(k);
   M->bounds.push_back(M->nt);
   const int S = M->nsteps(), nt = M->nt, W = M->W;
@@ -140,6 +175,12 @@ static int mg_create(const int* devices, int ndev, int64_t m, int mode, const b2
       return rc;
     }
     size_t need = 2 * (size_t)nt * W * TILE_BYTES + (size_t)NSTAGE * T * nt * T * 8;
+    const int64_t ldb = (int64_t)W * T;
+    if (M->ldl) {  // row-k block grids (2 per own stage + 4 receive), the dense block and its state
+      need += 4 * (size_t)nt * W * TILE_BYTES + (size_t)ldb * ldb * 9 + (size_t)(m + 8 * ldb) * 8 +
+              2 * (size_t)W * TILE_BYTES;
+      for (int s = d; s < S; s += ndev) need += 2 * (size_t)(nt - M->bounds[s + 1]) * W * TILE_BYTES;
+    }
     for (int s = d; s < S; s += ndev) need += (size_t)(nt - M->bounds[s]) * W * TILE_BYTES;
     if ((int64_t)need > budget) {
       mg_destroy(M);
@@ -157,9 +198,47 @@ static int mg_create(const int* devices, int ndev, int64_t m, int mode, const b2
     if (ndev > 1)
       for (double*& q : R.recv) ok = ok && cudaMalloc((void**)&q, (size_t)nt * W * TILE_BYTES) == cudaSuccess;
     for (int b = 0; b < NSTAGE && ok; ++b) ok = cudaMalloc(&R.c->strip[b], (size_t)T * nt * T * 8) == cudaSuccess;
+    if (M->ldl && ok) {
+      // the block factor's state (ldl_factor_block), as the single-device in-core LDL has it
+      Ooc& o = R.c->o;
+      o.nb = (int)ref_nb;
+      o.b = ref_b;
+      o.tail = ref_tail;
+      o.nbt = W;
+      const size_t tiles = (size_t)nt * W * TILE_BYTES;
+      for (int s = d; s < S && ok; s += ndev) {
+        const size_t rows = (size_t)(nt - M->bounds[s + 1]);
+        double *u = nullptr, *v = nullptr;
+        if (rows > 0)
+          ok = cudaMalloc((void**)&u, rows * W * TILE_BYTES) == cudaSuccess &&
+               cudaMalloc((void**)&v, rows * W * TILE_BYTES) == cudaSuccess;
+        R.pu[s] = u;
+        R.ps[s] = v;
+      }
+      if (ndev > 1)
+        for (double** q : {&R.recv_u[0], &R.recv_u[1], &R.recv_s[0], &R.recv_s[1]})
+          ok = ok && cudaMalloc((void**)q, tiles) == cudaSuccess;
+      ok = ok && cudaMalloc((void**)&o.dense, (size_t)ldb * ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.swaps, (size_t)ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.perm_local, (size_t)ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.perm_global, (size_t)(m + ldb) * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.dblk, (size_t)ldb * 8) == cudaSuccess && cudaMalloc((void**)&o.amax, 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.ltag, (size_t)ldb * ldb) == cudaSuccess &&
+           cudaMalloc((void**)&o.lC, (size_t)LDL_NB * ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.lW, (size_t)LDL_NB * ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.ldiag, (size_t)ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.lcol, (size_t)ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.inv_odd, (size_t)W * TILE_BYTES) == cudaSuccess &&
+           cudaMalloc((void**)&o.perm_odd, (size_t)ldb * 8) == cudaSuccess &&
+           cudaMalloc((void**)&o.dblk_odd, (size_t)ldb * 8) == cudaSuccess;
+    }
     if (!ok) {
+      const cudaError_t e = cudaGetLastError();
+      size_t fb = 0, tb = 0;
+      cudaMemGetInfo(&fb, &tb);
       mg_destroy(M);
-      return set_err(B2D_ERR_NOMEM, "multi-device: allocation failed on device %d", M->devs[d]);
+      return set_err(B2D_ERR_NOMEM, "multi-device: allocation failed on device %d (rank %d, need %.2f GB, %.2f GB free): %s",
+                     devices[d], d, need / 1e9, fb / 1e9, cudaGetErrorString(e));
     }
     for (auto* v : {&R.ev_ready, &R.ev_in, &R.ev_src_done}) {
       v->resize(S);
@@ -253,16 +332,49 @@ static void mg_factor_panel(MCtx* M, int d, int s) {
   cudaEventRecord(R.ev_ready[s], c->s_mid);
 }
 
+// Block-pivoted LDL stage s on its owner (run_ldl_incore's stage on the panel grid): factor the
+// diagonal block with block-local 1x1 pivots, then the row-k blocks below it -- permuted by the
+// stage's pivots (memdet.py:365-366), solved with the unit factor (dense.py:94-99) into pu and
+// D^{-1}-scaled into ps (memdet.py:368-371), rows indexed by global tile row.
+static int mg_ldl_stage(MCtx* M, int d, int s) {
+  MRank& R = M->r[d];
+  Ctx* c = R.c;
+  Ooc& o = c->o;
+  const int k0 = M->bounds[s], ke = M->bounds[s + 1], nt = M->nt, W = M->W, kb = ke - k0;
+  const TileMap blk{R.pan.at(s), W, 0};  // block-local tile (I, J) of the diagonal block
+  if (int rc = ldl_factor_block(c, blk, s, c->s_main)) return rc;
+  if (ke < nt) {
+    const double* inv_k = (s & 1) && o.inv_odd ? o.inv_odd : c->inv;
+    const TileMap src{R.pan.at(s) + (size_t)kb * W * TILE_ELEMS, W, 0};  // panel rows [ke, nt)
+    const TileMap pu{R.pu.at(s), W, 0};
+    const TileMap ps{R.ps.at(s), W, 0};
+    permute_cols_kernel<<<2048, 256, 0, c->s_main>>>(src, pu, nt - ke, kb, o.size(s), o.perm_of(s));
+    trsm_panel(c, c->s_main, pu, nt - ke, blk, kb, inv_k);
+    scale_cols_kernel<<<2048, 256, 0, c->s_main>>>(pu, ps, nt - ke, kb, o.size(s), o.dblk_of(s));
+    c->launches += 2;
+  }
+  cudaEventRecord(R.ev_ready[s], c->s_main);
+  return B2D_OK;
+}
+
 // T(own panel t) -= L(., s) L(., s)^T over the tiles of t (rows >= its first column), K = panel s.
-static void mg_update(MCtx* M, int d, cudaStream_t st, const TileMap& src, int s, int t) {
+// LDL: T -= (L D^{-1})(., s) L(., s)^T from the stage's scaled / unscaled grids (a = ps, b = pu).
+static void mg_update(MCtx* M, int d, cudaStream_t st, const TileMap& src, int s, int t,
+                      const TileMap* scaled = nullptr) {
   MRank& R = M->r[d];
   const int k0 = M->bounds[s], ke = M->bounds[s + 1], t0 = M->bounds[t], t1 = M->bounds[t + 1];
   GemmTask u{};
   u.a = u.b = src;
-  u.c = mg_panel_map(M, R.pan.at(t), t);
-  u.out = TileSet{t0, M->nt, t0, t1, 1, 0};
   u.p0 = k0;
   u.p1 = ke;
+  if (scaled) {
+    u.a = *scaled;
+    u.p0 = 0;
+    u.p1 = ke - k0;
+  }
+  u.c = mg_panel_map(M, R.pan.at(t), t);
+  u.out = TileSet{t0, M->nt, t0, t1, 1, 0};
+  cudaStreamWaitEvent(st, R.ev_in[t], 0);  // the target panel has arrived
   launch_gemm(R.c, st, MODE_UPDATE, u, s + 1 != t, (double)u.out.count() * 2.0 * T * T * (double)(ke - k0) * T);
 }
 
@@ -294,7 +406,16 @@ static int mg_rank_run(MCtx* M, int d, const void* a, int64_t lda, int dtype, bo
     if (own) {
       cudaStreamWaitEvent(c->s_main, R.ev_in[s], 0);                    // ingested
       if (s >= 2) cudaStreamWaitEvent(c->s_main, R.ev_src_done[s - 2], 0);  // rest updates of s-2
-      mg_factor_panel(M, d, s);
+      if (M->ldl) {
+        if ((rc = mg_ldl_stage(M, d, s))) {
+          std::lock_guard<std::mutex> lk(M->mu);
+          M->recorded[s] = 1;
+          M->cv.notify_all();
+          break;
+        }
+      } else {
+        mg_factor_panel(M, d, s);
+      }
       {
         std::lock_guard<std::mutex> lk(M->mu);
         M->recorded[s] = 1;
@@ -309,10 +430,14 @@ static int mg_rank_run(MCtx* M, int d, const void* a, int64_t lda, int dtype, bo
       cudaEventRecord(R.ev_src_done[s], c->s_side);
       continue;
     }
-    TileMap src;
+    TileMap src, src_s;
     cudaEvent_t src_ev;
     if (own) {
       src = mg_panel_map(M, R.pan.at(s), s);
+      if (M->ldl) {  // rows indexed by global tile row: base shifted back by ke rows
+        src = TileMap{R.pu.at(s) - (size_t)ke * M->W * TILE_ELEMS, M->W, 0};
+        src_s = TileMap{R.ps.at(s) - (size_t)ke * M->W * TILE_ELEMS, M->W, 0};
+      }
       src_ev = R.ev_ready[s];
     } else {
       mg_wait_recorded(M, s);
@@ -324,28 +449,39 @@ static int mg_rank_run(MCtx* M, int d, const void* a, int64_t lda, int dtype, bo
       double* buf = R.recv[s & 1];
       if (used[s & 1]) cudaStreamWaitEvent(c->s_copy, R.ev_free[s & 1], 0);
       cudaStreamWaitEvent(c->s_copy, M->r[o].ev_ready[s], 0);
-      const size_t off = (size_t)(first - k0) * W * TILE_ELEMS;
       const size_t bytes = (size_t)(nt - first) * W * TILE_BYTES;
-      if (c->device == M->r[o].c->device)
-        CUDA_TRY(cudaMemcpyAsync(buf + off, M->r[o].pan.at(s) + off, bytes, cudaMemcpyDeviceToDevice, c->s_copy));
-      else
-        CUDA_TRY(cudaMemcpyPeerAsync(buf + off, c->device, M->r[o].pan.at(s) + off, M->r[o].c->device, bytes,
-                                     c->s_copy));
+      auto pull = [&](double* dst, const double* from) -> int {
+        if (c->device == M->r[o].c->device)
+          CUDA_TRY(cudaMemcpyAsync(dst, from, bytes, cudaMemcpyDeviceToDevice, c->s_copy));
+        else
+          CUDA_TRY(cudaMemcpyPeerAsync(dst, c->device, from, M->r[o].c->device, bytes, c->s_copy));
+        return B2D_OK;
+      };
+      if (M->ldl) {  // the stage's row-k block grids (rows indexed by global tile row)
+        const size_t off = (size_t)first * W * TILE_ELEMS, soff = (size_t)(first - ke) * W * TILE_ELEMS;
+        if ((rc = pull(R.recv_u[s & 1] + off, M->r[o].pu.at(s) + soff))) break;
+        if ((rc = pull(R.recv_s[s & 1] + off, M->r[o].ps.at(s) + soff))) break;
+        src = TileMap{R.recv_u[s & 1], W, 0};
+        src_s = TileMap{R.recv_s[s & 1], W, 0};
+      } else {
+        const size_t off = (size_t)(first - k0) * W * TILE_ELEMS;
+        if ((rc = pull(buf + off, M->r[o].pan.at(s) + off))) break;
+        src = mg_panel_map(M, buf, s);
+      }
       cudaEventRecord(c->ev_catch[s], c->s_copy);
-      src = mg_panel_map(M, buf, s);
       src_ev = c->ev_catch[s];
       used[s & 1] = true;
     }
     // next-cols: the panel the next factor needs (its owner's critical path)
     if (M->owner(s + 1) == d) {
       cudaStreamWaitEvent(c->s_main, src_ev, 0);
-      mg_update(M, d, c->s_main, src, s, s + 1);
+      mg_update(M, d, c->s_main, src, s, s + 1, M->ldl ? &src_s : nullptr);
       cudaEventRecord(c->ev_panel[s], c->s_main);
     }
     // the rest of this rank's panels (low priority, beside the next factor)
     cudaStreamWaitEvent(c->s_side, src_ev, 0);
     for (auto& kv : R.pan)
-      if (kv.first > s + 1) mg_update(M, d, c->s_side, src, s, kv.first);
+      if (kv.first > s + 1) mg_update(M, d, c->s_side, src, s, kv.first, M->ldl ? &src_s : nullptr);
     if (M->owner(s + 1) == d) cudaStreamWaitEvent(c->s_side, c->ev_panel[s], 0);
     cudaEventRecord(R.ev_src_done[s], c->s_side);
     if (!own) cudaEventRecord(R.ev_free[s & 1], c->s_side);
@@ -364,11 +500,11 @@ static int mg_rank_run(MCtx* M, int d, const void* a, int64_t lda, int dtype, bo
     for (auto& kv : R.pan) {
       const int64_t g0 = (int64_t)M->bounds[kv.first] * T, g1 = std::min<int64_t>(M->m, (int64_t)M->bounds[kv.first + 1] * T);
       if (g1 <= g0) continue;
-      for (double* const* v : {&c->ell, &c->diag}) {
-        double* dst = (v == &c->ell ? c0->ell : c0->diag) + g0;
-        const double* srcp = *v + g0;
-        if (c->device == c0->device) cudaMemcpyAsync(dst, srcp, (g1 - g0) * 8, cudaMemcpyDeviceToDevice, c->s_main);
-        else cudaMemcpyPeerAsync(dst, c0->device, srcp, c->device, (g1 - g0) * 8, c->s_main);
+      std::vector<std::pair<void*, const void*>> segs{{c0->ell + g0, c->ell + g0}, {c0->diag + g0, c->diag + g0}};
+      if (M->ldl) segs.emplace_back(c0->o.perm_global + g0, c->o.perm_global + g0);
+      for (auto& sg : segs) {
+        if (c->device == c0->device) cudaMemcpyAsync(sg.first, sg.second, (g1 - g0) * 8, cudaMemcpyDeviceToDevice, c->s_main);
+        else cudaMemcpyPeerAsync(sg.first, c0->device, sg.second, c->device, (g1 - g0) * 8, c->s_main);
       }
     }
   }
@@ -478,7 +614,19 @@ static int mg_fetch(MCtx* M, double* d_out, double* prefix_out, int64_t* fail_in
     info->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - c0->t0).count();
   }
   if (fail_index) *fail_index = fail == ULLONG_MAX ? -1 : (int64_t)fail;
+  if (fail != ULLONG_MAX && M->ldl)
+    return set_err(B2D_ERR_INDEFINITE, "LDL pivot %lld below tolerance (block-local 1x1 pivoting)", (long long)fail);
   if (fail != ULLONG_MAX)
     return set_err(B2D_ERR_NOT_SPD, "leading minor of order %lld is not positive definite", (long long)fail + 1);
+  return B2D_OK;
+}
+
+static int mg_fetch_perm(MCtx* M, int64_t* perm) {
+  if (!M->ldl) {
+    for (int64_t g = 0; g < M->m; ++g) perm[g] = g;
+    return B2D_OK;
+  }
+  CUDA_TRY(cudaSetDevice(M->r[0].c->device));
+  CUDA_TRY(cudaMemcpy(perm, M->r[0].c->o.perm_global, M->m * 8, cudaMemcpyDeviceToHost));
   return B2D_OK;
 }

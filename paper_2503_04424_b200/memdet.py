@@ -298,7 +298,7 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
     m = src.m
     if len(devices) > 1:
-        return _run_multi(src, mode, dcode, devices, hbm_budget, out_of_core)
+        return _run_multi(src, mode, dcode, devices, hbm_budget, out_of_core, lay.n_b)
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
     ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
     if src.device_ptr is not None and mode == _native.MODE_LU:
@@ -348,14 +348,15 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
     return d, prefix, info, ooc, perm
 
 
-def _run_multi(src: MatrixSource, mode: int, dcode: int, devices, hbm_budget, out_of_core):
+def _run_multi(src: MatrixSource, mode: int, dcode: int, devices, hbm_budget, out_of_core, num_blocks):
     """Several devices in this process (engine multi-device context): each device
     ingests only its own outer panels -- from host memory, or read in place from a device tensor
     over NVLink peer access."""
     if out_of_core:
         raise ValueError("out_of_core=True is single-device (the multi-device plan shards the matrix in HBM)")
     m = src.m
-    with _lease(m, mode, devices[0], hbm_budget=hbm_budget, devices=devices) as ctx:
+    # the block-pivoted LDL's stages are the reference's blocks (num_blocks)
+    with _lease(m, mode, devices[0], hbm_budget=hbm_budget, num_blocks=num_blocks, devices=devices) as ctx:
         if src.device_ptr is not None:
             import torch
 
@@ -370,8 +371,14 @@ def _run_multi(src: MatrixSource, mode: int, dcode: int, devices, hbm_budget, ou
         if rc == _native.B2D_ERR_NOT_SPD:
             raise NotSpdError(f"leading minor of order {fail + 1} is not positive-definite "
                               f"(global pivot {fail})")
+        if rc == _native.B2D_ERR_INDEFINITE:
+            raise IndefiniteBlockError(f"LDL pivot {fail} below tolerance: {_native.last_error()}")
         _native.check(rc, "memdet engine (multi-device)")
-    return d, prefix, info, False, None
+        perm = None
+        if mode == _native.MODE_LDL_PIV:
+            perm = np.empty(m, np.int64)
+            ctx.fetch_perm(perm)
+    return d, prefix, info, False, perm
 
 
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,

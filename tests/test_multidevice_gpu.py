@@ -83,14 +83,35 @@ def test_multidevice_c2_full_size_equals_single_device():
     multi = eng.memdet_cholesky(a, num_blocks=8, devices=[0, 0])
     eng.release_engine_cache()
     assert rel_err(multi.prefix, single.prefix) <= 1e-12, rel_err(multi.prefix, single.prefix)
+    # the north star's LDL^T (block-pivoted, 8 blocks): bit-identical to one device
+    lsingle = eng.memdet_ldl(a, num_blocks=8)
+    eng.release_engine_cache()
+    lmulti = eng.memdet_ldl(a, num_blocks=8, devices=[0, 0, 0])
+    eng.release_engine_cache()
+    np.testing.assert_array_equal(lmulti.perm, lsingle.perm)
+    np.testing.assert_array_equal(lmulti.prefix, lsingle.prefix)
 
 
-def test_multidevice_pivoted_ldl_is_explicit_about_support():
-    a = gen.random_symmetric(3000, seed=3)
-    try:
-        res = eng.memdet_ldl(a, num_blocks=3, devices=[0, 0])
-    except NotImplementedError:
-        pytest.skip("block-pivoted LDL over several devices not built")
-    perm, prefix, signs, _ = O.memdet_ldl(a, 3)
+@pytest.mark.parametrize("m,nb,devices", [(3072, 3, [0, 0]), (4096, 4, [0, 0, 0]), (2560, 5, [0, 0]), (1000, 1, [0, 0])])
+def test_multidevice_block_pivoted_ldl_matches_oracle_and_single_device(m, nb, devices):
+    """Stages on their owners, row-k block grids copied across ranks: perm / signs exact vs the
+    oracle (the reference's pivoting), and every output bit-identical to one device."""
+    a = gen.random_symmetric(m, seed=m + nb)
+    perm, prefix, signs, _ = O.memdet_ldl(a, nb)
+    res = eng.memdet_ldl(a, num_blocks=nb, devices=devices)
     np.testing.assert_array_equal(res.perm, perm)
+    np.testing.assert_array_equal(res.prefix_signs, signs)
     assert rel_err(res.prefix, prefix) <= 1e-10
+    single = eng.memdet_ldl(a, num_blocks=nb)
+    np.testing.assert_array_equal(res.d, single.d)
+    np.testing.assert_array_equal(res.prefix, single.prefix)
+
+
+def test_multidevice_ldl_indefinite_and_unaligned_blocks():
+    z = gen.random_symmetric(2048, seed=1)
+    z[1024:, :] = 0.0
+    z[:, 1024:] = 0.0  # the second block is all zero after no updates: the reference raises
+    with pytest.raises(eng.IndefiniteBlockError):
+        eng.memdet_ldl(z, num_blocks=2, devices=[0, 0])
+    with pytest.raises(NotImplementedError):  # b = 1000 is not on a 128-row boundary
+        eng.memdet_ldl(gen.random_symmetric(3000, seed=2), num_blocks=3, devices=[0, 0])
