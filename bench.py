@@ -1,7 +1,7 @@
 """Benchmark: FP64 logdet TFLOP/s (n^3/3 flops per logdet) of the B200 MEMDET engine.
 
-Workload (BASELINE.json configs[1], "C2"): n = 32768 RBF Gram, x_i in R^16 i.i.d. N(0,1)
-(seed 0), l = 4, jitter 1e-6, reference tiling num_blocks = 8.  Synthetic (the paper's
+Headline workload (BASELINE.json configs[1], "C2"): n = 32768 RBF Gram, x_i in R^16 i.i.d.
+N(0,1) (seed 0), l = 4, jitter 1e-6, reference tiling num_blocks = 8.  Synthetic (the paper's
 NTK / kernel matrices are not available offline); generated on the device, untimed.
 
 One step = one full logdet + all 32768 prefix log-determinants of that matrix:
@@ -11,11 +11,19 @@ One step = one full logdet + all 32768 prefix log-determinants of that matrix:
   e2e   : the same metric through the public API memdet_cholesky(host pinned array,
           num_blocks=8): host->device copy of the upper triangle and device->host copy of the
           prefix and d are inside the timed region.
-N > 1 (torchrun): one C2 logdet per step factored across all ranks (distributed.py: row-cyclic
-tile rows, NCCL panel collectives) -> scaling "strong", value = n^3/3 per step / max time.
+Beside it (same JSON line): memdet_ldl (block-pivoted, the north star's LDL^T) on C2; C3
+(configs[2]: n = 65536 NTK-like, 16 blocks, formed on the device) for both drivers, device and
+end to end from pinned host memory; the out-of-core walk on the C3 bytes, first (cold) and warm
+calls, against max(compute, PCIe); the opt-in Ozaki line; a MEMDET01-file e2e line.
+N > 1 (torchrun): C3 per step, factored across the N devices by the engine's multi-device
+context (devices=[0..N-1]: 1-D block-cyclic outer panels, sharded ingest, panels over NVLink),
+driven from rank 0 -> scaling "strong"; the other ranks hold their GPU for the launch contract
+and join the barriers.
 
 `--impl reference` times the reference's CPU path (oracle port of oocdet.memdet_cholesky: the
-same SciPy LAPACK / NumPy BLAS calls, all host threads) on a bounded sample of the workload.
+same SciPy LAPACK / NumPy BLAS calls, all host threads) on C2 itself (n = 32768, num_blocks = 8,
+b = 4096): each step is stage 0 of its 8-stage walk (one 4096 potrf, 7 TRSMs, 28 GEMMs of
+4096^3 -- the block shapes of every stage), rate = that stage's exact flops / its time.
 """
 
 from __future__ import annotations
@@ -40,7 +48,6 @@ UNIT = "TFLOP/s"
 INT8_PEAK_TOPS = 4500.0  # nominal B200 dense int8 tensor throughput (TOPS), for the opt-in Ozaki line
 C2 = dict(n=32768, num_blocks=8, d=16, ell=4.0, jitter=1e-6, seed=0)
 OOC = dict(n=65536, num_blocks=4, hbm_budget=int(24e9))  # out-of-core line: C3-sized RBF, forced walk
-SAMPLE_N = 16384  # CPU baseline sample: leading principal 16384 submatrix of C2, b = 4096
 PROFILE_SUMMARY = os.path.join(REPO, "profiles", "r01_gemm_update_ncu.json")
 
 
@@ -112,21 +119,18 @@ class ClockSampler:
 # ------------------------------------------------------------------------------ CPU sample
 
 
-def cpu_sample_matrix(torch=None, dev_x=None):
-    """Leading SAMPLE_N principal submatrix of the C2 matrix (the generator is nested)."""
+def c2_host_matrix():
+    """The C2 matrix on the host (NumPy, threaded; bit-identical to tests/golden/c2.json's input)."""
     from paper_2503_04424_b200 import gen
 
-    if torch is not None and dev_x is not None:
-        a = generate_rbf_device(torch, dev_x[:SAMPLE_N].contiguous(), SAMPLE_N)
-        out = a.cpu().numpy()
-        del a
-        return out
-    return gen.rbf(SAMPLE_N, C2["d"], C2["ell"], C2["jitter"], C2["seed"])
+    return gen.rbf(C2["n"], C2["d"], C2["ell"], C2["jitter"], C2["seed"], threads=os.cpu_count() or 1)
 
 
 def run_cpu_reference(a: np.ndarray, steps: int, warmup: int):
-    """The reference's CPU path (oracle port of memdet_cholesky, same LAPACK/BLAS calls) on
-    the sample; returns (TFLOP/s, seconds per step, threads)."""
+    """The reference's CPU path (oracle port of memdet_cholesky's walk, the same LAPACK / BLAS
+    calls, all host threads) on C2 at full size: each step is stage 0 of the num_blocks = 8 walk
+    (memdet.py:346-387, k = 0: the block shapes of every stage).  Returns (TFLOP/s, seconds per
+    step, threads, stage flops)."""
     from oracle import memdet_oracle as O
 
     try:
@@ -139,16 +143,25 @@ def run_cpu_reference(a: np.ndarray, steps: int, warmup: int):
     except Exception:  # pragma: no cover
         ctx = None
         threads = os.cpu_count()
-    nb = SAMPLE_N // 4096
+    nb = C2["num_blocks"]
+    flops = O.stage0_flops(a.shape[0], nb)
     for _ in range(warmup):
-        O.memdet_cholesky(a, nb)
+        O.run_stage0(a, nb)
     t = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        O.memdet_cholesky(a, nb)
+        O.run_stage0(a, nb)
         t.append(time.perf_counter() - t0)
     sec = float(np.mean(t))
-    return SAMPLE_N ** 3 / 3.0 / sec / 1e12, sec, threads
+    del ctx
+    return flops / sec / 1e12, sec, threads, flops
+
+
+def cpu_sample_text(sec, steps):
+    return (f"oracle port of oocdet.memdet_cholesky (SciPy LAPACK potrf/trtrs + NumPy BLAS, as the reference "
+            f"calls them) on C2 itself (n=32768, num_blocks=8, b=4096): stage 0 of the 8-stage walk per step "
+            f"(1 potrf + 7 TRSM + 28 GEMM of 4096, incl. the block copies), rate = its exact flops / time; "
+            f"mean of {steps} run(s), {sec:.2f} s each")
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -189,6 +202,113 @@ def traffic_from_profile():
             return json.load(f)
     except (OSError, ValueError):
         return None
+
+
+def pin_host(torch, arr: np.ndarray):
+    """Page-lock an existing host array in place (exact size; torch's pinned allocator would
+    round 34 GB up to 64 GB).  Returns an unregister callback."""
+    cr = torch.cuda.cudart()
+    rc = cr.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister failed: {rc}")
+    return lambda: cr.cudaHostUnregister(arr.ctypes.data)
+
+
+def timed_calls(torch, stream, fn, steps):
+    """CUDA-event time per call of a public-API call on a device tensor (the engine enqueues on
+    the current stream and the call returns after its fetch)."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        res = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, res
+
+
+def run_c3(args, torch, eng, gen, peak, e0, e1, stream):
+    cfg = gen.BIG_CONFIGS["C3"]
+    n, nb = cfg["n"], cfg["num_blocks"]
+    flops = n ** 3 / 3.0
+    t0 = time.perf_counter()
+    a = gen.big_config_device("C3")
+    torch.cuda.synchronize()
+    t_form = time.perf_counter() - t0
+    steps = max(1, min(args.steps, 2))
+    out = {"config": {"workload": "C3 (BASELINE.json configs[2])", "n": n, "num_blocks": nb,
+                      "kind": f"NTK-like Z S^2 Z^T/p + 1e-8 I, p={cfg['p']}, s_j=j^-{cfg['alpha']}",
+                      "formation_s_untimed": t_form},
+           "steps": steps}
+    prefixes = {}
+    for name, fn in (("cholesky", eng.memdet_cholesky), ("ldl", eng.memdet_ldl)):
+        fn(a, num_blocks=nb)  # warm (allocates the workspace)
+        ms, res = timed_calls(torch, stream, lambda: fn(a, num_blocks=nb), steps)
+        eng.release_engine_cache()
+        prefixes[name] = res.prefix
+        out[name] = {"value": flops / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+                     "frac_of_fp64_peak": flops / (ms * 1e-3) / 1e12 / peak, "logdet": res.logabsdet,
+                     "gpu_launches": int(res.info.kernel_launches),
+                     "api": f"paper_2503_04424_b200.memdet_{name}(CUDA tensor, num_blocks={nb})"}
+        if name == "ldl":
+            out[name]["interchanged_rows"] = int(np.sum(res.perm != np.arange(n)))
+    ks = np.array([2 ** k for k in range(int(np.log2(n)) + 1)]) - 1
+    out["prefix_at_2k"] = {int(q + 1): float(prefixes["cholesky"][q]) for q in ks}
+    host = np.empty((n, n))
+    at = torch.from_numpy(host)
+    unpin = pin_host(torch, host)
+    at.copy_(a)
+    del a
+    torch.cuda.empty_cache()
+    for name, fn in (("cholesky", eng.memdet_cholesky), ("ldl", eng.memdet_ldl)):
+        fn(host, num_blocks=nb)  # warm
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = fn(host, num_blocks=nb)
+        sec = (time.perf_counter() - t0) / steps
+        eng.release_engine_cache()
+        out[name]["e2e"] = {"value": flops / sec / 1e12, "unit": UNIT, "seconds_per_step": sec,
+                            "h2d_bytes_per_step": int(res.info.h2d_bytes), "d2h_bytes_per_step": int(res.info.d2h_bytes),
+                            "api": f"paper_2503_04424_b200.memdet_{name}(pinned host ndarray, num_blocks={nb})"}
+    out["_host"] = (host, unpin)
+    return out
+
+
+def run_ooc_line(torch, eng, host_unpin, peak, h2d_gbs, d2h_gbs):
+    host, unpin = host_unpin
+    on = host.shape[0]
+    oflops = on ** 3 / 3.0
+    budget = OOC["hbm_budget"]
+    nb = OOC["num_blocks"]
+    eng.release_engine_cache()
+    t0 = time.perf_counter()  # cold: a fresh context (pins its scratchpad) -- the one-shot case
+    cold = eng.memdet_cholesky(host, num_blocks=nb, hbm_budget=budget, out_of_core=True)
+    cold_sec = time.perf_counter() - t0
+    steps = 2
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = eng.memdet_cholesky(host, num_blocks=nb, hbm_budget=budget, out_of_core=True)
+    sec = (time.perf_counter() - t0) / steps
+    eng.release_engine_cache()
+    unpin()
+    oi = res.info
+    roof = max(oflops / (peak * 1e12), oi.h2d_bytes / (h2d_gbs * 1e9), oi.d2h_bytes / (d2h_gbs * 1e9))
+    return {"value": oflops / sec / 1e12, "unit": UNIT, "seconds_per_step": sec, "steps": steps,
+            "cold": {"value": oflops / cold_sec / 1e12, "seconds": cold_sec, "roofline_frac": roof / cold_sec,
+                     "note": "first call of a fresh context: includes allocating / pinning the scratchpad"},
+            "config": {"workload": "C3 bytes (configs[2], n=65536 NTK-like) through the reference's out-of-core "
+                                   "tile walk", "n": on, "num_blocks": nb, "b": int(oi.b), "hbm_budget_bytes": budget,
+                       "out_of_core": bool(oi.out_of_core), "scratchpad": "pinned host"},
+            "blocks_read": int(oi.blocks_read), "blocks_written": int(oi.blocks_written),
+            "scratch_slots": int(oi.scratch_slots), "engine_reads": int(oi.ooc_reads),
+            "engine_writes": int(oi.ooc_writes),
+            "h2d_bytes_per_step": int(oi.h2d_bytes), "d2h_bytes_per_step": int(oi.d2h_bytes),
+            "roofline": {"bound": "max(FP64 tensor, PCIe H2D, PCIe D2H)", "time_s": roof, "frac": roof / sec,
+                         "peak_tflops": peak, "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                         "pcie_source": "pinned 1 GiB cudaMemcpy each way, this run"},
+            "logdet": res.logabsdet, "cold_equals_warm": bool(np.array_equal(cold.prefix, res.prefix)),
+            "api": f"paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks={nb}, "
+                   f"hbm_budget=24e9, out_of_core=True)"}
 
 
 def run_engine(args):
@@ -419,59 +539,30 @@ def run_engine(args):
             if os.path.exists(fpath):
                 os.remove(fpath)
 
-    # out-of-core (the north star's configs[4] schedule): the reference's tile walk on a C3-sized
-    # RBF Gram (n = 65536, 34 GB in pinned host memory; the C2 points extended, nested) with
-    # num_blocks=4 (b = 16384) under a 24 GB HBM budget -- 6 block slots in HBM, the 17 GB
-    # scratchpad in pinned host memory -- against its roofline max(flops/peak, H2D/PCIe, D2H/PCIe)
+    # CPU baseline: the reference's CPU path on C2 itself (stage 0 of its walk), rank 0, N = 1
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, sec, threads, _ = run_cpu_reference(host, 1, 0)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "same_config": True,
+               "sample": cpu_sample_text(sec, 1)}
+
+    # C3 (configs[2]): n = 65536 NTK-like Gram formed on the device; both drivers at 16 blocks,
+    # device-resident and end to end from pinned host memory; then the out-of-core walk on the
+    # same host bytes (num_blocks = 4 under a 24 GB HBM budget), first call (pins its scratchpad)
+    # and warm, against max(compute, PCIe)
+    c3 = None
     ooc = None
-    if not args.no_ooc:
+    if not args.no_c3:
         h2d_gbs, d2h_gbs = measure_pcie(torch)
         del pinned, host
-        on = OOC["n"]
-        oflops = on ** 3 / 3.0
-        ox = torch.from_numpy(gen.rbf_points(on, C2["d"], C2["seed"])).cuda()
-        oa = generate_rbf_device(torch, ox, on)
-        ohost_t = torch.empty((on, on), dtype=torch.float64, pin_memory=True)
-        ohost_t.copy_(oa)
-        del oa, ox
         torch.cuda.empty_cache()
-        ohost = ohost_t.numpy()
-        budget = OOC["hbm_budget"]
-        eng.memdet_cholesky(ohost, num_blocks=OOC["num_blocks"], hbm_budget=budget, out_of_core=True)  # warm: pins the scratchpad
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            ores2 = eng.memdet_cholesky(ohost, num_blocks=OOC["num_blocks"], hbm_budget=budget, out_of_core=True)
-        osec2 = (time.perf_counter() - t0) / e2e_steps
-        eng.release_engine_cache()
-        oi = ores2.info
-        roof = max(oflops / (peak * 1e12), oi.h2d_bytes / (h2d_gbs * 1e9), oi.d2h_bytes / (d2h_gbs * 1e9))
-        ooc = {"value": oflops / osec2 / 1e12, "unit": UNIT, "seconds_per_step": osec2, "steps": e2e_steps,
-               "config": {"workload": "RBF Gram n=65536 (C3 size; C2's recipe and points, nested)",
-                          "n": on, "num_blocks": OOC["num_blocks"], "b": int(oi.b), "hbm_budget_bytes": budget,
-                          "out_of_core": bool(oi.out_of_core), "scratchpad": "pinned host"},
-               "blocks_read": int(oi.blocks_read), "blocks_written": int(oi.blocks_written),
-               "scratch_slots": int(oi.scratch_slots), "engine_reads": int(oi.ooc_reads),
-               "engine_writes": int(oi.ooc_writes),
-               "h2d_bytes_per_step": int(oi.h2d_bytes), "d2h_bytes_per_step": int(oi.d2h_bytes),
-               "roofline": {"bound": "max(FP64 tensor, PCIe H2D, PCIe D2H)", "time_s": roof, "frac": roof / osec2,
-                            "peak_tflops": peak, "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
-                            "pcie_source": "pinned 1 GiB cudaMemcpy each way, this run"},
-               "logdet": ores2.logabsdet,
-               "nested_prefix_rel_diff_vs_c2": float(np.max(np.abs(ores2.prefix[:n] - res.prefix)
-                                                            / np.maximum(1.0, np.abs(res.prefix)))),
-               "api": "paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks=4, hbm_budget=24e9, out_of_core=True)"}
+        c3 = run_c3(args, torch, eng, gen, peak, e0, e1, stream)
+        if not args.no_ooc:
+            ooc = run_ooc_line(torch, eng, c3.pop("_host"), peak, h2d_gbs, d2h_gbs)
+        c3.pop("_host", None)
 
     out = None
     if rank == 0:
-        cpu = None
-        if ws == 1 and not args.no_cpu_baseline:
-            sample = cpu_sample_matrix(torch, dev_x)
-            v, sec, threads = run_cpu_reference(sample, 1, 0)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"oracle port of oocdet.memdet_cholesky on the leading {SAMPLE_N}^2 "
-                             f"principal submatrix of C2 (num_blocks=4, b=4096 = C2's tile), one run, "
-                             f"{sec:.2f} s"}
         prof = traffic_from_profile()
         achieved = upd_flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
         out = {
@@ -516,6 +607,7 @@ def run_engine(args):
             "ozaki": ozaki,
             "ldl": ldl,
             "e2e_file": e2e_file,
+            "c3": c3,
             "out_of_core": ooc,
             "clocks": clocks.summary(),
         }
@@ -526,100 +618,94 @@ def run_engine(args):
 
 
 def run_engine_multi(args):
-    """N > 1: one C2 logdet per step, factored across all ranks (row-cyclic tile rows; per panel
-    an NCCL all-reduce of the diagonal block and a stream-ordered barrier, after which every
-    rank's Schur-update kernels read the solved panel tiles in place from their owners' grids
-    over NVLink peer memory) -> strong scaling."""
+    """N > 1: C3 (configs[2], the north star's multi-GPU config) per step, factored across the N
+    devices by the engine's multi-device context (devices=[0..N-1]), driven from
+    rank 0; the other ranks keep their GPU for the launch contract and join the barriers.
+    Strong scaling on a fixed C3 logdet; timed with CUDA events on rank 0's stream, which the
+    multi-device call joins after every device's work (so the time is the max over devices)."""
     import torch
     import torch.distributed as dist
 
+    import paper_2503_04424_b200 as eng
     from paper_2503_04424_b200 import _native, gen
-    from paper_2503_04424_b200.distributed import DistributedMemdet
 
     ws, rank, local = dist_env()
-    # B2D_DIST_BACKEND=gloo lets a functional check run several ranks on one GPU (collectives
-    # staged through host memory); the measured configuration is NCCL, one rank per GPU
     backend = os.environ.get("B2D_DIST_BACKEND", "nccl")
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    import datetime
+
     kw = dict(device_id=torch.device("cuda", local)) if backend == "nccl" else {}
-    dist.init_process_group(backend, **kw)
-    n = int(os.environ.get("B2D_BENCH_N", C2["n"]))
-    flops = n ** 3 / 3.0
-    dev_x = torch.from_numpy(gen.rbf_points(n, C2["d"], C2["seed"])).cuda()
-    a = generate_rbf_device(torch, dev_x, n)
-    torch.cuda.synchronize()
-    peak = _native.probe_fp64_peak(local, 0.3)
-    peer_env = os.environ.get("B2D_DIST_PEER")  # default: peer mode with NCCL, gather with gloo
-    runner = DistributedMemdet(n, None, 8, torch.device("cuda", local),
-                               peer=None if peer_env is None else peer_env == "1")
-    for _ in range(args.warmup):
-        prefix, fail = runner.run(a)
-        if fail != -1:
-            raise RuntimeError(f"not SPD at {fail}")
-    torch.cuda.synchronize()
-    launches0 = runner.ops.launches
-    stream = torch.cuda.current_stream()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.steps):
-            prefix, fail = runner.run(a)
-        e1.record(stream)
-        dist.barrier()
-        torch.cuda.synchronize()
-    launches = (runner.ops.launches - launches0) // max(1, args.steps)
-    t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    logdet = float(prefix[-1].item())
-    value = flops * args.steps / (ms_max * 1e-3) / 1e12
-    # e2e: pinned host matrix -> each rank's device copy -> distributed factorisation -> prefix
-    pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-    pinned.copy_(a)
-    e2e_steps = max(1, min(args.steps, 3))
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        a.copy_(pinned, non_blocking=True)
-        prefix, fail = runner.run(a)
-        host_prefix = prefix.cpu()
-    torch.cuda.synchronize()
-    te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_sec = float(te.item())
+    # the other ranks wait in a barrier while rank 0 forms the matrix and drives every device
+    dist.init_process_group(backend, timeout=datetime.timedelta(minutes=60), **kw)
     out = None
     if rank == 0:
+        devices = [d % torch.cuda.device_count() for d in range(ws)]
+        which = os.environ.get("B2D_BENCH_CONFIG", "C3")
+        cfg = gen.BIG_CONFIGS[which] if which in gen.BIG_CONFIGS else None
+        n = cfg["n"] if cfg else int(os.environ.get("B2D_BENCH_N", C2["n"]))
+        nb = cfg["num_blocks"] if cfg else C2["num_blocks"]
+        flops = n ** 3 / 3.0
+        if cfg:
+            a = gen.big_config_device(which)
+        else:
+            a = generate_rbf_device(torch, torch.from_numpy(gen.rbf_points(n, C2["d"], C2["seed"])).cuda(), n)
+        torch.cuda.synchronize()
+        peak = _native.probe_fp64_peak(local, 0.3)
+        stream = torch.cuda.current_stream()
+        lines = {}
+        with ClockSampler(local) as clocks:
+            for name, fn in (("cholesky", eng.memdet_cholesky), ("ldl", eng.memdet_ldl)):
+                for _ in range(args.warmup if name == "cholesky" else 1):
+                    fn(a, num_blocks=nb, devices=devices)
+                ms, res = timed_calls(torch, stream, lambda: fn(a, num_blocks=nb, devices=devices),
+                                      args.steps if name == "cholesky" else max(1, min(args.steps, 2)))
+                lines[name] = (ms, res)
+        eng.release_engine_cache()
+        ms, res = lines["cholesky"]
+        value = flops / (ms * 1e-3) / 1e12
+        lms, lres = lines["ldl"]
+        # e2e: pinned host -> each device ingests its own panels -> prefix on the host
+        host = np.empty((n, n))
+        unpin = pin_host(torch, host)
+        torch.from_numpy(host).copy_(a)
+        del a
+        torch.cuda.empty_cache()
+        eng.memdet_cholesky(host, num_blocks=nb, devices=devices)
+        e2e_steps = max(1, min(args.steps, 2))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eres = eng.memdet_cholesky(host, num_blocks=nb, devices=devices)
+        e2e_sec = (time.perf_counter() - t0) / e2e_steps
+        eng.release_engine_cache()
+        unpin()
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: C2 RBF Gram generated on device (seeded), not the paper's NTKs",
-            "config": {"workload": "C2", "n": n, "num_blocks": C2["num_blocks"], "kind": "rbf d=16 l=4 jitter=1e-6",
-                       "engine_tile": 128, "l2": "inputs (8.6 GB) larger than L2 (126 MB)",
-                       "parallelism": f"row-cyclic tile rows x{ws}, " + (
-                           f"panels read in place over NVLink peer memory (CUDA IPC) after a {backend} barrier"
-                           if runner.shared is not None else f"{backend} panel all-gather")},
-            "matrices_per_s": args.steps / (ms_max * 1e-3),
+            "data": f"synthetic: {which} formed on the device (seeded), not the paper's NTKs",
+            "config": {"workload": which, "n": n, "num_blocks": nb, "engine_tile": 128,
+                       "l2": "inputs larger than L2 (126 MB)",
+                       "parallelism": f"1-D block-cyclic outer panels (16 tile-columns) over {ws} devices, "
+                                      f"sharded ingest, panels copied over NVLink (multi-device context driven "
+                                      f"from rank 0)", "devices": devices},
+            "matrices_per_s": 1.0 / (ms * 1e-3),
             "frac_of_fp64_peak": value / (ws * peak),
-            "logdet": logdet,
-            "roofline": {"bound": "tensor", "kernel": "all engine kernels, whole step",
+            "logdet": res.logabsdet,
+            "roofline": {"bound": "tensor", "kernel": "all engine kernels, whole step, every device",
                          "achieved": value / ws, "peak": peak, "unit": UNIT, "frac": value / ws / peak,
-                         "peak_source": "live DMMA m8n8k4 microbenchmark (b2d_probe_fp64_peak), rank 0",
+                         "peak_source": "live DMMA m8n8k4 microbenchmark (b2d_probe_fp64_peak), device 0",
                          "achieved_note": "per-GPU share of the step's n^3/3 flops / step time", "traffic": None},
+            "ldl": {"value": flops / (lms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": lms, "logdet": lres.logabsdet,
+                    "api": f"memdet_ldl(CUDA tensor, num_blocks={nb}, devices={devices})"},
             "cpu_baseline": None,
-            "e2e": {"value": flops / e2e_sec / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(n * n * 8 * ws),
-                    "d2h_bytes_per_step": int(n * 8), "seconds_per_step": e2e_sec, "steps": e2e_steps,
-                    "api": "paper_2503_04424_b200.distributed.DistributedMemdet.run after a pinned H2D copy per rank",
-                    "logdet": float(host_prefix[-1])},
-            "gpu_launches": launches * args.steps,
+            "e2e": {"value": flops / e2e_sec / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(eres.info.h2d_bytes),
+                    "d2h_bytes_per_step": int(eres.info.d2h_bytes), "seconds_per_step": e2e_sec, "steps": e2e_steps,
+                    "api": f"paper_2503_04424_b200.memdet_cholesky(pinned host ndarray, num_blocks={nb}, "
+                           f"devices={devices})", "logdet": eres.logabsdet},
+            "gpu_launches": int(res.info.kernel_launches) * args.steps,
             "clocks": clocks.summary(),
         }
-    runner.close()
     dist.barrier()
     dist.destroy_process_group()
     return out
@@ -629,18 +715,19 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
-    a = cpu_sample_matrix()
-    v, sec, threads = run_cpu_reference(a, args.steps, args.warmup)
-    cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-           "sample": f"oracle port of oocdet.memdet_cholesky (SciPy LAPACK potrf/trtrs + NumPy BLAS, "
-                     f"as the reference calls them) on the leading {SAMPLE_N}^2 principal submatrix of "
-                     f"C2 (num_blocks=4, b=4096); mean of {args.steps} runs, {sec:.2f} s each"}
+    t0 = time.perf_counter()
+    a = c2_host_matrix()
+    t_gen = time.perf_counter() - t0
+    v, sec, threads, flops = run_cpu_reference(a, args.steps, args.warmup)
+    cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "same_config": True,
+           "sample": cpu_sample_text(sec, args.steps)}
     return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: C2 RBF Gram (host, seeded), bounded sample",
-            "config": {"workload": "C2", "n": C2["n"], "num_blocks": C2["num_blocks"],
-                       "sample_n": SAMPLE_N, "parallelism": "cpu"},
+            "data": "synthetic: C2 RBF Gram (host NumPy, seeded; the bytes of tests/golden/c2.json)",
+            "config": {"workload": "C2", "n": C2["n"], "num_blocks": C2["num_blocks"], "b": 4096,
+                       "step": "stage 0 of the reference walk (same block shapes as every stage)",
+                       "stage_flops": flops, "parallelism": "cpu", "generation_s_untimed": t_gen},
             "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -656,6 +743,7 @@ def main():
     ap.add_argument("--no-ozaki", action="store_true", help="skip the opt-in int8-emulated Schur line")
     ap.add_argument("--no-ldl", action="store_true", help="skip the memdet_ldl (block-pivoted) line")
     ap.add_argument("--no-ooc", action="store_true", help="skip the out-of-core line")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 lines (and the out-of-core line)")
     ap.add_argument("--no-file", action="store_true", help="skip the MEMDET01-file e2e line")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
