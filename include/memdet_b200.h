@@ -37,6 +37,7 @@ extern "C" {
 #define B2D_ERR_CUDA 5         /* device / driver failure                           */
 #define B2D_ERR_NOMEM 6        /* HBM budget exceeded                               */
 #define B2D_ERR_UNSUPPORTED 7  /* feature not built                                 */
+#define B2D_ERR_STORAGE 8      /* StorageError: scratchpad file (exit 4)            */
 
 /* dtype codes: identical to the MEMDET01 header byte (storage.py:40-41) */
 #define B2D_F64 0
@@ -95,6 +96,15 @@ typedef struct b2d_options {
                               exchanged by peer copies over NVLink; the `device`
                               argument of b2d_ctx_create_ex is then ignored.  0 / 1: one device */
   int32_t devices[8];
+  int32_t scratch_mode;    /* out-of-core scratchpad when it lives in host memory (storage.py:147-204):
+                              0 auto (= 2); 1 pinned host memory allocated at context creation;
+                              2 pageable memory, touched lazily, every transfer staged through a
+                              small pinned ring by the library's host threads (no up-front
+                              pinning: a one-shot call pays no pinning); 3 a file (mkstemp +
+                              ftruncate in scratch_dir, memory-mapped, unlinked at once), staged
+                              like 2 -- capacity bounded by disk, not RAM                       */
+  const char *scratch_dir; /* mode 3 directory (NULL: $OOCDET_SCRATCH_DIR, else /tmp); a non-NULL
+                              scratch_dir with mode 0 selects mode 3 (the reference's behaviour)  */
 } b2d_options;
 
 typedef struct b2d_ctx b2d_ctx;

@@ -20,6 +20,7 @@ B2D_ERR_INDEFINITE = 4
 B2D_ERR_CUDA = 5
 B2D_ERR_NOMEM = 6
 B2D_ERR_UNSUPPORTED = 7
+B2D_ERR_STORAGE = 8
 
 B2D_F64, B2D_F32 = 0, 1
 MODE_CHOLESKY, MODE_LDL_NOPIV, MODE_LDL_PIV, MODE_LU = 0, 1, 2, 3
@@ -39,7 +40,8 @@ class OptionsC(ctypes.Structure):
                 ("max_mem", ctypes.c_int64), ("force_out_of_core", ctypes.c_int32),
                 ("host_scratch", ctypes.c_int32), ("emulation", ctypes.c_int32),
                 ("f32_arith", ctypes.c_int32), ("ndev", ctypes.c_int32),
-                ("devices", ctypes.c_int32 * 8)]
+                ("devices", ctypes.c_int32 * 8), ("scratch_mode", ctypes.c_int32),
+                ("scratch_dir", ctypes.c_char_p)]
 
 
 MAX_PEERS = 8
@@ -152,6 +154,8 @@ def check(rc: int, what: str = "engine call", fail_index: int | None = None):
         raise NotImplementedError(msg)
     if rc == B2D_ERR_NOMEM:
         raise MemoryError(msg)
+    if rc == B2D_ERR_STORAGE:
+        raise errors.StorageError(msg)
     if rc == B2D_ERR_CUDA and "no CUDA device" in msg:
         raise errors.EngineUnavailableError(msg)
     raise RuntimeError(msg)
@@ -163,12 +167,15 @@ class Context:
     def __init__(self, m: int, mode: int = MODE_CHOLESKY, device: int = 0, hbm_budget: int = 0,
                  num_blocks: int = 0, max_mem: int = 0, force_out_of_core: bool = False,
                  host_scratch: bool = False, emulation: bool = False, f32_arith: bool = False,
-                 devices=None):
+                 devices=None, scratch_dir: str | None = None, scratch_mode: int = 0):
         lib = load()
         h = ctypes.c_void_p()
         opt = OptionsC(int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
                        int(bool(force_out_of_core)), int(bool(host_scratch)), int(bool(emulation)),
                        int(bool(f32_arith)))
+        opt.scratch_mode = int(scratch_mode)
+        self._scratch_dir = os.fsencode(scratch_dir) if scratch_dir else None  # kept alive with opt
+        opt.scratch_dir = self._scratch_dir
         devices = tuple(int(x) for x in devices) if devices else ()
         if len(devices) > 8:
             raise ValueError(f"at most 8 devices, got {len(devices)}")
@@ -184,7 +191,8 @@ class Context:
         self.mode = mode
         self.device = device
         self.key = (device, m, mode, int(hbm_budget or 0), int(num_blocks or 0), int(max_mem or 0),
-                    bool(force_out_of_core), bool(host_scratch), bool(emulation), bool(f32_arith), devices)
+                    bool(force_out_of_core), bool(host_scratch), bool(emulation), bool(f32_arith), devices,
+                    scratch_dir, int(scratch_mode))
         self.devices = devices or (device,)
 
     @property

@@ -10,6 +10,9 @@
 // (dense.py:94-99), Schur-update the trailing tiles (dense.py:109-116); the prefix is the
 // running sum of 2 log L_ii (memdet.py:428).
 #include <algorithm>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -205,6 +208,16 @@ struct Ooc {
   std::map<std::pair<int, int>, cudaEvent_t> ev_key;  // last store of each scratch block
   std::vector<double*> pool;                       // scratch slots, bound in first-write order
   bool dev_scratch = false;                        // pool in HBM (fits next to the slots) or pinned host
+  // host scratchpad not pinned (scratch_mode 2 / 3): one mapping (anonymous or a temp file),
+  // transfers staged through pinned rings by the host pool
+  int scratch_mode = 1;
+  char* scratch_map = nullptr;
+  size_t scratch_map_bytes = 0;
+  static constexpr int NDBUF = 4;
+  void* dbuf[NDBUF] = {};
+  cudaEvent_t ev_ddma[NDBUF] = {}, ev_dfree[NDBUF] = {};
+  bool dbuf_used[NDBUF] = {};
+  uint64_t dseq = 0;
   std::set<std::pair<int, int>> written;           // cache table of the current run
   int64_t reads = 0, writes = 0;
   int rr = 0;
@@ -433,9 +446,18 @@ static void destroy(Ctx* c) {
                   (void*)c->f.amax})
     cudaFree(q);
   cudaFree(o.stage);
-  for (double* h : o.pool) {
-    if (o.dev_scratch) cudaFree(h);
-    else cudaFreeHost(h);
+  if (o.scratch_map) {
+    munmap(o.scratch_map, o.scratch_map_bytes);
+  } else {
+    for (double* h : o.pool) {
+      if (o.dev_scratch) cudaFree(h);
+      else cudaFreeHost(h);
+    }
+  }
+  for (int k = 0; k < Ooc::NDBUF; ++k) {
+    if (o.dbuf[k]) cudaFreeHost(o.dbuf[k]);
+    if (o.ev_ddma[k]) cudaEventDestroy(o.ev_ddma[k]);
+    if (o.ev_dfree[k]) cudaEventDestroy(o.ev_dfree[k]);
   }
   for (auto& kv : o.ev_key) cudaEventDestroy(kv.second);
   if (o.s_h2d) cudaStreamDestroy(o.s_h2d);
@@ -838,15 +860,62 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     cudaMemGetInfo(&fb, &tb);
     used = free_b > fb ? free_b - fb : 0;
     o.dev_scratch = !(opt && opt->host_scratch) && used + (size_t)nsc * o.slot_bytes() <= budget;
-    for (int64_t q = 0; q < nsc; ++q) {
-      double* h = nullptr;
-      const cudaError_t e = o.dev_scratch ? cudaMalloc((void**)&h, o.slot_bytes())
-                                          : cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault);
-      if (e != cudaSuccess) {
-        destroy(c);
-        return set_err(B2D_ERR_NOMEM, "scratchpad of %lld x %.2f GB failed", (long long)nsc, o.slot_bytes() / 1e9);
+    // host scratchpad: pinned up front (mode 1), or pageable / a temp file staged through pinned
+    // rings (modes 2 / 3, the default: nothing is pinned up front, so a one-shot call does not
+    // pay for pinning the whole scratchpad; a file bounds the capacity by disk, as the
+    // reference's mkstemp scratchpad, storage.py:147-204).  B2D_SCRATCH=pinned|staged|file.
+    int smode = opt ? opt->scratch_mode : 0;
+    if (smode == 0) smode = (opt && opt->scratch_dir && opt->scratch_dir[0]) ? 3 : 2;
+    if (const char* e = getenv("B2D_SCRATCH"))
+      smode = strcmp(e, "pinned") == 0 ? 1 : strcmp(e, "file") == 0 ? 3 : strcmp(e, "staged") == 0 ? 2 : smode;
+    o.scratch_mode = smode;
+    if (!o.dev_scratch && smode >= 2 && nsc > 0) {
+      const size_t bytes = (size_t)nsc * o.slot_bytes();
+      int fd = -1;
+      if (smode == 3) {
+        std::string dir = opt && opt->scratch_dir && opt->scratch_dir[0] ? opt->scratch_dir : "";
+        if (dir.empty()) {
+          const char* env = getenv("OOCDET_SCRATCH_DIR");  // storage.py:200-204
+          dir = env && env[0] ? env : "/tmp";
+        }
+        std::string tmpl = dir + "/oocdet-b200-scratch-XXXXXX";
+        std::vector<char> path(tmpl.begin(), tmpl.end());
+        path.push_back('\0');
+        fd = mkstemp(path.data());
+        if (fd < 0) {
+          destroy(c);
+          return set_err(B2D_ERR_STORAGE, "scratchpad file in %s: %s", dir.c_str(), strerror(errno));
+        }
+        unlink(path.data());  // the mapping keeps it; nothing is left behind on any exit
+        if (ftruncate(fd, (off_t)bytes) != 0) {
+          close(fd);
+          destroy(c);
+          return set_err(B2D_ERR_STORAGE, "scratchpad file of %.2f GB in %s: %s", bytes / 1e9, dir.c_str(),
+                         strerror(errno));
+        }
       }
-      o.pool.push_back(h);
+      void* mp = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, fd >= 0 ? MAP_SHARED : (MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE),
+                      fd, 0);
+      if (fd >= 0) close(fd);
+      if (mp == MAP_FAILED) {
+        destroy(c);
+        return set_err(B2D_ERR_NOMEM, "scratchpad mapping of %.2f GB failed: %s", bytes / 1e9, strerror(errno));
+      }
+      if (fd < 0) madvise(mp, bytes, MADV_HUGEPAGE);
+      o.scratch_map = (char*)mp;
+      o.scratch_map_bytes = bytes;
+      for (int64_t q = 0; q < nsc; ++q) o.pool.push_back((double*)(o.scratch_map + (size_t)q * o.slot_bytes()));
+    } else {
+      for (int64_t q = 0; q < nsc; ++q) {
+        double* h = nullptr;
+        const cudaError_t e = o.dev_scratch ? cudaMalloc((void**)&h, o.slot_bytes())
+                                            : cudaHostAlloc((void**)&h, o.slot_bytes(), cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+          destroy(c);
+          return set_err(B2D_ERR_NOMEM, "scratchpad of %lld x %.2f GB failed", (long long)nsc, o.slot_bytes() / 1e9);
+        }
+        o.pool.push_back(h);
+      }
     }
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1487,6 +1556,80 @@ static std::vector<Visit> stage_visits(int nb, int k) {
 // slot s as the engine's lower block (rj, ri): from the scratchpad if it was written this run
 // (the reference cache table, storage.py:134-144), else from the input in 128-row strips
 // (H2D + pack_block_kernel).  Waits until the slot's previous contents are consumed and stored.
+// Staged scratchpad transfers (scratch_mode 2 / 3): contiguous ranges split into pinned-buffer
+// sized pieces.  HBM -> scratch: the DMA into ring buffer k (on `s`), then a host callback on
+// s_fill drains it into the pageable / file mapping with the host pool; the buffer is reused once
+// drained.  Scratch -> HBM: h2d_linear through the input-staging ring (fill callback, then DMA).
+// Both directions' callbacks are on s_fill, so a load issued after a store of the same block
+// reads the drained bytes (FIFO).  Returns after enqueueing; `drained` (optional) is recorded
+// after the last drain.
+static void CUDART_CB drain_cb(void* p) {
+  std::unique_ptr<FillJob> j(static_cast<FillJob*>(p));
+  const size_t per = (size_t)1 << 20;
+  const int ntask = (int)((j->width + per - 1) / per);
+  j->pool->run(ntask, [&](int t) {
+    const size_t off = (size_t)t * per, n = std::min(per, j->width - off);
+    memcpy(j->dst + off, j->src + off, n);
+  });
+}
+static int ensure_staging(Ctx* c) {
+  if (c->s_fill) return B2D_OK;
+  c->hbuf_bytes = HBUF_BYTES;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_fill, cudaStreamNonBlocking));
+  for (int k = 0; k < NHBUF; ++k) {
+    CUDA_TRY(cudaHostAlloc(&c->hbuf[k], c->hbuf_bytes, cudaHostAllocDefault));
+    cudaEventCreateWithFlags(&c->ev_hfill[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_hcopy[k], cudaEventDisableTiming);
+  }
+  return B2D_OK;
+}
+static int d2h_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s, cudaEvent_t drained) {
+  Ooc& o = c->o;
+  if (int rc = ensure_staging(c)) return rc;
+  if (!o.dbuf[0])
+    for (int k = 0; k < Ooc::NDBUF; ++k) {
+      CUDA_TRY(cudaHostAlloc(&o.dbuf[k], HBUF_BYTES, cudaHostAllocDefault));
+      cudaEventCreateWithFlags(&o.ev_ddma[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&o.ev_dfree[k], cudaEventDisableTiming);
+    }
+  for (size_t off = 0; off < bytes; off += HBUF_BYTES) {
+    const size_t n = std::min(HBUF_BYTES, bytes - off);
+    const int k = (int)(o.dseq++ % Ooc::NDBUF);
+    if (o.dbuf_used[k]) cudaStreamWaitEvent(s, o.ev_dfree[k], 0);
+    CUDA_TRY(cudaMemcpyAsync(o.dbuf[k], (const char*)src + off, n, cudaMemcpyDeviceToHost, s));
+    cudaEventRecord(o.ev_ddma[k], s);
+    cudaStreamWaitEvent(c->s_fill, o.ev_ddma[k], 0);
+    auto* job = new FillJob{host_pool(), (char*)dst + off, (const char*)o.dbuf[k], 0, n, 1};
+    if (cudaLaunchHostFunc(c->s_fill, drain_cb, job) != cudaSuccess) {
+      delete job;
+      return set_err(B2D_ERR_CUDA, "cudaLaunchHostFunc failed");
+    }
+    cudaEventRecord(o.ev_dfree[k], c->s_fill);
+    o.dbuf_used[k] = true;
+  }
+  if (drained) cudaEventRecord(drained, c->s_fill);
+  return B2D_OK;
+}
+static int h2d_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (int rc = ensure_staging(c)) return rc;
+  for (size_t off = 0; off < bytes; off += c->hbuf_bytes) {
+    const size_t n = std::min(c->hbuf_bytes, bytes - off);
+    const int k = (int)(c->hseq++ % NHBUF);
+    if (c->hbuf_used[k]) cudaStreamWaitEvent(c->s_fill, c->ev_hcopy[k], 0);
+    auto* job = new FillJob{host_pool(), (char*)c->hbuf[k], (const char*)src + off, 0, n, 1};
+    if (cudaLaunchHostFunc(c->s_fill, drain_cb, job) != cudaSuccess) {
+      delete job;
+      return set_err(B2D_ERR_CUDA, "cudaLaunchHostFunc failed");
+    }
+    cudaEventRecord(c->ev_hfill[k], c->s_fill);
+    cudaStreamWaitEvent(s, c->ev_hfill[k], 0);
+    CUDA_TRY(cudaMemcpyAsync((char*)dst + off, c->hbuf[k], n, cudaMemcpyHostToDevice, s));
+    cudaEventRecord(c->ev_hcopy[k], s);
+    c->hbuf_used[k] = true;
+  }
+  return B2D_OK;
+}
+
 static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, int dtype, bool trans = true) {
   Ooc& o = c->o;
   cudaStreamWaitEvent(o.s_h2d, o.ev_used[s], 0);
@@ -1494,7 +1637,11 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
   auto key = std::make_pair(ri, rj);
   if (o.written.count(key)) {
     cudaStreamWaitEvent(o.s_h2d, o.ev_key[key], 0);  // the scratch copy must have landed
-    CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyDefault, o.s_h2d));
+    if (o.scratch_map) {
+      if (int rc = h2d_linear(c, o.slot[s], o.scratch[key], o.slot_bytes(), o.s_h2d)) return rc;
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyDefault, o.s_h2d));
+    }
     if (!o.dev_scratch) c->h2d += (int64_t)o.slot_bytes();
   } else if (!trans) {
     // generic blocks (LU): reference block (ri, rj) as the engine block (ri, rj), strip J of
@@ -1556,15 +1703,21 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
     it = o.scratch.emplace(key, o.pool[o.scratch.size()]).first;
   }
   cudaStreamWaitEvent(o.s_d2h, o.ev_used[s], 0);
-  CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDefault, o.s_d2h));
-  cudaEventRecord(o.ev_stored[s], o.s_d2h);
   auto ek = o.ev_key.find(key);
   if (ek == o.ev_key.end()) {
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     ek = o.ev_key.emplace(key, e).first;
   }
-  cudaEventRecord(ek->second, o.s_d2h);
+  if (o.scratch_map) {
+    // the slot is free once its DMA pieces are out; the block is in the scratchpad once drained
+    if (int rc = d2h_linear(c, it->second, o.slot[s], o.slot_bytes(), o.s_d2h, ek->second)) return rc;
+    cudaEventRecord(o.ev_stored[s], o.s_d2h);
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(it->second, o.slot[s], o.slot_bytes(), cudaMemcpyDefault, o.s_d2h));
+    cudaEventRecord(o.ev_stored[s], o.s_d2h);
+    cudaEventRecord(ek->second, o.s_d2h);
+  }
   if (!o.dev_scratch) c->d2h += (int64_t)o.slot_bytes();
   o.written.insert(key);
   o.writes++;

@@ -19,6 +19,7 @@ There is no CPU fallback: without the engine or a GPU these raise EngineUnavaila
 from __future__ import annotations
 
 import math
+import os
 import threading
 import time
 from contextlib import contextmanager
@@ -248,13 +249,14 @@ def _ctx_matches(ctx: _native.Context, mode: int, num_blocks: int, max_mem: int)
 
 @contextmanager
 def _lease(m: int, mode: int, device: int, hbm_budget=None, num_blocks=None, max_mem=None,
-           out_of_core=None, emulation=False, f32_arith=False, devices=()) -> Iterator[_native.Context]:
+           out_of_core=None, emulation=False, f32_arith=False, devices=(),
+           scratch_dir=None) -> Iterator[_native.Context]:
     global _ctx_generation
     kw = dict(hbm_budget=int(hbm_budget or 0), num_blocks=int(num_blocks or 0),
               max_mem=int(max_mem or 0), force_out_of_core=bool(out_of_core), emulation=bool(emulation),
-              f32_arith=bool(f32_arith), devices=tuple(devices))
+              f32_arith=bool(f32_arith), devices=tuple(devices), scratch_dir=scratch_dir)
     base = (device, m, mode, kw["hbm_budget"], kw["force_out_of_core"], kw["emulation"], kw["f32_arith"],
-            kw["devices"])
+            kw["devices"], scratch_dir)
     ctx = None
     stale = []
     with _ctx_lock:
@@ -293,14 +295,22 @@ def release_engine_cache():
         c.close()
 
 
+def _scratch_dir(scratch_dir):
+    """The reference's scratch directory rule (storage.py:200-204) minus its final fallback: the
+    argument, else $OOCDET_SCRATCH_DIR, else None -- then the engine keeps an out-of-core
+    scratchpad in lazily touched host memory rather than a file."""
+    d = scratch_dir if scratch_dir is not None else os.environ.get("OOCDET_SCRATCH_DIR")
+    return os.fspath(d) if d else None
+
+
 def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max_mem, hbm_budget,
-                out_of_core, emulation=False, devices=()):
+                out_of_core, emulation=False, devices=(), scratch_dir=None):
     dcode = _native.B2D_F64 if src.dtype == np.float64 else _native.B2D_F32
     m = src.m
     if len(devices) > 1:
         return _run_multi(src, mode, dcode, devices, hbm_budget, out_of_core, lay.n_b)
     # the out-of-core tile walk starts from the reference tiling (num_blocks / max_mem)
-    ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core)
+    ooc_kw = dict(hbm_budget=hbm_budget, num_blocks=lay.n_b, out_of_core=out_of_core, scratch_dir=scratch_dir)
     if src.device_ptr is not None and mode == _native.MODE_LU:
         # the generic walk streams reference blocks from host memory
         src.host, src.device_ptr = src.keepalive.cpu().numpy(), None
@@ -382,7 +392,7 @@ def _run_multi(src: MatrixSource, mode: int, dcode: int, devices, hbm_budget, ou
 
 
 def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_budget=None,
-            out_of_core=None, schur="dmma", devices=None):
+            out_of_core=None, schur="dmma", devices=None, scratch_dir=None):
     if schur not in ("dmma", "ozaki"):
         raise ValueError(f"schur must be 'dmma' or 'ozaki', got {schur!r}")
     t0 = time.perf_counter()
@@ -394,7 +404,7 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
     if len(devices) > 1 and schur != "dmma":
         raise ValueError("schur='ozaki' is single-device")
     d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core,
-                                              schur == "ozaki", devices)
+                                              schur == "ozaki", devices, _scratch_dir(scratch_dir))
     nb = lay.n_b
     case = "generic" if mode == _native.MODE_LU else "symmetric"
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
@@ -418,16 +428,17 @@ def memdet_cholesky(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, 
     prefix[q-1] = logdet of the leading q x q principal submatrix, summed from 2 log L_ii;
     NotSpdError on the first non-positive leading minor.  A matrix whose packed lower triangle
     exceeds `hbm_budget` (default: free HBM) — or any host matrix with out_of_core=True — runs
-    the reference's out-of-core tile walk, blocks streamed between host memory and HBM (the
-    scratchpad lives in pinned host memory; `scratch_dir` is accepted for signature parity).
+    the reference's out-of-core tile walk, blocks streamed between host memory and HBM.  Its
+    scratchpad lives in a temp file under `scratch_dir` (else $OOCDET_SCRATCH_DIR; reference
+    storage.py:147-204: capacity bounded by disk), or, with neither, in lazily touched host memory;
+    either way transfers are staged through small pinned rings, so nothing is pinned up front.
     schur="ozaki" runs the in-core trailing Schur updates as FP64 emulated on the int8 tcgen05
     tensor cores (8-slice Ozaki scheme, error ~3 u relative to sum |a b|); the
     default "dmma" uses the FP64 tensor cores.  devices=[d0, d1, ...] shards the factorisation over
     several devices of this process (1-D block-cyclic outer panels, each device ingesting only its
     own panels, panels exchanged over NVLink); hbm_budget is then per device."""
-    del scratch_dir
     d, prefix, info, _ = _memdet(matrix, _native.MODE_CHOLESKY, "spd", max_mem, num_blocks, device, assume,
-                                 hbm_budget, out_of_core, schur, devices)
+                                 hbm_budget, out_of_core, schur, devices, scratch_dir)
     res = SpdResult(prefix=prefix, info=info, d=d)
     if prefix_out is not None:
         with PrefixWriter(prefix_out) as w:
@@ -461,9 +472,8 @@ def memdet_lu(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, device
     blocks, as the reference's (a block-local pivot search sees only its block, so the grid is
     never refined); blocks over 6144 rows raise NotImplementedError (the cluster panel kernel's
     reach) and a walk that does not fit the HBM budget raises MemoryError."""
-    del scratch_dir
     d, prefix, info, (perm, fail) = _memdet(matrix, _native.MODE_LU, "generic", max_mem, num_blocks, device,
-                                            assume or "generic", hbm_budget, out_of_core)
+                                            assume or "generic", hbm_budget, out_of_core, scratch_dir=scratch_dir)
     # the reference's counters for its walk (scratch = the peak number of distinct blocks
     # written, storage.py:265-267); it stops at a singular stage (memdet.py:293-294), whose
     # position the engine reports when its block grid is the reference's
@@ -510,12 +520,11 @@ def memdet_ldl(matrix, *, max_mem=None, num_blocks=None, scratch_dir=None, prefi
     unpivoted LDL^T (D = L_ii^2 of the Cholesky factor, perm = identity): its prefixes are
     the natural-order leading minors and coincide with the pivoted ones at every block
     boundary q = k*b and at q = m.  schur and devices as memdet_cholesky."""
-    del scratch_dir
     if pivoting not in ("block", "none"):
         raise ValueError(f"pivoting must be 'block' or 'none', got {pivoting!r}")
     mode = _native.MODE_LDL_PIV if pivoting == "block" else _native.MODE_LDL_NOPIV
     d, prefix, info, perm = _memdet(matrix, mode, "symmetric", max_mem, num_blocks, device, assume, hbm_budget,
-                                    out_of_core, schur, devices)
+                                    out_of_core, schur, devices, scratch_dir)
     m = len(prefix)
     if mode == _native.MODE_LDL_NOPIV:
         perm = np.arange(m, dtype=np.int64)

@@ -69,5 +69,5 @@ def test_run_info_struct_matches_header():
             decl = decl.strip()
             if not decl:
                 continue
-            names += [n.strip().lstrip("*").split("[")[0] for n in decl.split(None, 1)[1].split(",")]
+            names += [re.findall(r"(\w+)\s*(?:\[[^\]]*\])?\s*$", n)[0] for n in decl.split(",")]
         assert names == [f[0] for f in getattr(_native, pyname)._fields_], cname
