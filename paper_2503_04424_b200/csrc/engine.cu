@@ -155,6 +155,9 @@ struct FillJob {
   char* dst;
   const char* src;
   size_t spitch, width, rows;
+  int fd = -1;      // file-backed scratchpad: pwrite(dst -> fd) / pread(fd -> dst) at foff instead
+  int64_t foff = 0;
+  int dir = 0;      // 0: memory copy; 1: src -> file (drain); 2: file -> dst (fill)
 };
 static void CUDART_CB fill_cb(void* p) {
   std::unique_ptr<FillJob> j(static_cast<FillJob*>(p));
@@ -211,9 +214,11 @@ struct Ooc {
   // host scratchpad not pinned (scratch_mode 2 / 3): one mapping (anonymous or a temp file),
   // transfers staged through pinned rings by the host pool
   int scratch_mode = 1;
+  int scratch_fd = -1;           // mode 3: the (unlinked) scratch file; pool entries are offsets
   char* scratch_map = nullptr;
   size_t scratch_map_bytes = 0;
   static constexpr int NDBUF = 4;
+  cudaStream_t s_drain = nullptr;  // host drains of staged HBM -> scratch copies (not behind fills)
   void* dbuf[NDBUF] = {};
   cudaEvent_t ev_ddma[NDBUF] = {}, ev_dfree[NDBUF] = {};
   bool dbuf_used[NDBUF] = {};
@@ -446,7 +451,13 @@ static void destroy(Ctx* c) {
                   (void*)c->f.amax})
     cudaFree(q);
   cudaFree(o.stage);
-  if (o.scratch_map) {
+  if (o.s_drain) {
+    cudaStreamSynchronize(o.s_drain);
+    cudaStreamDestroy(o.s_drain);
+  }
+  if (o.scratch_fd >= 0) {
+    close(o.scratch_fd);
+  } else if (o.scratch_map) {
     munmap(o.scratch_map, o.scratch_map_bytes);
   } else {
     for (double* h : o.pool) {
@@ -859,7 +870,9 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     size_t used = 0, fb = 0, tb = 0;
     cudaMemGetInfo(&fb, &tb);
     used = free_b > fb ? free_b - fb : 0;
-    o.dev_scratch = !(opt && opt->host_scratch) && used + (size_t)nsc * o.slot_bytes() <= budget;
+    const char* hse = getenv("B2D_HOST_SCRATCH");  // 1: keep the scratchpad in host memory (tests)
+    const bool host_scr = (opt && opt->host_scratch) || (hse && atoi(hse) != 0);
+    o.dev_scratch = !host_scr && used + (size_t)nsc * o.slot_bytes() <= budget;
     // host scratchpad: pinned up front (mode 1), or pageable / a temp file staged through pinned
     // rings (modes 2 / 3, the default: nothing is pinned up front, so a one-shot call does not
     // pay for pinning the whole scratchpad; a file bounds the capacity by disk, as the
@@ -894,17 +907,22 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
                          strerror(errno));
         }
       }
-      void* mp = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, fd >= 0 ? MAP_SHARED : (MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE),
-                      fd, 0);
-      if (fd >= 0) close(fd);
-      if (mp == MAP_FAILED) {
-        destroy(c);
-        return set_err(B2D_ERR_NOMEM, "scratchpad mapping of %.2f GB failed: %s", bytes / 1e9, strerror(errno));
+      if (fd >= 0) {
+        // read / written with pread / pwrite by the host pool (no page-fault storm on a fresh file
+        // mapping); pool entries are byte offsets into the file
+        o.scratch_fd = fd;
+        for (int64_t q = 0; q < nsc; ++q) o.pool.push_back((double*)(uintptr_t)((size_t)q * o.slot_bytes()));
+      } else {
+        void* mp = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+        if (mp == MAP_FAILED) {
+          destroy(c);
+          return set_err(B2D_ERR_NOMEM, "scratchpad mapping of %.2f GB failed: %s", bytes / 1e9, strerror(errno));
+        }
+        madvise(mp, bytes, MADV_HUGEPAGE);
+        o.scratch_map = (char*)mp;
+        o.scratch_map_bytes = bytes;
+        for (int64_t q = 0; q < nsc; ++q) o.pool.push_back((double*)(o.scratch_map + (size_t)q * o.slot_bytes()));
       }
-      if (fd < 0) madvise(mp, bytes, MADV_HUGEPAGE);
-      o.scratch_map = (char*)mp;
-      o.scratch_map_bytes = bytes;
-      for (int64_t q = 0; q < nsc; ++q) o.pool.push_back((double*)(o.scratch_map + (size_t)q * o.slot_bytes()));
     } else {
       for (int64_t q = 0; q < nsc; ++q) {
         double* h = nullptr;
@@ -1559,9 +1577,9 @@ static std::vector<Visit> stage_visits(int nb, int k) {
 // Staged scratchpad transfers (scratch_mode 2 / 3): contiguous ranges split into pinned-buffer
 // sized pieces.  HBM -> scratch: the DMA into ring buffer k (on `s`), then a host callback on
 // s_fill drains it into the pageable / file mapping with the host pool; the buffer is reused once
-// drained.  Scratch -> HBM: h2d_linear through the input-staging ring (fill callback, then DMA).
-// Both directions' callbacks are on s_fill, so a load issued after a store of the same block
-// reads the drained bytes (FIFO).  Returns after enqueueing; `drained` (optional) is recorded
+// drained (callbacks on s_drain).  Scratch -> HBM: h2d_linear through the input-staging ring (fill
+// callback on s_fill, then DMA); a load of a stored block waits for its last drain (ev_key), so
+// it reads the drained bytes.  Returns after enqueueing; `drained` (optional) is recorded
 // after the last drain.
 static void CUDART_CB drain_cb(void* p) {
   std::unique_ptr<FillJob> j(static_cast<FillJob*>(p));
@@ -1569,7 +1587,24 @@ static void CUDART_CB drain_cb(void* p) {
   const int ntask = (int)((j->width + per - 1) / per);
   j->pool->run(ntask, [&](int t) {
     const size_t off = (size_t)t * per, n = std::min(per, j->width - off);
-    memcpy(j->dst + off, j->src + off, n);
+    if (j->dir == 1) {
+      for (size_t w = 0; w < n;) {
+        const ssize_t r = pwrite(j->fd, j->src + off + w, n - w, (off_t)(j->foff + off + w));
+        if (r <= 0) break;
+        w += (size_t)r;
+      }
+    } else if (j->dir == 2) {
+      for (size_t w = 0; w < n;) {
+        const ssize_t r = pread(j->fd, j->dst + off + w, n - w, (off_t)(j->foff + off + w));
+        if (r <= 0) {
+          memset(j->dst + off + w, 0, n - w);
+          break;
+        }
+        w += (size_t)r;
+      }
+    } else {
+      memcpy(j->dst + off, j->src + off, n);
+    }
   });
 }
 static int ensure_staging(Ctx* c) {
@@ -1586,6 +1621,7 @@ static int ensure_staging(Ctx* c) {
 static int d2h_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s, cudaEvent_t drained) {
   Ooc& o = c->o;
   if (int rc = ensure_staging(c)) return rc;
+  if (!o.s_drain) CUDA_TRY(cudaStreamCreateWithFlags(&o.s_drain, cudaStreamNonBlocking));
   if (!o.dbuf[0])
     for (int k = 0; k < Ooc::NDBUF; ++k) {
       CUDA_TRY(cudaHostAlloc(&o.dbuf[k], HBUF_BYTES, cudaHostAllocDefault));
@@ -1598,16 +1634,22 @@ static int d2h_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStre
     if (o.dbuf_used[k]) cudaStreamWaitEvent(s, o.ev_dfree[k], 0);
     CUDA_TRY(cudaMemcpyAsync(o.dbuf[k], (const char*)src + off, n, cudaMemcpyDeviceToHost, s));
     cudaEventRecord(o.ev_ddma[k], s);
-    cudaStreamWaitEvent(c->s_fill, o.ev_ddma[k], 0);
+    cudaStreamWaitEvent(o.s_drain, o.ev_ddma[k], 0);
     auto* job = new FillJob{host_pool(), (char*)dst + off, (const char*)o.dbuf[k], 0, n, 1};
-    if (cudaLaunchHostFunc(c->s_fill, drain_cb, job) != cudaSuccess) {
+    if (o.scratch_fd >= 0) {
+      job->fd = o.scratch_fd;
+      job->foff = (int64_t)(uintptr_t)dst + (int64_t)off;
+      job->dst = nullptr;
+      job->dir = 1;
+    }
+    if (cudaLaunchHostFunc(o.s_drain, drain_cb, job) != cudaSuccess) {
       delete job;
       return set_err(B2D_ERR_CUDA, "cudaLaunchHostFunc failed");
     }
-    cudaEventRecord(o.ev_dfree[k], c->s_fill);
+    cudaEventRecord(o.ev_dfree[k], o.s_drain);
     o.dbuf_used[k] = true;
   }
-  if (drained) cudaEventRecord(drained, c->s_fill);
+  if (drained) cudaEventRecord(drained, o.s_drain);
   return B2D_OK;
 }
 static int h2d_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -1617,6 +1659,12 @@ static int h2d_linear(Ctx* c, void* dst, const void* src, size_t bytes, cudaStre
     const int k = (int)(c->hseq++ % NHBUF);
     if (c->hbuf_used[k]) cudaStreamWaitEvent(c->s_fill, c->ev_hcopy[k], 0);
     auto* job = new FillJob{host_pool(), (char*)c->hbuf[k], (const char*)src + off, 0, n, 1};
+    if (c->o.scratch_fd >= 0) {
+      job->fd = c->o.scratch_fd;
+      job->foff = (int64_t)(uintptr_t)src + (int64_t)off;
+      job->src = nullptr;
+      job->dir = 2;
+    }
     if (cudaLaunchHostFunc(c->s_fill, drain_cb, job) != cudaSuccess) {
       delete job;
       return set_err(B2D_ERR_CUDA, "cudaLaunchHostFunc failed");
@@ -1637,7 +1685,8 @@ static int ooc_load(Ctx* c, int ri, int rj, int s, const void* a, int64_t lda, i
   auto key = std::make_pair(ri, rj);
   if (o.written.count(key)) {
     cudaStreamWaitEvent(o.s_h2d, o.ev_key[key], 0);  // the scratch copy must have landed
-    if (o.scratch_map) {
+    if (o.scratch_map || o.scratch_fd >= 0) {
+      cudaStreamWaitEvent(c->s_fill, o.ev_key[key], 0);  // the host reads it only once drained
       if (int rc = h2d_linear(c, o.slot[s], o.scratch[key], o.slot_bytes(), o.s_h2d)) return rc;
     } else {
       CUDA_TRY(cudaMemcpyAsync(o.slot[s], o.scratch[key], o.slot_bytes(), cudaMemcpyDefault, o.s_h2d));
@@ -1709,7 +1758,7 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     ek = o.ev_key.emplace(key, e).first;
   }
-  if (o.scratch_map) {
+  if (o.scratch_map || o.scratch_fd >= 0) {
     // the slot is free once its DMA pieces are out; the block is in the scratchpad once drained
     if (int rc = d2h_linear(c, it->second, o.slot[s], o.slot_bytes(), o.s_d2h, ek->second)) return rc;
     cudaEventRecord(o.ev_stored[s], o.s_d2h);

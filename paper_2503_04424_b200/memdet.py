@@ -30,7 +30,7 @@ import numpy as np
 
 from . import _native
 from .cost import predicted_reads, predicted_writes, scratch_slots
-from .errors import IndefiniteBlockError, NotSpdError
+from .errors import IndefiniteBlockError, NotSpdError, StorageError
 from .layout import BlockLayout
 from .prefixio import PrefixWriter
 from .storage import MatrixFile, MatrixSource
@@ -400,11 +400,15 @@ def _memdet(matrix, mode, case_label, max_mem, num_blocks, device, assume, hbm_b
     if src.symmetry == "generic" and mode != _native.MODE_LU:
         raise ValueError("symmetric driver requires a symmetric or spd input file")
     lay = _pick_layout(src.m, src.dtype.itemsize, max_mem, num_blocks)
+    sdir = _scratch_dir(scratch_dir)
+    if sdir is not None and lay.n_b > 2 and not os.path.isdir(sdir):
+        # the reference creates its scratchpad file there whenever it has slots (storage.py:147-165)
+        raise StorageError(f"scratch directory {sdir!r} does not exist")
     devices = tuple(int(x) for x in devices) if devices else ()
     if len(devices) > 1 and schur != "dmma":
         raise ValueError("schur='ozaki' is single-device")
     d, prefix, cinfo, ooc, perm = _run_engine(src, mode, device, lay, max_mem, hbm_budget, out_of_core,
-                                              schur == "ozaki", devices, _scratch_dir(scratch_dir))
+                                              schur == "ozaki", devices, sdir)
     nb = lay.n_b
     case = "generic" if mode == _native.MODE_LU else "symmetric"
     info = RunInfo(m=src.m, case=case_label, n_b=nb, b=lay.b,
