@@ -12,6 +12,8 @@ import threading
 from . import errors
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmemdet_b200.so")
+# A/B experiments only (tools/): another build of the same library
+LIB_PATH = os.environ.get("B2D_LIB_OVERRIDE", LIB_PATH)
 
 B2D_OK = 0
 B2D_ERR_USAGE = 2

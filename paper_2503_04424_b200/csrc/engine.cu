@@ -10,6 +10,7 @@
 // (dense.py:94-99), Schur-update the trailing tiles (dense.py:109-116); the prefix is the
 // running sum of 2 log L_ii (memdet.py:428).
 #include <algorithm>
+#include <cstdint>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <unistd.h>
@@ -39,6 +40,8 @@
 #include "ldl32.cu"
 
 namespace b2d {
+
+typedef unsigned long long CUdeviceptr_v2_compat;  // CUdeviceptr (driver API) for the entry points
 
 static thread_local std::string g_err;
 
@@ -192,6 +195,9 @@ struct Ooc {
   int64_t* perm_global = nullptr;
   double* dblk = nullptr;
   unsigned long long* amax = nullptr;
+  unsigned* lflags = nullptr;       // panel-server hand-off counters (ldl_panel_server_kernel)
+  cudaStream_t s_bulk = nullptr;    // panel-server bulk launches (high priority)
+  cudaEvent_t ev_lreset = nullptr, ev_lbulk = nullptr;
   uint8_t* ltag = nullptr;  // blocked pivoted LDL: per-entry tags, panel columns C / W, diagonal, pivot column
   double *lC = nullptr, *lW = nullptr, *ldiag = nullptr, *lcol = nullptr;
   double* inv2 = nullptr;  // LU: inverses of the diagonal tiles of U^T (column-block solves)
@@ -278,7 +284,7 @@ struct Ctx {
   cudaStream_t s_mid = nullptr;  // panel work off the potrf chain (rows below the panel block)
   cudaEvent_t ev_m2s = nullptr;  // s_main -> s_mid hand-off (potrf + in-block solve of a column)
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_join = nullptr;
-  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_resta, ev_catch, ev_stage, ev_copied, ev_band;
+  std::vector<cudaEvent_t> ev_panel, ev_rest, ev_resta, ev_catch, ev_stage, ev_copied, ev_band, ev_ub;
   // band activation (host ingest): band b = tile-columns [b*BAND, (b+1)*BAND) joins the
   // right-looking updates at outer step act[b] (-1: from the start) after one catch-up update
   std::vector<int> act;
@@ -310,6 +316,10 @@ struct Ctx {
   double* ublk[2] = {};
   double* bstage[2] = {};                     // host ingest: one reference block each
   std::vector<cudaEvent_t> ev_bstage, ev_cross;  // staging buffer free; stage k's blocks packed
+  // in-core pivoted LDL: one low-priority stream per block column (mod LDL_COL_STREAMS): a block
+  // column's updates are ordered by stage on its stream, independently of the other columns'
+  std::vector<cudaStream_t> s_cols;
+  std::vector<cudaEvent_t> ev_cols;
   // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
   // block column-major in dense, the stage's solved row-k blocks X and their D^{-1}-scaled copy S
   bool ldl32 = false;
@@ -359,6 +369,13 @@ static int configure_kernels() {
                                 (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L32_TRSM_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_server_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_server_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ldl_cluster_smem(LC_RMAX)));
+  {  // the server spins on the bulk kernel's progress: load it now, not lazily at its first launch
+    cudaFuncAttributes fa{};
+    CUDA_TRY(cudaFuncGetAttributes(&fa, ldl_bulk_kernel));
+  }
   done = true;
   return B2D_OK;
 }
@@ -402,7 +419,7 @@ static void destroy(Ctx* c) {
     cudaFree(c->oz_expo[b]);
   }
   if (c->s_pack) cudaStreamSynchronize(c->s_pack);
-  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_resta, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band,
+  for (auto* v : {&c->ev_panel, &c->ev_rest, &c->ev_resta, &c->ev_catch, &c->ev_stage, &c->ev_copied, &c->ev_band, &c->ev_ub,
                   &c->prof_ev})
     for (auto e : *v) cudaEventDestroy(e);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
@@ -414,6 +431,11 @@ static void destroy(Ctx* c) {
   if (c->s_side) cudaStreamDestroy(c->s_side);
   if (c->s_copy) cudaStreamDestroy(c->s_copy);
   if (c->s_pack) cudaStreamDestroy(c->s_pack);
+  for (auto st : c->s_cols) {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+  for (auto e : c->ev_cols) cudaEventDestroy(e);
   Ooc& o = c->o;
   if (o.s_h2d) cudaStreamSynchronize(o.s_h2d);
   if (o.s_d2h) cudaStreamSynchronize(o.s_d2h);
@@ -429,6 +451,13 @@ static void destroy(Ctx* c) {
   cudaFree(o.perm_global);
   cudaFree(o.dblk);
   cudaFree(o.amax);
+  if (o.s_bulk) {
+    cudaStreamSynchronize(o.s_bulk);
+    cudaStreamDestroy(o.s_bulk);
+  }
+  cudaFree(o.lflags);
+  if (o.ev_lreset) cudaEventDestroy(o.ev_lreset);
+  if (o.ev_lbulk) cudaEventDestroy(o.ev_lbulk);
   cudaFree(o.ltag);
   cudaFree(o.lC);
   cudaFree(o.lW);
@@ -557,6 +586,8 @@ static int create_streams_events(Ctx* c) {
   c->ev_panel.resize(nsteps);
   c->ev_rest.resize(nsteps);
   c->ev_resta.resize(nsteps);
+  c->ev_ub.resize(nsteps);
+  for (auto& e : c->ev_ub) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   c->ev_catch.resize(nsteps);
   c->trace = getenv("B2D_TRACE") != nullptr;
   const unsigned evf = c->trace ? cudaEventDefault : cudaEventDisableTiming;
@@ -1857,6 +1888,80 @@ static void ooc_schur(Ctx* c, int st, int j, int i, int sbj, int sci, int k) {
 // Pivoted LDL^T of the diagonal block in slot sa (stage k): dense copy, tolerance scale, the
 // cooperative 1x1-pivot factorisation, permutation / log|d| bookkeeping, then the unit factor
 // back into the slot and the inverses of its diagonal tiles for the panel solves.
+// Stream memory operations (driver API, through the runtime's entry-point lookup: no -lcuda).
+typedef int (*PFN_streamValue32)(cudaStream_t, CUdeviceptr_v2_compat, unsigned, unsigned);
+static PFN_streamValue32 stream_wait_value32() {
+  static PFN_streamValue32 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+    return (PFN_streamValue32)p;
+  }();
+  return fn;
+}
+static PFN_streamValue32 stream_write_value32() {
+  static PFN_streamValue32 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess) p = nullptr;
+    return (PFN_streamValue32)p;
+  }();
+  return fn;
+}
+constexpr unsigned B2D_STREAM_WAIT_VALUE_GEQ = 0;  // CU_STREAM_WAIT_VALUE_GEQ
+
+// The block factor with the panel server (ldl_panel_server_kernel) on s and the bulk updates on
+// o.s_bulk, each gated on the server's panel counter and bumping the bulk counter.
+static int ldl_server_factor(Ctx* c, const LdlArgs& g, cudaStream_t s) {
+  Ooc& o = c->o;
+  auto waitv = stream_wait_value32();
+  auto writev = stream_write_value32();
+  if (!waitv || !writev) return set_err(B2D_ERR_UNSUPPORTED, "stream memory operations unavailable");
+  if (!o.lflags) {
+    CUDA_TRY(cudaMalloc((void**)&o.lflags, 8));
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CUDA_TRY(cudaStreamCreateWithPriority(&o.s_bulk, cudaStreamNonBlocking, hi));
+    cudaEventCreateWithFlags(&o.ev_lreset, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&o.ev_lbulk, cudaEventDisableTiming);
+  }
+  const int64_t n = g.n;
+  cudaMemsetAsync(o.lflags, 0, 8, s);
+  cudaEventRecord(o.ev_lreset, s);
+  cudaStreamWaitEvent(o.s_bulk, o.ev_lreset, 0);  // the counters are reset (and the block is ready)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = LC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(LC);
+  cfg.blockDim = dim3(LC_THREADS);
+  cfg.dynamicSmemBytes = ldl_cluster_smem((int)((n + LC - 1) / LC));
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_server_kernel, g, o.lflags));
+  c->launches++;
+  const CUdeviceptr_v2_compat panels = (CUdeviceptr_v2_compat)(uintptr_t)o.lflags;
+  const CUdeviceptr_v2_compat bulks = panels + 4;
+  unsigned p = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB, ++p) {
+    const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
+    const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
+    if (waitv(o.s_bulk, panels, p + 1, B2D_STREAM_WAIT_VALUE_GEQ) != 0)
+      return set_err(B2D_ERR_CUDA, "cuStreamWaitValue32 failed");
+    if (ntile > 0) {
+      ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, o.s_bulk>>>(g, r0, nbk, ntile);
+      c->launches++;
+    }
+    if (writev(o.s_bulk, bulks, p + 1, 0) != 0) return set_err(B2D_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+  cudaEventRecord(o.ev_lbulk, o.s_bulk);
+  cudaStreamWaitEvent(s, o.ev_lbulk, 0);
+  return B2D_OK;
+}
+
 static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, bool overlapped = false) {
   Ooc& o = c->o;
   const int nt = o.tiles(k);
@@ -1881,6 +1986,14 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   // 16 SMs only: 58 ms vs 23 ms alone at b = 4096, so it loses at C2); 2 = always
   const char* pe = getenv("B2D_LDL_PERSIST");
   const int persist = pe ? atoi(pe) : 0;
+  // B2D_LDL_SERVER (1: beside other work, 2: always; default 0 -- measured slower at C2, 467 vs 453
+  // ms: the bulk steps then share the FP64 pipe with the DMMA updates): the panel server (one cluster holding its SMs)
+  // with each panel's bulk update gated by stream memory operations on s_bulk
+  const char* sve = getenv("B2D_LDL_SERVER");
+  const int server = sve ? atoi(sve) : 0;
+  if (n <= (int64_t)LC * LC_RMAX && !single_cta && persist == 0 && (server == 2 || (server == 1 && overlapped))) {
+    if (int rc = ldl_server_factor(c, g, s)) return rc;
+  } else
   if (n <= (int64_t)LC * LC_RMAX && !single_cta && (persist == 2 || (persist == 1 && overlapped))) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -2374,6 +2487,26 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     return t;
   };
   int rc = 0;
+  // column streams (urgent schedule): block column q on s_cols[q % n]
+  if (c->s_cols.empty()) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const int ncs = std::max(1, std::min(16, env_int("B2D_LDL_COL_STREAMS", 8)));
+    c->s_cols.resize(ncs);
+    c->ev_cols.resize(ncs);
+    for (int q = 0; q < ncs; ++q) {
+      cudaStreamCreateWithPriority(&c->s_cols[q], cudaStreamNonBlocking, lo);
+      cudaEventCreateWithFlags(&c->ev_cols[q], cudaEventDisableTiming);
+    }
+  }
+  for (auto cs : c->s_cols) cudaStreamWaitEvent(cs, c->ev_start, 0);
+  auto col_stream = [&](int q) { return c->s_cols[q % c->s_cols.size()]; };
+  // `st` waits for everything enqueued so far on block column q's stream
+  auto col_sync = [&](int q, cudaStream_t st) {
+    const int i = q % (int)c->s_cols.size();
+    cudaEventRecord(c->ev_cols[i], c->s_cols[i]);
+    cudaStreamWaitEvent(st, c->ev_cols[i], 0);
+  };
   // B2D_LDL_TRACE: timing events (name, stage) printed after the run
   const bool ltrace = getenv("B2D_LDL_TRACE") != nullptr;
   std::vector<std::pair<std::string, cudaEvent_t>> tev;
@@ -2427,7 +2560,12 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     u.p0 = 0;
     u.p1 = kb;
     const double K = (double)kb * T;
-    if (k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // block column k+1 current
+    // B2D_LDL_URGENT (default 1): each stage's update of block column k+2 runs on s_mid right
+    // after its panel (U_k below), so block column k+1 is current here by stream order; without
+    // it, that update heads the trailing update on s_side and queues behind the previous stage's
+    const char* ue = getenv("B2D_LDL_URGENT");
+    const bool urgent = (ue ? atoi(ue) != 0 : true) && !getenv("B2D_LDL_SCHED");
+    if (!urgent && k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // block column k+1 current
     if ((rc = wait_cols(c->s_mid, i0 + kb1))) return rc;
     u.out = TileSet{i0, r_split, i0, i0 + kb1, 1, 0};
     launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
@@ -2444,12 +2582,38 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     cudaEventRecord(c->ev_catch[k + 1], c->s_main);
     if (r_split < nt) {  // the rows below block k+1: solve, then their block-column k+1 update
       panel_rows(r_split, nt);
+      if (urgent) col_sync(k + 1, c->s_mid);  // stage k-1's update of those rows (column stream)
       u.out = TileSet{r_split, nt, i0, i0 + kb1, 1, 0};
       launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
       tmark("below-end", k, c->s_mid);
     }
     cudaEventRecord(c->ev_panel[k], c->s_mid);
-    if (i0 + kb1 < nt) {
+    if (i0 + kb1 < nt && urgent) {
+      // U_k: the diagonal block of block column k+2 on s_mid (the factor after next needs it),
+      // after every earlier update of that column; the rest of stage k's trailing update --
+      // block column j on its own low-priority column stream, after the whole panel -- so a
+      // column's stages are ordered on its stream and no column waits behind another's.
+      const int i2 = k + 2 < nb ? std::min(nt, i0 + kb1 + o.tiles(k + 2)) : nt;
+      if (k + 2 < nb) {
+        col_sync(k + 2, c->s_mid);
+        if ((rc = wait_cols(c->s_mid, i2))) return rc;
+        u.out = TileSet{i0 + kb1, i2, i0 + kb1, i2, 1, 0};
+        launch_update_kchunked(c, c->s_mid, u);
+      }
+      tmark("urgent-end", k, c->s_mid);
+      for (int q = k + 2, j0 = i0 + kb1; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
+        const int j1 = std::min(nt, j0 + o.tiles(q));
+        cudaStream_t cs = col_stream(q);
+        cudaStreamWaitEvent(cs, c->ev_panel[k], 0);
+        if ((rc = wait_cols(cs, j1))) return rc;
+        // block column k+2: its rows below the diagonal block (the diagonal block went above)
+        u.out = q == k + 2 ? TileSet{j1, nt, j0, j1, 0, 0} : TileSet{j0, nt, j0, j1, 1, 0};
+        if (u.out.count() > 0) launch_update_kchunked(c, cs, u);
+      }
+      // join stage k's readers of its panel buffers on s_side (ev_rest[k]: panel k+3 reuses them)
+      for (int q = k + 2; q < nb; ++q) col_sync(q, c->s_side);
+    } else if (i0 + kb1 < nt) {
+      // after the whole panel (issued after the next factor, which takes its SMs first)    } else if (i0 + kb1 < nt) {
       // after the whole panel (issued after the next factor, which takes its SMs first)
       cudaStreamWaitEvent(c->s_side, c->ev_panel[k], 0);
       if (serial) cudaStreamWaitEvent(c->s_side, c->ev_catch[k + 1], 0);
@@ -2484,6 +2648,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
   cudaEventRecord(o.ev_diag, c->s_side);
   cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+  for (int q = 0; q < (int)c->s_cols.size(); ++q) col_sync(q, c->s_main);
   cudaEventRecord(c->ev_join, c->s_pack);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
   enqueue_prefix(c);

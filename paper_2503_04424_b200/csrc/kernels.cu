@@ -433,7 +433,10 @@ struct GemmTask {
 
 constexpr int KC = 16;                  // columns per pipeline stage (two octets)
 constexpr int STAGE_ELEMS = T * KC;     // 2048 doubles = 16 KB per operand
-constexpr int STAGES = 4;
+#ifndef B2D_GEMM_STAGES
+#define B2D_GEMM_STAGES 4
+#endif
+constexpr int STAGES = B2D_GEMM_STAGES;
 constexpr int GEMM_THREADS = 288;       // 8 consumer warps + 1 producer warp
 constexpr int RASTER_G = 8;             // super-tile edge of the CTA raster (tile_order)
 constexpr size_t GEMM_SMEM = (size_t)STAGES * 2 * STAGE_ELEMS * 8 + 2 * STAGES * 8 + 128;

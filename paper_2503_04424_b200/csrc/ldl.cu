@@ -227,6 +227,9 @@ constexpr int LC = 16;                 // CTAs per cluster (non-portable size)
 constexpr int LC_THREADS = 256;
 constexpr int LC_LD = LDL_NB + 1;      // padded smem row (conflict-free column access)
 constexpr int LC_RMAX = 384;           // local rows per CTA (n <= LC * LC_RMAX)
+#ifndef LDL_PANEL_MINB
+#define LDL_PANEL_MINB 1
+#endif
 __host__ __device__ constexpr size_t ldl_cluster_smem(int rows) { return (size_t)rows * (2 * LC_LD + 2) * 8; }
 
 // Cluster-panel helpers.  Candidates: (|d| bits as hi + 1 : lo, index); hi = 0 marks "none"
@@ -523,7 +526,7 @@ __device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_
   }
 }
 
-__global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
+__global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
@@ -628,6 +631,12 @@ __global__ void __launch_bounds__(256) ldl_store_l_kernel(LdlArgs g, int64_t r0,
 // order, for j >= r0 + nbk, i >= j; tags reset.  64 x 64 entry tiles, 4 x 4 per thread (256
 // threads); tile b of the lower tile triangle (column-major).
 constexpr int LDL_BT = 64;
+// 4 CTAs per SM worth of registers (<= 64 per thread): a bulk CTA then fits on an SM that runs a
+// DMMA Schur-update CTA (288 threads x 168 registers, 128 KB shared), so the factor's bulk steps
+// start at once beside the trailing updates instead of waiting for SMs to drain
+#ifndef LDL_BULK_MINB
+#define LDL_BULK_MINB 4
+#endif
 __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int nbk, int64_t b, double* sC,
                                               double* sW) {
   const int64_t re = r0 + nbk, m = g.n - re, ld = g.ld, n = g.n;
@@ -729,7 +738,7 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
 
 // Blocks [0, ntile): the bulk tiles; blocks [ntile, gridDim.x): the panel's row interchanges on
 // the finished L columns (after the cluster panel kernel, which stores the panel's L itself).
-__global__ void __launch_bounds__(256) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile) {
+__global__ void __launch_bounds__(256, LDL_BULK_MINB) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile) {
   if (*g.fail != ~0ull) return;
   __shared__ __align__(16) double sC[LDL_NB * LDL_BT];
   __shared__ __align__(16) double sW[LDL_NB * LDL_BT];
@@ -804,6 +813,64 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlAr
     for (int q = 0; q < 8; ++q) ldl_prof[8 + q] += prof_acc[q];
 #endif
 #undef FMARK
+}
+
+// Panel server: the block's panels on one 16-CTA cluster that holds its SMs for the whole factor
+// (so the latency-bound pivot steps never share an SM with the trailing DMMA updates), while each
+// panel's bulk update runs as an ordinary kernel on every SM (ldl_bulk_kernel: <= 64 registers,
+// so its CTAs fit beside a Schur-update CTA).  Hand-off through two counters in global memory:
+// flags[0] = panels finished (the server releases it after the panel's L columns and row
+// interchanges are stored; the host gates panel p's bulk launch on it with a stream wait-value),
+// flags[1] = bulk updates finished (a stream write-value after each bulk launch; the server
+// acquires it before the next panel).  Same steps, same arithmetic as the per-panel kernels.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_server_kernel(LdlArgs g, unsigned* flags) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  extern __shared__ double sm[];
+  const int64_t n = g.n, ld = g.ld;
+  const int R = (int)((n + LC - 1) / LC);
+  double* Cs = sm;                      // [R][LC_LD]
+  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
+  double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal (kept across panels)
+  __shared__ ClusterShared sh;
+  cluster_shared_init(sh);
+  if (*g.fail != ~0ull) {  // an earlier block failed: release every gated bulk launch
+    if (c == 0 && threadIdx.x == 0) st_release_u32(flags, 0x7fffffffu);
+    return;
+  }
+  for (int li = threadIdx.x; li < R; li += LC_THREADS) {
+    const int64_t i = (int64_t)li * LC + c;
+    dg[li] = i < n ? __ldcg(g.A + i * ld + i) : 0.0;
+  }
+  __syncthreads();
+  cl.sync();
+  unsigned p = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB, ++p) {
+    const int nbk = (int)(n - r0 < LDL_NB ? n - r0 : LDL_NB);
+    if (p > 0) {  // panel p - 1's bulk update is in
+      if (threadIdx.x == 0)
+        while (ld_acquire_u32(flags + 1) < p) __nanosleep(128);
+      __syncthreads();
+    }
+    if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, (int)r0)) {
+      if (c == 0 && threadIdx.x == 0) st_release_u32(flags, 0x7fffffffu);
+      return;
+    }
+    cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c, false);
+    cl.sync();  // C / W rows and the panel's interchanges visible cluster-wide
+    ldl_store_part(g, r0, nbk, sh.spos, sh.ssrc, c, LC);
+    __threadfence();
+    cl.sync();  // every CTA's stores done before the release
+    if (c == 0 && threadIdx.x == 0) st_release_u32(flags, p + 1);
+  }
 }
 
 // swaps -> block permutation (kernels/dense.py:25-30), global perm (memdet.py:352-353),
