@@ -215,6 +215,27 @@ int b2d_ipc_get_handle(void *p, void *handle_out);
 int b2d_ipc_open_handle(int device, const void *handle, void **out);
 int b2d_ipc_close_handle(void *p);
 
+/* Tile seam: the reference's kernel module on the GPU (oocdet.kernels, kernels/__init__.py:24-45;
+ * dense.py:57-116), HOST row-major tiles (leading dimension in elements) updated in place, in the
+ * tile's dtype (B2D_F64 / B2D_F32) with the golden host's LAPACK / BLAS rounding sequence (LDL,
+ * TRSM and GEMM bit-identical there; paper_2503_04424_b200/kernels.py wraps them so the
+ * reference's own driver can be patched onto the engine).  Synchronous.
+ *   b2d_tile_ldl_host          <- ldl_inplace / _ldl.pyx:21-61: lower triangle -> unit L (strict)
+ *                                 and D (diagonal), swaps (LAPACK style), d; tol as dense.py:73;
+ *                                 *fail_step = failing step or -1 (the caller raises)
+ *   b2d_tile_cholesky_host     <- cholesky_inplace (dense.py:84-91): a = L (zeros above), diag
+ *   b2d_tile_solve_lower_host  <- solve_lower_inplace (dense.py:94-99): B <- L^{-1} B
+ *   b2d_tile_schur_update_host <- schur_update(s, c, b, "ct_b") (dense.py:109-116): S -= C^T B,
+ *                                 S m x n, C k x m, B k x n */
+int b2d_tile_ldl_host(void *a, int64_t n, int64_t lda, int dtype, double tol, int64_t *swaps, void *d,
+                      int64_t *fail_step, int device);
+int b2d_tile_cholesky_host(void *a, int64_t n, int64_t lda, int dtype, void *diag, int64_t *fail_step,
+                           int device);
+int b2d_tile_solve_lower_host(const void *l, int64_t n, int64_t ldl, void *b, int64_t w, int64_t ldb,
+                              int dtype, int unit_diag, int device);
+int b2d_tile_schur_update_host(void *s, int64_t m, int64_t n, int64_t lds, const void *c, int64_t ldc,
+                               const void *b, int64_t ldb, int64_t k, int dtype, int device);
+
 /* FP64 roofline calibration (off the timed path): sustained DMMA m8n8k4 rate over every SM for
  * about `seconds`, in TFLOP/s (2 flops per FMA). */
 int b2d_probe_fp64_peak(int device, double seconds, double *tflops);

@@ -209,6 +209,11 @@ def lower_solve(l: np.ndarray, b: np.ndarray, unit: bool):
     b[:] = _lapack_trtrs(l, b, lower=True, unit_diagonal=unit, check_finite=False)
 
 
+def schur_update(tile: np.ndarray, c: np.ndarray, b: np.ndarray):
+    """kernels/dense.py:109-116 (form "ct_b") — T <- T - C^T B (NumPy matmul -> BLAS ?gemm)."""
+    tile -= c.T @ b
+
+
 # ----------------------------------------------------------------------------- driver
 
 
@@ -278,8 +283,7 @@ def memdet_symmetric(mat: np.ndarray, n_b: int, pivoted: bool, inplace: bool = F
             reads += 1  # the target tile (memdet.py:384)
             c_t = solved[i]
             b_t = solved[j] / dk[:, None] if pivoted else solved[j]
-            tile = work[lay.span(i), lay.span(j)]
-            tile -= c_t.T @ b_t
+            schur_update(work[lay.span(i), lay.span(j)], c_t, b_t)
             if not v["next_diag"]:
                 writes += 1
                 slots.add((i, j))

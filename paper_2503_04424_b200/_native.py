@@ -95,6 +95,10 @@ SIGNATURES = {
     "b2d_ctx_gram_accumulate": (_I, [_P, _P, _I64, _I64, _D, _P]),
     "b2d_ctx_factor_packed_async": (_I, [_P, _P]),
     "b2d_probe_fp64_peak": (_I, [_I, _D, ctypes.POINTER(_D)]),
+    "b2d_tile_ldl_host": (_I, [_P, _I64, _I64, _I, _D, _P, _P, ctypes.POINTER(_I64), _I]),
+    "b2d_tile_cholesky_host": (_I, [_P, _I64, _I64, _I, _P, ctypes.POINTER(_I64), _I]),
+    "b2d_tile_solve_lower_host": (_I, [_P, _I64, _I64, _P, _I64, _I64, _I, _I, _I]),
+    "b2d_tile_schur_update_host": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _I64, _I, _I]),
     "b2d_tile_potrf_inv": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _P]),
     "b2d_tile_gemm": (_I, [_I, ctypes.POINTER(TileMapC), ctypes.POINTER(TileMapC),
                            ctypes.POINTER(TileMapC), _P, ctypes.POINTER(TileSetC), ctypes.c_int32,

@@ -332,7 +332,7 @@ struct Ctx {
     int64_t ldx = 0;
     float* work = nullptr;
     float* d = nullptr;
-    unsigned* amax = nullptr;
+    unsigned long long* amax = nullptr;
   } f;
 };
 
@@ -368,7 +368,10 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L32_TRSM_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)l32_trsm_smem<float>()));
+  CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)l32_trsm_smem<double>()));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_server_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_server_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
@@ -734,7 +737,7 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     }
     ALLOC(f.work, (size_t)b * 4);
     ALLOC(f.d, (size_t)m * 4);
-    ALLOC(f.amax, 4);
+    ALLOC(f.amax, 8);
     ALLOC(o.swaps, (size_t)b * 8);
     ALLOC(o.perm_local, (size_t)b * 8);
     ALLOC(o.perm_global, (size_t)m * 8);
@@ -2700,26 +2703,26 @@ static int run_ldl32(Ctx* c, const void* a, int64_t lda, int dtype, bool host, c
   const int nkb = l32_kblocks(b, kb);
   for (int k = 0; k < nb; ++k) {
     const int64_t k0 = (int64_t)k * b, hk = o.size(k);
-    cudaMemsetAsync(f.amax, 0, 4, s);
+    cudaMemsetAsync(f.amax, 0, 8, s);
     const dim3 gb((unsigned)((hk + 31) / 32), (unsigned)((hk + 31) / 32));
-    l32_block_in_kernel<<<gb, 256, 0, s>>>(f.M, f.ldm, k0, hk, f.dense, f.ldd, f.amax);
-    const L32Step g{f.dense, f.ldd, hk, k0, f.work, f.d + k0, o.swaps, c->fail, f.amax};
+    l32_block_in_kernel<float><<<gb, 256, 0, s>>>(f.M, f.ldm, k0, hk, f.dense, f.ldd, f.amax);
+    const L32Step<float> g{f.dense, f.ldd, hk, k0, f.work, f.d + k0, o.swaps, c->fail, f.amax, -1.0};
     for (int64_t r = 0; r < hk; ++r) {
-      l32_step_kernel<<<1, 1024, 0, s>>>(g, r);
-      if (r + 1 < hk) l32_update_kernel<<<(unsigned)(hk - r - 1), 256, 0, s>>>(g, r);
+      l32_step_kernel<float><<<1, 1024, 0, s>>>(g, r);
+      if (r + 1 < hk) l32_update_kernel<float><<<(unsigned)(hk - r - 1), 256, 0, s>>>(g, r);
     }
-    l32_finish_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (hk + 255) / 256)), 256, 0, s>>>(
+    l32_finish_kernel<float><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(64, (hk + 255) / 256)), 256, 0, s>>>(
         o.swaps, f.d + k0, hk, k0, o.perm_local, o.perm_global, c->ell, c->diag, c->fail);
     c->launches += 3 + 2 * hk - 1;
     if (k == nb - 1) break;
     const int64_t c0 = k0 + b, W = m - c0;
     // row-k blocks in pivot order (memdet.py:365-366, 378-379), solved (dense.py:94-99)
-    l32_gather_kernel<<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)),
+    l32_gather_kernel<float><<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)),
                         256, 0, s>>>(f.M, f.ldm, k0, c0, o.perm_local, b, W, f.X, f.ldx);
     for (int64_t ls = 0; ls < b; ls += L32_Q) {
       const int64_t le = std::min<int64_t>(b, ls + L32_Q);
-      l32_trsm_diag_kernel<<<(unsigned)((W + L32_TW - 1) / L32_TW), 256, L32_TRSM_SMEM, s>>>(f.dense, f.ldd, f.X, f.ldx,
-                                                                                           W, ls, le, c->fail);
+      l32_trsm_diag_kernel<float><<<(unsigned)((W + TrsmTW<float>::v - 1) / TrsmTW<float>::v), 256,
+                                    l32_trsm_smem<float>(), s>>>(f.dense, f.ldd, f.X, f.ldx, W, ls, le, 1, c->fail);
       c->launches++;
       if (le < b) {  // rows below the row block: X -= L(le:, ls:le) X(ls:le, :), one chain each
         G32 u{};
@@ -2735,13 +2738,13 @@ static int run_ldl32(Ctx* c, const void* a, int64_t lda, int dtype, bool host, c
         u.kb[0] = 0;
         u.kb[1] = (int)(le - ls);
         u.blk = 1;
-        l32_gemm_kernel<<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((b - le + G32_BM - 1) / G32_BM)), 256, 0,
-                          s>>>(u, c->fail);
+        l32_gemm_kernel<float><<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((b - le + G32_BM - 1) / G32_BM)),
+                                 256, 0, s>>>(u, c->fail);
         c->launches++;
       }
     }
     // S = X / d (memdet.py:368-371); T(i, j) -= X_i^T S_j for every trailing block i <= j (memdet.py:385)
-    l32_scale_kernel<<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0,
+    l32_scale_kernel<float><<<dim3((unsigned)std::min<int64_t>(64, (W + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0,
                        s>>>(f.X, f.S, f.ldx, b, W, f.d + k0);
     G32 u{};
     u.A = f.X;
@@ -2757,8 +2760,8 @@ static int run_ldl32(Ctx* c, const void* a, int64_t lda, int dtype, bool host, c
     u.tri = 1;
     u.blk = b;
     u.roff = u.coff = c0;
-    l32_gemm_kernel<<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((W + G32_BM - 1) / G32_BM)), 256, 0, s>>>(
-        u, c->fail);
+    l32_gemm_kernel<float><<<dim3((unsigned)((W + G32_BN - 1) / G32_BN), (unsigned)((W + G32_BM - 1) / G32_BM)), 256, 0,
+                             s>>>(u, c->fail);
     c->launches += 4;
   }
   enqueue_prefix(c);
@@ -3407,4 +3410,232 @@ extern "C" int b2d_ctx_factor_packed_async(b2d_ctx* ctx, void* stream) {
   end(ctx, user);
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;
+}
+
+// ---------------------------------------------------------------- tile seam: oocdet.kernels on the GPU
+// Host tiles in, host tiles out (the reference's kernel module, kernels/__init__.py:24-45,
+// dense.py:57-116): each call uploads its operands, runs the ldl32.cu kernels in the file dtype
+// with the golden host's BLAS / LAPACK rounding sequence (LDL, TRSM, GEMM: bit-identical there),
+// and writes the results back in place.  Synchronous; for the reference's own driver patched
+// onto this engine (paper_2503_04424_b200/kernels.py), not the hot path.
+namespace b2d {
+
+template <typename E>
+__global__ void seam_lower_to_rowmajor_kernel(const E* __restrict__ dense, int64_t n, E* __restrict__ M, int zero_upper) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    if (j <= i) M[e] = dense[j * n + i];
+    else if (zero_upper) M[e] = (E)0;
+  }
+}
+
+// Unblocked right-looking Cholesky step j on a column-major block: l_jj = sqrt(a_jj) (fail when
+// a_jj is not positive), l_ij = a_ij / l_jj; then the trailing update a_ik -= l_ij l_kj.
+template <typename E>
+__global__ void seam_chol_step_kernel(E* a, int64_t n, int64_t j, unsigned long long* fail) {
+  __shared__ E piv;
+  if (*fail != ~0ull) return;
+  if (threadIdx.x == 0) {
+    const E v = a[j * n + j];
+    piv = v > (E)0 ? sqrt(v) : (E)-1;
+    if (!(v > (E)0)) atomicMin(fail, (unsigned long long)j);
+    else a[j * n + j] = piv;
+  }
+  __syncthreads();
+  if (piv < (E)0) return;
+  for (int64_t i = j + 1 + threadIdx.x; i < n; i += blockDim.x) a[j * n + i] = Blas<E>::div(a[j * n + i], piv);
+}
+template <typename E>
+__global__ void seam_chol_update_kernel(E* a, int64_t n, int64_t j, const unsigned long long* fail) {
+  if (*fail != ~0ull) return;
+  const int64_t k = j + 1 + blockIdx.x;
+  const E lkj = a[j * n + k];
+  for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) a[k * n + i] = Blas<E>::fma(-a[j * n + i], lkj, a[k * n + i]);
+}
+
+struct SeamMem {
+  std::vector<void*> p;
+  ~SeamMem() {
+    for (void* q : p) cudaFree(q);
+  }
+  template <typename X>
+  X* get(size_t count) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(X)) != cudaSuccess) return nullptr;
+    p.push_back(q);
+    return (X*)q;
+  }
+};
+
+template <typename E>
+static int seam_ldl(E* a, int64_t n, int64_t lda, double tol, int64_t* swaps, E* d, int64_t* fail_step) {
+  SeamMem mem;
+  E *M = mem.get<E>(n * n), *dense = mem.get<E>(n * n), *work = mem.get<E>(n), *dd = mem.get<E>(n);
+  int64_t *sw = mem.get<int64_t>(n);
+  unsigned long long *fail = mem.get<unsigned long long>(1), *amax = mem.get<unsigned long long>(1);
+  if (!M || !dense || !work || !dd || !sw || !fail || !amax) return set_err(B2D_ERR_NOMEM, "tile seam: device allocation");
+  CUDA_TRY(cudaMemcpy2D(M, n * sizeof(E), a, lda * sizeof(E), n * sizeof(E), n, cudaMemcpyHostToDevice));
+  cudaMemset(fail, 0xff, 8);
+  cudaMemset(amax, 0, 8);
+  const dim3 gb((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  l32_block_in_kernel<E><<<gb, 256>>>(M, n, 0, n, dense, n, amax);
+  const L32Step<E> g{dense, n, n, 0, work, dd, sw, fail, amax, tol};
+  for (int64_t r = 0; r < n; ++r) {
+    l32_step_kernel<E><<<1, 1024>>>(g, r);
+    if (r + 1 < n) l32_update_kernel<E><<<(unsigned)(n - r - 1), 256>>>(g, r);
+  }
+  unsigned long long f = ~0ull;
+  CUDA_TRY(cudaMemcpy(&f, fail, 8, cudaMemcpyDeviceToHost));
+  *fail_step = f == ~0ull ? -1 : (int64_t)f;
+  if (f != ~0ull) return B2D_OK;  // the caller raises (dense.py:74-80)
+  seam_lower_to_rowmajor_kernel<E><<<1024, 256>>>(dense, n, M, 0);  // the strict upper part stays the input's
+  CUDA_TRY(cudaMemcpy2D(a, lda * sizeof(E), M, n * sizeof(E), n * sizeof(E), n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(swaps, sw, n * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(d, dd, n * sizeof(E), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+template <typename E>
+static int seam_cholesky(E* a, int64_t n, int64_t lda, E* diag, int64_t* fail_step) {
+  SeamMem mem;
+  E *M = mem.get<E>(n * n), *dense = mem.get<E>(n * n);
+  unsigned long long *fail = mem.get<unsigned long long>(1), *amax = mem.get<unsigned long long>(1);
+  if (!M || !dense || !fail || !amax) return set_err(B2D_ERR_NOMEM, "tile seam: device allocation");
+  CUDA_TRY(cudaMemcpy2D(M, n * sizeof(E), a, lda * sizeof(E), n * sizeof(E), n, cudaMemcpyHostToDevice));
+  cudaMemset(fail, 0xff, 8);
+  const dim3 gb((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  l32_block_in_kernel<E><<<gb, 256>>>(M, n, 0, n, dense, n, amax);
+  for (int64_t j = 0; j < n; ++j) {
+    seam_chol_step_kernel<E><<<1, 256>>>(dense, n, j, fail);
+    if (j + 1 < n) seam_chol_update_kernel<E><<<(unsigned)(n - j - 1), 256>>>(dense, n, j, fail);
+  }
+  unsigned long long f = ~0ull;
+  CUDA_TRY(cudaMemcpy(&f, fail, 8, cudaMemcpyDeviceToHost));
+  *fail_step = f == ~0ull ? -1 : (int64_t)f;
+  if (f != ~0ull) return B2D_OK;
+  seam_lower_to_rowmajor_kernel<E><<<1024, 256>>>(dense, n, M, 1);  // L, zeros above (scipy's lower factor)
+  CUDA_TRY(cudaMemcpy2D(a, lda * sizeof(E), M, n * sizeof(E), n * sizeof(E), n, cudaMemcpyDeviceToHost));
+  for (int64_t j = 0; j < n; ++j) diag[j] = a[j * lda + j];
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+template <typename E>
+static int seam_trsm(const E* l, int64_t n, int64_t ldl, E* b, int64_t w, int64_t ldb, int unit) {
+  SeamMem mem;
+  E *M = mem.get<E>(n * n), *dense = mem.get<E>(n * n), *X = mem.get<E>(n * w);
+  unsigned long long *fail = mem.get<unsigned long long>(1), *amax = mem.get<unsigned long long>(1);
+  if (!M || !dense || !X || !fail || !amax) return set_err(B2D_ERR_NOMEM, "tile seam: device allocation");
+  CUDA_TRY(cudaMemcpy2D(M, n * sizeof(E), l, ldl * sizeof(E), n * sizeof(E), n, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy2D(X, w * sizeof(E), b, ldb * sizeof(E), w * sizeof(E), n, cudaMemcpyHostToDevice));
+  cudaMemset(fail, 0xff, 8);
+  const dim3 gb((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  l32_block_in_kernel<E><<<gb, 256>>>(M, n, 0, n, dense, n, amax);  // L column-major
+  constexpr int Q = Blas<E>::Q, TW = TrsmTW<E>::v;
+  for (int64_t ls = 0; ls < n; ls += Q) {
+    const int64_t le = std::min<int64_t>(n, ls + Q);
+    l32_trsm_diag_kernel<E><<<(unsigned)((w + TW - 1) / TW), 256, l32_trsm_smem<E>()>>>(dense, n, X, w, w, ls, le, unit,
+                                                                                      fail);
+    if (le < n) {
+      GT<E> u{};
+      u.A = dense + ls * n + le;
+      u.lda = n;
+      u.B = X + ls * w;
+      u.ldb = w;
+      u.C = X + le * w;
+      u.ldc = w;
+      u.Mr = n - le;
+      u.Nc = w;
+      u.nkb = 1;
+      u.kb[1] = (int)(le - ls);
+      u.blk = 1;
+      l32_gemm_kernel<E><<<dim3((unsigned)((w + G32_BN - 1) / G32_BN), (unsigned)((n - le + gemm_bm<E>() - 1) / gemm_bm<E>())),
+                           256>>>(u, fail);
+    }
+  }
+  CUDA_TRY(cudaMemcpy2D(b, ldb * sizeof(E), X, w * sizeof(E), w * sizeof(E), n, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+template <typename E>
+static int seam_schur(E* s, int64_t m, int64_t nn, int64_t lds, const E* c, int64_t ldc, const E* b, int64_t ldb,
+                      int64_t K) {
+  SeamMem mem;
+  E *S = mem.get<E>(m * nn), *C = mem.get<E>(K * m), *B = mem.get<E>(K * nn);
+  unsigned long long* fail = mem.get<unsigned long long>(1);
+  if (!S || !C || !B || !fail) return set_err(B2D_ERR_NOMEM, "tile seam: device allocation");
+  CUDA_TRY(cudaMemcpy2D(S, nn * sizeof(E), s, lds * sizeof(E), nn * sizeof(E), m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy2D(C, m * sizeof(E), c, ldc * sizeof(E), m * sizeof(E), K, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy2D(B, nn * sizeof(E), b, ldb * sizeof(E), nn * sizeof(E), K, cudaMemcpyHostToDevice));
+  cudaMemset(fail, 0xff, 8);
+  GT<E> u{};
+  u.A = C;
+  u.lda = m;
+  u.B = B;
+  u.ldb = nn;
+  u.C = S;
+  u.ldc = nn;
+  u.Mr = m;
+  u.Nc = nn;
+  u.nkb = l32_kblocks(K, u.kb, Blas<E>::Q);
+  u.blk = 1;
+  if (K > 0)
+    l32_gemm_kernel<E><<<dim3((unsigned)((nn + G32_BN - 1) / G32_BN), (unsigned)((m + gemm_bm<E>() - 1) / gemm_bm<E>())),
+                         256>>>(u, fail);
+  CUDA_TRY(cudaMemcpy2D(s, lds * sizeof(E), S, nn * sizeof(E), nn * sizeof(E), m, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaGetLastError());
+  return B2D_OK;
+}
+
+static int seam_begin(int device, int dtype) {
+  if (dtype != B2D_F64 && dtype != B2D_F32) return set_err(B2D_ERR_USAGE, "dtype code %d", dtype);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(B2D_ERR_CUDA, "no CUDA device visible: the B200 engine has no CPU fallback");
+  if (device < 0 || device >= ndev) return set_err(B2D_ERR_USAGE, "bad device %d", device);
+  CUDA_TRY(cudaSetDevice(device));
+  return configure_kernels();
+}
+
+}  // namespace b2d
+
+extern "C" int b2d_tile_ldl_host(void* a, int64_t n, int64_t lda, int dtype, double tol, int64_t* swaps, void* d,
+                                 int64_t* fail_step, int device) {
+  if (!a || !swaps || !d || !fail_step || n < 0 || lda < n) return set_err(B2D_ERR_USAGE, "bad b2d_tile_ldl_host arguments");
+  if (int rc = seam_begin(device, dtype)) return rc;
+  *fail_step = -1;
+  if (n == 0) return B2D_OK;
+  return dtype == B2D_F64 ? seam_ldl<double>((double*)a, n, lda, tol, swaps, (double*)d, fail_step)
+                          : seam_ldl<float>((float*)a, n, lda, tol, swaps, (float*)d, fail_step);
+}
+
+extern "C" int b2d_tile_cholesky_host(void* a, int64_t n, int64_t lda, int dtype, void* diag, int64_t* fail_step,
+                                      int device) {
+  if (!a || !diag || !fail_step || n < 0 || lda < n) return set_err(B2D_ERR_USAGE, "bad b2d_tile_cholesky_host arguments");
+  if (int rc = seam_begin(device, dtype)) return rc;
+  *fail_step = -1;
+  if (n == 0) return B2D_OK;
+  return dtype == B2D_F64 ? seam_cholesky<double>((double*)a, n, lda, (double*)diag, fail_step)
+                          : seam_cholesky<float>((float*)a, n, lda, (float*)diag, fail_step);
+}
+
+extern "C" int b2d_tile_solve_lower_host(const void* l, int64_t n, int64_t ldl, void* b, int64_t w, int64_t ldb, int dtype,
+                                         int unit_diag, int device) {
+  if (!l || !b || n < 0 || w < 0 || ldl < n || ldb < w) return set_err(B2D_ERR_USAGE, "bad b2d_tile_solve_lower_host arguments");
+  if (int rc = seam_begin(device, dtype)) return rc;
+  if (n == 0 || w == 0) return B2D_OK;
+  return dtype == B2D_F64 ? seam_trsm<double>((const double*)l, n, ldl, (double*)b, w, ldb, unit_diag)
+                          : seam_trsm<float>((const float*)l, n, ldl, (float*)b, w, ldb, unit_diag);
+}
+
+extern "C" int b2d_tile_schur_update_host(void* s, int64_t m, int64_t n, int64_t lds, const void* c, int64_t ldc,
+                                          const void* b, int64_t ldb, int64_t k, int dtype, int device) {
+  if (!s || !c || !b || m < 0 || n < 0 || k < 0 || lds < n || ldc < m || ldb < n)
+    return set_err(B2D_ERR_USAGE, "bad b2d_tile_schur_update_host arguments");
+  if (int rc = seam_begin(device, dtype)) return rc;
+  if (m == 0 || n == 0) return B2D_OK;
+  return dtype == B2D_F64 ? seam_schur<double>((double*)s, m, n, lds, (const double*)c, ldc, (const double*)b, ldb, k)
+                          : seam_schur<float>((float*)s, m, n, lds, (const float*)c, ldc, (const float*)b, ldb, k);
 }
