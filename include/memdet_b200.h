@@ -203,6 +203,10 @@ int b2d_tile_gemm(int mode, const b2d_tilemap *a, const b2d_tilemap *b, const b2
  * stored row row_base; only the row-major upper tile triangle is read, identity beyond m). */
 int b2d_pack_tiles(const void *src, int64_t lda, int dtype, int64_t row_base, int64_t m,
                    const b2d_tilemap *out, const b2d_tileset *set, void *stream);
+/* Host -> device 2D copy on `stream` (bytes; cudaMemcpy2DAsync): the distributed driver's sharded
+ * ingest, each rank copying only its own tile rows' column strips of a host matrix. */
+int b2d_h2d_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width, int64_t height,
+               void *stream);
 /* prefix[q] = sum_{g <= q} ell[g] (double-double, rounded once), q < m. */
 int b2d_prefix_scan(const double *ell, int64_t m, double *prefix, void *stream);
 /* Peer-shared device buffers for the multi-GPU driver (replaces the panel all-gather: every rank

@@ -106,6 +106,7 @@ SIGNATURES = {
     "b2d_pack_tiles": (_I, [_P, _I64, _I, _I64, _I64, ctypes.POINTER(TileMapC),
                             ctypes.POINTER(TileSetC), _P]),
     "b2d_prefix_scan": (_I, [_P, _I64, _P, _P]),
+    "b2d_h2d_2d": (_I, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "b2d_dev_alloc": (_I, [_I, _I64, ctypes.POINTER(_P)]),
     "b2d_dev_free": (_I, [_P]),
     "b2d_ipc_get_handle": (_I, [_P, _P]),

@@ -3349,6 +3349,15 @@ extern "C" int b2d_pack_tiles(const void* src, int64_t lda, int dtype, int64_t r
   return B2D_OK;
 }
 
+extern "C" int b2d_h2d_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                          void* stream) {
+  if (!dst || !src || width < 0 || height < 0) return set_err(B2D_ERR_USAGE, "bad b2d_h2d_2d arguments");
+  if (width == 0 || height == 0) return B2D_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                             cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return B2D_OK;
+}
+
 extern "C" int b2d_prefix_scan(const double* ell, int64_t m, double* prefix, void* stream) {
   if (!ell || !prefix || m < 1) return set_err(B2D_ERR_USAGE, "bad b2d_prefix_scan arguments");
   prefix_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ell, m, prefix);

@@ -174,6 +174,39 @@ class CudaTileOps:
                       "b2d_pack_tiles")
         self.launches += 1
 
+    def load_host(self, a, lda: int | None = None):
+        """Sharded ingest from a HOST row-major matrix (NumPy; pinned or pageable): this rank copies
+        only its own tile rows -- tile row i is the file's column strip [128 i, 128 i + 128) over
+        rows [0, 128 (i + 1)) (the upper triangle the reference reads) -- and packs them; no rank
+        holds the matrix.  Returns the bytes copied."""
+        import numpy as np
+
+        torch = self.torch
+        a = np.asarray(a)
+        dcode = _native.B2D_F64 if a.dtype == np.float64 else _native.B2D_F32
+        esz = a.itemsize
+        lda = lda or a.strides[0] // esz
+        d, m, nt = self.dist, self.m, self.dist.nt
+        buf = torch.empty(nt * T * T * esz, dtype=torch.uint8, device=self.dev)
+        moved = 0
+        for li, i in enumerate(d.rows):
+            c0 = i * T
+            width, rows = max(0, min(T, m - c0)), min(m, (i + 1) * T)
+            if width > 0:
+                _native.check(self.lib.b2d_h2d_2d(ctypes.c_void_p(buf.data_ptr()), T * esz,
+                                                  ctypes.c_void_p(a.ctypes.data + c0 * esz), lda * esz, width * esz,
+                                                  rows, self._stream()), "b2d_h2d_2d")
+                moved += width * rows * esz
+            # element (R, C) of tile (i, J) is file[C][R]: the strip holds column R - 128 i of row C
+            src = buf.data_ptr() - c0 * esz
+            s = _native.TileSetC(li, li + 1, 0, i + 1, 0, 0, d.world, d.rank)
+            _native.check(self.lib.b2d_pack_tiles(ctypes.c_void_p(src), T, dcode, 0, m,
+                                                  ctypes.byref(self._grid_map()), ctypes.byref(s), self._stream()),
+                          "b2d_pack_tiles")
+            self.launches += 1
+        self._keep = buf  # released with the next load (stream-ordered reuse)
+        return moved
+
     def begin(self):
         self.ell.zero_()
         self.diag.zero_()
@@ -438,20 +471,29 @@ class DistributedMemdet:
             self.shared = None
 
     def run(self, a):
-        """Enqueue pack + factorisation of the CUDA row-major matrix `a` (every rank passes the
-        matrix; each packs its own tile rows).  Returns (device prefix view, fail)."""
-        self.ops.load(a)
+        """Enqueue pack + factorisation of the row-major matrix `a` -- a CUDA tensor every rank can
+        address, or a HOST array (NumPy) from which each rank copies only its own tile rows.
+        Returns (device prefix view, fail)."""
+        if hasattr(a, "is_cuda") and a.is_cuda:
+            self.ops.load(a)
+        else:
+            self.h2d_bytes = self.ops.load_host(a)
         return factor_distributed(self.ops, self.comm, self.dist, self.panel_tiles)
 
 
-def memdet_cholesky_distributed(a, group=None, panel_tiles: int = 8, peer=None):
-    """Distributed logdet of a CUDA row-major SPD matrix visible to every rank (each rank packs
-    only its own tile rows).  Returns (prefix as a NumPy array, fail index) on every rank."""
+def memdet_cholesky_distributed(a, group=None, panel_tiles: int = 8, peer=None, device=None):
+    """Distributed logdet of a row-major SPD matrix: a CUDA tensor visible to every rank, or a host
+    array (each rank copies and packs only its own tile rows).  Returns (prefix as a NumPy array,
+    fail index) on every rank."""
     import torch
 
-    runner = DistributedMemdet(int(a.shape[0]), group, panel_tiles, a.device, peer=peer)
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        device = a.device
+    elif device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    runner = DistributedMemdet(int(a.shape[0]), group, panel_tiles, device, peer=peer)
     prefix, fail = runner.run(a)
-    torch.cuda.synchronize(a.device)
+    torch.cuda.synchronize(device)
     out = prefix.cpu().numpy()
     runner.close()
     return out, fail

@@ -267,7 +267,7 @@ def test_out_of_core_not_spd():
 # ------------------------------------------------------------------ multi-rank driver on the GPU
 
 
-def _dist_worker(rank, world, port, backend, m, panel, peer, q):
+def _dist_worker(rank, world, port, backend, m, panel, peer, q, host=False):
     import os
     import sys
 
@@ -283,22 +283,30 @@ def _dist_worker(rank, world, port, backend, m, panel, peer, q):
     from paper_2503_04424_b200 import gen
     from paper_2503_04424_b200.distributed import memdet_cholesky_distributed
 
-    a = torch.from_numpy(gen.spd_wishart(m, m, seed=11, shift=1e-2)).cuda()
+    a = gen.spd_wishart(m, m, seed=11, shift=1e-2)
+    if not host:
+        a = torch.from_numpy(a).cuda()
     prefix, fail = memdet_cholesky_distributed(a, panel_tiles=panel, peer=peer)
     q.put((rank, prefix, fail))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,backend,m,panel,peer", [(1, "nccl", 1000, 4, None), (2, "gloo", 1000, 3, False),
-                                                        (3, "gloo", 777, 2, False), (2, "gloo", 1000, 3, True),
-                                                        (3, "gloo", 900, 2, True)])
-def test_distributed_driver_cuda_tile_ops(world, backend, m, panel, peer):
+@pytest.mark.parametrize("world,backend,m,panel,peer,host", [(1, "nccl", 1000, 4, None, False),
+                                                             (2, "gloo", 1000, 3, False, False),
+                                                             (3, "gloo", 777, 2, False, False),
+                                                             (2, "gloo", 1000, 3, True, False),
+                                                             (3, "gloo", 900, 2, True, False),
+                                                             (2, "gloo", 1000, 3, True, True),
+                                                             (3, "gloo", 777, 2, True, True),
+                                                             (3, "gloo", 900, 2, False, True)])
+def test_distributed_driver_cuda_tile_ops(world, backend, m, panel, peer, host):
     """The row-cyclic multi-GPU driver with the real CUDA tile kernels.  One GPU is available,
     so world > 1 runs several ranks on cuda:0 with gloo (collectives and barriers are host-side,
     no rank waits on another's kernels); world = 1 exercises the NCCL path.  peer=True is the
     product exchange: every rank's grid is cudaMalloc'd, mapped into the other ranks with CUDA
-    IPC, and the Schur-update kernels read the owners' solved panel tiles in place."""
+    IPC, and the Schur-update kernels read the owners' solved panel tiles in place.  host=True:
+    each rank ingests only its own tile rows from a host array (sharded ingest, no replica)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -309,7 +317,7 @@ def test_distributed_driver_cuda_tile_ops(world, backend, m, panel, peer):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, backend, m, panel, peer, q))
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, backend, m, panel, peer, q, host))
              for r in range(world)]
     for p in procs:
         p.start()
