@@ -318,7 +318,8 @@ def _run_engine(src: MatrixSource, mode: int, device: int, lay: BlockLayout, max
         raise ValueError("out_of_core=True needs a host matrix (the device copy already fits)")
     # float32 files under block pivoting factor in f32 with the reference's own rounding sequence
     # (memdet.py:337-338, _ldl.pyx `floating`, dense.py:73 eps of the file dtype): in core
-    f32_arith = mode == _native.MODE_LDL_PIV and src.dtype == np.float32
+    f32_arith = (mode == _native.MODE_LDL_PIV and src.dtype == np.float32
+                 and os.environ.get("B2D_F32_ARITH", "1") != "0")
     if f32_arith and out_of_core:
         raise ValueError("float32 memdet_ldl factors in core (f32 arithmetic); out_of_core=True is not available")
     on_device = src.device_ptr is not None

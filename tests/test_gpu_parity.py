@@ -391,9 +391,12 @@ def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, monkeypatch):
 
 
 @pytest.mark.parametrize("m,nb", [(1022, 4), (768, 3)])
-def test_in_core_f32_inputs_equal_block_walk(m, nb):
-    """float32 inputs (converted on the device) through the in-core LDL and LU equal the block
+def test_in_core_f32_inputs_equal_block_walk(m, nb, monkeypatch):
+    """float32 inputs converted to FP64 on the device (B2D_F32_ARITH=0 for the LDL; the default
+    float32 arithmetic is tests/test_f32_gpu.py's) through the in-core LDL and LU equal the block
     walks bit for bit."""
+    monkeypatch.setenv("B2D_F32_ARITH", "0")
+    eng.release_engine_cache()
     a = gen.random_symmetric(m, seed=m).astype(np.float32)
     r1, r2 = eng.memdet_ldl(a, num_blocks=nb), eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
     assert not r1.info.out_of_core and r2.info.out_of_core
@@ -404,6 +407,7 @@ def test_in_core_f32_inputs_equal_block_walk(m, nb):
     u1, u2 = eng.memdet_lu(g, num_blocks=nb), eng.memdet_lu(g, num_blocks=nb, out_of_core=True)
     assert not u1.info.out_of_core and u2.info.out_of_core
     assert (u1.sign, u1.logabsdet) == (u2.sign, u2.logabsdet)
+    eng.release_engine_cache()
 
 
 def test_pivoted_ldl_in_core_failing_block_matches_walk():
