@@ -2520,6 +2520,16 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     cudaEventRecord(e, st);
     tev.emplace_back(std::string(what) + " " + std::to_string(k), e);
   };
+  // B2D_LDL_TL=<file>: per-launch globaltimer spans of the panel / bulk kernels (diagnostic)
+  const char* tl_path = getenv("B2D_LDL_TL");
+  unsigned long long* tl_buf = nullptr;
+  const size_t tl_n = 4 * ((size_t)c->m / LDL_NB + 4);
+  if (tl_path) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMalloc(&tl_buf, tl_n * 8));
+    CUDA_TRY(cudaMemset(tl_buf, 0xff, tl_n * 8));
+    CUDA_TRY(cudaMemcpyToSymbol(g_ldl_tl, &tl_buf, sizeof(tl_buf)));
+  }
   tmark("start", 0, c->s_main);
   if (skip > 0) cudaStreamWaitEvent(c->s_main, o.ev_fac, 0);
   else if ((rc = wait_cols(c->s_main, col0(0) + o.tiles(0)))) return rc;
@@ -2665,6 +2675,21 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       fprintf(stderr, "[ldl trace] %-14s %8.2f ms\n", tev[q].first.c_str(), ms);
     }
     for (auto& e : tev) cudaEventDestroy(e.second);
+  }
+  if (tl_buf) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(tl_n);
+    CUDA_TRY(cudaMemcpy(h.data(), tl_buf, tl_n * 8, cudaMemcpyDeviceToHost));
+    unsigned long long* null_buf = nullptr;
+    CUDA_TRY(cudaMemcpyToSymbol(g_ldl_tl, &null_buf, sizeof(null_buf)));
+    cudaFree(tl_buf);
+    if (FILE* f = fopen(tl_path, "a")) {
+      fprintf(f, "# run m=%lld b=%lld: row kind start_ns end_ns\n", (long long)c->m, (long long)o.b);
+      for (size_t q = 0; 2 * q + 1 < tl_n; ++q)
+        if (h[2 * q] != ~0ull)
+          fprintf(f, "%lld %d %llu %llu\n", (long long)((q / 2) * LDL_NB), (int)(q & 1), h[2 * q], ~h[2 * q + 1]);
+      fclose(f);
+    }
   }
   CUDA_TRY(cudaGetLastError());
   return B2D_OK;

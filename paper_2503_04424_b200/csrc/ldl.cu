@@ -59,6 +59,22 @@ __global__ void block_absmax_kernel(const double* __restrict__ dense, int64_t ld
   if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, (unsigned long long)__double_as_longlong(best));
 }
 
+// B2D_LDL_TL (diagnostic): per-launch first-start / last-end %globaltimer of the panel (kind 0)
+// and bulk (kind 1) launches, slot = 2 * ((g0 + r0) / LDL_NB) + kind; both fields are
+// atomicMin'd (the end as its complement), the buffer starts all-ones.  Null: off.
+__device__ unsigned long long* g_ldl_tl = nullptr;
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(int64_t slot, bool end) {
+  unsigned long long* b = g_ldl_tl;
+  if (b == nullptr || threadIdx.x != 0) return;
+  const unsigned long long t = gtimer_ns();
+  atomicMin(b + 2 * slot + (end ? 1 : 0), end ? ~t : t);
+}
+
 struct ArgMax {
   double v;
   int64_t i;
@@ -528,6 +544,8 @@ __device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_
 
 __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
   if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
+  const int64_t tls = 2 * ((g.g0 + r0) / LDL_NB);
+  tl_mark(tls, false);
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
   extern __shared__ double sm[];
@@ -549,6 +567,7 @@ __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_
     const int64_t i = (int64_t)li * LC + c;
     if (i < g.n && i > r0) g.diag[i] = dg[li];
   }
+  tl_mark(tls, true);
 }
 
 // Finished columns [r0, r0 + nbk): L = W below the diagonal (_ldl.pyx:59-60); and the panel's
@@ -740,16 +759,20 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
 // the finished L columns (after the cluster panel kernel, which stores the panel's L itself).
 __global__ void __launch_bounds__(256, LDL_BULK_MINB) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile) {
   if (*g.fail != ~0ull) return;
+  const int64_t tls = 2 * ((g.g0 + r0) / LDL_NB) + 1;
+  tl_mark(tls, false);
   __shared__ __align__(16) double sC[LDL_NB * LDL_BT];
   __shared__ __align__(16) double sW[LDL_NB * LDL_BT];
   if ((int64_t)blockIdx.x >= ntile) {
     __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
     ldl_swap_part(g, r0, nbk, spos, ssrc, (int64_t)blockIdx.x - ntile, (int64_t)gridDim.x - ntile);
+    tl_mark(tls, true);
     return;
   }
   // the first tile-column (the next panel's columns) last, so that it is L2-resident when the
   // next panel kernel reads it
   ldl_bulk_tile(g, r0, nbk, ntile - 1 - blockIdx.x, sC, sW);
+  tl_mark(tls, true);
 }
 
 // The whole pivoted factorisation of the block on one 16-CTA cluster (one launch): per panel
