@@ -236,8 +236,23 @@ struct Ooc {
   int tiles(int k) const { return (int)((size(k) + T - 1) / T); }
   TileMap map(int s) const { return TileMap{slot[s], nbt, 0}; }
   size_t slot_bytes() const { return (size_t)nbt * nbt * TILE_BYTES; }
-  int64_t* perm_of(int k) const { return (k & 1) && perm_odd ? perm_odd : perm_local; }
-  double* dblk_of(int k) const { return (k & 1) && dblk_odd ? dblk_odd : dblk; }
+  // row-ordered in-core LDL (B2D_LDL_ROWS): one set of factor outputs per stage, so a factor
+  // never waits for the panel solves of the stage two before it
+  bool use_ring = false;
+  std::vector<double*> ring_inv, ring_dblk;
+  std::vector<int64_t*> ring_perm;
+  int64_t* perm_of(int k) const {
+    if (use_ring) return ring_perm[k];
+    return (k & 1) && perm_odd ? perm_odd : perm_local;
+  }
+  double* dblk_of(int k) const {
+    if (use_ring) return ring_dblk[k];
+    return (k & 1) && dblk_odd ? dblk_odd : dblk;
+  }
+  double* inv_of(int k, double* even) const {
+    if (use_ring) return ring_inv[k];
+    return (k & 1) && inv_odd ? inv_odd : even;
+  }
 };
 
 struct MCtx;  // multi-device context (mgpu.cu)
@@ -306,7 +321,13 @@ struct Ctx {
   // triangle holds the matrix, o.* the block factor state; the stage's solved panel lives in
   // full-height grids of nt x nbt tiles, unscaled and D^{-1}-scaled, double-buffered by stage
   bool ldl_ic = false;
-  double* pan[3][2] = {};  // [stage % 3][0: unscaled, 1: scaled]
+  // in-core pivoted LDL panel grids [stage % npan][0: unscaled, 1: scaled]: three for the column
+  // schedule; the row schedule takes up to MAX_PAN when HBM allows (a stage's far rows read its
+  // panel grid long after the next stages start)
+  static constexpr int MAX_PAN = 16;
+  double* pan[MAX_PAN][2] = {};
+  int npan = 3;
+  bool ldl_rows = false;  // in-core pivoted LDL: row-ordered schedule (B2D_LDL_ROWS)
   // generic LU in core (the same conditions): the matrix as a full nt x nt tile grid; per stage
   // parity the column panel X, the transposed row panel Y^T and a transpose buffer (nt x nbt
   // tiles each, rows = global tile index), and the U^T factor of the diagonal block
@@ -320,6 +341,11 @@ struct Ctx {
   // column's updates are ordered by stage on its stream, independently of the other columns'
   std::vector<cudaStream_t> s_cols;
   std::vector<cudaEvent_t> ev_cols;
+  // row-ordered schedule (B2D_LDL_ROWS): block rows at distance <= 2, 3, 4, 5 from the stage
+  // on streams of falling priority (farther rows on s_cols); per block row the events after its
+  // last update and after its panel rows of the current stage
+  cudaStream_t s_pr[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_row, ev_prow;
   // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
   // block column-major in dense, the stage's solved row-k blocks X and their D^{-1}-scaled copy S
   bool ldl32 = false;
@@ -438,6 +464,13 @@ static void destroy(Ctx* c) {
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
   }
+  for (auto st : c->s_pr)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (auto* v : {&c->ev_row, &c->ev_prow})
+    for (auto e : *v) cudaEventDestroy(e);
   for (auto e : c->ev_cols) cudaEventDestroy(e);
   Ooc& o = c->o;
   if (o.s_h2d) cudaStreamSynchronize(o.s_h2d);
@@ -473,6 +506,9 @@ static void destroy(Ctx* c) {
     for (double* q : pp) cudaFree(q);
   for (double* q : c->ublk) cudaFree(q);
   cudaFree(c->grid);
+  for (double* q : o.ring_inv) cudaFree(q);
+  for (double* q : o.ring_dblk) cudaFree(q);
+  for (int64_t* q : o.ring_perm) cudaFree(q);
   cudaFree(o.inv_odd);
   cudaFree(o.inv2_odd);
   cudaFree(o.perm_odd);
@@ -779,8 +815,25 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
     const int64_t ld = (int64_t)o.nbt * T;
     ALLOC(c->tiles, (size_t)n_packed_tiles(c->nt) * TILE_BYTES);
     ALLOC(c->inv, (size_t)c->nt * TILE_BYTES);
-    for (auto& pp : c->pan)
-      for (double*& q : pp) ALLOC(q, (size_t)c->nt * o.nbt * TILE_BYTES);
+    {
+      // panel grids: three, plus up to half of the HBM left over (one pair per further stage)
+      const size_t pair = 2 * (size_t)c->nt * o.nbt * TILE_BYTES;
+      const int64_t bt = o.nbt;
+      const size_t ic_need = (size_t)n_packed_tiles(nt_full) * TILE_BYTES + 6 * (size_t)nt_full * bt * TILE_BYTES +
+                             (size_t)(nt_full + bt) * TILE_BYTES + (size_t)ld * ld * 9 + 3 * (size_t)npad_full * 8 +
+                             (size_t)NSTAGE * T * npad_full * 8 + (size_t)(m + 8 * ld) * 8;
+      const size_t spare = budget > ic_need ? (budget - ic_need) / 2 : 0;
+      // B2D_LDL_ROWS: 1 = row-ordered schedule, 0 = column schedule; unset: rows for <= 8 blocks
+      // (there the chain of factors bounds the step: C2 452 -> 444 ms), columns above (DMMA
+      // throughput bounds it and the column schedule keeps more of it: C3 2876 vs 2950 ms)
+      const char* re = getenv("B2D_LDL_ROWS");
+      c->ldl_rows = re ? atoi(re) != 0 : o.nb <= 8;
+      c->npan = c->ldl_rows ? (int)std::min<int64_t>({(int64_t)Ctx::MAX_PAN, std::max<int64_t>(3, o.nb),
+                                                      3 + (int64_t)(spare / pair)})
+                            : 3;
+      for (int q = 0; q < c->npan; ++q)
+        for (double*& pq : c->pan[q]) ALLOC(pq, (size_t)c->nt * o.nbt * TILE_BYTES);
+    }
     ALLOC(o.dense, (size_t)ld * ld * 8);
     ALLOC(o.swaps, (size_t)ld * 8);
     ALLOC(o.perm_local, (size_t)ld * 8);
@@ -1972,7 +2025,7 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   const int64_t ld = (int64_t)o.nbt * T, g0 = (int64_t)k * o.b;
   double* dblk = o.dblk_of(k);
   int64_t* perm = o.perm_of(k);
-  double* inv = (k & 1) && o.inv_odd ? o.inv_odd : c->inv;
+  double* inv = o.inv_of(k, c->inv);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
   unpack_block_kernel<<<ntri, 256, 0, s>>>(blk, nt, o.dense, ld, 1);
   cudaMemsetAsync(o.amax, 0, 8, s);
@@ -2537,6 +2590,132 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   if ((rc = ldl_factor_block(c, diag_map(0), 0, c->s_main))) return rc;
   tmark("factor-end", 0, c->s_main);
   cudaEventRecord(c->ev_catch[0], c->s_main);
+  // Row-ordered schedule (c->ldl_rows, B2D_LDL_ROWS): stage k's work is issued block row by block
+  // row r = k+1 .. nb-1 -- the panel rows of block r (permuted, solved, D^{-1}-scaled), then the
+  // tiles (r, k+1 .. r) -- each row on a stream whose priority falls with its distance d = r - k
+  // from the stage (d <= 2, 3, 4, 5: s_pr[0..3]; farther rows one low-priority stream per row):
+  // the factor of block r needs block row r complete, so the rows are needed in that order.  A
+  // row's work is ordered across stages by its event (ev_row), a row's update waits for the panel
+  // rows of the blocks before it (ev_prow); every tile receives its stages' updates in order with
+  // the same operands and K: bit-identical to the column schedule and to the block walk.  The
+  // factors' outputs (L_kk^{-1} tiles, block permutation, D) get one buffer per stage, and up to
+  // MAX_PAN panel grids decouple the stages' far rows from the next stages' panels.  In the
+  // column schedule (below) the nearest rows' updates could queue behind whole-column work.
+  const bool rows_sched = c->ldl_rows && !getenv("B2D_LDL_SCHED") &&
+                          (getenv("B2D_LDL_URGENT") ? atoi(getenv("B2D_LDL_URGENT")) != 0 : true) &&
+                          (getenv("B2D_LDL_SPLIT") ? atoi(getenv("B2D_LDL_SPLIT")) != 0 : true);
+  if (rows_sched && nb > 1) {
+    if (!c->s_pr[0]) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      // distance 1-2, 3, 4, 5: priorities one below s_main's downwards (clamped to the range)
+      for (int q = 0; q < 4; ++q) {
+        const int pr = std::min(lo, hi + 1 + q);
+        CUDA_TRY(cudaStreamCreateWithPriority(&c->s_pr[q], cudaStreamNonBlocking, pr));
+      }
+    }
+    if ((int)o.ring_inv.size() < nb) {
+      for (int q = (int)o.ring_inv.size(); q < nb; ++q) {
+        double *iv = nullptr, *db = nullptr;
+        int64_t* pm = nullptr;
+        CUDA_TRY(cudaMalloc(&iv, (size_t)o.nbt * TILE_BYTES));
+        CUDA_TRY(cudaMalloc(&db, (size_t)o.nbt * T * 8));
+        CUDA_TRY(cudaMalloc(&pm, (size_t)o.nbt * T * 8));
+        o.ring_inv.push_back(iv);
+        o.ring_dblk.push_back(db);
+        o.ring_perm.push_back(pm);
+      }
+    }
+    for (auto* v : {&c->ev_row, &c->ev_prow})
+      while ((int)v->size() < std::max(nb, 2)) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        v->push_back(e);
+      }
+    for (auto st : c->s_pr) cudaStreamWaitEvent(st, c->ev_start, 0);
+    // factor 0 was enqueued above with the parity buffers: its outputs move to ring slot 0
+    // (enqueued on s_main after it; the ring is used from here on)
+    CUDA_TRY(cudaMemcpyAsync(o.ring_inv[0], o.inv_of(0, c->inv), (size_t)o.nbt * TILE_BYTES, cudaMemcpyDeviceToDevice,
+                             c->s_main));
+    CUDA_TRY(cudaMemcpyAsync(o.ring_dblk[0], o.dblk_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
+    CUDA_TRY(cudaMemcpyAsync(o.ring_perm[0], o.perm_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
+    o.use_ring = true;
+    // row r's last update so far: none (every block row's first work waits for factor 0)
+    for (int r = 0; r < nb; ++r) cudaEventRecord(c->ev_row[r], c->s_main);
+    auto bstart = [&](int q) { return std::min(nt, col0(q)); };
+    auto bend = [&](int q) { return q + 1 < nb ? std::min(nt, col0(q + 1)) : nt; };
+    // block row r at distance d = r - k: streams of falling priority, then one stream per row
+    auto dstream = [&](int r, int k) {
+      const int d = r - k;
+      return d <= 2 ? c->s_pr[0] : d <= 5 ? c->s_pr[d - 2] : col_stream(r);
+    };
+    for (int k = 0; k + 1 < nb; ++k) {
+      const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb;
+      const double* inv_k = o.inv_of(k, c->inv);
+      const int np = c->npan, pb = k % np;  // panel grids: stage k waits for the readers of stage k-np
+      auto panel_rows = [&](cudaStream_t st, int r0, int r1) {  // global tile rows [r0, r1)
+        TileMap src = packed;
+        src.roff = r0;
+        src.coff = k0;
+        const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+        const TileMap ps{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+        permute_cols_kernel<<<2048, 256, 0, st>>>(src, pu, r1 - r0, kb, o.size(k), o.perm_of(k));
+        trsm_panel(c, st, pu, r1 - r0, diag_map(k), kb, inv_k);
+        scale_cols_kernel<<<2048, 256, 0, st>>>(pu, ps, r1 - r0, kb, o.size(k), o.dblk_of(k));
+        c->launches += 2;
+      };
+      GemmTask u{};
+      u.a = TileMap{c->pan[pb][1], o.nbt, 0};  // rows indexed by global tile row
+      u.b = TileMap{c->pan[pb][0], o.nbt, 0};
+      u.c = packed;
+      u.p0 = 0;
+      u.p1 = kb;
+      const double K = (double)kb * T;
+      for (int r = k + 1; r < nb; ++r) {
+        const int r0 = bstart(r), r1 = bend(r);
+        cudaStream_t st = dstream(r, k);
+        // the stage's factor, free panel grids, row r's previous update
+        cudaStreamWaitEvent(st, c->ev_catch[k], 0);
+        if (k >= np) cudaStreamWaitEvent(st, c->ev_rest[k - np], 0);
+        if ((rc = wait_cols(st, i0))) return rc;
+        cudaStreamWaitEvent(st, c->ev_row[r], 0);
+        if (r == k + 1) tmark("p1-ready", k, st);
+        panel_rows(st, r0, r1);
+        cudaEventRecord(c->ev_prow[r], st);
+        if (r == k + 1) tmark("panel-end", k, st);
+        // tiles (r, k+1 .. r): the panel rows of every block up to r
+        for (int q = k + 1; q < r; ++q)
+          if (dstream(q, k) != st) cudaStreamWaitEvent(st, c->ev_prow[q], 0);
+        if ((rc = wait_cols(st, r1))) return rc;
+        u.out = TileSet{r0, r1, i0, r1, 1, 0};
+        if (r == k + 1) {
+          launch_gemm(c, st, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+          cudaEventRecord(c->ev_row[r], st);
+          tmark("next-col-end", k, st);
+          cudaEventRecord(o.ev_diag, st);
+          cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+          tmark("factor-begin", k + 1, c->s_main);
+          if ((rc = ldl_factor_block(c, diag_map(k + 1), k + 1, c->s_main, k + 2 < nb))) return rc;
+          tmark("factor-end", k + 1, c->s_main);
+          cudaEventRecord(c->ev_catch[k + 1], c->s_main);
+        } else {
+          launch_update_kchunked(c, st, u);
+          cudaEventRecord(c->ev_row[r], st);
+          if (r == k + 2) tmark("urgent-end", k, st);
+        }
+      }
+      // ev_rest[k]: every reader of stage k's panel buffers (panel k+np reuses them)
+      for (int r = k + 1; r < nb; ++r) cudaStreamWaitEvent(c->s_side, c->ev_row[r], 0);
+      cudaEventRecord(c->ev_rest[k], c->s_side);
+      tmark("rest-end", k, c->s_side);
+    }
+    for (int r = 0; r < nb; ++r) cudaStreamWaitEvent(c->s_main, c->ev_row[r], 0);
+    for (auto st : {c->s_pr[0], c->s_pr[1], c->s_pr[2], c->s_pr[3], c->s_side}) {
+      cudaEventRecord(o.ev_work, st);
+      cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
+    }
+    o.use_ring = false;  // (host-side selection only: every launch above has its pointers)
+  } else
   for (int k = 0; k + 1 < nb; ++k) {
     const int par = k & 1;
     const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb, kb1 = o.tiles(k + 1);
@@ -2669,6 +2848,15 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   end(c, user);
   if (ltrace) {
     cudaDeviceSynchronize();
+    {
+      int plo = 0, phi = 0, pm = 0, pd = 0, pf = 0;
+      cudaDeviceGetStreamPriorityRange(&plo, &phi);
+      if (c->s_pr[0]) cudaStreamGetPriority(c->s_pr[0], &pm);
+      if (c->s_pr[1]) cudaStreamGetPriority(c->s_pr[1], &pd);
+      if (c->s_pr[3]) cudaStreamGetPriority(c->s_pr[3], &pf);
+      fprintf(stderr, "[ldl trace] priorities: range [%d, %d], d<=2 %d, d=3 %d, d=5 %d, npan %d\n", plo, phi, pm, pd, pf,
+              c->npan);
+    }
     for (size_t q = 1; q < tev.size(); ++q) {
       float ms = 0;
       cudaEventElapsedTime(&ms, tev[0].second, tev[q].second);

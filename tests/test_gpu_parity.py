@@ -366,16 +366,20 @@ def test_pivoted_ldl_matches_reference_golden(golden, name):
                 (ref["blocks_read"], ref["blocks_written"], ref["scratch_slots"])
 
 
-@pytest.mark.parametrize("m,nb", [(1024, 4), (1022, 4), (1280, 5), (768, 2), (2048, 8), (700, 1)])
+@pytest.mark.parametrize("m,nb", [(1024, 4), (1022, 4), (1280, 5), (768, 2), (2048, 8), (700, 1), (1536, 12)])
 @pytest.mark.parametrize("kchunk", ["8", "1"])
-def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, monkeypatch):
+@pytest.mark.parametrize("sched", ["rows", "cols"])
+def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, sched, monkeypatch):
     """B2D_REST_KCHUNK splits the trailing update over K into sequential launches (1 = one
-    tile-column each), which must not change a bit.
+    tile-column each), which must not change a bit; neither may the stage schedule
+    (B2D_LDL_ROWS: block rows by distance on prioritised streams, or block columns).
     Tile-aligned reference blocks run in core (the matrix resident, one large update per
     stage, the next block's factor overlapped); every tile gets the walk's updates with the same
     operands and K, so perm, D and the prefixes equal the out-of-core block walk's bit for bit,
     and the walk makes the reference's transfers."""
     monkeypatch.setenv("B2D_REST_KCHUNK", kchunk)
+    monkeypatch.setenv("B2D_LDL_ROWS", "1" if sched == "rows" else "0")
+    eng.release_engine_cache()
     a = gen.random_symmetric(m, seed=m + nb)
     res = eng.memdet_ldl(a, num_blocks=nb)
     walk = eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
@@ -388,6 +392,7 @@ def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, monkeypatch):
     np.testing.assert_array_equal(res.perm, ref_perm)
     assert rel_err(res.prefix, ref_prefix) <= 1e-10
     assert (walk.info.ooc_reads, walk.info.ooc_writes) == (rinfo.blocks_read, rinfo.blocks_written)
+    eng.release_engine_cache()
 
 
 @pytest.mark.parametrize("m,nb", [(1022, 4), (768, 3)])
