@@ -1073,12 +1073,15 @@ static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, boo
 // for K = 128 * chunk instead of the whole block width, so the factor's cluster and bulk
 // launches find free SMs sooner.  Exact: the accumulators start from C and the chunks continue
 // the same k order, and a stored FP64 accumulator reloads unchanged.
-static int rest_kchunk() {
+// K chunk (tile-columns) of the in-core LDL / LU trailing updates: B2D_REST_KCHUNK, else 16 for
+// the pivoted LDL (C2 row schedule 444 -> 437 ms, C3 2882 -> 2864 ms vs 8) and 8 for the LU
+static int rest_kchunk(int dflt = 8) {
   const char* e = getenv("B2D_REST_KCHUNK");
-  return e ? atoi(e) : 8;
+  return e ? atoi(e) : dflt;
 }
-static void launch_update_kchunked(Ctx* c, cudaStream_t s, GemmTask u) {
-  const int p0 = u.p0, p1 = u.p1, kc = rest_kchunk() > 0 ? rest_kchunk() : p1 - p0;
+static void launch_update_kchunked(Ctx* c, cudaStream_t s, GemmTask u, int dflt = 8) {
+  const int kcv = rest_kchunk(dflt);
+  const int p0 = u.p0, p1 = u.p1, kc = kcv > 0 ? kcv : p1 - p0;
   for (int q = p0; q < p1; q += kc) {
     u.p0 = q;
     u.p1 = std::min(p1, q + kc);
@@ -2699,7 +2702,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
           tmark("factor-end", k + 1, c->s_main);
           cudaEventRecord(c->ev_catch[k + 1], c->s_main);
         } else {
-          launch_update_kchunked(c, st, u);
+          launch_update_kchunked(c, st, u, 16);
           cudaEventRecord(c->ev_row[r], st);
           if (r == k + 2) tmark("urgent-end", k, st);
         }
@@ -2790,7 +2793,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         col_sync(k + 2, c->s_mid);
         if ((rc = wait_cols(c->s_mid, i2))) return rc;
         u.out = TileSet{i0 + kb1, i2, i0 + kb1, i2, 1, 0};
-        launch_update_kchunked(c, c->s_mid, u);
+        launch_update_kchunked(c, c->s_mid, u, 16);
       }
       tmark("urgent-end", k, c->s_mid);
       for (int q = k + 2, j0 = i0 + kb1; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
@@ -2800,7 +2803,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         if ((rc = wait_cols(cs, j1))) return rc;
         // block column k+2: its rows below the diagonal block (the diagonal block went above)
         u.out = q == k + 2 ? TileSet{j1, nt, j0, j1, 0, 0} : TileSet{j0, nt, j0, j1, 1, 0};
-        if (u.out.count() > 0) launch_update_kchunked(c, cs, u);
+        if (u.out.count() > 0) launch_update_kchunked(c, cs, u, 16);
       }
       // join stage k's readers of its panel buffers on s_side (ev_rest[k]: panel k+3 reuses them)
       for (int q = k + 2; q < nb; ++q) col_sync(q, c->s_side);
@@ -2817,18 +2820,18 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const bool by_cols = host && k == 0;
       if ((rc = wait_cols(c->s_side, by_cols ? i2 : nt))) return rc;
       u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 1, 0};
-      launch_update_kchunked(c, c->s_side, u);
+      launch_update_kchunked(c, c->s_side, u, 16);
       cudaEventRecord(c->ev_resta[k], c->s_side);
       if (by_cols) {
         for (int q = k + 3, j0 = i2; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
           const int j1 = std::min(nt, j0 + o.tiles(q));
           if ((rc = wait_cols(c->s_side, j1))) return rc;
           u.out = TileSet{j0, nt, j0, j1, 1, 0};
-          launch_update_kchunked(c, c->s_side, u);
+          launch_update_kchunked(c, c->s_side, u, 16);
         }
       } else if (i2 < nt) {
         u.out = TileSet{i2, nt, i2, nt, 1, 0};
-        launch_update_kchunked(c, c->s_side, u);
+        launch_update_kchunked(c, c->s_side, u, 16);
       }
     } else {
       cudaEventRecord(c->ev_resta[k], c->s_side);
