@@ -196,6 +196,9 @@ struct Ooc {
   double* dblk = nullptr;
   unsigned long long* amax = nullptr;
   unsigned* lflags = nullptr;       // panel-server hand-off counters (ldl_panel_server_kernel)
+  unsigned* lpipe = nullptr;        // panel / bulk pipeline counters (ldl.cu, B2D_LDL_PIPE)
+  cudaStream_t s_lalt = nullptr;    // pipeline: odd panels and their bulk updates
+  cudaEvent_t ev_lpanel[2] = {nullptr, nullptr}, ev_lalt = nullptr;
   cudaStream_t s_bulk = nullptr;    // panel-server bulk launches (high priority)
   cudaEvent_t ev_lreset = nullptr, ev_lbulk = nullptr;
   uint8_t* ltag = nullptr;  // blocked pivoted LDL: per-entry tags, panel columns C / W, diagonal, pivot column
@@ -492,6 +495,13 @@ static void destroy(Ctx* c) {
     cudaStreamDestroy(o.s_bulk);
   }
   cudaFree(o.lflags);
+  cudaFree(o.lpipe);
+  if (o.s_lalt) {
+    cudaStreamSynchronize(o.s_lalt);
+    cudaStreamDestroy(o.s_lalt);
+  }
+  for (cudaEvent_t e : {o.ev_lpanel[0], o.ev_lpanel[1], o.ev_lalt})
+    if (e) cudaEventDestroy(e);
   if (o.ev_lreset) cudaEventDestroy(o.ev_lreset);
   if (o.ev_lbulk) cudaEventDestroy(o.ev_lbulk);
   cudaFree(o.ltag);
@@ -2011,7 +2021,7 @@ static int ldl_server_factor(Ctx* c, const LdlArgs& g, cudaStream_t s) {
     if (waitv(o.s_bulk, panels, p + 1, B2D_STREAM_WAIT_VALUE_GEQ) != 0)
       return set_err(B2D_ERR_CUDA, "cuStreamWaitValue32 failed");
     if (ntile > 0) {
-      ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, o.s_bulk>>>(g, r0, nbk, ntile);
+      ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, o.s_bulk>>>(g, r0, nbk, ntile, (unsigned*)nullptr, 0u);
       c->launches++;
     }
     if (writev(o.s_bulk, bulks, p + 1, 0) != 0) return set_err(B2D_ERR_CUDA, "cuStreamWriteValue32 failed");
@@ -2068,10 +2078,36 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_factor_cluster_kernel, g));
     c->launches += 1;
-  } else
-  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB) {
+  } else {
+  // B2D_LDL_PIPE (default 1): panel p+1 is launched as soon as panel p is done, on the other of
+  // two streams, and waits in the kernel for bulk update p (ldl.cu pipe_wait): its cluster takes
+  // its SMs while bulk p runs, instead of after it (beside the trailing DMMA updates a launch
+  // waits ~100 us for SMs).  Bulk p follows panel p on the panel's stream.
+  const char* pie = getenv("B2D_LDL_PIPE");
+  const bool pipe = (pie ? atoi(pie) != 0 : true) && n <= (int64_t)LC * LC_RMAX && !single_cta;
+  cudaStream_t pst[2] = {s, s};
+  if (pipe) {
+    if (!o.lpipe) {
+      CUDA_TRY(cudaMalloc((void**)&o.lpipe, 16));
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      int sp = hi;
+      cudaStreamGetPriority(s, &sp);
+      CUDA_TRY(cudaStreamCreateWithPriority(&o.s_lalt, cudaStreamNonBlocking, sp));
+      for (auto* e : {&o.ev_lpanel[0], &o.ev_lpanel[1], &o.ev_lalt})
+        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    pst[1] = o.s_lalt;
+    CUDA_TRY(cudaMemsetAsync(o.lpipe, 0, 16, s));
+    cudaEventRecord(o.ev_lalt, s);
+    cudaStreamWaitEvent(o.s_lalt, o.ev_lalt, 0);  // counters reset, block state ready
+  }
+  unsigned pidx = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += LDL_NB, ++pidx) {
     const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
     if (n <= (int64_t)LC * LC_RMAX && !single_cta) {
+      cudaStream_t ps = pst[pidx & 1];
+      if (pipe && pidx > 0) cudaStreamWaitEvent(ps, o.ev_lpanel[(pidx - 1) & 1], 0);  // panel pidx-1 done
       // the panel on a 16-CTA cluster with its rows in distributed shared memory
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute attr[1];
@@ -2082,16 +2118,18 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
       cfg.gridDim = dim3(LC);
       cfg.blockDim = dim3(LC_THREADS);
       cfg.dynamicSmemBytes = ldl_cluster_smem((int)((n + LC - 1) / LC));
-      cfg.stream = s;
+      cfg.stream = ps;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk));
+      unsigned* pp = pipe ? o.lpipe : nullptr;
+      CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk, pp, pidx));
+      if (pipe) cudaEventRecord(o.ev_lpanel[pidx & 1], ps);
       // the cluster kernel stored the panel's L; the row interchanges of the finished columns
       // ride along the bulk update as extra blocks
       const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
       const int64_t nswap = r0 > 0 ? std::min<int64_t>(148, (r0 + 63) / 64) : 0;
       if (ntile + nswap > 0) {
-        ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256, 0, s>>>(g, r0, nbk, ntile);
+        ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256, 0, ps>>>(g, r0, nbk, ntile, pp, pidx);
         c->launches += 1;
       }
       c->launches += 1;
@@ -2101,8 +2139,13 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
     const int64_t st_ctas = std::max<int64_t>(((n - r0) * nbk + 255) / 256, (r0 + 7) / 8);
     ldl_store_l_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(1024, st_ctas)), 256, 0, s>>>(g, r0, nbk);
     const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
-    if (ntile > 0) ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, s>>>(g, r0, nbk, ntile);
+    if (ntile > 0) ldl_bulk_kernel<<<(unsigned)ntile, 256, 0, s>>>(g, r0, nbk, ntile, (unsigned*)nullptr, 0u);
     c->launches += ntile > 0 ? 3 : 2;
+  }
+  if (pipe) {  // the odd panels' stream joins the factor's stream
+    cudaEventRecord(o.ev_lalt, o.s_lalt);
+    cudaStreamWaitEvent(s, o.ev_lalt, 0);
+  }
   }
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
                       n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,

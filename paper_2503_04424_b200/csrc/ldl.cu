@@ -75,6 +75,30 @@ __device__ __forceinline__ void tl_mark(int64_t slot, bool end) {
   atomicMin(b + 2 * slot + (end ? 1 : 0), end ? ~t : t);
 }
 
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Panel / bulk pipeline (ldl_factor_block, B2D_LDL_PIPE): each panel kernel and each bulk
+// update is launched ahead of its predecessor's completion -- panels on the factor's stream, bulks
+// on a second one -- and waits in the kernel (thread 0 of every CTA polls a counter with acquire
+// loads) instead of in the stream, so its CTAs take SMs while the predecessor still runs (a launch
+// beside the trailing DMMA updates otherwise waits ~100 us for SMs, 256 times per 4096 block).
+//   pipe[0] = panels done (panel p releases p + 1 after its writes; 0x7fffffff after a failure)
+//   pipe[1] = bulk updates done (the last CTA of bulk p releases p + 1)
+//   pipe[2] = CTAs of the running bulk update that finished (reset by its last CTA)
+// Every kernel signals even when it returns early (an earlier failure), so nothing waits forever.
+constexpr unsigned PIPE_FAIL = 0x7fffffffu;
+__device__ __forceinline__ void pipe_wait(const unsigned* c, unsigned v) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(c) < v) __nanosleep(64);
+  __syncthreads();
+}
+
 struct ArgMax {
   double v;
   int64_t i;
@@ -542,12 +566,17 @@ __device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_
   }
 }
 
-__global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk) {
-  if (*g.fail != ~0ull) return;  // uniform: written by earlier kernels only
-  const int64_t tls = 2 * ((g.g0 + r0) / LDL_NB);
-  tl_mark(tls, false);
+__global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk,
+                                                                                   unsigned* pipe, unsigned pidx) {
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
+  if (pipe && pidx > 0) pipe_wait(pipe + 1, pidx);  // bulk update pidx - 1 done
+  if (*g.fail != ~0ull) {  // uniform: written by earlier kernels only
+    if (pipe && c == 0 && threadIdx.x == 0) st_release_u32(pipe, PIPE_FAIL);
+    return;
+  }
+  const int64_t tls = 2 * ((g.g0 + r0) / LDL_NB);
+  tl_mark(tls, false);
   extern __shared__ double sm[];
   const int R = (int)((g.n + LC - 1) / LC);
   double* Cs = sm;                      // [R][LC_LD]
@@ -561,11 +590,19 @@ __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_
   }
   __syncthreads();  // dg loaded, barriers initialised
   cl.sync();        // every CTA's barriers initialised before any remote arrive
-  if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) return;
+  if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) {
+    if (pipe && c == 0 && threadIdx.x == 0) st_release_u32(pipe, PIPE_FAIL);
+    return;
+  }
   cluster_panel_writeback(g, r0, nbk, Cs, Ws, R, c, true);
   for (int li = threadIdx.x; li < R; li += LC_THREADS) {
     const int64_t i = (int64_t)li * LC + c;
     if (i < g.n && i > r0) g.diag[i] = dg[li];
+  }
+  if (pipe) {  // every CTA's writes visible device-wide, then panel pidx is released
+    __threadfence();
+    cl.sync();
+    if (c == 0 && threadIdx.x == 0) st_release_u32(pipe, pidx + 1);
   }
   tl_mark(tls, true);
 }
@@ -757,8 +794,26 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
 
 // Blocks [0, ntile): the bulk tiles; blocks [ntile, gridDim.x): the panel's row interchanges on
 // the finished L columns (after the cluster panel kernel, which stores the panel's L itself).
-__global__ void __launch_bounds__(256, LDL_BULK_MINB) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile) {
-  if (*g.fail != ~0ull) return;
+// pipeline: this CTA's writes visible device-wide; the last CTA of the launch releases bulk pidx
+__device__ __forceinline__ void bulk_done(unsigned* pipe, unsigned pidx) {
+  if (!pipe) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(pipe + 2, 1u) == gridDim.x - 1) {
+      pipe[2] = 0u;  // (the next bulk launch is stream-ordered after this one)
+      __threadfence();
+      st_release_u32(pipe + 1, pidx + 1);
+    }
+  }
+}
+__global__ void __launch_bounds__(256, LDL_BULK_MINB) ldl_bulk_kernel(LdlArgs g, int64_t r0, int nbk, int64_t ntile,
+                                                                     unsigned* pipe, unsigned pidx) {
+  if (pipe) pipe_wait(pipe, pidx + 1);  // panel pidx done (or failed)
+  if (*g.fail != ~0ull) {
+    bulk_done(pipe, pidx);
+    return;
+  }
   const int64_t tls = 2 * ((g.g0 + r0) / LDL_NB) + 1;
   tl_mark(tls, false);
   __shared__ __align__(16) double sC[LDL_NB * LDL_BT];
@@ -767,12 +822,14 @@ __global__ void __launch_bounds__(256, LDL_BULK_MINB) ldl_bulk_kernel(LdlArgs g,
     __shared__ int64_t spos[2 * LDL_NB], ssrc[2 * LDL_NB];
     ldl_swap_part(g, r0, nbk, spos, ssrc, (int64_t)blockIdx.x - ntile, (int64_t)gridDim.x - ntile);
     tl_mark(tls, true);
+    bulk_done(pipe, pidx);
     return;
   }
   // the first tile-column (the next panel's columns) last, so that it is L2-resident when the
   // next panel kernel reads it
   ldl_bulk_tile(g, r0, nbk, ntile - 1 - blockIdx.x, sC, sW);
   tl_mark(tls, true);
+  bulk_done(pipe, pidx);
 }
 
 // The whole pivoted factorisation of the block on one 16-CTA cluster (one launch): per panel
@@ -846,14 +903,6 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_factor_cluster_kernel(LdlAr
 // interchanges are stored; the host gates panel p's bulk launch on it with a stream wait-value),
 // flags[1] = bulk updates finished (a stream write-value after each bulk launch; the server
 // acquires it before the next panel).  Same steps, same arithmetic as the per-panel kernels.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
 __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_server_kernel(LdlArgs g, unsigned* flags) {
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();

@@ -70,7 +70,7 @@ int main(int argc, char** argv) {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       cudaEventRecord(e0);
-      CK(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk));
+      CK(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk, (unsigned*)nullptr, 0u));
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -79,7 +79,7 @@ int main(int argc, char** argv) {
       const int64_t mt = (n - r0 - nbk + LDL_BT - 1) / LDL_BT, ntile = mt * (mt + 1) / 2;
       const int64_t nswap = r0 > 0 ? std::min<int64_t>(148, (r0 + 63) / 64) : 0;
       cudaEventRecord(e0);
-      if (ntile + nswap > 0) ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256>>>(g, r0, nbk, ntile);
+      if (ntile + nswap > 0) ldl_bulk_kernel<<<(unsigned)(ntile + nswap), 256>>>(g, r0, nbk, ntile, (unsigned*)nullptr, 0u);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
