@@ -2686,6 +2686,10 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     CUDA_TRY(cudaMemcpyAsync(o.ring_dblk[0], o.dblk_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
     CUDA_TRY(cudaMemcpyAsync(o.ring_perm[0], o.perm_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
     o.use_ring = true;
+    struct RingOff {  // the ring selection ends with this schedule, also on an error return
+      Ooc& o;
+      ~RingOff() { o.use_ring = false; }
+    } ring_off{o};
     // row r's last update so far: none (every block row's first work waits for factor 0)
     for (int r = 0; r < nb; ++r) cudaEventRecord(c->ev_row[r], c->s_main);
     auto bstart = [&](int q) { return std::min(nt, col0(q)); };
@@ -2760,7 +2764,6 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       cudaEventRecord(o.ev_work, st);
       cudaStreamWaitEvent(c->s_main, o.ev_work, 0);
     }
-    o.use_ring = false;  // (host-side selection only: every launch above has its pointers)
   } else
   for (int k = 0; k + 1 < nb; ++k) {
     const int par = k & 1;
