@@ -177,6 +177,29 @@ def generate_rbf_device(torch, dev_x, n):
     return a
 
 
+def measure_int8_peak(torch, n=8192, reps=5):
+    """Dense int8 tensor throughput for the opt-in Ozaki line's roofline: cuBLASLt's int8 GEMM
+    (torch._int_mm, int8 x int8 -> int32) at n^3, best of `reps` by CUDA events (a library
+    measurement of the denominator, as MEASURED_PEAKS.json's bf16 figure; not on the path)."""
+    try:
+        a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda").t()
+        torch._int_mm(a, b)
+        best = None
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12, f"measured: cuBLASLt int8 GEMM {n}^3, best of {reps}"
+    except Exception as ex:  # noqa: BLE001
+        return INT8_PEAK_TOPS, f"nominal (int8 GEMM probe failed: {type(ex).__name__})"
+
+
 def measure_pcie(torch, nbytes=1 << 30, reps=3):
     """Pinned host <-> HBM copy rates (GB/s) for the out-of-core roofline."""
     h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
@@ -418,7 +441,8 @@ def run_engine(args):
         _native.check(rc)
         oz_flops, oz_ms, oz_launches = octx.update_stats()
         octx.close()
-        oz_peak = INT8_PEAK_TOPS / 36.0
+        int8_tops, int8_src = measure_int8_peak(torch)
+        oz_peak = int8_tops / 36.0
         oz_ach = oz_flops / (oz_ms * 1e-3) / 1e12 if oz_ms > 0 else None
         ozaki = {"value": flops / (oms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": oms,
                  "max_prefix_rel_diff_vs_fp64_dmma": diff, "logdet": float(oprefix[-1]),
@@ -428,8 +452,8 @@ def run_engine(args):
                  "roofline": {"bound": "tensor (int8)", "kernel": "oz_expo + oz_slice + oz_update (rest updates)",
                               "achieved": oz_ach, "peak": oz_peak, "unit": UNIT,
                               "frac": (oz_ach / oz_peak) if oz_ach else None,
-                              "peak_source": f"nominal B200 dense int8 {INT8_PEAK_TOPS / 1e3:.1f} POPS / 36 slice "
-                                             "products per FP64 multiply-add (not measured)",
+                              "peak_source": f"dense int8 {int8_tops / 1e3:.2f} POPS ({int8_src}) / 36 slice "
+                                             "products per FP64 multiply-add",
                               "launches": oz_launches, "kernel_ms": oz_ms}}
 
     # the second entry point of the path: memdet_ldl with the reference's block-local 1x1 pivoting
