@@ -48,7 +48,7 @@ UNIT = "TFLOP/s"
 INT8_PEAK_TOPS = 4500.0  # nominal B200 dense int8 tensor throughput (TOPS), for the opt-in Ozaki line
 C2 = dict(n=32768, num_blocks=8, d=16, ell=4.0, jitter=1e-6, seed=0)
 OOC = dict(n=65536, num_blocks=4, hbm_budget=int(24e9))  # out-of-core line: C3-sized RBF, forced walk
-PROFILE_SUMMARY = os.path.join(REPO, "profiles", "r01_gemm_update_ncu.json")
+PROFILE_SUMMARY = os.path.join(REPO, "profiles", "r02_gemm_update_ncu.json")
 
 
 def dist_env():
