@@ -197,6 +197,8 @@ struct Ooc {
   unsigned long long* amax = nullptr;
   unsigned* lflags = nullptr;       // panel-server hand-off counters (ldl_panel_server_kernel)
   unsigned* lpipe = nullptr;        // panel / bulk pipeline counters (ldl.cu, B2D_LDL_PIPE)
+  double* lrows = nullptr;          // big-block cluster panel: the rows' C / W histories
+  size_t lrows_bytes = 0;
   cudaStream_t s_lalt = nullptr;    // pipeline: odd panels and their bulk updates
   cudaEvent_t ev_lpanel[2] = {nullptr, nullptr}, ev_lalt = nullptr;
   cudaStream_t s_bulk = nullptr;    // panel-server bulk launches (high priority)
@@ -381,7 +383,8 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(pack_block_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(tile_inv_unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T * 129 * 8));
-  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CUDA_TRY(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CUDA_TRY(cudaFuncSetAttribute(ldl_factor_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_factor_smem(LC_RMAX)));
@@ -394,7 +397,7 @@ static int configure_kernels() {
                                 (int)TRANSPOSE_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(ldl_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(LDL_FINISH_SMEM_MAX * 8)));
-  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
   CUDA_TRY(cudaFuncSetAttribute(pack_set_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PACK_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(l32_trsm_diag_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -496,6 +499,7 @@ static void destroy(Ctx* c) {
   }
   cudaFree(o.lflags);
   cudaFree(o.lpipe);
+  cudaFree(o.lrows);
   if (o.s_lalt) {
     cudaStreamSynchronize(o.s_lalt);
     cudaStreamDestroy(o.s_lalt);
@@ -2083,8 +2087,20 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   // two streams, and waits in the kernel for bulk update p (ldl.cu pipe_wait): its cluster takes
   // its SMs while bulk p runs, instead of after it (beside the trailing DMMA updates a launch
   // waits ~100 us for SMs).  Bulk p follows panel p on the panel's stream.
+  // clusters: the rows' C / W in shared memory up to LC * LC_RMAX rows, in global memory up to
+  // LC * LC_RMAX_BIG (B2D_LDL_BIG=0: the one-CTA panel above LC * LC_RMAX, as round 1)
+  const char* bge = getenv("B2D_LDL_BIG");
+  const bool big = n > (int64_t)LC * LC_RMAX && n <= (int64_t)LC * LC_RMAX_BIG && (bge ? atoi(bge) != 0 : true);
+  const bool clus = (n <= (int64_t)LC * LC_RMAX || big) && !single_cta;
+  if (big && o.lrows_bytes < ldl_big_rows_bytes(n)) {
+    cudaFree(o.lrows);
+    o.lrows = nullptr;
+    o.lrows_bytes = 0;
+    CUDA_TRY(cudaMalloc((void**)&o.lrows, ldl_big_rows_bytes(n)));
+    o.lrows_bytes = ldl_big_rows_bytes(n);
+  }
   const char* pie = getenv("B2D_LDL_PIPE");
-  const bool pipe = (pie ? atoi(pie) != 0 : true) && n <= (int64_t)LC * LC_RMAX && !single_cta;
+  const bool pipe = (pie ? atoi(pie) != 0 : true) && clus;
   cudaStream_t pst[2] = {s, s};
   if (pipe) {
     if (!o.lpipe) {
@@ -2105,7 +2121,7 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   unsigned pidx = 0;
   for (int64_t r0 = 0; r0 < n; r0 += LDL_NB, ++pidx) {
     const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
-    if (n <= (int64_t)LC * LC_RMAX && !single_cta) {
+    if (clus) {
       cudaStream_t ps = pst[pidx & 1];
       if (pipe && pidx > 0) cudaStreamWaitEvent(ps, o.ev_lpanel[(pidx - 1) & 1], 0);  // panel pidx-1 done
       // the panel on a 16-CTA cluster with its rows in distributed shared memory
@@ -2117,12 +2133,15 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
       attr[0].val.clusterDim.z = 1;
       cfg.gridDim = dim3(LC);
       cfg.blockDim = dim3(LC_THREADS);
-      cfg.dynamicSmemBytes = ldl_cluster_smem((int)((n + LC - 1) / LC));
+      cfg.dynamicSmemBytes = big ? (size_t)((n + LC - 1) / LC) * 8 : ldl_cluster_smem((int)((n + LC - 1) / LC));
       cfg.stream = ps;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       unsigned* pp = pipe ? o.lpipe : nullptr;
-      CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk, pp, pidx));
+      if (big)
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel<true>, g, r0, nbk, pp, pidx, o.lrows));
+      else
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel<false>, g, r0, nbk, pp, pidx, (double*)nullptr));
       if (pipe) cudaEventRecord(o.ev_lpanel[pidx & 1], ps);
       // the cluster kernel stored the panel's L; the row interchanges of the finished columns
       // ride along the bulk update as extra blocks

@@ -380,6 +380,9 @@ __device__ __forceinline__ Cand cand_of(int64_t i, double v) {
 // The nbk steps of the panel at r0; gs0 = steps this kernel ran before (mbarrier phases and
 // buffer parity).  Returns false if a step failed (uniform across the cluster, after a cluster
 // barrier).  On return the C / W rows of the panel are final in shared memory.
+// MRT: rows per thread (R <= MRT * LC_THREADS); Cs / Ws may be shared (<= LC_RMAX rows) or
+// global memory (the big-block panel, ldl_panel_cluster_kernel<true>).
+template <int MRT = (LC_RMAX + LC_THREADS - 1) / LC_THREADS>
 __device__ __forceinline__ bool cluster_panel_steps(const LdlArgs& g, int64_t r0, int nbk, double* Cs, double* Ws,
                                                     double* dg, int R, ClusterShared& sh, int gs0) {
   cg::cluster_group cl = cg::this_cluster();
@@ -417,7 +420,7 @@ __device__ __forceinline__ bool cluster_panel_steps(const LdlArgs& g, int64_t r0
     LDL_MARK(2);
     // raw entries (i, r) of this thread's rows and their tags: every case needs them, and r is
     // known before the pivot (the loads overlap the reduction and the row exchange)
-    constexpr int MR = (LC_RMAX + LC_THREADS - 1) / LC_THREADS;
+    constexpr int MR = MRT;
     double ar[MR], a2[MR];
     int gr[MR], g2[MR];
 #pragma unroll
@@ -566,8 +569,18 @@ __device__ __forceinline__ void cluster_panel_writeback(const LdlArgs& g, int64_
   }
 }
 
+// BIG: blocks of up to LC * LC_RMAX_BIG rows (the reference's memory-sized blocks, C5: b = 39322):
+// the rows' C / W histories live in global memory (`rows`, [LC][2][R][LC_LD], each CTA its own
+// slab, read back through L2 after every step's barrier), only the eager diagonal stays in shared
+// memory.  Same steps and arithmetic as the shared-memory panel.
+constexpr int LC_RMAX_BIG = 2560;
+__host__ __device__ constexpr size_t ldl_big_rows_bytes(int64_t n) {
+  return (size_t)LC * 2 * (size_t)((n + LC - 1) / LC) * LC_LD * 8;
+}
+template <bool BIG>
 __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_kernel(LdlArgs g, int64_t r0, int nbk,
-                                                                                   unsigned* pipe, unsigned pidx) {
+                                                                                   unsigned* pipe, unsigned pidx,
+                                                                                   double* rows) {
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
   if (pipe && pidx > 0) pipe_wait(pipe + 1, pidx);  // bulk update pidx - 1 done
@@ -579,9 +592,9 @@ __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_
   tl_mark(tls, false);
   extern __shared__ double sm[];
   const int R = (int)((g.n + LC - 1) / LC);
-  double* Cs = sm;                      // [R][LC_LD]
-  double* Ws = Cs + (size_t)R * LC_LD;  // [R][LC_LD]
-  double* dg = Ws + (size_t)R * LC_LD;  // [R] eager diagonal
+  double* Cs = BIG ? rows + (size_t)c * 2 * R * LC_LD : sm;  // [R][LC_LD]
+  double* Ws = Cs + (size_t)R * LC_LD;                        // [R][LC_LD]
+  double* dg = BIG ? sm : Ws + (size_t)R * LC_LD;             // [R] eager diagonal
   __shared__ ClusterShared sh;
   cluster_shared_init(sh);
   for (int li = threadIdx.x; li < R; li += LC_THREADS) {
@@ -590,7 +603,8 @@ __global__ void __launch_bounds__(LC_THREADS, LDL_PANEL_MINB) ldl_panel_cluster_
   }
   __syncthreads();  // dg loaded, barriers initialised
   cl.sync();        // every CTA's barriers initialised before any remote arrive
-  if (!cluster_panel_steps(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) {
+  constexpr int MRT = BIG ? (LC_RMAX_BIG + LC_THREADS - 1) / LC_THREADS : (LC_RMAX + LC_THREADS - 1) / LC_THREADS;
+  if (!cluster_panel_steps<MRT>(g, r0, nbk, Cs, Ws, dg, R, sh, 0)) {
     if (pipe && c == 0 && threadIdx.x == 0) st_release_u32(pipe, PIPE_FAIL);
     return;
   }

@@ -718,3 +718,22 @@ def test_pivoted_ldl_out_of_core_keeps_reference_blocks():
     ref_perm, ref_prefix, _, _ = O.memdet_ldl(a, 2)
     np.testing.assert_array_equal(res.perm, ref_perm)
     assert rel_err(res.prefix, ref_prefix) <= 1e-10
+
+
+@pytest.mark.parametrize("m,nb", [(8192, 1), (13000, 2)])
+def test_pivoted_ldl_big_blocks_cluster_equals_one_cta(m, nb, monkeypatch):
+    """Reference blocks above the shared-memory cluster panel's 16 x 384 rows (the paper's
+    memory-sized blocks) run on the big-block cluster panel (the rows' C / W histories in global
+    memory); it must reproduce the one-CTA panel (B2D_LDL_BIG=0, itself pinned to the oracle on
+    smaller blocks) bit for bit: perm, prefix and signs."""
+    a = gen.rbf(m, seed=m)
+    eng.release_engine_cache()
+    big = eng.memdet_ldl(a, num_blocks=nb)
+    monkeypatch.setenv("B2D_LDL_BIG", "0")
+    eng.release_engine_cache()
+    one = eng.memdet_ldl(a, num_blocks=nb)
+    eng.release_engine_cache()
+    np.testing.assert_array_equal(big.perm, one.perm)
+    np.testing.assert_array_equal(big.prefix_signs, one.prefix_signs)
+    assert np.array_equal(big.prefix.view(np.int64), one.prefix.view(np.int64))
+    assert int(np.sum(big.perm != np.arange(m))) > m // 2  # the pivoting is exercised

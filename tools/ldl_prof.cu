@@ -41,9 +41,9 @@ int main(int argc, char** argv) {
   unsigned long long ab;
   memcpy(&ab, &amax, 8);
   CK(cudaMemcpy(amax_bits, &ab, 8, cudaMemcpyHostToDevice));
-  CK(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(ldl_panel_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const size_t smem = ldl_cluster_smem((int)((n + LC - 1) / LC));
-  CK(cudaFuncSetAttribute(ldl_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(ldl_panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const LdlArgs g{A, tag, C, W, diag, col, d, swaps, fail, amax_bits, ld, n, 0};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -70,7 +70,7 @@ int main(int argc, char** argv) {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       cudaEventRecord(e0);
-      CK(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel, g, r0, nbk, (unsigned*)nullptr, 0u));
+      CK(cudaLaunchKernelEx(&cfg, ldl_panel_cluster_kernel<false>, g, r0, nbk, (unsigned*)nullptr, 0u, (double*)nullptr));
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
