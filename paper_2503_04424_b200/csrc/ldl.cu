@@ -720,9 +720,12 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
     sC[q * LDL_BT + x] = i0 + x < n ? __ldcg(g.C + q * ld + i0 + x) : 0.0;
     sW[q * LDL_BT + x] = j0 + x < n ? __ldcg(g.W + q * ld + j0 + x) : 0.0;
   }
-  // thread (tx, ty): rows i0 + 4 tx + a, columns j0 + 4 ty + c (a, c < 4)
+  // thread (tx, ty): rows i0 + 2 tx + (a & 1) + 32 (a >> 1), columns j0 + 4 ty + c (a, c < 4): the
+  // C pairs (2 tx, 2 tx + 1) are conflict-free 16-byte shared loads (a stride of 4 rows per thread
+  // made them 2-way bank conflicts, ncu: short-scoreboard stalls first)
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int64_t ib = i0 + 4 * tx, jb = j0 + 4 * ty;
+  const int64_t ib = i0 + 2 * tx, jb = j0 + 4 * ty;
+  auto roff = [](int a) { return (a & 1) + 32 * (a >> 1); };
   // interior off-diagonal tiles: vector loads / stores (i0 is a multiple of 32, ld of 128)
   const bool vec = bi > bj && i0 + LDL_BT <= n && j0 + LDL_BT <= n;
   double v[4][4];
@@ -732,18 +735,19 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   for (int c = 0; c < 4; ++c) {
     const int64_t j = jb + c;
     if (vec) {
-      const double2* p = reinterpret_cast<const double2*>(g.A + j * ld + ib);
-      const double2 x0 = __ldcg(p), x1 = __ldcg(p + 1);
+      const double2 x0 = __ldcg(reinterpret_cast<const double2*>(g.A + j * ld + ib));
+      const double2 x1 = __ldcg(reinterpret_cast<const double2*>(g.A + j * ld + ib + 32));
       v[0][c] = x0.x;
       v[1][c] = x0.y;
       v[2][c] = x1.x;
       v[3][c] = x1.y;
-      tw[c] = __ldcg(reinterpret_cast<const unsigned int*>(g.tag + j * ld + ib));
+      tw[c] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib)) |
+              ((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib + 32)) << 16);
     } else {
       tw[c] = 0;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const int64_t i = ib + a;
+        const int64_t i = ib + roff(a);
         const bool ok = i < n && j < n && i >= j;
         v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
         tw[c] |= (uint32_t)(ok ? __ldcg(g.tag + j * ld + i) : 0) << (8 * a);
@@ -758,8 +762,8 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
     // from their loaded value with the terms [tag, nbk) only -- each entry still sees exactly
     // its terms, in order, with the reference's two roundings
     for (int q = 0; q < nbk; ++q) {
-      const double2 c01 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx);
-      const double2 c23 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 4 * tx + 2);
+      const double2 c01 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 2 * tx);
+      const double2 c23 = *reinterpret_cast<const double2*>(sC + q * LDL_BT + 32 + 2 * tx);
       const double2 w01 = *reinterpret_cast<const double2*>(sW + q * LDL_BT + 4 * ty);
       const double2 w23 = *reinterpret_cast<const double2*>(sW + q * LDL_BT + 4 * ty + 2);
       const double cc[4] = {c01.x, c01.y, c23.x, c23.y}, ww[4] = {w01.x, w01.y, w23.x, w23.y};
@@ -775,10 +779,10 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
         for (int c = 0; c < 4; ++c) {
           const int tg = (int)((tw[c] >> (8 * a)) & 0xffu);
           if (tg) {
-            const int64_t i = ib + a, j = jb + c;
+            const int64_t i = ib + roff(a), j = jb + c;
             double x = __ldcg(g.A + j * ld + i);
             for (int q = tg; q < nbk; ++q)
-              x = __dsub_rn(x, __dmul_rn(sC[q * LDL_BT + 4 * tx + a], sW[q * LDL_BT + 4 * ty + c]));
+              x = __dsub_rn(x, __dmul_rn(sC[q * LDL_BT + 2 * tx + roff(a)], sW[q * LDL_BT + 4 * ty + c]));
             v[a][c] = x;
           }
         }
@@ -788,14 +792,14 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   for (int c = 0; c < 4; ++c) {
     const int64_t j = jb + c;
     if (vec) {
-      double2* p = reinterpret_cast<double2*>(g.A + j * ld + ib);
-      p[0] = make_double2(v[0][c], v[1][c]);
-      p[1] = make_double2(v[2][c], v[3][c]);
-      if (tw[c]) *reinterpret_cast<unsigned int*>(g.tag + j * ld + ib) = 0u;
+      *reinterpret_cast<double2*>(g.A + j * ld + ib) = make_double2(v[0][c], v[1][c]);
+      *reinterpret_cast<double2*>(g.A + j * ld + ib + 32) = make_double2(v[2][c], v[3][c]);
+      if (tw[c] & 0xffffu) *reinterpret_cast<unsigned short*>(g.tag + j * ld + ib) = 0;
+      if (tw[c] >> 16) *reinterpret_cast<unsigned short*>(g.tag + j * ld + ib + 32) = 0;
     } else {
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const int64_t i = ib + a;
+        const int64_t i = ib + roff(a);
         if (i < n && j < n && i >= j) {
           g.A[j * ld + i] = v[a][c];
           if ((tw[c] >> (8 * a)) & 0xffu) g.tag[j * ld + i] = 0;
