@@ -737,8 +737,6 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   // interior off-diagonal tiles: vector loads / stores (i0 is a multiple of 32, ld of 128)
   const bool vec = bi > bj && i0 + LDL_BT <= n && j0 + LDL_BT <= n;
   double v[4][4];
-  uint32_t tw[4];  // tags of the 4 rows of column c, one byte each
-  bool tagged = false;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int64_t j = jb + c;
@@ -749,21 +747,18 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
       v[1][c] = x0.y;
       v[2][c] = x1.x;
       v[3][c] = x1.y;
-      tw[c] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib)) |
-              ((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib + 32)) << 16);
     } else {
-      tw[c] = 0;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int64_t i = ib + roff(a);
         const bool ok = i < n && j < n && i >= j;
         v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
-        tw[c] |= (uint32_t)(ok ? __ldcg(g.tag + j * ld + i) : 0) << (8 * a);
       }
     }
-    tagged |= tw[c] != 0;
   }
   __syncthreads();
+  uint32_t tw[4];  // tags of the 4 rows of column c, one byte each
+  bool tagged = false;
   {
     // every term on every entry (the fast path); entries that already hold some of the panel's
     // steps (tag > 0, rare: rows / columns moved by the panel's interchanges) are redone below
@@ -779,6 +774,25 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[a][c] = __dsub_rn(v[a][c], __dmul_rn(cc[a], ww[c]));
+    }
+    // the tags (only read now: nothing before the terms needs them, and their loads would hold
+    // registers or the first term)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t j = jb + c;
+      if (vec) {
+        tw[c] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib)) |
+                ((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib + 32)) << 16);
+      } else {
+        tw[c] = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int64_t i = ib + roff(a);
+          const bool ok = i < n && j < n && i >= j;
+          tw[c] |= (uint32_t)(ok ? __ldcg(g.tag + j * ld + i) : 0) << (8 * a);
+        }
+      }
+      tagged |= tw[c] != 0;
     }
     if (tagged) {
 #pragma unroll
