@@ -723,11 +723,21 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   b -= off(bj);
   const int64_t bi = bj + b;
   const int64_t i0 = re + bi * LDL_BT, j0 = re + bj * LDL_BT;
-  for (int e = threadIdx.x; e < nbk * LDL_BT; e += 256) {
-    const int q = e / LDL_BT, x = e % LDL_BT;
-    sC[q * LDL_BT + x] = i0 + x < n ? __ldcg(g.C + q * ld + i0 + x) : 0.0;
-    sW[q * LDL_BT + x] = j0 + x < n ? __ldcg(g.W + q * ld + j0 + x) : 0.0;
+  // the panel's C / W rows of this tile staged with asynchronous 16-byte copies (zero-filled past
+  // the block), in flight while the entries themselves are loaded (a register round trip per
+  // element made every copy wait for its load)
+  for (int e = threadIdx.x; e < nbk * (LDL_BT / 2); e += 256) {
+    const int q = e / (LDL_BT / 2), x = 2 * (e % (LDL_BT / 2));
+    const int64_t ci = i0 + x, wj = j0 + x;
+    const uint32_t cb = ci < n ? (ci + 1 < n ? 16u : 8u) : 0u, wb = wj < n ? (wj + 1 < n ? 16u : 8u) : 0u;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sC + q * LDL_BT + x)),
+                 "l"(g.C + q * ld + (cb ? ci : 0)), "r"(cb)
+                 : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sW + q * LDL_BT + x)),
+                 "l"(g.W + q * ld + (wb ? wj : 0)), "r"(wb)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   // thread (tx, ty): rows i0 + 2 tx + (a & 1) + 32 (a >> 1), columns j0 + 4 ty + c (a, c < 4): the
   // C pairs (2 tx, 2 tx + 1) are conflict-free 16-byte shared loads (a stride of 4 rows per thread
   // made them 2-way bank conflicts, ncu: short-scoreboard stalls first)
@@ -756,6 +766,7 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
       }
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   uint32_t tw[4];  // tags of the 4 rows of column c, one byte each
   bool tagged = false;
