@@ -743,6 +743,11 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   // made them 2-way bank conflicts, ncu: short-scoreboard stalls first)
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t ib = i0 + 2 * tx, jb = j0 + 4 * ty;
+  // per-thread base pointers and 32-bit column strides (the block has < 2^31 entries): fewer
+  // 64-bit index registers under the kernel's 64-register cap
+  double* const Ab = g.A + jb * ld + ib;
+  uint8_t* const Tb = g.tag + jb * ld + ib;
+  const int ldi = (int)ld;
   auto roff = [](int a) { return (a & 1) + 32 * (a >> 1); };
   // interior off-diagonal tiles: vector loads / stores (i0 is a multiple of 32, ld of 128)
   const bool vec = bi > bj && i0 + LDL_BT <= n && j0 + LDL_BT <= n;
@@ -751,8 +756,8 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   for (int c = 0; c < 4; ++c) {
     const int64_t j = jb + c;
     if (vec) {
-      const double2 x0 = __ldcg(reinterpret_cast<const double2*>(g.A + j * ld + ib));
-      const double2 x1 = __ldcg(reinterpret_cast<const double2*>(g.A + j * ld + ib + 32));
+      const double2 x0 = __ldcg(reinterpret_cast<const double2*>(Ab + c * ldi));
+      const double2 x1 = __ldcg(reinterpret_cast<const double2*>(Ab + c * ldi + 32));
       v[0][c] = x0.x;
       v[1][c] = x0.y;
       v[2][c] = x1.x;
@@ -762,7 +767,7 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
       for (int a = 0; a < 4; ++a) {
         const int64_t i = ib + roff(a);
         const bool ok = i < n && j < n && i >= j;
-        v[a][c] = ok ? __ldcg(g.A + j * ld + i) : 0.0;
+        v[a][c] = ok ? __ldcg(Ab + c * ldi + roff(a)) : 0.0;
       }
     }
   }
@@ -792,15 +797,15 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
     for (int c = 0; c < 4; ++c) {
       const int64_t j = jb + c;
       if (vec) {
-        tw[c] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib)) |
-                ((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(g.tag + j * ld + ib + 32)) << 16);
+        tw[c] = (uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(Tb + c * ldi)) |
+                ((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(Tb + c * ldi + 32)) << 16);
       } else {
         tw[c] = 0;
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           const int64_t i = ib + roff(a);
           const bool ok = i < n && j < n && i >= j;
-          tw[c] |= (uint32_t)(ok ? __ldcg(g.tag + j * ld + i) : 0) << (8 * a);
+          tw[c] |= (uint32_t)(ok ? __ldcg(Tb + c * ldi + roff(a)) : 0) << (8 * a);
         }
       }
       tagged |= tw[c] != 0;
@@ -813,7 +818,7 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
           const int tg = (int)((tw[c] >> (8 * a)) & 0xffu);
           if (tg) {
             const int64_t i = ib + roff(a), j = jb + c;
-            double x = __ldcg(g.A + j * ld + i);
+            double x = __ldcg(Ab + c * ldi + roff(a));
             for (int q = tg; q < nbk; ++q)
               x = __dsub_rn(x, __dmul_rn(sC[q * LDL_BT + 2 * tx + roff(a)], sW[q * LDL_BT + 4 * ty + c]));
             v[a][c] = x;
@@ -825,17 +830,17 @@ __device__ __forceinline__ void ldl_bulk_tile(const LdlArgs& g, int64_t r0, int 
   for (int c = 0; c < 4; ++c) {
     const int64_t j = jb + c;
     if (vec) {
-      *reinterpret_cast<double2*>(g.A + j * ld + ib) = make_double2(v[0][c], v[1][c]);
-      *reinterpret_cast<double2*>(g.A + j * ld + ib + 32) = make_double2(v[2][c], v[3][c]);
-      if (tw[c] & 0xffffu) *reinterpret_cast<unsigned short*>(g.tag + j * ld + ib) = 0;
-      if (tw[c] >> 16) *reinterpret_cast<unsigned short*>(g.tag + j * ld + ib + 32) = 0;
+      *reinterpret_cast<double2*>(Ab + c * ldi) = make_double2(v[0][c], v[1][c]);
+      *reinterpret_cast<double2*>(Ab + c * ldi + 32) = make_double2(v[2][c], v[3][c]);
+      if (tw[c] & 0xffffu) *reinterpret_cast<unsigned short*>(Tb + c * ldi) = 0;
+      if (tw[c] >> 16) *reinterpret_cast<unsigned short*>(Tb + c * ldi + 32) = 0;
     } else {
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int64_t i = ib + roff(a);
         if (i < n && j < n && i >= j) {
-          g.A[j * ld + i] = v[a][c];
-          if ((tw[c] >> (8 * a)) & 0xffu) g.tag[j * ld + i] = 0;
+          Ab[c * ldi + roff(a)] = v[a][c];
+          if ((tw[c] >> (8 * a)) & 0xffu) Tb[c * ldi + roff(a)] = 0;
         }
       }
     }
