@@ -351,6 +351,8 @@ struct Ctx {
   // last update and after its panel rows of the current stage
   cudaStream_t s_pr[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_row, ev_prow;
+  cudaStream_t s_la[2] = {nullptr, nullptr};  // look-ahead solve of the critical block row
+  std::vector<cudaEvent_t> ev_la;
   // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
   // block column-major in dense, the stage's solved row-k blocks X and their D^{-1}-scaled copy S
   bool ldl32 = false;
@@ -475,6 +477,12 @@ static void destroy(Ctx* c) {
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
     }
+  for (auto st : c->s_la)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (auto e : c->ev_la) cudaEventDestroy(e);
   for (auto* v : {&c->ev_row, &c->ev_prow})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : c->ev_cols) cudaEventDestroy(e);
@@ -1879,9 +1887,12 @@ static int ooc_store(Ctx* c, int ri, int rj, int s) {
 
 // Panel solve X <- X L^{-T} of R x Q tiles against the factored diagonal block lkk (Q x Q tiles,
 // unit or not per inv): right-looking over L's tile-columns in groups of W (dense.py:94-99).
+// Wg: group width in tile-columns (0 = the panel width W_TILES).  Any grouping gives every tile
+// its k-chunks in increasing order, so the result does not depend on it; narrow groups shorten
+// the chain of left-looking launches (R tiles each) for a solve on the critical path.
 static void trsm_panel(Ctx* c, cudaStream_t s, const TileMap& x, int R, const TileMap& lkk, int Q,
-                       const double* inv) {
-  const int W = c->W_TILES;
+                       const double* inv, int Wg = 0) {
+  const int W = Wg > 0 ? Wg : c->W_TILES;
   const char* lbe = getenv("B2D_LEFT_BELOW");
   const bool left = lbe ? atoi(lbe) != 0 : true;
   for (int q0 = 0; q0 < Q; q0 += W) {
@@ -1927,6 +1938,94 @@ static void trsm_panel(Ctx* c, cudaStream_t s, const TileMap& x, int R, const Ti
       launch_gemm(c, s, MODE_UPDATE, u, false, 0.0);
     }
   }
+}
+
+// Look-ahead panel solve of the critical block row (the rows of block k+1: factor k -> these
+// rows -> the update of diagonal block (k+1, k+1) -> factor k+1), with that diagonal update
+// folded in.  The row's Q tile-columns go in groups G_0, G_1, ... of Wg; U(g -> h) is the update
+// of group h by the solved group g (K = 128 Wg).  Stream A carries the chain: solve(g) (left-
+// looking inside the group), then U(g -> g+1); stream B the rest of each group's updates
+// U(g -> h >= g+2); stream C the D^{-1} scaling of group g and its K-chunk of the diagonal update
+// (du: output tiles = the diagonal block, A = ps, B = pu).  Every tile still receives its K-chunks
+// in increasing order -- the FP64 accumulators continue exactly across launches -- so pu, ps and
+// the diagonal block equal those of trsm_panel + scale_cols + one K = 128 Q update bit for bit.
+// On return A has joined B and C.
+static int trsm_panel_la(Ctx* c, cudaStream_t A, const TileMap& pu, const TileMap& ps, int R, const TileMap& lkk,
+                         int Q, const double* inv, int Wg, int64_t nsize, const double* dblk, GemmTask du) {
+  if (!c->s_la[0]) {
+    int pr = 0;
+    cudaStreamGetPriority(A, &pr);
+    for (auto& st : c->s_la) CUDA_TRY(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, pr));
+  }
+  const int G = (Q + Wg - 1) / Wg;
+  while ((int)c->ev_la.size() < 2 * G + 2) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ev_la.push_back(e);
+  }
+  cudaStream_t B = c->s_la[0], C = c->s_la[1];
+  cudaEvent_t* es = c->ev_la.data();      // es[g]: group g solved (A)
+  cudaEvent_t* er = es + G;               // er[g]: U(g -> h >= g+2) done (B)
+  cudaEvent_t ec = c->ev_la[2 * G], eb = c->ev_la[2 * G + 1];
+  auto gcol = [&](int g) { return std::min(Q, g * Wg); };
+  auto upd = [&](cudaStream_t st, int g, int h0, int h1) {  // U(g -> columns [h0, h1))
+    if (h1 <= h0) return;
+    GemmTask u{};
+    u.a = pu;
+    u.b = lkk;
+    u.c = pu;
+    u.out = TileSet{0, R, h0, h1, 0, 0};
+    u.p0 = gcol(g);
+    u.p1 = gcol(g + 1);
+    launch_gemm(c, st, MODE_UPDATE, u, false, 0.0);
+  };
+  for (int g = 0; g < G; ++g) {
+    const int q0 = gcol(g), qe = gcol(g + 1);
+    if (g >= 1) {
+      // U(g-1 -> g) on the chain, after every earlier update of group g (B's U(g-2 -> g))
+      if (g >= 2) cudaStreamWaitEvent(A, er[g - 2], 0);
+      upd(A, g - 1, q0, qe);
+    }
+    for (int q = q0; q < qe; ++q) {
+      if (q > q0) {
+        GemmTask u{};
+        u.a = pu;
+        u.b = lkk;
+        u.c = pu;
+        u.out = TileSet{0, R, q, q + 1, 0, 0};
+        u.p0 = q0;
+        u.p1 = q;
+        launch_gemm(c, A, MODE_UPDATE, u, false, 0.0);
+      }
+      GemmTask t{};
+      t.c = pu;
+      t.binv = inv + (int64_t)q * TILE_ELEMS;
+      t.out = TileSet{0, R, q, q + 1, 0, 0};
+      t.k = q;
+      launch_gemm(c, A, MODE_TRSM, t, false, 0.0);
+    }
+    cudaEventRecord(es[g], A);
+    // B: the rest of group g's updates (groups g+2 ..), after group g is solved
+    cudaStreamWaitEvent(B, es[g], 0);
+    upd(B, g, gcol(g + 2), Q);
+    cudaEventRecord(er[g], B);
+    // C: scale group g, then its K-chunk of the diagonal update
+    cudaStreamWaitEvent(C, es[g], 0);
+    TileMap su = pu, ss = ps;
+    su.base += (int64_t)q0 * TILE_ELEMS;
+    ss.base += (int64_t)q0 * TILE_ELEMS;
+    const int64_t nrem = std::max<int64_t>(0, nsize - (int64_t)q0 * T);
+    scale_cols_kernel<<<1024, 256, 0, C>>>(su, ss, R, qe - q0, nrem, dblk + (int64_t)q0 * T);
+    c->launches++;
+    du.p0 = q0;
+    du.p1 = qe;
+    launch_gemm(c, C, MODE_UPDATE, du, true, (double)du.out.count() * 2.0 * T * T * (qe - q0) * T);
+  }
+  cudaEventRecord(ec, C);
+  cudaEventRecord(eb, B);
+  cudaStreamWaitEvent(A, ec, 0);
+  cudaStreamWaitEvent(A, eb, 0);
+  return B2D_OK;
 }
 
 // Panel solve of slot s (engine lower block (x, k), x's rows) against the factored diagonal
@@ -2714,6 +2813,11 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     auto bstart = [&](int q) { return std::min(nt, col0(q)); };
     auto bend = [&](int q) { return q + 1 < nb ? std::min(nt, col0(q + 1)) : nt; };
     // block row r at distance d = r - k: streams of falling priority, then one stream per row
+    // B2D_LDL_NEXT_W: solve group width of block row k+1 (the chain factor k -> factor k+1)
+    const int next_w = env_int("B2D_LDL_NEXT_W", 0);
+    // B2D_LDL_LA: group width of the look-ahead solve of block row k+1 (0 = trsm_panel); 4
+    // measured best (C2 432.6 -> 431.0 ms, C3 2837 -> 2831 ms; 2 and 8 no better)
+    const int la_w = env_int("B2D_LDL_LA", 4);
     auto dstream = [&](int r, int k) {
       const int d = r - k;
       return d <= 2 ? c->s_pr[0] : d <= 5 ? c->s_pr[d - 2] : col_stream(r);
@@ -2722,14 +2826,14 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb;
       const double* inv_k = o.inv_of(k, c->inv);
       const int np = c->npan, pb = k % np;  // panel grids: stage k waits for the readers of stage k-np
-      auto panel_rows = [&](cudaStream_t st, int r0, int r1) {  // global tile rows [r0, r1)
+      auto panel_rows = [&](cudaStream_t st, int r0, int r1, int wg) {  // global tile rows [r0, r1)
         TileMap src = packed;
         src.roff = r0;
         src.coff = k0;
         const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
         const TileMap ps{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
         permute_cols_kernel<<<2048, 256, 0, st>>>(src, pu, r1 - r0, kb, o.size(k), o.perm_of(k));
-        trsm_panel(c, st, pu, r1 - r0, diag_map(k), kb, inv_k);
+        trsm_panel(c, st, pu, r1 - r0, diag_map(k), kb, inv_k, wg);
         scale_cols_kernel<<<2048, 256, 0, st>>>(pu, ps, r1 - r0, kb, o.size(k), o.dblk_of(k));
         c->launches += 2;
       };
@@ -2749,16 +2853,30 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         if ((rc = wait_cols(st, i0))) return rc;
         cudaStreamWaitEvent(st, c->ev_row[r], 0);
         if (r == k + 1) tmark("p1-ready", k, st);
-        panel_rows(st, r0, r1);
+        u.out = TileSet{r0, r1, i0, r1, 1, 0};
+        const bool la = r == k + 1 && la_w > 0;
+        if (la) {
+          // block row k+1 with its diagonal update folded into the look-ahead solve
+          if ((rc = wait_cols(st, r1))) return rc;
+          TileMap src = packed;
+          src.roff = r0;
+          src.coff = k0;
+          const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+          const TileMap ps{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+          permute_cols_kernel<<<2048, 256, 0, st>>>(src, pu, r1 - r0, kb, o.size(k), o.perm_of(k));
+          c->launches++;
+          if ((rc = trsm_panel_la(c, st, pu, ps, r1 - r0, diag_map(k), kb, inv_k, la_w, o.size(k), o.dblk_of(k), u)))
+            return rc;
+        } else
+          panel_rows(st, r0, r1, r == k + 1 ? next_w : 0);
         cudaEventRecord(c->ev_prow[r], st);
         if (r == k + 1) tmark("panel-end", k, st);
         // tiles (r, k+1 .. r): the panel rows of every block up to r
         for (int q = k + 1; q < r; ++q)
           if (dstream(q, k) != st) cudaStreamWaitEvent(st, c->ev_prow[q], 0);
         if ((rc = wait_cols(st, r1))) return rc;
-        u.out = TileSet{r0, r1, i0, r1, 1, 0};
         if (r == k + 1) {
-          launch_gemm(c, st, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+          if (!la) launch_gemm(c, st, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
           cudaEventRecord(c->ev_row[r], st);
           tmark("next-col-end", k, st);
           cudaEventRecord(o.ev_diag, st);
@@ -2798,21 +2916,19 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     // updated first, so the next factor starts on them while the rows below are solved
     const char* spe = getenv("B2D_LDL_SPLIT");
     const int r_split = (spe ? atoi(spe) != 0 : true) ? i0 + kb1 : nt;
-    auto panel_rows = [&](int r0, int r1) {  // global tile rows [r0, r1) of the panel
+    auto panel_rows = [&](int r0, int r1, int wg) {  // global tile rows [r0, r1) of the panel
       TileMap src = packed;
       src.roff = r0;
       src.coff = k0;
       const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
       const TileMap ps{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
       permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(src, pu, r1 - r0, kb, o.size(k), o.perm_of(k));
-      trsm_panel(c, c->s_mid, pu, r1 - r0, diag_map(k), kb, inv_k);
+      trsm_panel(c, c->s_mid, pu, r1 - r0, diag_map(k), kb, inv_k, wg);
       scale_cols_kernel<<<2048, 256, 0, c->s_mid>>>(pu, ps, r1 - r0, kb, o.size(k), o.dblk_of(k));
       c->launches += 2;
     };
-    panel_rows(i0, r_split);
-    tmark("panel-end", k, c->s_mid);
-    // T -= (L D^{-1})_rows L_cols^T (dense.py:109-116) over block column k+1 first (its
-    // diagonal block first of all)
+    // B2D_LDL_LA: block row k+1 by the look-ahead solve, its diagonal update folded in
+    const int la_w = r_split == i0 + kb1 ? env_int("B2D_LDL_LA", 4) : 0;
     GemmTask u{};
     u.a = TileMap{c->pan[pb][1], o.nbt, 0};  // rows indexed by global tile row
     u.b = TileMap{c->pan[pb][0], o.nbt, 0};
@@ -2820,6 +2936,24 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     u.p0 = 0;
     u.p1 = kb;
     const double K = (double)kb * T;
+    if (la_w > 0) {
+      if ((rc = wait_cols(c->s_mid, i0 + kb1))) return rc;
+      TileMap src = packed;
+      src.roff = i0;
+      src.coff = k0;
+      const TileMap pu{c->pan[pb][0] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+      const TileMap ps{c->pan[pb][1] + (size_t)i0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+      permute_cols_kernel<<<2048, 256, 0, c->s_mid>>>(src, pu, r_split - i0, kb, o.size(k), o.perm_of(k));
+      c->launches++;
+      u.out = TileSet{i0, r_split, i0, i0 + kb1, 1, 0};
+      if ((rc = trsm_panel_la(c, c->s_mid, pu, ps, r_split - i0, diag_map(k), kb, inv_k, la_w, o.size(k),
+                              o.dblk_of(k), u)))
+        return rc;
+    } else
+      panel_rows(i0, r_split, env_int("B2D_LDL_NEXT_W", 0));
+    tmark("panel-end", k, c->s_mid);
+    // T -= (L D^{-1})_rows L_cols^T (dense.py:109-116) over block column k+1 first (its
+    // diagonal block first of all)
     // B2D_LDL_URGENT (default 1): each stage's update of block column k+2 runs on s_mid right
     // after its panel (U_k below), so block column k+1 is current here by stream order; without
     // it, that update heads the trailing update on s_side and queues behind the previous stage's
@@ -2828,7 +2962,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     if (!urgent && k >= 1) cudaStreamWaitEvent(c->s_mid, c->ev_resta[k - 1], 0);  // block column k+1 current
     if ((rc = wait_cols(c->s_mid, i0 + kb1))) return rc;
     u.out = TileSet{i0, r_split, i0, i0 + kb1, 1, 0};
-    launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
+    if (la_w == 0) launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
     tmark("next-col-end", k, c->s_mid);
     cudaEventRecord(o.ev_diag, c->s_mid);
     cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
@@ -2841,7 +2975,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     tmark("factor-end", k + 1, c->s_main);
     cudaEventRecord(c->ev_catch[k + 1], c->s_main);
     if (r_split < nt) {  // the rows below block k+1: solve, then their block-column k+1 update
-      panel_rows(r_split, nt);
+      panel_rows(r_split, nt, 0);
       if (urgent) col_sync(k + 1, c->s_mid);  // stage k-1's update of those rows (column stream)
       u.out = TileSet{r_split, nt, i0, i0 + kb1, 1, 0};
       launch_gemm(c, c->s_mid, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);

@@ -395,6 +395,28 @@ def test_pivoted_ldl_in_core_equals_block_walk(m, nb, kchunk, sched, monkeypatch
     eng.release_engine_cache()
 
 
+@pytest.mark.parametrize("m,nb", [(2048, 2), (2560, 2), (3072, 3), (1024, 4)])
+@pytest.mark.parametrize("la", ["0", "1", "3", "4"])
+@pytest.mark.parametrize("sched", ["rows", "cols"])
+def test_pivoted_ldl_lookahead_solve_equals_block_walk(m, nb, la, sched, monkeypatch):
+    """B2D_LDL_LA: the rows of block k+1 solved in groups of `la` tile-columns with look-ahead
+    (the chain on one stream, the rest of each group's updates and the group's K-chunk of the
+    diagonal update on two others).  Every tile still receives its K-chunks in increasing order,
+    so perm, D and the prefixes equal the block walk's bit for bit."""
+    monkeypatch.setenv("B2D_LDL_LA", la)
+    monkeypatch.setenv("B2D_LDL_ROWS", "1" if sched == "rows" else "0")
+    eng.release_engine_cache()
+    a = gen.random_symmetric(m, seed=m + 7 * nb)
+    res = eng.memdet_ldl(a, num_blocks=nb)
+    walk = eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
+    assert not res.info.out_of_core and walk.info.out_of_core
+    np.testing.assert_array_equal(res.perm, walk.perm)
+    np.testing.assert_array_equal(res.prefix_signs, walk.prefix_signs)
+    assert np.array_equal(res.prefix.view(np.int64), walk.prefix.view(np.int64)), \
+        np.max(np.abs(res.prefix - walk.prefix))
+    eng.release_engine_cache()
+
+
 @pytest.mark.parametrize("m,nb", [(1022, 4), (768, 3)])
 def test_in_core_f32_inputs_equal_block_walk(m, nb, monkeypatch):
     """float32 inputs converted to FP64 on the device (B2D_F32_ARITH=0 for the LDL; the default
