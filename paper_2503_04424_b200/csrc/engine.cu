@@ -200,6 +200,8 @@ struct Ooc {
   double* lrows = nullptr;          // big-block cluster panel: the rows' C / W histories
   size_t lrows_bytes = 0;
   cudaStream_t s_lalt = nullptr;    // pipeline: odd panels and their bulk updates
+  cudaStream_t s_lgrp = nullptr;    // group pipeline: early outputs of finished column groups
+  cudaEvent_t ev_lgrp = nullptr;
   cudaEvent_t ev_lpanel[2] = {nullptr, nullptr}, ev_lalt = nullptr;
   cudaStream_t s_bulk = nullptr;    // panel-server bulk launches (high priority)
   cudaEvent_t ev_lreset = nullptr, ev_lbulk = nullptr;
@@ -353,6 +355,10 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_row, ev_prow;
   cudaStream_t s_la[2] = {nullptr, nullptr};  // look-ahead solve of the critical block row
   std::vector<cudaEvent_t> ev_la;
+  std::vector<std::vector<cudaEvent_t>> ev_grp;  // group pipeline: [stage][group] early factor outputs
+  std::vector<cudaEvent_t> ev_rowg;  // group pipeline: block row r's latest solved group
+  cudaStream_t s_grpu = nullptr;     // group pipeline: the chain row's scaling + diagonal update
+  cudaEvent_t ev_grpu = nullptr;
   // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
   // block column-major in dense, the stage's solved row-k blocks X and their D^{-1}-scaled copy S
   bool ldl32 = false;
@@ -398,6 +404,8 @@ static int configure_kernels() {
   CUDA_TRY(cudaFuncSetAttribute(transpose_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)TRANSPOSE_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(ldl_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(LDL_FINISH_SMEM_MAX * 8)));
+  CUDA_TRY(cudaFuncSetAttribute(ldl_partial_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(LDL_FINISH_SMEM_MAX * 8)));
   CUDA_TRY(cudaFuncSetAttribute(ldl_panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ldl_cluster_smem(LC_RMAX)));
@@ -483,6 +491,14 @@ static void destroy(Ctx* c) {
       cudaStreamDestroy(st);
     }
   for (auto e : c->ev_la) cudaEventDestroy(e);
+  for (auto& v : c->ev_grp)
+    for (auto e : v) cudaEventDestroy(e);
+  for (auto e : c->ev_rowg) cudaEventDestroy(e);
+  if (c->s_grpu) {
+    cudaStreamSynchronize(c->s_grpu);
+    cudaStreamDestroy(c->s_grpu);
+  }
+  if (c->ev_grpu) cudaEventDestroy(c->ev_grpu);
   for (auto* v : {&c->ev_row, &c->ev_prow})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : c->ev_cols) cudaEventDestroy(e);
@@ -512,6 +528,11 @@ static void destroy(Ctx* c) {
     cudaStreamSynchronize(o.s_lalt);
     cudaStreamDestroy(o.s_lalt);
   }
+  if (o.s_lgrp) {
+    cudaStreamSynchronize(o.s_lgrp);
+    cudaStreamDestroy(o.s_lgrp);
+  }
+  if (o.ev_lgrp) cudaEventDestroy(o.ev_lgrp);
   for (cudaEvent_t e : {o.ev_lpanel[0], o.ev_lpanel[1], o.ev_lalt})
     if (e) cudaEventDestroy(e);
   if (o.ev_lreset) cudaEventDestroy(o.ev_lreset);
@@ -845,11 +866,13 @@ static int create(int device, int64_t m, int mode, const b2d_options* opt, Ctx**
                              (size_t)(nt_full + bt) * TILE_BYTES + (size_t)ld * ld * 9 + 3 * (size_t)npad_full * 8 +
                              (size_t)NSTAGE * T * npad_full * 8 + (size_t)(m + 8 * ld) * 8;
       const size_t spare = budget > ic_need ? (budget - ic_need) / 2 : 0;
-      // B2D_LDL_ROWS: 1 = row-ordered schedule, 0 = column schedule; unset: rows for <= 8 blocks
-      // (there the chain of factors bounds the step: C2 452 -> 444 ms), columns above (DMMA
-      // throughput bounds it and the column schedule keeps more of it: C3 2876 vs 2950 ms)
+      // B2D_LDL_ROWS: 1 = row-ordered schedule, 0 = column schedule; unset: rows for <= 8 blocks, and
+      // for <= 16 blocks of at most 6144 rows (the blocks whose factors hand out column groups)
+      // (with the factors' group pipeline, B2D_LDL_GROUPS, and one-launch trailing updates the row
+      // schedule wins at C2, 431 -> 418 ms, and at C3, 2833 -> 2798 ms; before the group pipeline
+      // the column schedule kept more of the DMMA throughput at 16 blocks: 2876 vs 2950 ms)
       const char* re = getenv("B2D_LDL_ROWS");
-      c->ldl_rows = re ? atoi(re) != 0 : o.nb <= 8;
+      c->ldl_rows = re ? atoi(re) != 0 : o.nb <= 8 || (o.nb <= 16 && o.b <= (int64_t)LC * LC_RMAX);
       c->npan = c->ldl_rows ? (int)std::min<int64_t>({(int64_t)Ctx::MAX_PAN, std::max<int64_t>(3, o.nb),
                                                       3 + (int64_t)(spare / pair)})
                             : 3;
@@ -1095,8 +1118,9 @@ static void launch_gemm(Ctx* c, cudaStream_t s, int mode, const GemmTask& t, boo
 // for K = 128 * chunk instead of the whole block width, so the factor's cluster and bulk
 // launches find free SMs sooner.  Exact: the accumulators start from C and the chunks continue
 // the same k order, and a stored FP64 accumulator reloads unchanged.
-// K chunk (tile-columns) of the in-core LDL / LU trailing updates: B2D_REST_KCHUNK, else 16 for
-// the pivoted LDL (C2 row schedule 444 -> 437 ms, C3 2882 -> 2864 ms vs 8) and 8 for the LU
+// K chunk (tile-columns) of the in-core LDL / LU trailing updates: B2D_REST_KCHUNK, else 32 for
+// the pivoted LDL (one launch per 4096-row block; 16 was best before the factors' group pipeline
+// gave the chain its slack: C2 422.6 -> 418.5 ms, C3 2821 -> 2798 ms) and 8 for the LU
 static int rest_kchunk(int dflt = 8) {
   const char* e = getenv("B2D_REST_KCHUNK");
   return e ? atoi(e) : dflt;
@@ -2134,7 +2158,22 @@ static int ldl_server_factor(Ctx* c, const LdlArgs& g, cudaStream_t s) {
   return B2D_OK;
 }
 
-static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, bool overlapped = false) {
+// Group pipeline of the pivoted factor (B2D_LDL_GROUPS, default on; in-core row schedule): the
+// finished column groups of gw tile-columns are handed out while the factor is still running --
+// after the last panel of group g (and its bulk launch, which carries the row interchanges of the
+// finished columns) rows < e1 = (g + 1) gw T of L, the pivots and D of steps < e1 and the block
+// permutation's entries < e1 are final (step r only touches rows >= r), so the group's L tile rows,
+// its diagonal-tile inverses and its permutation entries are written on a side stream and ev[g]
+// recorded; the panel rows of the stage then solve and apply group g while the factor works on
+// group g + 1 (factor 0 no longer runs alone on the GPU; the chain row's solve hides behind the
+// factor).  `count` groups were handed out early; the remaining ones are ready with the factor.
+struct LdlGroups {
+  int gw = 4;
+  std::vector<cudaEvent_t>* ev = nullptr;
+  int count = 0;
+};
+static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, bool overlapped = false,
+                            LdlGroups* grp = nullptr) {
   Ooc& o = c->o;
   const int nt = o.tiles(k);
   int64_t n = o.size(k);
@@ -2143,6 +2182,8 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
   int64_t* perm = o.perm_of(k);
   double* inv = o.inv_of(k, c->inv);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
+  bool groups = false;
+  if (grp) grp->count = 0;
   unpack_block_kernel<<<ntri, 256, 0, s>>>(blk, nt, o.dense, ld, 1);
   cudaMemsetAsync(o.amax, 0, 8, s);
   block_absmax_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (n * n + 255) / 256)), 256, 0, s>>>(o.dense, ld, n, o.amax);
@@ -2217,6 +2258,13 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
     cudaEventRecord(o.ev_lalt, s);
     cudaStreamWaitEvent(o.s_lalt, o.ev_lalt, 0);  // counters reset, block state ready
   }
+  groups = grp && grp->ev && grp->gw > 0 && clus && !big && n <= LDL_FINISH_SMEM_MAX;
+  if (groups && !o.s_lgrp) {
+    int sp = 0;
+    cudaStreamGetPriority(s, &sp);
+    CUDA_TRY(cudaStreamCreateWithPriority(&o.s_lgrp, cudaStreamNonBlocking, sp));
+    CUDA_TRY(cudaEventCreateWithFlags(&o.ev_lgrp, cudaEventDisableTiming));
+  }
   unsigned pidx = 0;
   for (int64_t r0 = 0; r0 < n; r0 += LDL_NB, ++pidx) {
     const int nbk = (int)std::min<int64_t>(LDL_NB, n - r0);
@@ -2251,6 +2299,26 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
         c->launches += 1;
       }
       c->launches += 1;
+      if (groups) {
+        const int64_t e1 = r0 + nbk, gcols = (int64_t)grp->gw * T;
+        if (e1 < n && e1 % gcols == 0) {
+          const int gi = (int)(e1 / gcols) - 1, I0 = gi * grp->gw, I1 = I0 + grp->gw;
+          while ((int)grp->ev->size() <= gi) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            grp->ev->push_back(e);
+          }
+          // bulk pidx done => panel pidx done => bulk pidx-1 done (pipe_wait): everything up to e1
+          cudaEventRecord(o.ev_lgrp, ps);
+          cudaStreamWaitEvent(o.s_lgrp, o.ev_lgrp, 0);
+          ldl_partial_perm_kernel<<<1, 256, (size_t)n * 8, o.s_lgrp>>>(o.swaps, n, e1 - gcols, e1, perm);
+          pack_unit_lower_rows_kernel<<<(unsigned)(grp->gw * I1), 256, 0, o.s_lgrp>>>(o.dense, ld, n, blk, I0, I1);
+          tile_inv_unit_kernel<<<grp->gw, T, T * 129 * 8, o.s_lgrp>>>(blk, inv, I0);
+          cudaEventRecord((*grp->ev)[gi], o.s_lgrp);
+          c->launches += 3;
+          grp->count = gi + 1;
+        }
+      }
       continue;
     }
     ldl_panel_kernel<<<1, LDL_PANEL_THREADS, 0, s>>>(g, r0, nbk);
@@ -2265,11 +2333,20 @@ static int ldl_factor_block(Ctx* c, const TileMap& blk, int k, cudaStream_t s, b
     cudaStreamWaitEvent(s, o.ev_lalt, 0);
   }
   }
+  // the groups handed out early keep their outputs (the panel rows may be reading them)
+  const int gdone = groups ? grp->count * grp->gw : 0;
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
                       n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,
-                                                                        o.perm_global, c->ell, c->diag);
-  pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, blk, nt);
-  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv);
+                                                                        o.perm_global, c->ell, c->diag,
+                                                                        (int64_t)gdone * T);
+  if (gdone > 0) {
+    pack_unit_lower_rows_kernel<<<(unsigned)((nt - gdone) * nt), 256, 0, s>>>(o.dense, ld, n, blk, gdone, nt);
+    tile_inv_unit_kernel<<<nt - gdone, T, T * 129 * 8, s>>>(blk, inv, gdone);
+    cudaStreamWaitEvent(s, (*grp->ev)[grp->count - 1], 0);  // the factor's end covers every group
+  } else {
+    pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, blk, nt);
+    tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv, 0);
+  }
   c->launches += 7;
   return B2D_OK;
 }
@@ -2324,11 +2401,11 @@ static int lu_factor_block(Ctx* c, const TileMap& blk, const TileMap& umap, int 
   }
   ldl_finish_kernel<<<(unsigned)std::max<int64_t>(1, (n + 255) / 256), 256,
                       n <= LDL_FINISH_SMEM_MAX ? (size_t)n * 8 : 0, s>>>(o.swaps, dblk, n, g0, perm,
-                                                                        o.perm_global, c->ell, c->diag);
+                                                                        o.perm_global, c->ell, c->diag, 0);
   const unsigned ntri = (unsigned)(nt * (nt + 1) / 2);
   pack_unit_lower_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, blk, nt);
   pack_upper_t_kernel<<<ntri, 256, 0, s>>>(o.dense, ld, n, umap, nt);
-  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv);
+  tile_inv_unit_kernel<<<nt, T, T * 129 * 8, s>>>(blk, inv, 0);
   tile_inv_lower_kernel<<<nt, T, T * 129 * 8, s>>>(umap, inv2);
   c->launches += 7;
   return B2D_OK;
@@ -2750,8 +2827,65 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   tmark("start", 0, c->s_main);
   if (skip > 0) cudaStreamWaitEvent(c->s_main, o.ev_fac, 0);
   else if ((rc = wait_cols(c->s_main, col0(0) + o.tiles(0)))) return rc;
+  const bool rows_sched = c->ldl_rows && !getenv("B2D_LDL_SCHED") &&
+                          (getenv("B2D_LDL_URGENT") ? atoi(getenv("B2D_LDL_URGENT")) != 0 : true) &&
+                          (getenv("B2D_LDL_SPLIT") ? atoi(getenv("B2D_LDL_SPLIT")) != 0 : true);
+  // one set of factor outputs per stage (row schedule), selected until this function returns
+  struct RingOff {
+    Ooc& o;
+    ~RingOff() { o.use_ring = false; }
+  } ring_off{o};
+  // B2D_LDL_GROUPS (tile-columns per group, default 4; 0 = off): the factors hand out their
+  // finished column groups early (LdlGroups) -- stage 0's panel rows and trailing updates then run
+  // beside factor 0, and every stage's chain row (block row k+1) is solved behind its factor
+  const int grp_w = rows_sched && nb > 1 ? std::max(0, env_int("B2D_LDL_GROUPS", 4)) : 0;
+  std::vector<int> grp_count((size_t)nb, 0);
+  auto factor = [&](int k, bool overlapped) -> int {
+    LdlGroups lg;
+    lg.gw = grp_w;
+    if (grp_w > 0) {
+      if ((int)c->ev_grp.size() < nb) c->ev_grp.resize((size_t)nb);
+      lg.ev = &c->ev_grp[(size_t)k];
+    }
+    const int e = ldl_factor_block(c, diag_map(k), k, c->s_main, overlapped, grp_w > 0 && k + 1 < nb ? &lg : nullptr);
+    grp_count[(size_t)k] = lg.count;
+    return e;
+  };
+  if (rows_sched && nb > 1) {
+    if ((int)o.ring_inv.size() < nb) {
+      for (int q = (int)o.ring_inv.size(); q < nb; ++q) {
+        double *iv = nullptr, *db = nullptr;
+        int64_t* pm = nullptr;
+        CUDA_TRY(cudaMalloc(&iv, (size_t)o.nbt * TILE_BYTES));
+        CUDA_TRY(cudaMalloc(&db, (size_t)o.nbt * T * 8));
+        CUDA_TRY(cudaMalloc(&pm, (size_t)o.nbt * T * 8));
+        o.ring_inv.push_back(iv);
+        o.ring_dblk.push_back(db);
+        o.ring_perm.push_back(pm);
+      }
+    }
+    o.use_ring = true;
+    if (!c->s_pr[0]) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      // distance 1-2, 3, 4, 5: priorities one below s_main's downwards (clamped to the range)
+      for (int q = 0; q < 4; ++q) {
+        const int pr = std::min(lo, hi + 1 + q);
+        CUDA_TRY(cudaStreamCreateWithPriority(&c->s_pr[q], cudaStreamNonBlocking, pr));
+      }
+    }
+    for (auto* v : {&c->ev_row, &c->ev_prow})
+      while ((int)v->size() < std::max(nb, 2)) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        v->push_back(e);
+      }
+    // row r's last update so far: none (recorded before factor 0, which the rows wait for
+    // themselves -- as a whole, or group by group)
+    for (int r = 0; r < nb; ++r) cudaEventRecord(c->ev_row[r], c->s_main);
+  }
   tmark("factor-begin", 0, c->s_main);
-  if ((rc = ldl_factor_block(c, diag_map(0), 0, c->s_main))) return rc;
+  if ((rc = factor(0, false))) return rc;
   tmark("factor-end", 0, c->s_main);
   cudaEventRecord(c->ev_catch[0], c->s_main);
   // Row-ordered schedule (c->ldl_rows, B2D_LDL_ROWS): stage k's work is issued block row by block
@@ -2765,51 +2899,8 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   // factors' outputs (L_kk^{-1} tiles, block permutation, D) get one buffer per stage, and up to
   // MAX_PAN panel grids decouple the stages' far rows from the next stages' panels.  In the
   // column schedule (below) the nearest rows' updates could queue behind whole-column work.
-  const bool rows_sched = c->ldl_rows && !getenv("B2D_LDL_SCHED") &&
-                          (getenv("B2D_LDL_URGENT") ? atoi(getenv("B2D_LDL_URGENT")) != 0 : true) &&
-                          (getenv("B2D_LDL_SPLIT") ? atoi(getenv("B2D_LDL_SPLIT")) != 0 : true);
   if (rows_sched && nb > 1) {
-    if (!c->s_pr[0]) {
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      // distance 1-2, 3, 4, 5: priorities one below s_main's downwards (clamped to the range)
-      for (int q = 0; q < 4; ++q) {
-        const int pr = std::min(lo, hi + 1 + q);
-        CUDA_TRY(cudaStreamCreateWithPriority(&c->s_pr[q], cudaStreamNonBlocking, pr));
-      }
-    }
-    if ((int)o.ring_inv.size() < nb) {
-      for (int q = (int)o.ring_inv.size(); q < nb; ++q) {
-        double *iv = nullptr, *db = nullptr;
-        int64_t* pm = nullptr;
-        CUDA_TRY(cudaMalloc(&iv, (size_t)o.nbt * TILE_BYTES));
-        CUDA_TRY(cudaMalloc(&db, (size_t)o.nbt * T * 8));
-        CUDA_TRY(cudaMalloc(&pm, (size_t)o.nbt * T * 8));
-        o.ring_inv.push_back(iv);
-        o.ring_dblk.push_back(db);
-        o.ring_perm.push_back(pm);
-      }
-    }
-    for (auto* v : {&c->ev_row, &c->ev_prow})
-      while ((int)v->size() < std::max(nb, 2)) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        v->push_back(e);
-      }
     for (auto st : c->s_pr) cudaStreamWaitEvent(st, c->ev_start, 0);
-    // factor 0 was enqueued above with the parity buffers: its outputs move to ring slot 0
-    // (enqueued on s_main after it; the ring is used from here on)
-    CUDA_TRY(cudaMemcpyAsync(o.ring_inv[0], o.inv_of(0, c->inv), (size_t)o.nbt * TILE_BYTES, cudaMemcpyDeviceToDevice,
-                             c->s_main));
-    CUDA_TRY(cudaMemcpyAsync(o.ring_dblk[0], o.dblk_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
-    CUDA_TRY(cudaMemcpyAsync(o.ring_perm[0], o.perm_of(0), (size_t)o.size(0) * 8, cudaMemcpyDeviceToDevice, c->s_main));
-    o.use_ring = true;
-    struct RingOff {  // the ring selection ends with this schedule, also on an error return
-      Ooc& o;
-      ~RingOff() { o.use_ring = false; }
-    } ring_off{o};
-    // row r's last update so far: none (every block row's first work waits for factor 0)
-    for (int r = 0; r < nb; ++r) cudaEventRecord(c->ev_row[r], c->s_main);
     auto bstart = [&](int q) { return std::min(nt, col0(q)); };
     auto bend = [&](int q) { return q + 1 < nb ? std::min(nt, col0(q + 1)) : nt; };
     // block row r at distance d = r - k: streams of falling priority, then one stream per row
@@ -2822,10 +2913,162 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const int d = r - k;
       return d <= 2 ? c->s_pr[0] : d <= 5 ? c->s_pr[d - 2] : col_stream(r);
     };
+    // Group pipeline (grp_w > 0): block rows k+1 .. rlast of stage k solved and applied column
+    // group by column group as factor k hands the groups out (group-major, so rows that share a
+    // stream interleave): per group and row the permuted columns, the left-looking update by the
+    // groups before (K = q0 T), the group's solves, the D^{-1} scaling; then the row's tiles
+    // (r, k+1 .. r) take the K-chunk of the group (far rows: every front_ue groups).  Every entry
+    // still receives its terms in increasing k through exact FP64 continuation across launches:
+    // bit-identical to the whole-panel path.  Block row k+1 ends with the next factor's launch.
+    const int front_ue = std::max(1, env_int("B2D_LDL_FRONT_UE", 4));
+    // B2D_LDL_FRONT: stage 0 groups every block row (1) or only the chain row (0).  Default 1 for
+    // device-resident input; 0 for host input -- there stage 0's far rows wait for their own
+    // columns to arrive, and on the streams they share with the chain row those waits would hold
+    // the chain's next group (C2 from pinned memory: 459 ms with, 443 ms without)
+    const bool front_all = env_int("B2D_LDL_FRONT", host ? 0 : 1) != 0;
+    if (grp_w > 0 && !c->s_grpu) {
+      int pr = 0;
+      cudaStreamGetPriority(c->s_pr[0], &pr);
+      CUDA_TRY(cudaStreamCreateWithPriority(&c->s_grpu, cudaStreamNonBlocking, pr));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_grpu, cudaEventDisableTiming));
+    }
+    if (c->s_grpu) cudaStreamWaitEvent(c->s_grpu, c->ev_start, 0);
+    while (grp_w > 0 && (int)c->ev_rowg.size() < nb) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_rowg.push_back(e);
+    }
+    auto stage_rows_grouped = [&](int k, int rlast) -> int {
+      const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb;
+      const double* inv_k = o.inv_of(k, c->inv);
+      const int np = c->npan, pb = k % np;
+      const int G = (kb + grp_w - 1) / grp_w;
+      const TileMap lkk = diag_map(k);
+      std::vector<int> pend((size_t)nb, 0);
+      GemmTask u{};
+      u.a = TileMap{c->pan[pb][1], o.nbt, 0};  // rows indexed by global tile row
+      u.b = TileMap{c->pan[pb][0], o.nbt, 0};
+      u.c = packed;
+      for (int r = k + 1; r <= rlast; ++r) {
+        cudaStream_t st = dstream(r, k);
+        if (k >= np) cudaStreamWaitEvent(st, c->ev_rest[k - np], 0);
+        if (int e = wait_cols(st, i0)) return e;
+        cudaStreamWaitEvent(st, c->ev_row[r], 0);
+        if (r == k + 1) tmark("p1-ready", k, st);
+      }
+      // solve of group [q0, qe) for block row r on st (permute, left-looking update, in-group solves)
+      auto solve_group = [&](int r, cudaStream_t st, int q0, int qe, cudaEvent_t ready) {
+        const int r0 = bstart(r), R = bend(r) - r0;
+        cudaStreamWaitEvent(st, ready, 0);
+        TileMap src = packed;
+        src.roff = r0;
+        src.coff = k0;
+        const TileMap pu{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+        permute_cols_range_kernel<<<1024, 256, 0, st>>>(src, pu, R, (int64_t)q0 * T, qe - q0, o.size(k), o.perm_of(k));
+        c->launches++;
+        if (q0 > 0) {
+          GemmTask w{};
+          w.a = pu;
+          w.b = lkk;
+          w.c = pu;
+          w.out = TileSet{0, R, q0, qe, 0, 0};
+          w.p0 = 0;
+          w.p1 = q0;
+          launch_gemm(c, st, MODE_UPDATE, w, false, 0.0);
+        }
+        for (int q = q0; q < qe; ++q) {
+          if (q > q0) {
+            GemmTask w{};
+            w.a = pu;
+            w.b = lkk;
+            w.c = pu;
+            w.out = TileSet{0, R, q, q + 1, 0, 0};
+            w.p0 = q0;
+            w.p1 = q;
+            launch_gemm(c, st, MODE_UPDATE, w, false, 0.0);
+          }
+          GemmTask t{};
+          t.c = pu;
+          t.binv = inv_k + (int64_t)q * TILE_ELEMS;
+          t.out = TileSet{0, R, q, q + 1, 0, 0};
+          t.k = q;
+          launch_gemm(c, st, MODE_TRSM, t, false, 0.0);
+        }
+        cudaEventRecord(c->ev_rowg[r], st);  // the group's unscaled columns (what other rows read)
+      };
+      // D^{-1} scaling of the group, then tiles (r, k+1 .. r) take K = [pend, qe) on st
+      auto scale_group = [&](int r, cudaStream_t st, int q0, int qe) {
+        const int r0 = bstart(r), R = bend(r) - r0;
+        TileMap su{c->pan[pb][0] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+        TileMap ss{c->pan[pb][1] + (size_t)r0 * o.nbt * TILE_ELEMS, o.nbt, 0};
+        su.base += (int64_t)q0 * TILE_ELEMS;
+        ss.base += (int64_t)q0 * TILE_ELEMS;
+        const int64_t nrem = std::max<int64_t>(0, o.size(k) - (int64_t)q0 * T);
+        scale_cols_kernel<<<1024, 256, 0, st>>>(su, ss, R, qe - q0, nrem, o.dblk_of(k) + (int64_t)q0 * T);
+        c->launches++;
+      };
+      auto update_row = [&](int r, cudaStream_t st, int qe) -> int {
+        const int r0 = bstart(r), r1 = bend(r);
+        if (pend[(size_t)r] == 0)
+          if (int e = wait_cols(st, r1)) return e;  // host input: the row's own columns are in
+        u.out = TileSet{r0, r1, i0, r1, 1, 0};
+        u.p0 = pend[(size_t)r];
+        u.p1 = qe;
+        launch_gemm(c, st, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * (double)(qe - pend[(size_t)r]) * T);
+        pend[(size_t)r] = qe;
+        return B2D_OK;
+      };
+      const int rc1 = k + 1;  // the chain row: its scaling and diagonal update on a side stream
+      cudaStream_t sc1 = dstream(rc1, k);
+      for (int g = 0; g < G; ++g) {
+        const int q0 = g * grp_w, qe = std::min(kb, q0 + grp_w);
+        cudaEvent_t ready = g < grp_count[(size_t)k] ? c->ev_grp[(size_t)k][(size_t)g] : c->ev_catch[k];
+        const bool last = g == G - 1;
+        solve_group(rc1, sc1, q0, qe, ready);
+        cudaStreamWaitEvent(c->s_grpu, c->ev_rowg[rc1], 0);
+        scale_group(rc1, c->s_grpu, q0, qe);
+        if (int e = update_row(rc1, c->s_grpu, qe)) return e;
+        if (last) {
+          cudaEventRecord(c->ev_grpu, c->s_grpu);
+          cudaStreamWaitEvent(sc1, c->ev_grpu, 0);
+          cudaEventRecord(c->ev_prow[rc1], sc1);
+          cudaEventRecord(c->ev_row[rc1], sc1);
+          tmark("next-col-end", k, sc1);
+          cudaEventRecord(o.ev_diag, sc1);
+          cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
+          tmark("factor-begin", k + 1, c->s_main);
+          if (int e = factor(k + 1, k + 2 < nb)) return e;
+          tmark("factor-end", k + 1, c->s_main);
+          cudaEventRecord(c->ev_catch[k + 1], c->s_main);
+        }
+        for (int r = k + 2; r <= rlast; ++r) {
+          cudaStream_t st = dstream(r, k);
+          solve_group(r, st, q0, qe, ready);
+          scale_group(r, st, q0, qe);
+        }
+        for (int r = k + 2; r <= rlast; ++r) {
+          const int ue = r - k <= 2 ? 1 : front_ue;
+          if (!last && (g + 1) % ue != 0) continue;
+          cudaStream_t st = dstream(r, k);
+          for (int q = k + 1; q < r; ++q)
+            if (dstream(q, k) != st) cudaStreamWaitEvent(st, c->ev_rowg[q], 0);
+          if (int e = update_row(r, st, qe)) return e;
+          if (!last) continue;
+          cudaEventRecord(c->ev_prow[r], st);
+          cudaEventRecord(c->ev_row[r], st);
+          if (r == k + 2) tmark("urgent-end", k, st);
+        }
+      }
+      return B2D_OK;
+    };
     for (int k = 0; k + 1 < nb; ++k) {
       const int k0 = col0(k), kb = o.tiles(k), i0 = k0 + kb;
       const double* inv_k = o.inv_of(k, c->inv);
       const int np = c->npan, pb = k % np;  // panel grids: stage k waits for the readers of stage k-np
+      // grouped rows: all of stage 0's (nothing else runs beside factor 0), the chain row after
+      const int rgrp = grp_w > 0 ? (k == 0 && front_all ? nb - 1 : k + 1) : k;
+      if (rgrp > k)
+        if ((rc = stage_rows_grouped(k, rgrp))) return rc;
       auto panel_rows = [&](cudaStream_t st, int r0, int r1, int wg) {  // global tile rows [r0, r1)
         TileMap src = packed;
         src.roff = r0;
@@ -2844,7 +3087,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       u.p0 = 0;
       u.p1 = kb;
       const double K = (double)kb * T;
-      for (int r = k + 1; r < nb; ++r) {
+      for (int r = rgrp + 1; r < nb; ++r) {
         const int r0 = bstart(r), r1 = bend(r);
         cudaStream_t st = dstream(r, k);
         // the stage's factor, free panel grids, row r's previous update
@@ -2882,11 +3125,11 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
           cudaEventRecord(o.ev_diag, st);
           cudaStreamWaitEvent(c->s_main, o.ev_diag, 0);
           tmark("factor-begin", k + 1, c->s_main);
-          if ((rc = ldl_factor_block(c, diag_map(k + 1), k + 1, c->s_main, k + 2 < nb))) return rc;
+          if ((rc = factor(k + 1, k + 2 < nb))) return rc;
           tmark("factor-end", k + 1, c->s_main);
           cudaEventRecord(c->ev_catch[k + 1], c->s_main);
         } else {
-          launch_update_kchunked(c, st, u, 16);
+          launch_update_kchunked(c, st, u, 32);
           cudaEventRecord(c->ev_row[r], st);
           if (r == k + 2) tmark("urgent-end", k, st);
         }
@@ -2992,7 +3235,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         col_sync(k + 2, c->s_mid);
         if ((rc = wait_cols(c->s_mid, i2))) return rc;
         u.out = TileSet{i0 + kb1, i2, i0 + kb1, i2, 1, 0};
-        launch_update_kchunked(c, c->s_mid, u, 16);
+        launch_update_kchunked(c, c->s_mid, u, 32);
       }
       tmark("urgent-end", k, c->s_mid);
       for (int q = k + 2, j0 = i0 + kb1; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
@@ -3002,12 +3245,11 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         if ((rc = wait_cols(cs, j1))) return rc;
         // block column k+2: its rows below the diagonal block (the diagonal block went above)
         u.out = q == k + 2 ? TileSet{j1, nt, j0, j1, 0, 0} : TileSet{j0, nt, j0, j1, 1, 0};
-        if (u.out.count() > 0) launch_update_kchunked(c, cs, u, 16);
+        if (u.out.count() > 0) launch_update_kchunked(c, cs, u, 32);
       }
       // join stage k's readers of its panel buffers on s_side (ev_rest[k]: panel k+3 reuses them)
       for (int q = k + 2; q < nb; ++q) col_sync(q, c->s_side);
     } else if (i0 + kb1 < nt) {
-      // after the whole panel (issued after the next factor, which takes its SMs first)    } else if (i0 + kb1 < nt) {
       // after the whole panel (issued after the next factor, which takes its SMs first)
       cudaStreamWaitEvent(c->s_side, c->ev_panel[k], 0);
       if (serial) cudaStreamWaitEvent(c->s_side, c->ev_catch[k + 1], 0);
@@ -3019,18 +3261,18 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const bool by_cols = host && k == 0;
       if ((rc = wait_cols(c->s_side, by_cols ? i2 : nt))) return rc;
       u.out = TileSet{i0 + kb1, nt, i0 + kb1, i2, 1, 0};
-      launch_update_kchunked(c, c->s_side, u, 16);
+      launch_update_kchunked(c, c->s_side, u, 32);
       cudaEventRecord(c->ev_resta[k], c->s_side);
       if (by_cols) {
         for (int q = k + 3, j0 = i2; q < nb && j0 < nt; j0 += o.tiles(q), ++q) {
           const int j1 = std::min(nt, j0 + o.tiles(q));
           if ((rc = wait_cols(c->s_side, j1))) return rc;
           u.out = TileSet{j0, nt, j0, j1, 1, 0};
-          launch_update_kchunked(c, c->s_side, u, 16);
+          launch_update_kchunked(c, c->s_side, u, 32);
         }
       } else if (i2 < nt) {
         u.out = TileSet{i2, nt, i2, nt, 1, 0};
-        launch_update_kchunked(c, c->s_side, u, 16);
+        launch_update_kchunked(c, c->s_side, u, 32);
       }
     } else {
       cudaEventRecord(c->ev_resta[k], c->s_side);

@@ -1007,7 +1007,9 @@ __global__ void __launch_bounds__(LC_THREADS, 1) ldl_panel_server_kernel(LdlArgs
 constexpr int64_t LDL_FINISH_SMEM_MAX = 24576;
 __global__ void ldl_finish_kernel(const int64_t* __restrict__ swaps, const double* __restrict__ d, int64_t n,
                                   int64_t g0, int64_t* __restrict__ perm_local, int64_t* __restrict__ perm_global,
-                                  double* __restrict__ ell, double* __restrict__ dout) {
+                                  double* __restrict__ ell, double* __restrict__ dout, int64_t perm_lo) {
+  // perm_lo: block-permutation entries below it were already written by ldl_partial_perm_kernel
+  // (group pipeline; shared-memory walk only) and may be in use: not rewritten
   extern __shared__ int64_t sperm[];
   if (blockIdx.x == 0) {
     const bool sm = n <= LDL_FINISH_SMEM_MAX;
@@ -1030,13 +1032,53 @@ __global__ void ldl_finish_kernel(const int64_t* __restrict__ swaps, const doubl
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      if (sm) perm_local[i] = pl[i];
+      if (sm && i >= perm_lo) perm_local[i] = pl[i];
       perm_global[g0 + i] = g0 + pl[i];
     }
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     ell[g0 + i] = log(fabs(d[i]));
     dout[g0 + i] = d[i];
+  }
+}
+
+// Group pipeline (engine.cu ldl_factor_block, B2D_LDL_GROUPS): entries [e0, e1) of the block
+// permutation once steps [0, e1) are done -- step r interchanges positions r and t > r, so
+// positions below e1 never change again (kernels/dense.py:25-30 applied to a prefix of the swaps).
+__global__ void ldl_partial_perm_kernel(const int64_t* __restrict__ swaps, int64_t n, int64_t e0, int64_t e1,
+                                        int64_t* __restrict__ perm_local) {
+  extern __shared__ int64_t sperm[];  // n entries (n <= LDL_FINISH_SMEM_MAX)
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sperm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int64_t r = 0; r < e1; ++r) {
+      const int64_t t = __ldcg(swaps + r);
+      if (t > r && t < n) {
+        const int64_t x = sperm[r];
+        sperm[r] = sperm[t];
+        sperm[t] = x;
+      }
+    }
+  __syncthreads();
+  for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) perm_local[i] = sperm[i];
+}
+
+// Tile rows [I0, I0 + gridDim.x / ncol) of the dense unit-lower factor -> tile grid, tile columns
+// J <= I (the rows of a finished column group: final once its last panel's interchanges are in).
+__global__ void __launch_bounds__(256) pack_unit_lower_rows_kernel(const double* __restrict__ dense, int64_t ld,
+                                                                   int64_t n, TileMap dst, int I0, int ncol) {
+  const int I = I0 + (int)(blockIdx.x / (unsigned)ncol), J = (int)(blockIdx.x % (unsigned)ncol);
+  if (J > I) return;
+  double* t = dst.tile(I, J);
+  for (int o = threadIdx.x; o < TILE_ELEMS; o += 256) {
+    const int r = (o >> 3) & 127;
+    const int c = ((o >> 10) << 3) + iperm8(o & 7);
+    const int64_t R = (int64_t)I * T + r, C = (int64_t)J * T + c;
+    double v;
+    if (R == C) v = 1.0;
+    else if (R > C && R < n) v = __ldcg(dense + C * ld + R);
+    else v = 0.0;
+    t[o] = v;
   }
 }
 
@@ -1061,11 +1103,12 @@ __global__ void __launch_bounds__(256) pack_unit_lower_kernel(const double* __re
 
 // X = L^{-1} of a unit-lower 128 x 128 tile: one thread per column, forward substitution in
 // 8-row blocks; X[r][c] (r > c) kept transposed in the upper triangle of the staging array.
-// One CTA per diagonal tile q of `map` (blockIdx.x = q): inv + q * TILE_ELEMS = L_qq^{-1}.
-__global__ void __launch_bounds__(128) tile_inv_unit_kernel(TileMap map, double* __restrict__ inv_base) {
+// One CTA per diagonal tile q = q0 + blockIdx.x of `map`: inv + q * TILE_ELEMS = L_qq^{-1}.
+__global__ void __launch_bounds__(128) tile_inv_unit_kernel(TileMap map, double* __restrict__ inv_base, int q0) {
   extern __shared__ double M[];  // [T][129]
-  const double* __restrict__ tile = map.tile(blockIdx.x, blockIdx.x);
-  double* __restrict__ inv = inv_base + (int64_t)blockIdx.x * TILE_ELEMS;
+  const int q = q0 + (int)blockIdx.x;
+  const double* __restrict__ tile = map.tile(q, q);
+  double* __restrict__ inv = inv_base + (int64_t)q * TILE_ELEMS;
   const int c = threadIdx.x;
   for (int o = c; o < TILE_ELEMS; o += T) {
     const int r = (o >> 3) & 127;
@@ -1094,6 +1137,19 @@ __global__ void permute_cols_kernel(TileMap src, TileMap dst, int rtiles, int ct
   const int64_t rows = (int64_t)rtiles * T, cols = (int64_t)ctiles * T;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / rows, i = e % rows;
+    const int64_t sc = c < n ? perm[c] : c;
+    const double v = src.tile((int)(i / T), (int)(sc / T))[elem((int)(i % T), (int)(sc % T))];
+    dst.tile((int)(i / T), (int)(c / T))[elem((int)(i % T), (int)(c % T))] = v;
+  }
+}
+
+// The same for panel columns [c0, c0 + ctiles T) only (group pipeline: the permutation's entries
+// of a finished column group are final before the factor ends); dst, perm and n are the whole panel's.
+__global__ void permute_cols_range_kernel(TileMap src, TileMap dst, int rtiles, int64_t c0, int ctiles, int64_t n,
+                                          const int64_t* __restrict__ perm) {
+  const int64_t rows = (int64_t)rtiles * T, cols = (int64_t)ctiles * T;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = c0 + e / rows, i = e % rows;
     const int64_t sc = c < n ? perm[c] : c;
     const double v = src.tile((int)(i / T), (int)(sc / T))[elem((int)(i % T), (int)(sc % T))];
     dst.tile((int)(i / T), (int)(c / T))[elem((int)(i % T), (int)(c % T))] = v;

@@ -417,6 +417,35 @@ def test_pivoted_ldl_lookahead_solve_equals_block_walk(m, nb, la, sched, monkeyp
     eng.release_engine_cache()
 
 
+@pytest.mark.parametrize("m,nb", [(2048, 2), (2560, 2), (3072, 3), (2560, 4), (3840, 5)])
+@pytest.mark.parametrize("groups,front,ue", [("0", "1", "2"), ("1", "1", "1"), ("2", "1", "2"), ("4", "1", "2"),
+                                             ("4", "0", "2"), ("3", "1", "3")])
+def test_pivoted_ldl_group_pipeline_equals_block_walk(m, nb, groups, front, ue, monkeypatch):
+    """B2D_LDL_GROUPS: the factors hand out their finished column groups (L tile rows, tile
+    inverses, permutation entries) while they run; stage 0's block rows (B2D_LDL_FRONT) and every
+    stage's chain row solve and apply them group by group (far rows every B2D_LDL_FRONT_UE
+    groups).  Every entry still receives its terms in increasing k, so perm, D and the prefixes
+    equal the block walk's (and the whole-panel schedule's, groups = 0) bit for bit."""
+    monkeypatch.setenv("B2D_LDL_GROUPS", groups)
+    monkeypatch.setenv("B2D_LDL_FRONT", front)
+    monkeypatch.setenv("B2D_LDL_FRONT_UE", ue)
+    eng.release_engine_cache()
+    a = gen.random_symmetric(m, seed=3 * m + nb)
+    res = eng.memdet_ldl(a, num_blocks=nb)
+    again = eng.memdet_ldl(a, num_blocks=nb)  # event / buffer reuse across runs of one context
+    walk = eng.memdet_ldl(a, num_blocks=nb, out_of_core=True)
+    assert not res.info.out_of_core and walk.info.out_of_core
+    for r in (res, again):
+        np.testing.assert_array_equal(r.perm, walk.perm)
+        np.testing.assert_array_equal(r.prefix_signs, walk.prefix_signs)
+        assert np.array_equal(r.prefix.view(np.int64), walk.prefix.view(np.int64)), \
+            np.max(np.abs(r.prefix - walk.prefix))
+    ref_perm, ref_prefix, _, _ = O.memdet_ldl(a, nb)
+    np.testing.assert_array_equal(res.perm, ref_perm)
+    assert rel_err(res.prefix, ref_prefix) <= 1e-10
+    eng.release_engine_cache()
+
+
 @pytest.mark.parametrize("m,nb", [(1022, 4), (768, 3)])
 def test_in_core_f32_inputs_equal_block_walk(m, nb, monkeypatch):
     """float32 inputs converted to FP64 on the device (B2D_F32_ARITH=0 for the LDL; the default

@@ -1,5 +1,6 @@
-"""C2 memdet_cholesky end to end from pinned host memory: median of 3 (after one warm call);
-env switches apply per process (tools/e2e_trace.py has the per-step trace)."""
+"""C2 memdet_cholesky (or memdet_ldl with FN=ldl) end to end from pinned host memory: median of 3
+(after one warm call); env switches apply per process (tools/e2e_trace.py has the per-step trace).
+   [FN=ldl] [NB=8] python tools/e2e_time.py [n]"""
 import ctypes, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -15,11 +16,13 @@ h.copy_(a)
 del a
 torch.cuda.empty_cache()
 hn = h.numpy()
-eng.memdet_cholesky(hn, num_blocks=8)
+fn = eng.memdet_ldl if os.environ.get("FN", "cholesky") == "ldl" else eng.memdet_cholesky
+nb = int(os.environ.get("NB", "8"))
+fn(hn, num_blocks=nb)
 ts = []
 for _ in range(3):
     t0 = time.perf_counter()
-    r = eng.memdet_cholesky(hn, num_blocks=8)
+    r = fn(hn, num_blocks=nb)
     ts.append(time.perf_counter() - t0)
 dt = float(np.median(ts))
 print(f"{os.environ.get('TAG', '')} e2e {dt*1e3:.1f} ms ({n**3/3/dt/1e12:.2f} TF/s) device_ms {r.info.device_ms:.1f}", flush=True)
