@@ -3066,7 +3066,8 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
       const double* inv_k = o.inv_of(k, c->inv);
       const int np = c->npan, pb = k % np;  // panel grids: stage k waits for the readers of stage k-np
       // grouped rows: all of stage 0's (nothing else runs beside factor 0), the chain row after
-      const int rgrp = grp_w > 0 ? (k == 0 && front_all ? nb - 1 : k + 1) : k;
+      // (a factor that handed nothing out early -- a big block, a single group -- keeps the whole-panel path)
+      const int rgrp = grp_w > 0 && grp_count[(size_t)k] > 0 ? (k == 0 && front_all ? nb - 1 : k + 1) : k;
       if (rgrp > k)
         if ((rc = stage_rows_grouped(k, rgrp))) return rc;
       auto panel_rows = [&](cudaStream_t st, int r0, int r1, int wg) {  // global tile rows [r0, r1)
