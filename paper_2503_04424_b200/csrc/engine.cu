@@ -357,6 +357,8 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_la;
   std::vector<std::vector<cudaEvent_t>> ev_grp;  // group pipeline: [stage][group] early factor outputs
   std::vector<cudaEvent_t> ev_rowg;  // group pipeline: block row r's latest solved group
+  cudaStream_t s_catch[2] = {nullptr, nullptr};  // host ingest: eager catch-ups of bands not yet active (by step parity)
+  std::vector<cudaEvent_t> ev_caught;            // band b's latest eager catch-up
   cudaStream_t s_grpu = nullptr;     // group pipeline: the chain row's scaling + diagonal update
   cudaEvent_t ev_grpu = nullptr;
   // float32 memdet_ldl in f32 arithmetic (ldl32.cu): the matrix row-major in M, the diagonal
@@ -494,6 +496,12 @@ static void destroy(Ctx* c) {
   for (auto& v : c->ev_grp)
     for (auto e : v) cudaEventDestroy(e);
   for (auto e : c->ev_rowg) cudaEventDestroy(e);
+  for (auto& q : c->s_catch)
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
+  for (auto e : c->ev_caught) cudaEventDestroy(e);
   if (c->s_grpu) {
     cudaStreamSynchronize(c->s_grpu);
     cudaStreamDestroy(c->s_grpu);
@@ -1269,6 +1277,27 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
     for (int b = 0; b < nbands; ++b)
       if (c->act[b] < 0) cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
   }
+  // B2D_EAGER_CATCH (default 1; pinned host input, whose strips are all enqueued up front): a
+  // band that joins at step s takes the panels of steps t < s one by one, each as soon as that
+  // panel is solved and the band has arrived (low-priority streams by step parity, a band's
+  // pieces ordered by its event), instead of one K = 128 k0 catch-up when it joins -- the pieces
+  // fill the SMs while the first panels' chains run with few bands active.  Same k order with
+  // exact FP64 continuation across launches: bit-identical.
+  const bool eager = wait_bands && c->ing.active && c->ing.next >= nt && c->profiling != 2 &&
+                     env_int("B2D_EAGER_CATCH", 1) != 0;
+  if (eager) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (auto& q : c->s_catch) {
+      if (!q) cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, lo);
+      cudaStreamWaitEvent(q, c->ev_join, 0);
+    }
+    while ((int)c->ev_caught.size() < nbands) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      c->ev_caught.push_back(e);
+    }
+  }
   int main_waited = 0;  // initial bands s_main has waited for (waited lazily, per panel)
   // B2D_LEFT_BELOW (default 1): the rows below each panel are updated left-looking per column
   const char* lbe = getenv("B2D_LEFT_BELOW");
@@ -1322,6 +1351,19 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
     }
     cudaEventRecord(c->ev_panel[st], c->s_mid);
     if (ke >= nt) break;
+    if (eager) {
+      cudaStream_t cs = c->s_catch[st & 1];
+      bool first = true;
+      for (int b = 0; b < nbands; ++b) {
+        if (c->act[b] <= st) continue;  // active, or joining at this step
+        if (first) cudaStreamWaitEvent(cs, c->ev_panel[st], 0);
+        first = false;
+        cudaStreamWaitEvent(cs, c->ev_band[b], 0);
+        if (st > 0) cudaStreamWaitEvent(cs, c->ev_caught[b], 0);  // its piece of step st - 1 (other stream)
+        launch_update(c, cs, ft, b * BAND, std::min(nt, (b + 1) * BAND), k0, ke, false);
+        cudaEventRecord(c->ev_caught[b], cs);
+      }
+    }
     const int ne = c->bounds[st + 2 <= nsteps ? st + 2 : nsteps];
     // catch-up of the bands that join at this step (panels of steps < st, already factored).
     // Bands the next-cols update reads (deadline st) go before ev_catch; the others after it,
@@ -1335,6 +1377,10 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
         if (pass == 1) cudaEventRecord(c->ev_catch[st], c->s_side);
         for (int b = 0; b < nbands; ++b) {
           if (c->act[b] != st || (band_deadline(c, b * BAND) <= st) != (pass == 0)) continue;
+          if (eager && st > 0) {  // panels of steps < st applied piece by piece as they were solved
+            cudaStreamWaitEvent(c->s_side, c->ev_caught[b], 0);
+            continue;
+          }
           cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
           launch_update(c, c->s_side, ft, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
         }
@@ -1363,6 +1409,11 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
   }
   if (step_hook) (*step_hook)(INT_MAX);
   // join the side streams
+  if (eager)
+    for (auto q : c->s_catch) {
+      cudaEventRecord(c->ev_join, q);
+      cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
+    }
   cudaEventRecord(c->ev_join, c->s_side);
   cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
   cudaEventRecord(c->ev_join, c->s_mid);

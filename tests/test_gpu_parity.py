@@ -757,6 +757,35 @@ def test_memdet01_file_input_staged_equals_pinned(tmp_path, dtype, monkeypatch):
         assert np.array_equal(staged.view(np.uint8), driver.view(np.uint8)), name
 
 
+@pytest.mark.parametrize("m", [8192, 6016])
+@pytest.mark.parametrize("gbs", ["0.5", "4", "50"])
+def test_pinned_input_eager_band_catch_up_is_bit_identical(m, gbs, monkeypatch):
+    """B2D_EAGER_CATCH (pinned host input): a band that joins the right-looking updates at step s
+    takes the panels of steps < s one by one as they are solved (low-priority streams) instead
+    of one catch-up GEMM when it joins.  Same k order, exact FP64 continuation: every prefix must
+    equal the one-catch-up schedule's and the device-resident path's bit for bit.  A slow modelled
+    PCIe rate (B2D_PCIE_GBS) makes the band plan join bands late, so pieces are really issued."""
+    torch = pytest.importorskip("torch")
+    a = gen.spd_wishart(m, m, seed=11, shift=1e-2)
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    t.numpy()[:] = a
+    monkeypatch.setenv("B2D_PCIE_GBS", gbs)
+    out = {}
+    for eager in ("1", "0"):
+        monkeypatch.setenv("B2D_EAGER_CATCH", eager)
+        eng.release_engine_cache()
+        first = eng.memdet_cholesky(t.numpy(), num_blocks=4).prefix
+        again = eng.memdet_cholesky(t.numpy(), num_blocks=4).prefix  # events / streams reused
+        assert np.array_equal(first.view(np.int64), again.view(np.int64))
+        out[eager] = first
+    dev = eng.memdet_cholesky(t.cuda(), num_blocks=4).prefix
+    eng.release_engine_cache()
+    assert np.array_equal(out["1"].view(np.int64), out["0"].view(np.int64)), np.max(np.abs(out["1"] - out["0"]))
+    assert np.array_equal(out["1"].view(np.int64), dev.view(np.int64)), np.max(np.abs(out["1"] - dev))
+    ref, _ = O.memdet_cholesky(a, 4)
+    assert rel_err(out["1"], ref) <= 1e-10
+
+
 def test_pivoted_ldl_out_of_core_keeps_reference_blocks():
     """The out-of-core planner may refine the block grid for Cholesky (results do not depend on
     it), never for the block-pivoted LDL, whose pivots are searched inside the reference's
