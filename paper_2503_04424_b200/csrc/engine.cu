@@ -2977,6 +2977,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     // columns to arrive, and on the streams they share with the chain row those waits would hold
     // the chain's next group (C2 from pinned memory: 459 ms with, 443 ms without)
     const bool front_all = env_int("B2D_LDL_FRONT", host ? 0 : 1) != 0;
+    const bool host_cols = env_int("B2D_LDL_HOST_COLS", 1) != 0;
     if (grp_w > 0 && !c->s_grpu) {
       int pr = 0;
       cudaStreamGetPriority(c->s_pr[0], &pr);
@@ -3169,7 +3170,12 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
         // tiles (r, k+1 .. r): the panel rows of every block up to r
         for (int q = k + 1; q < r; ++q)
           if (dstream(q, k) != st) cudaStreamWaitEvent(st, c->ev_prow[q], 0);
-        if ((rc = wait_cols(st, r1))) return rc;
+        // B2D_LDL_HOST_COLS (default 1): stage 0 from host memory -- a far row's tiles go block
+        // column by block column, each as soon as that column's strips are in, instead of the
+        // whole row after its last column (disjoint tiles, same operands and K: bit-identical)
+        const bool by_cols = host && k == 0 && r > k + 1 && host_cols;
+        if (!by_cols)
+          if ((rc = wait_cols(st, r1))) return rc;
         if (r == k + 1) {
           if (!la) launch_gemm(c, st, MODE_UPDATE, u, true, (double)u.out.count() * 2.0 * T * T * K);
           cudaEventRecord(c->ev_row[r], st);
@@ -3181,7 +3187,15 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
           tmark("factor-end", k + 1, c->s_main);
           cudaEventRecord(c->ev_catch[k + 1], c->s_main);
         } else {
-          launch_update_kchunked(c, st, u, 32);
+          if (by_cols) {
+            for (int q = k + 1; q <= r; ++q) {
+              if ((rc = wait_cols(st, bend(q)))) return rc;
+              GemmTask uq = u;
+              uq.out = TileSet{r0, r1, bstart(q), bend(q), 1, 0};
+              launch_update_kchunked(c, st, uq, 32);
+            }
+          } else
+            launch_update_kchunked(c, st, u, 32);
           cudaEventRecord(c->ev_row[r], st);
           if (r == k + 2) tmark("urgent-end", k, st);
         }
