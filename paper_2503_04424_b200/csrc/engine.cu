@@ -1283,8 +1283,11 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
   // pieces ordered by its event), instead of one K = 128 k0 catch-up when it joins -- the pieces
   // fill the SMs while the first panels' chains run with few bands active.  Same k order with
   // exact FP64 continuation across launches: bit-identical.
-  const bool eager = wait_bands && c->ing.active && c->ing.next >= nt && c->profiling != 2 &&
-                     env_int("B2D_EAGER_CATCH", 1) != 0;
+  // Pageable inputs enqueue their strips band by band (the step hook), so a band takes its first
+  // piece once it is enqueued (its event is then this run's): K = every panel solved so far.
+  const bool eager = wait_bands && c->ing.active && c->profiling != 2 &&
+                     env_int("B2D_EAGER_CATCH", 1) != 0 && (c->ing.next >= nt || env_int("B2D_EAGER_PAGEABLE", 1) != 0);
+  std::vector<int> caught((size_t)nbands, 0);  // K tile-columns [0, caught[b]) already applied to band b
   if (eager) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1356,11 +1359,13 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
       bool first = true;
       for (int b = 0; b < nbands; ++b) {
         if (c->act[b] <= st) continue;  // active, or joining at this step
+        if (std::min(nt, (b + 1) * BAND) > c->ing.next) continue;  // strips not enqueued yet
         if (first) cudaStreamWaitEvent(cs, c->ev_panel[st], 0);
         first = false;
         cudaStreamWaitEvent(cs, c->ev_band[b], 0);
-        if (st > 0) cudaStreamWaitEvent(cs, c->ev_caught[b], 0);  // its piece of step st - 1 (other stream)
-        launch_update(c, cs, ft, b * BAND, std::min(nt, (b + 1) * BAND), k0, ke, false);
+        if (caught[(size_t)b] > 0) cudaStreamWaitEvent(cs, c->ev_caught[b], 0);  // its previous piece (other stream)
+        launch_update(c, cs, ft, b * BAND, std::min(nt, (b + 1) * BAND), caught[(size_t)b], ke, false);
+        caught[(size_t)b] = ke;
         cudaEventRecord(c->ev_caught[b], cs);
       }
     }
@@ -1377,12 +1382,11 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
         if (pass == 1) cudaEventRecord(c->ev_catch[st], c->s_side);
         for (int b = 0; b < nbands; ++b) {
           if (c->act[b] != st || (band_deadline(c, b * BAND) <= st) != (pass == 0)) continue;
-          if (eager && st > 0) {  // panels of steps < st applied piece by piece as they were solved
-            cudaStreamWaitEvent(c->s_side, c->ev_caught[b], 0);
-            continue;
-          }
+          // panels already applied piece by piece as they were solved: wait for the last piece
+          if (caught[(size_t)b] > 0) cudaStreamWaitEvent(c->s_side, c->ev_caught[b], 0);
+          if (caught[(size_t)b] >= k0 && st > 0) continue;
           cudaStreamWaitEvent(c->s_side, c->ev_band[b], 0);
-          launch_update(c, c->s_side, ft, b * BAND, std::min(nt, (b + 1) * BAND), 0, k0, false);
+          launch_update(c, c->s_side, ft, b * BAND, std::min(nt, (b + 1) * BAND), caught[(size_t)b], k0, false);
         }
       }
     } else {

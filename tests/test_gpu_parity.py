@@ -770,18 +770,23 @@ def test_pinned_input_eager_band_catch_up_is_bit_identical(m, gbs, monkeypatch):
     t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
     t.numpy()[:] = a
     monkeypatch.setenv("B2D_PCIE_GBS", gbs)
+    monkeypatch.setenv("B2D_STAGE_GBS", gbs)
     out = {}
-    for eager in ("1", "0"):
-        monkeypatch.setenv("B2D_EAGER_CATCH", eager)
-        eng.release_engine_cache()
-        first = eng.memdet_cholesky(t.numpy(), num_blocks=4).prefix
-        again = eng.memdet_cholesky(t.numpy(), num_blocks=4).prefix  # events / streams reused
-        assert np.array_equal(first.view(np.int64), again.view(np.int64))
-        out[eager] = first
+    # pinned: every strip enqueued up front, one piece per solved panel; pageable (a plain ndarray,
+    # staged): strips enqueued band by band, a band's first piece covers the panels solved so far
+    for kind, inp in (("pinned", t.numpy()), ("pageable", a)):
+        for eager in ("1", "0"):
+            monkeypatch.setenv("B2D_EAGER_CATCH", eager)
+            eng.release_engine_cache()
+            first = eng.memdet_cholesky(inp, num_blocks=4).prefix
+            again = eng.memdet_cholesky(inp, num_blocks=4).prefix  # events / streams reused
+            assert np.array_equal(first.view(np.int64), again.view(np.int64)), (kind, eager)
+            out[kind, eager] = first
     dev = eng.memdet_cholesky(t.cuda(), num_blocks=4).prefix
     eng.release_engine_cache()
-    assert np.array_equal(out["1"].view(np.int64), out["0"].view(np.int64)), np.max(np.abs(out["1"] - out["0"]))
-    assert np.array_equal(out["1"].view(np.int64), dev.view(np.int64)), np.max(np.abs(out["1"] - dev))
+    for key, val in out.items():
+        assert np.array_equal(val.view(np.int64), dev.view(np.int64)), (key, np.max(np.abs(val - dev)))
+    out = {"1": out["pinned", "1"]}
     ref, _ = O.memdet_cholesky(a, 4)
     assert rel_err(out["1"], ref) <= 1e-10
 
