@@ -2923,7 +2923,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     if (!c->s_pr[0]) {
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      // distance 1-2, 3, 4, 5: priorities one below s_main's downwards (clamped to the range)
+      // four row levels: priorities one below s_main's downwards (clamped to the range)
       for (int q = 0; q < 4; ++q) {
         const int pr = std::min(lo, hi + 1 + q);
         CUDA_TRY(cudaStreamCreateWithPriority(&c->s_pr[q], cudaStreamNonBlocking, pr));
@@ -2946,7 +2946,7 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
   // Row-ordered schedule (c->ldl_rows, B2D_LDL_ROWS): stage k's work is issued block row by block
   // row r = k+1 .. nb-1 -- the panel rows of block r (permuted, solved, D^{-1}-scaled), then the
   // tiles (r, k+1 .. r) -- each row on a stream whose priority falls with its distance d = r - k
-  // from the stage (d <= 2, 3, 4, 5: s_pr[0..3]; farther rows one low-priority stream per row):
+  // from the stage (d = 1, 2, 3, 4: s_pr[0..3]; farther rows one low-priority stream per row):
   // the factor of block r needs block row r complete, so the rows are needed in that order.  A
   // row's work is ordered across stages by its event (ev_row), a row's update waits for the panel
   // rows of the blocks before it (ev_prow); every tile receives its stages' updates in order with
@@ -2964,8 +2964,13 @@ static int run_ldl_incore(Ctx* c, const void* a, int64_t lda, int dtype, bool ho
     // B2D_LDL_LA: group width of the look-ahead solve of block row k+1 (0 = trsm_panel); 4
     // measured best (C2 432.6 -> 431.0 ms, C3 2837 -> 2831 ms; 2 and 8 no better)
     const int la_w = env_int("B2D_LDL_LA", 4);
+    // B2D_LDL_PRMAP: 1 (default) = one priority level per distance 1 .. 4, farther rows on their
+    // low-priority row streams; 0 = distances 1-2 share the first level (3, 4, 5 the next ones).
+    // C2 419.9 -> 417.0 ms, C3 neutral; two coarser maps measured slower (421 ms)
+    const int prmap = env_int("B2D_LDL_PRMAP", 1);
     auto dstream = [&](int r, int k) {
       const int d = r - k;
+      if (prmap == 1) return d <= 4 ? c->s_pr[d - 1] : col_stream(r);
       return d <= 2 ? c->s_pr[0] : d <= 5 ? c->s_pr[d - 2] : col_stream(r);
     };
     // Group pipeline (grp_w > 0): block rows k+1 .. rlast of stage k solved and applied column
