@@ -357,7 +357,8 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_la;
   std::vector<std::vector<cudaEvent_t>> ev_grp;  // group pipeline: [stage][group] early factor outputs
   std::vector<cudaEvent_t> ev_rowg;  // group pipeline: block row r's latest solved group
-  cudaStream_t s_catch[2] = {nullptr, nullptr};  // host ingest: eager catch-ups of bands not yet active (by step parity)
+  static constexpr int NCATCH = 8;
+  cudaStream_t s_catch[NCATCH] = {};  // host ingest: eager catch-ups of bands not yet active (one stream per step, mod NCATCH)
   std::vector<cudaEvent_t> ev_caught;            // band b's latest eager catch-up
   cudaStream_t s_grpu = nullptr;     // group pipeline: the chain row's scaling + diagonal update
   cudaEvent_t ev_grpu = nullptr;
@@ -1279,7 +1280,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
   }
   // B2D_EAGER_CATCH (default 1; pinned host input, whose strips are all enqueued up front): a
   // band that joins at step s takes the panels of steps t < s one by one, each as soon as that
-  // panel is solved and the band has arrived (low-priority streams by step parity, a band's
+  // panel is solved and the band has arrived (low-priority streams, one per step; a band's
   // pieces ordered by its event), instead of one K = 128 k0 catch-up when it joins -- the pieces
   // fill the SMs while the first panels' chains run with few bands active.  Same k order with
   // exact FP64 continuation across launches: bit-identical.
@@ -1288,12 +1289,18 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
   const bool eager = wait_bands && c->ing.active && c->profiling != 2 &&
                      env_int("B2D_EAGER_CATCH", 1) != 0 && (c->ing.next >= nt || env_int("B2D_EAGER_PAGEABLE", 1) != 0);
   std::vector<int> caught((size_t)nbands, 0);  // K tile-columns [0, caught[b]) already applied to band b
+  // one stream per step that issues pieces (a step's queue ends with the last band to arrive, so a
+  // later step's pieces must not sit behind it): B2D_EAGER_STREAMS, default the plan's depth
+  int max_act = 0;
+  if (wait_bands)
+    for (int b = 0; b < nbands; ++b) max_act = std::max(max_act, c->act[b]);
+  const int ncatch = std::max(1, std::min((int)Ctx::NCATCH, env_int("B2D_EAGER_STREAMS", std::max(2, max_act))));
   if (eager) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    for (auto& q : c->s_catch) {
-      if (!q) cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, lo);
-      cudaStreamWaitEvent(q, c->ev_join, 0);
+    for (int q = 0; q < ncatch; ++q) {
+      if (!c->s_catch[q]) cudaStreamCreateWithPriority(&c->s_catch[q], cudaStreamNonBlocking, lo);
+      cudaStreamWaitEvent(c->s_catch[q], c->ev_join, 0);
     }
     while ((int)c->ev_caught.size() < nbands) {
       cudaEvent_t e;
@@ -1355,7 +1362,7 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
     cudaEventRecord(c->ev_panel[st], c->s_mid);
     if (ke >= nt) break;
     if (eager) {
-      cudaStream_t cs = c->s_catch[st & 1];
+      cudaStream_t cs = c->s_catch[st % ncatch];
       bool first = true;
       for (int b = 0; b < nbands; ++b) {
         if (c->act[b] <= st) continue;  // active, or joining at this step
@@ -1414,8 +1421,8 @@ static void enqueue_factor(Ctx* c, const FactorTarget& ft, bool wait_bands,
   if (step_hook) (*step_hook)(INT_MAX);
   // join the side streams
   if (eager)
-    for (auto q : c->s_catch) {
-      cudaEventRecord(c->ev_join, q);
+    for (int q = 0; q < ncatch; ++q) {
+      cudaEventRecord(c->ev_join, c->s_catch[q]);
       cudaStreamWaitEvent(c->s_main, c->ev_join, 0);
     }
   cudaEventRecord(c->ev_join, c->s_side);
